@@ -1,0 +1,372 @@
+// TEST INFRASTRUCTURE (oracle only) — a small extern "C" driver over the
+// UNMODIFIED reference library (proj/core, compiled from /root/reference by
+// oracle/Makefile against oracle/fftw_shim). It uses only the reference's
+// public API, exactly as its own run_worker / bench / verification code does:
+//   build_layout            proj/core/include/sdns/layout.hpp:48
+//   wavenumbers             proj/core/include/sdns/mesh.hpp:36
+//   DistributedFFT          proj/core/include/sdns/fft.hpp:26-62
+//   compute_rhs / project   proj/core/include/sdns/navier_stokes.hpp:17-49
+//   Rk4State / advance      proj/core/include/sdns/rk4.hpp:18-62
+//   collect_stats           proj/core/include/sdns/diagnostics.hpp:36-38
+//   run_group               proj/core/include/sdns/transport.hpp:103-106
+//   bench                   proj/core/include/sdns/runner.hpp:73-74
+// Global arrays passed across this ABI are row-major: spectral (n, n, n/2+1)
+// complex as interleaved doubles, real (n, n, n); vector fields are three
+// such arrays back to back (component-major).
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "sdns/diagnostics.hpp"
+#include "sdns/fft.hpp"
+#include "sdns/layout.hpp"
+#include "sdns/mesh.hpp"
+#include "sdns/navier_stokes.hpp"
+#include "sdns/rk4.hpp"
+#include "sdns/runner.hpp"
+#include "sdns/transport.hpp"
+
+using namespace sdns;
+
+namespace {
+
+thread_local std::string g_err;
+
+SolverConfig make_cfg(int n, int decomp, int p, int p1, int p2, double nu,
+                      double dt, double t_end, int dealias, int out_every) {
+  SolverConfig cfg;
+  cfg.n = n;
+  cfg.decomp = decomp == 0 ? Decomp::Slab : Decomp::Pencil;
+  cfg.p = p;
+  cfg.p1 = decomp == 0 ? 1 : p1;
+  cfg.p2 = decomp == 0 ? 1 : p2;
+  cfg.nu = nu;
+  cfg.dt = dt;
+  cfg.t_end = t_end;
+  cfg.dealias = dealias != 0;
+  cfg.out_every = out_every < 1 ? 1 : out_every;
+  cfg.validate();
+  return cfg;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const ProtocolError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const TimeoutError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const DivergenceError& e) {
+    g_err = e.what();
+    return 4;
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return 5;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 9;
+  }
+}
+
+void group(int p, const std::function<void(int, std::shared_ptr<Communicator>)>& body) {
+  if (p == 1) {
+    body(0, make_loopback());
+  } else {
+    run_group(p, body, std::chrono::seconds(600));
+  }
+}
+
+std::int64_t spec_index(std::int64_t n, std::int64_t nf, const Extents3& ex,
+                        std::int64_t i, std::int64_t j, std::int64_t k) {
+  return ((ex.offset[0] + i) * n + (ex.offset[1] + j)) * nf + (ex.offset[2] + k);
+}
+
+void scatter_spec(const double* g, std::int64_t n, const Extents3& ex,
+                  SpectralField3& f) {
+  const std::int64_t nf = n / 2 + 1;
+  const std::int64_t gsz = n * n * nf;
+  for (int c = 0; c < 3; ++c)
+    for (std::int64_t i = 0; i < ex.shape.n0; ++i)
+      for (std::int64_t j = 0; j < ex.shape.n1; ++j)
+        for (std::int64_t k = 0; k < ex.shape.n2; ++k) {
+          const std::int64_t m = c * gsz + spec_index(n, nf, ex, i, j, k);
+          f[c](i, j, k) = Complex(g[2 * m], g[2 * m + 1]);
+        }
+}
+
+void gather_spec(const SpectralField3& f, std::int64_t n, const Extents3& ex,
+                 double* g) {
+  const std::int64_t nf = n / 2 + 1;
+  const std::int64_t gsz = n * n * nf;
+  for (int c = 0; c < 3; ++c)
+    for (std::int64_t i = 0; i < ex.shape.n0; ++i)
+      for (std::int64_t j = 0; j < ex.shape.n1; ++j)
+        for (std::int64_t k = 0; k < ex.shape.n2; ++k) {
+          const std::int64_t m = c * gsz + spec_index(n, nf, ex, i, j, k);
+          const Complex v = f[c](i, j, k);
+          g[2 * m] = v.real();
+          g[2 * m + 1] = v.imag();
+        }
+}
+
+void scatter_real(const double* g, std::int64_t n, const Extents3& ex,
+                  RealField3& f) {
+  const std::int64_t gsz = n * n * n;
+  for (int c = 0; c < 3; ++c)
+    for (std::int64_t i = 0; i < ex.shape.n0; ++i)
+      for (std::int64_t j = 0; j < ex.shape.n1; ++j)
+        for (std::int64_t k = 0; k < ex.shape.n2; ++k)
+          f[c](i, j, k) = g[c * gsz + ((ex.offset[0] + i) * n + ex.offset[1] + j) * n +
+                            ex.offset[2] + k];
+}
+
+void gather_real(const RealField3& f, std::int64_t n, const Extents3& ex,
+                 double* g) {
+  const std::int64_t gsz = n * n * n;
+  for (int c = 0; c < 3; ++c)
+    for (std::int64_t i = 0; i < ex.shape.n0; ++i)
+      for (std::int64_t j = 0; j < ex.shape.n1; ++j)
+        for (std::int64_t k = 0; k < ex.shape.n2; ++k)
+          g[c * gsz + ((ex.offset[0] + i) * n + ex.offset[1] + j) * n + ex.offset[2] + k] =
+              f[c](i, j, k);
+}
+
+// stats row: t, E, Z, eps, div_max, then `shells` spectrum values
+void put_stats(const FlowStats& s, double* row) {
+  row[0] = s.t;
+  row[1] = s.energy;
+  row[2] = s.enstrophy;
+  row[3] = s.dissipation;
+  row[4] = s.divergence_max;
+  for (std::size_t i = 0; i < s.spectrum.size(); ++i) row[5 + i] = s.spectrum[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sdns_ref_last_error() { return g_err.c_str(); }
+
+int sdns_ref_spectrum_shells(int n) { return spectrum_shells(n); }
+
+/// Distributed forward transform of a global 3-component real field.
+int sdns_ref_forward(int n, int decomp, int p, int p1, int p2, const double* u,
+                     double* uhat) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, decomp, p, p1, p2, 0.0, 1.0, 0.0, 1, 1);
+    std::mutex mu;
+    group(p, [&](int rank, std::shared_ptr<Communicator> comm) {
+      const RankLayout lo = build_layout(cfg, rank);
+      DistributedFFT fft(cfg, lo, comm);
+      RealField3 f(lo.real.shape);
+      scatter_real(u, n, lo.real, f);
+      SpectralField3 fu(lo.spec.shape);
+      fft.forward(f, fu);
+      std::lock_guard lk(mu);
+      gather_spec(fu, n, lo.spec, uhat);
+    });
+  });
+}
+
+/// Distributed inverse transform (normalised) of a global spectral field.
+int sdns_ref_inverse(int n, int decomp, int p, int p1, int p2,
+                     const double* uhat, double* u) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, decomp, p, p1, p2, 0.0, 1.0, 0.0, 1, 1);
+    std::mutex mu;
+    group(p, [&](int rank, std::shared_ptr<Communicator> comm) {
+      const RankLayout lo = build_layout(cfg, rank);
+      DistributedFFT fft(cfg, lo, comm);
+      SpectralField3 fu(lo.spec.shape);
+      scatter_spec(uhat, n, lo.spec, fu);
+      RealField3 f(lo.real.shape);
+      fft.inverse(fu, f);
+      std::lock_guard lk(mu);
+      gather_real(f, n, lo.real, u);
+    });
+  });
+}
+
+/// compute_rhs on a global spectral state.
+int sdns_ref_compute_rhs(int n, int decomp, int p, int p1, int p2, double nu,
+                         int dealias, const double* uhat, double* du) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, decomp, p, p1, p2, nu, 1.0, 0.0, dealias, 1);
+    std::mutex mu;
+    group(p, [&](int rank, std::shared_ptr<Communicator> comm) {
+      const RankLayout lo = build_layout(cfg, rank);
+      const WavenumberMesh wm = wavenumbers(cfg, lo);
+      DistributedFFT fft(cfg, lo, comm);
+      RhsWorkspace ws(lo);
+      SpectralField3 u(lo.spec.shape), d(lo.spec.shape);
+      scatter_spec(uhat, n, lo.spec, u);
+      compute_rhs(u, wm, fft, ws, nu, d);
+      std::lock_guard lk(mu);
+      gather_spec(d, n, lo.spec, du);
+    });
+  });
+}
+
+/// Pointwise ops on a global spectral field (p = 1 semantics).
+///   op 0: curl_hat(in) -> out        op 1: project(in) -> out
+///   op 2: pressure_hat(in) -> out (component 0 only)
+int sdns_ref_spectral_op(int n, int op, int dealias, const double* in, double* out) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, 0, 1, 1, 1, 0.0, 1.0, 0.0, dealias, 1);
+    const RankLayout lo = build_layout(cfg, 0);
+    const WavenumberMesh wm = wavenumbers(cfg, lo);
+    SpectralField3 u(lo.spec.shape), o(lo.spec.shape);
+    scatter_spec(in, n, lo.spec, u);
+    if (op == 0) {
+      curl_hat(u, wm, o);
+    } else if (op == 1) {
+      o = u;
+      project(o, wm);
+    } else if (op == 2) {
+      pressure_hat(u, wm, o[0]);
+    } else {
+      throw ConfigError("unknown op");
+    }
+    gather_spec(o, n, lo.spec, out);
+  });
+}
+
+/// cross(a, b) on flat 3-component real arrays of `count` points each.
+int sdns_ref_cross(std::int64_t count, const double* a, const double* b, double* out) {
+  return guarded([&] {
+    RealField3 fa(Shape3{1, 1, count}), fb(Shape3{1, 1, count}), fo(Shape3{1, 1, count});
+    for (int c = 0; c < 3; ++c) {
+      std::memcpy(fa[c].data.data(), a + c * count, sizeof(double) * count);
+      std::memcpy(fb[c].data.data(), b + c * count, sizeof(double) * count);
+    }
+    cross(fa, fb, fo);
+    for (int c = 0; c < 3; ++c)
+      std::memcpy(out + c * count, fo[c].data.data(), sizeof(double) * count);
+  });
+}
+
+/// collect_stats of a global spectral state; row = t,E,Z,eps,div,spectrum.
+int sdns_ref_collect_stats(int n, int decomp, int p, int p1, int p2, double nu,
+                           const double* uhat, double* row) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, decomp, p, p1, p2, nu, 1.0, 0.0, 1, 1);
+    std::mutex mu;
+    group(p, [&](int rank, std::shared_ptr<Communicator> comm) {
+      const RankLayout lo = build_layout(cfg, rank);
+      const WavenumberMesh wm = wavenumbers(cfg, lo);
+      SpectralField3 u(lo.spec.shape);
+      scatter_spec(uhat, n, lo.spec, u);
+      const FlowStats s = collect_stats(0.0, u, wm, nu, *comm);
+      if (rank == 0) {
+        std::lock_guard lk(mu);
+        put_stats(s, row);
+      }
+    });
+  });
+}
+
+/// A production-style run (mirrors run_worker, proj/core/src/runner.cpp:67-111):
+/// state = uhat0 (optionally projected first), advance() to t_end = steps*dt
+/// with post_step = project and a collect_stats sample every out_every
+/// steps. `stats` receives one row per sample (step 0 included) of
+/// 5 + shells doubles; *n_samples is set. uhat_final receives the final
+/// global state.
+int sdns_ref_run(int n, int decomp, int p, int p1, int p2, double nu, double dt,
+                 int steps, int out_every, int dealias, int init_project,
+                 const double* uhat0, double* stats, int* n_samples,
+                 double* uhat_final) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, decomp, p, p1, p2, nu, dt,
+                                      static_cast<double>(steps) * dt, dealias, out_every);
+    const int shells = spectrum_shells(n);
+    std::mutex mu;
+    int count = 0;
+    group(p, [&](int rank, std::shared_ptr<Communicator> comm) {
+      const RankLayout lo = build_layout(cfg, rank);
+      const WavenumberMesh wm = wavenumbers(cfg, lo);
+      DistributedFFT fft(cfg, lo, comm);
+      RhsWorkspace ws(lo);
+      Rk4State st(lo.spec.shape);
+      scatter_spec(uhat0, n, lo.spec, st.u_hat);
+      if (init_project) project(st.u_hat, wm);
+      RhsFn rhs = [&](const SpectralField3& uh, SpectralField3& du) {
+        compute_rhs(uh, wm, fft, ws, cfg.nu, du);
+      };
+      AdvanceHooks hooks;
+      hooks.post_step = [&] { project(st.u_hat, wm); };
+      int local = 0;
+      hooks.sample = [&](std::int64_t, double t) {
+        const FlowStats s = collect_stats(t, st.u_hat, wm, cfg.nu, *comm);
+        if (rank == 0 && stats) put_stats(s, stats + static_cast<std::size_t>(local) * (5 + shells));
+        ++local;
+      };
+      advance(st, cfg, rhs, *comm, hooks);
+      std::lock_guard lk(mu);
+      if (rank == 0) count = local;
+      if (uhat_final) gather_spec(st.u_hat, n, lo.spec, uhat_final);
+    });
+    if (n_samples) *n_samples = count;
+  });
+}
+
+/// One classical RK4 step with a fixed dt (rk4_step_finite), optionally
+/// followed by project (the bench loop, proj/core/src/runner.cpp:356-359).
+/// The Neumaier carry starts at zero.
+int sdns_ref_rk4_steps(int n, int decomp, int p, int p1, int p2, double nu,
+                       double dt, int steps, int post_project, double* uhat) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, decomp, p, p1, p2, nu, dt, dt, 1, 1);
+    std::mutex mu;
+    group(p, [&](int rank, std::shared_ptr<Communicator> comm) {
+      const RankLayout lo = build_layout(cfg, rank);
+      const WavenumberMesh wm = wavenumbers(cfg, lo);
+      DistributedFFT fft(cfg, lo, comm);
+      RhsWorkspace ws(lo);
+      Rk4State st(lo.spec.shape);
+      scatter_spec(uhat, n, lo.spec, st.u_hat);
+      RhsFn rhs = [&](const SpectralField3& uh, SpectralField3& du) {
+        compute_rhs(uh, wm, fft, ws, cfg.nu, du);
+      };
+      for (int s = 0; s < steps; ++s) {
+        rk4_step(st, dt, rhs);
+        if (post_project) project(st.u_hat, wm);
+      }
+      std::lock_guard lk(mu);
+      gather_spec(st.u_hat, n, lo.spec, uhat);
+    });
+  });
+}
+
+/// The reference's own bench harness (proj/core/src/runner.cpp:336-397):
+/// 5 warm-up steps, then `steps` timed rk4_step + project between
+/// barriers; returns mean seconds per step from rank 0.
+int sdns_ref_bench(int n, int decomp, int p, int p1, int p2, int steps,
+                   double* sec_per_step) {
+  return guarded([&] {
+    BenchEntry e;
+    e.n = n;
+    e.decomp = decomp == 0 ? Decomp::Slab : Decomp::Pencil;
+    e.p = p;
+    e.p1 = p1;
+    e.p2 = p2;
+    RunOptions opts;
+    opts.backend = p == 1 ? "loopback" : "inprocess";
+    opts.collective_timeout = std::chrono::milliseconds(3600 * 1000);
+    const auto rows = bench({e}, steps, opts);
+    if (rows.empty() || rows[0].status != "ok")
+      throw ConfigError(rows.empty() ? "bench produced no rows" : rows[0].status);
+    *sec_per_step = rows[0].sec_per_step;
+  });
+}
+
+}  // extern "C"
