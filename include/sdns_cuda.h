@@ -1,0 +1,212 @@
+/*
+ * sdns_cuda.h — C ABI of the B200-native spectral-DNS hot path.
+ *
+ * Drop-in boundary for the reference solver's hot path (arXiv 1607.00850,
+ * C++ library `sdns`, /root/reference/proj). Every entry point replaces one
+ * reference interface; the citation after each declaration is the reference
+ * file:line it stands in for. Plain pointers and sizes only — no C++ or torch
+ * types cross this boundary. INTEGRATION.md shows the reference-side binding.
+ *
+ * Conventions
+ *  - Status codes map 1:1 onto the reference's exception types
+ *    (proj/core/include/sdns/types.hpp:28-62); the message of the last
+ *    failure on the calling thread is returned by sdns_last_error().
+ *  - Host arrays use the reference's rank-local block layout
+ *    (RankLayout, proj/core/include/sdns/layout.hpp:24-41): row-major,
+ *    z fastest; spectral values are interleaved (re, im) doubles; vector
+ *    fields are `ncomp` component blocks back to back (SoA, like
+ *    VectorField3, proj/core/include/sdns/fields.hpp:33-46).
+ *  - All allocation happens in the *_create / *_alloc calls; transforms and
+ *    steps never allocate (proj/core/include/sdns/fft.hpp:22-25).
+ *  - Every transform / RHS / step call is collective over the context's
+ *    communicator, in identical order on all ranks (fft.hpp:22-24).
+ *  - Work is enqueued on the context's CUDA stream; calls that return host
+ *    values (stats, finite flags, downloads) synchronise that stream.
+ */
+#ifndef SDNS_CUDA_H
+#define SDNS_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (types.hpp:28-62) ------------------------------------ */
+enum {
+  SDNS_OK = 0,
+  SDNS_CONFIG_ERROR = 1,     /* ConfigError      types.hpp:29-32 */
+  SDNS_PROTOCOL_ERROR = 2,   /* ProtocolError    types.hpp:36-39 */
+  SDNS_TIMEOUT_ERROR = 3,    /* TimeoutError     types.hpp:42-45 */
+  SDNS_DIVERGENCE_ERROR = 4, /* DivergenceError  types.hpp:48-56 */
+  SDNS_IO_ERROR = 5,         /* IoError          types.hpp:59-62 */
+  SDNS_CUDA_ERROR = 6,       /* device / driver failure (no reference analogue) */
+  SDNS_INTERNAL_ERROR = 9
+};
+
+enum { SDNS_SLAB = 0, SDNS_PENCIL = 1 };
+enum { SDNS_REAL = 0, SDNS_SPECTRAL = 1 };
+
+/* SolverConfig, proj/core/include/sdns/config.hpp:14-30 */
+typedef struct sdns_config {
+  int n;          /* grid points per axis */
+  int decomp;     /* SDNS_SLAB | SDNS_PENCIL */
+  int p, p1, p2;  /* ranks; pencil grid p = p1*p2 */
+  double nu;
+  double dt;
+  double t_end;
+  int dealias;    /* strict 2/3 rule */
+  int out_every;
+} sdns_config;
+
+/* RankLayout, proj/core/include/sdns/layout.hpp:24-41 (one transpose stage
+ * for slab, two for pencil; counts in complex elements, per group peer). */
+#define SDNS_MAX_PEERS 64
+typedef struct sdns_layout {
+  int rank, p, p1, p2, coord1, coord2;
+  int64_t n, nf;
+  int64_t real_shape[3], real_offset[3];
+  int64_t spec_shape[3], spec_offset[3];
+  int nstages;
+  int stage_peers[2];
+  int64_t send_counts[2][SDNS_MAX_PEERS];
+  int64_t recv_counts[2][SDNS_MAX_PEERS];
+} sdns_layout;
+
+typedef struct sdns_comm sdns_comm;
+typedef struct sdns_ctx sdns_ctx;
+typedef struct sdns_field sdns_field;
+typedef struct sdns_state sdns_state;
+
+/* ---- errors ------------------------------------------------------------- */
+const char* sdns_last_error(void);
+
+/* ---- host-only setup (no device needed) --------------------------------- */
+int sdns_config_validate(const sdns_config* cfg);                  /* config.cpp:17-50 */
+int sdns_build_layout(const sdns_config* cfg, int rank,
+                      sdns_layout* out);                            /* layout.hpp:48 */
+int64_t sdns_block_size(int64_t total, int parts, int index);       /* layout.hpp:44 */
+int64_t sdns_block_start(int64_t total, int parts, int index);      /* layout.hpp:45 */
+int64_t sdns_step_count(double t_end, double dt);                   /* rk4.hpp:43 */
+int sdns_spectrum_shells(int64_t n);                                /* diagnostics.hpp:22 */
+/* Seeded isotropic initial field (BASELINE configs 2-4):
+ * writes the rank's spectral block (3 comps) into `out`. Identical for every
+ * decomposition. The reference has no such case (navier_stokes.cpp:27-32). */
+int sdns_iso_init_host(int64_t n, uint64_t seed, double k0, double energy,
+                       const sdns_layout* lo, double* out);
+/* Library build string. */
+const char* sdns_version(void);
+
+/* ---- communicators (Communicator, transport.hpp:46-94) ------------------ */
+int sdns_comm_loopback(sdns_comm** out);                            /* transport.hpp:96-98 */
+/* Threads-as-ranks on ONE device (InProcessBackend, transport.hpp:109-131):
+ * out[r] is handed to the host thread driving rank r. Exchanges are
+ * stream-ordered device copies; no kernel waits on another. */
+int sdns_comm_inprocess_group(int size, int device, double timeout_s, sdns_comm** out);
+/* One process per GPU over NCCL (NVLink / NVSwitch). The 128-byte unique id
+ * is created on rank 0 and distributed by the caller. */
+int sdns_comm_nccl_unique_id(unsigned char id[128]);
+int sdns_comm_nccl_init(const unsigned char id[128], int size, int rank, int device,
+                        sdns_comm** out);
+int sdns_comm_rank(const sdns_comm* c);
+int sdns_comm_size(const sdns_comm* c);
+int sdns_comm_barrier(sdns_comm* c);                                 /* transport.hpp:64 */
+/* In-place reduction in ascending rank order (op 0 sum, 1 max, 2 min). */
+int sdns_comm_allreduce(sdns_comm* c, double* values, int count, int op); /* :61 */
+int sdns_comm_destroy(sdns_comm* c);
+
+/* ---- context (DistributedFFT ctor + wavenumbers + workspaces) ----------- */
+/* fft.cpp:15-57, mesh.cpp:23-72, navier_stokes.hpp:32-41. `stream` is a
+ * cudaStream_t or NULL (the context then owns a stream). */
+int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* comm,
+                    void* stream, sdns_ctx** out);
+int sdns_ctx_destroy(sdns_ctx* ctx);
+int sdns_ctx_layout(const sdns_ctx* ctx, sdns_layout* out);
+void* sdns_ctx_stream(const sdns_ctx* ctx);
+int sdns_ctx_sync(sdns_ctx* ctx);
+/* Device bytes held by the context (workspaces) and per field. */
+int64_t sdns_ctx_device_bytes(const sdns_ctx* ctx);
+
+/* ---- device fields (Field3d / VectorField3, fields.hpp:10-49) ----------- */
+int sdns_field_alloc(sdns_ctx* ctx, int kind, int ncomp, sdns_field** out);
+int sdns_field_free(sdns_field* f);
+int sdns_field_upload(sdns_ctx* ctx, sdns_field* f, const double* host);
+int sdns_field_download(sdns_ctx* ctx, const sdns_field* f, double* host);
+int sdns_field_copy(sdns_ctx* ctx, const sdns_field* src, sdns_field* dst);
+
+/* ---- DistributedFFT::forward / inverse (fft.hpp:34-38, fft.cpp:59-227) -- */
+/* Forward is unnormalised; inverse applies 1/n^3 once. All components. */
+int sdns_fft_forward(sdns_ctx* ctx, const sdns_field* real, sdns_field* spec);
+int sdns_fft_inverse(sdns_ctx* ctx, const sdns_field* spec, sdns_field* real);
+
+/* ---- pointwise operators (navier_stokes.hpp:17-29) ---------------------- */
+int sdns_curl_hat(sdns_ctx* ctx, const sdns_field* u_hat, sdns_field* omega_hat);
+int sdns_cross(sdns_ctx* ctx, const sdns_field* a, const sdns_field* b, sdns_field* out);
+int sdns_project(sdns_ctx* ctx, sdns_field* u_hat);
+int sdns_pressure_hat(sdns_ctx* ctx, const sdns_field* nl_hat, sdns_field* p_hat);
+
+/* ---- compute_rhs (navier_stokes.hpp:47-49, navier_stokes.cpp:104-139) --- */
+int sdns_compute_rhs(sdns_ctx* ctx, const sdns_field* u_hat, double nu, sdns_field* du_hat);
+
+/* ---- RK4 (Rk4State / rk4_step / advance, rk4.hpp:18-62) ----------------- */
+int sdns_state_create(sdns_ctx* ctx, sdns_state** out);
+int sdns_state_destroy(sdns_state* st);
+int sdns_state_set(sdns_ctx* ctx, sdns_state* st, const sdns_field* u_hat, double t,
+                   int64_t step);           /* carry reset to 0 */
+int sdns_state_get(sdns_ctx* ctx, const sdns_state* st, sdns_field* u_hat);
+/* The state's u_hat as a field view (owned by the state; do not free). */
+sdns_field* sdns_state_u_hat(sdns_state* st);
+int sdns_state_time(const sdns_state* st, double* t, int64_t* step);
+/* One classical RK4 step with the fused pipeline (rk4.cpp:27-71); if
+ * post_project, the solenoidal cleanup of runner.cpp:107 is fused into the
+ * last stage. *finite (if not NULL) receives the collective finite flag
+ * (rk4.cpp:97) and forces a stream synchronisation. */
+int sdns_rk4_step(sdns_ctx* ctx, sdns_state* st, double dt, int post_project, int* finite);
+/* advance(): rk4.cpp:86-107, including the shortened final step, t = k*dt,
+ * the collective divergence check (SDNS_DIVERGENCE_ERROR, *fail_step set)
+ * and the sample hook cadence (step 0, every out_every, final step). */
+typedef void (*sdns_sample_fn)(int64_t step, double t, void* user);
+int sdns_advance(sdns_ctx* ctx, sdns_state* st, sdns_sample_fn sample, void* user,
+                 int64_t* fail_step);
+/* Host-buffer tier (reference-facing, e2e): uploads u_hat, runs `steps`
+ * fused steps with post-step projection, downloads u_hat. */
+int sdns_rk4_step_host(sdns_ctx* ctx, sdns_state* st, double* host_u_hat, double dt,
+                       int steps);
+
+/* ---- diagnostics (diagnostics.hpp:22-44) -------------------------------- */
+/* row = [t, E, Z, eps, div_max, spectrum[shells]] identical on every rank. */
+int sdns_collect_stats(sdns_ctx* ctx, const sdns_field* u_hat, double nu, double t,
+                       double* row);
+int sdns_l2_diff(sdns_ctx* ctx, const sdns_field* a, const sdns_field* b, double* out);
+
+/* ---- per-pass timing (CUDA events on the context stream) --------------- */
+/* Pass tags of one RHS evaluation. */
+enum {
+  SDNS_PASS_X_INV_CURL = 0, /* P1 */
+  SDNS_PASS_Y_INV = 1,      /* P2 */
+  SDNS_PASS_Z_FUSED = 2,    /* P3 */
+  SDNS_PASS_Y_FWD = 3,      /* P4 */
+  SDNS_PASS_X_FWD_TAIL = 4, /* P5, compute_rhs tail */
+  SDNS_PASS_X_FWD_RK0 = 5,  /* P5, RK4 stage 0 */
+  SDNS_PASS_X_FWD_RK12 = 6, /* P5, RK4 stages 1-2 */
+  SDNS_PASS_X_FWD_RK3 = 7,  /* P5, RK4 stage 3 + projection */
+  SDNS_PASS_A2A_INV = 8,
+  SDNS_PASS_A2A_FWD = 9,
+  SDNS_NPASS = 10
+};
+/* Enables (and resets) event timing of every pipeline launch. */
+int sdns_ctx_timing(sdns_ctx* ctx, int enable);
+/* Synchronises, then returns per-tag total milliseconds and launch counts
+ * accumulated since the last enable/read (arrays of SDNS_NPASS). */
+int sdns_ctx_timing_read(sdns_ctx* ctx, double* ms, int64_t* launches);
+
+/* ---- host memory helpers (pinned buffers for the e2e tier) ------------- */
+void* sdns_host_alloc(size_t bytes);
+void sdns_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SDNS_CUDA_H */

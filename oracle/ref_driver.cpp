@@ -13,6 +13,7 @@
 // Global arrays passed across this ABI are row-major: spectral (n, n, n/2+1)
 // complex as interleaved doubles, real (n, n, n); vector fields are three
 // such arrays back to back (component-major).
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -344,6 +345,58 @@ int sdns_ref_rk4_steps(int n, int decomp, int p, int p1, int p2, double nu,
       std::lock_guard lk(mu);
       gather_spec(st.u_hat, n, lo.spec, uhat);
     });
+  });
+}
+
+/// bench_entry_seconds (proj/core/src/runner.cpp:336-373) with a
+/// configurable warm-up and an optional initial spectral state (NULL: the
+/// reference's own Taylor-Green init + forward + project). unit 0 times
+/// rk4_step + project (the reference's step), unit 1 times one compute_rhs
+/// (a quarter-step sample). Returns mean seconds per unit from rank 0.
+int sdns_ref_time_units(int n, int decomp, int p, int p1, int p2, double nu, double dt,
+                        int warmup, int units, int unit, const double* uhat0,
+                        double* seconds) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, decomp, p, p1, p2, nu, dt, dt, 1, 1);
+    double sec = 0.0;
+    std::mutex mu;
+    group(p, [&](int rank, std::shared_ptr<Communicator> comm) {
+      const RankLayout lo = build_layout(cfg, rank);
+      const PhysicalMesh mesh = physical_mesh(lo);
+      const WavenumberMesh wm = wavenumbers(cfg, lo);
+      DistributedFFT fft(cfg, lo, comm);
+      RhsWorkspace ws(lo);
+      Rk4State st(lo.spec.shape);
+      if (uhat0) {
+        scatter_spec(uhat0, n, lo.spec, st.u_hat);
+      } else {
+        RealField3 u = make_initial_condition("taylor_green", lo, mesh);
+        fft.forward(u, st.u_hat);
+        project(st.u_hat, wm);
+      }
+      RhsFn rhs = [&](const SpectralField3& uh, SpectralField3& du) {
+        compute_rhs(uh, wm, fft, ws, cfg.nu, du);
+      };
+      const auto one = [&] {
+        if (unit == 0) {
+          rk4_step(st, dt, rhs);
+          project(st.u_hat, wm);
+        } else {
+          compute_rhs(st.u_hat, wm, fft, ws, cfg.nu, st.rhs);
+        }
+      };
+      for (int k = 0; k < warmup; ++k) one();
+      comm->barrier();
+      const auto t0 = std::chrono::steady_clock::now();
+      for (int k = 0; k < units; ++k) one();
+      comm->barrier();
+      const auto t1 = std::chrono::steady_clock::now();
+      if (rank == 0) {
+        std::lock_guard lk(mu);
+        sec = std::chrono::duration<double>(t1 - t0).count() / static_cast<double>(units);
+      }
+    });
+    *seconds = sec;
   });
 }
 

@@ -1,0 +1,635 @@
+"""B200-native hot path of the triply periodic Fourier-Galerkin Navier-Stokes
+solver (arXiv 1607.00850), behind the reference solver's operator API.
+
+This package is a thin Python mirror of the reference C++ API
+(``sdns``: SolverConfig, build_layout, DistributedFFT, curl_hat, cross,
+project, pressure_hat, compute_rhs, Rk4State / rk4_step / advance,
+collect_stats, l2_diff) over the C ABI declared in ``include/sdns_cuda.h``
+and implemented by ``libsdns_cuda.so`` (sm_100a CUDA kernels + C++ host
+orchestration + NCCL). Every compute call runs on the GPU; there is no CPU
+fallback: if the library or a GPU is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+__all__ = [
+    "SolverConfig", "Layout", "ConfigError", "ProtocolError", "CollectiveTimeout",
+    "DivergenceError", "IoError", "CudaError", "SdnsError", "load_library", "validate",
+    "build_layout", "block_size", "block_start", "step_count", "spectrum_shells",
+    "iso_init", "Comm", "Context", "Field", "DistributedFFT", "curl_hat", "cross",
+    "project", "pressure_hat", "compute_rhs", "Rk4State", "FlowStats", "collect_stats",
+    "l2_diff", "run_group",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsdns_cuda.so")
+
+
+# --- errors (proj/core/include/sdns/types.hpp:28-62) ------------------------
+
+class SdnsError(RuntimeError):
+    code = 9
+
+
+class ConfigError(SdnsError):
+    code = 1
+
+
+class ProtocolError(SdnsError):
+    code = 2
+
+
+class CollectiveTimeout(SdnsError):
+    code = 3
+
+
+class DivergenceError(SdnsError):
+    code = 4
+
+    def __init__(self, msg, step=0):
+        super().__init__(msg)
+        self.step = step
+
+
+class IoError(SdnsError):
+    code = 5
+
+
+class CudaError(SdnsError):
+    code = 6
+
+
+_ERRORS = {1: ConfigError, 2: ProtocolError, 3: CollectiveTimeout, 4: DivergenceError,
+           5: IoError, 6: CudaError}
+
+
+# --- C structs ----------------------------------------------------------------
+
+class _Config(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("decomp", ctypes.c_int), ("p", ctypes.c_int),
+                ("p1", ctypes.c_int), ("p2", ctypes.c_int), ("nu", ctypes.c_double),
+                ("dt", ctypes.c_double), ("t_end", ctypes.c_double),
+                ("dealias", ctypes.c_int), ("out_every", ctypes.c_int)]
+
+
+MAX_PEERS = 64
+
+
+class _Layout(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("p", ctypes.c_int), ("p1", ctypes.c_int),
+                ("p2", ctypes.c_int), ("coord1", ctypes.c_int), ("coord2", ctypes.c_int),
+                ("n", ctypes.c_int64), ("nf", ctypes.c_int64),
+                ("real_shape", ctypes.c_int64 * 3), ("real_offset", ctypes.c_int64 * 3),
+                ("spec_shape", ctypes.c_int64 * 3), ("spec_offset", ctypes.c_int64 * 3),
+                ("nstages", ctypes.c_int), ("stage_peers", ctypes.c_int * 2),
+                ("send_counts", (ctypes.c_int64 * MAX_PEERS) * 2),
+                ("recv_counts", (ctypes.c_int64 * MAX_PEERS) * 2)]
+
+
+PASS_NAMES = ["x_inv_curl", "y_inv", "z_fused", "y_fwd", "x_fwd_tail", "x_fwd_rk0",
+              "x_fwd_rk12", "x_fwd_rk3", "a2a_inv", "a2a_fwd"]
+NPASS = len(PASS_NAMES)
+
+SAMPLE_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p)
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Loads libsdns_cuda.so (built by __graft_entry__.build()). Raises if absent."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise CudaError(f"{path} is missing: run __graft_entry__.build() first")
+        lib = ctypes.CDLL(path)
+        P, I, D, I64, V = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64, None
+        PP = ctypes.POINTER(ctypes.c_void_p)
+        sig = {
+            "sdns_last_error": (ctypes.c_char_p, []),
+            "sdns_version": (ctypes.c_char_p, []),
+            "sdns_config_validate": (I, [ctypes.POINTER(_Config)]),
+            "sdns_build_layout": (I, [ctypes.POINTER(_Config), I, ctypes.POINTER(_Layout)]),
+            "sdns_block_size": (I64, [I64, I, I]),
+            "sdns_block_start": (I64, [I64, I, I]),
+            "sdns_step_count": (I64, [D, D]),
+            "sdns_spectrum_shells": (I, [I64]),
+            "sdns_iso_init_host": (I, [I64, ctypes.c_uint64, D, D, ctypes.POINTER(_Layout), P]),
+            "sdns_comm_loopback": (I, [PP]),
+            "sdns_comm_inprocess_group": (I, [I, I, D, PP]),
+            "sdns_comm_nccl_unique_id": (I, [ctypes.c_char_p]),
+            "sdns_comm_nccl_init": (I, [ctypes.c_char_p, I, I, I, PP]),
+            "sdns_comm_rank": (I, [P]),
+            "sdns_comm_size": (I, [P]),
+            "sdns_comm_barrier": (I, [P]),
+            "sdns_comm_allreduce": (I, [P, P, I, I]),
+            "sdns_comm_destroy": (I, [P]),
+            "sdns_ctx_create": (I, [ctypes.POINTER(_Config), I, I, P, P, PP]),
+            "sdns_ctx_destroy": (I, [P]),
+            "sdns_ctx_layout": (I, [P, ctypes.POINTER(_Layout)]),
+            "sdns_ctx_stream": (P, [P]),
+            "sdns_ctx_sync": (I, [P]),
+            "sdns_ctx_device_bytes": (I64, [P]),
+            "sdns_field_alloc": (I, [P, I, I, PP]),
+            "sdns_field_free": (I, [P]),
+            "sdns_field_upload": (I, [P, P, P]),
+            "sdns_field_download": (I, [P, P, P]),
+            "sdns_field_copy": (I, [P, P, P]),
+            "sdns_fft_forward": (I, [P, P, P]),
+            "sdns_fft_inverse": (I, [P, P, P]),
+            "sdns_curl_hat": (I, [P, P, P]),
+            "sdns_cross": (I, [P, P, P, P]),
+            "sdns_project": (I, [P, P]),
+            "sdns_pressure_hat": (I, [P, P, P]),
+            "sdns_compute_rhs": (I, [P, P, D, P]),
+            "sdns_state_create": (I, [P, PP]),
+            "sdns_state_destroy": (I, [P]),
+            "sdns_state_set": (I, [P, P, P, D, I64]),
+            "sdns_state_get": (I, [P, P, P]),
+            "sdns_state_u_hat": (P, [P]),
+            "sdns_state_time": (I, [P, ctypes.POINTER(D), ctypes.POINTER(I64)]),
+            "sdns_rk4_step": (I, [P, P, D, I, ctypes.POINTER(I)]),
+            "sdns_advance": (I, [P, P, SAMPLE_FN, P, ctypes.POINTER(I64)]),
+            "sdns_rk4_step_host": (I, [P, P, P, D, I]),
+            "sdns_collect_stats": (I, [P, P, D, D, P]),
+            "sdns_l2_diff": (I, [P, P, P, ctypes.POINTER(D)]),
+            "sdns_ctx_timing": (I, [P, I]),
+            "sdns_ctx_timing_read": (I, [P, P, P]),
+            "sdns_host_alloc": (P, [ctypes.c_size_t]),
+            "sdns_host_free": (V, [P]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def _check(rc: int, step: int = 0):
+    if rc == 0:
+        return
+    msg = load_library().sdns_last_error().decode(errors="replace")
+    cls = _ERRORS.get(rc, SdnsError)
+    if cls is DivergenceError:
+        raise DivergenceError(msg, step)
+    raise cls(msg)
+
+
+def _ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+# --- config and layout (config.hpp, layout.hpp) --------------------------------
+
+@dataclass
+class SolverConfig:
+    """SolverConfig, proj/core/include/sdns/config.hpp:14-30."""
+    n: int = 32
+    decomp: str = "slab"
+    p: int = 1
+    p1: int = 1
+    p2: int = 1
+    nu: float = 1.0 / 1600.0
+    dt: float = 1e-3
+    t_end: float = 0.1
+    dealias: bool = True
+    initial_case: str = "taylor_green"
+    out_every: int = 10
+
+    def to_c(self) -> _Config:
+        if self.decomp not in ("slab", "pencil"):
+            raise ConfigError(f"unknown decomposition '{self.decomp}' (expected slab|pencil)")
+        slab = self.decomp == "slab"
+        return _Config(self.n, 0 if slab else 1, self.p, 1 if slab else self.p1,
+                       1 if slab else self.p2, self.nu, self.dt, self.t_end,
+                       1 if self.dealias else 0, self.out_every)
+
+    def validate(self):
+        validate(self)
+
+
+@dataclass
+class Layout:
+    """RankLayout, proj/core/include/sdns/layout.hpp:24-41."""
+    rank: int
+    p: int
+    p1: int
+    p2: int
+    coord1: int
+    coord2: int
+    n: int
+    nf: int
+    real_shape: tuple
+    real_offset: tuple
+    spec_shape: tuple
+    spec_offset: tuple
+    stages: list = field(default_factory=list)  # [(send_counts, recv_counts)]
+
+    @staticmethod
+    def _from_c(c: _Layout) -> "Layout":
+        stages = []
+        for s in range(c.nstages):
+            k = c.stage_peers[s]
+            stages.append(([c.send_counts[s][q] for q in range(k)],
+                           [c.recv_counts[s][q] for q in range(k)]))
+        return Layout(c.rank, c.p, c.p1, c.p2, c.coord1, c.coord2, c.n, c.nf,
+                      tuple(c.real_shape), tuple(c.real_offset), tuple(c.spec_shape),
+                      tuple(c.spec_offset), stages)
+
+    def _to_c(self) -> _Layout:
+        c = _Layout()
+        c.rank, c.p, c.p1, c.p2 = self.rank, self.p, self.p1, self.p2
+        c.coord1, c.coord2, c.n, c.nf = self.coord1, self.coord2, self.n, self.nf
+        for i in range(3):
+            c.real_shape[i] = self.real_shape[i]
+            c.real_offset[i] = self.real_offset[i]
+            c.spec_shape[i] = self.spec_shape[i]
+            c.spec_offset[i] = self.spec_offset[i]
+        c.nstages = len(self.stages)
+        for s, (sc, rc) in enumerate(self.stages):
+            c.stage_peers[s] = len(sc)
+            for q in range(len(sc)):
+                c.send_counts[s][q] = sc[q]
+                c.recv_counts[s][q] = rc[q]
+        return c
+
+
+def validate(cfg: SolverConfig):
+    """SolverConfig::validate, proj/core/src/config.cpp:17-50."""
+    c = cfg.to_c()
+    _check(load_library().sdns_config_validate(ctypes.byref(c)))
+
+
+def build_layout(cfg: SolverConfig, rank: int) -> Layout:
+    """build_layout, proj/core/src/layout.cpp:17-76."""
+    c = cfg.to_c()
+    out = _Layout()
+    _check(load_library().sdns_build_layout(ctypes.byref(c), rank, ctypes.byref(out)))
+    return Layout._from_c(out)
+
+
+def block_size(total: int, parts: int, index: int) -> int:
+    return load_library().sdns_block_size(total, parts, index)
+
+
+def block_start(total: int, parts: int, index: int) -> int:
+    return load_library().sdns_block_start(total, parts, index)
+
+
+def step_count(t_end: float, dt: float) -> int:
+    """proj/core/src/rk4.cpp:79-84."""
+    return load_library().sdns_step_count(t_end, dt)
+
+
+def spectrum_shells(n: int) -> int:
+    """proj/core/src/diagnostics.cpp:66-69."""
+    return load_library().sdns_spectrum_shells(n)
+
+
+def iso_init(n: int, layout: Layout, seed: int = 1607, k0: float = 4.0,
+             energy: float = 0.5) -> np.ndarray:
+    """Seeded isotropic initial u_hat for the rank's spectral block,
+    shape (3, *spec_shape) complex128 (BASELINE configs 2-4)."""
+    out = np.empty((3,) + tuple(layout.spec_shape), dtype=np.complex128)
+    lc = layout._to_c()
+    _check(load_library().sdns_iso_init_host(n, seed, k0, energy, ctypes.byref(lc), _ptr(out)))
+    return out
+
+
+# --- communicators (transport.hpp:46-131) ---------------------------------------
+
+class Comm:
+    """Communicator handle: loopback, in-process group or NCCL."""
+
+    def __init__(self, handle):
+        self._h = handle
+        self._lib = load_library()
+
+    @staticmethod
+    def loopback() -> "Comm":
+        h = ctypes.c_void_p()
+        _check(load_library().sdns_comm_loopback(ctypes.byref(h)))
+        return Comm(h)
+
+    @staticmethod
+    def inprocess_group(size: int, device: int = 0, timeout_s: float = 600.0) -> List["Comm"]:
+        arr = (ctypes.c_void_p * size)()
+        _check(load_library().sdns_comm_inprocess_group(size, device, timeout_s, arr))
+        return [Comm(ctypes.c_void_p(arr[i])) for i in range(size)]
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(load_library().sdns_comm_nccl_unique_id(buf))
+        return buf.raw
+
+    @staticmethod
+    def nccl(uid: bytes, size: int, rank: int, device: int) -> "Comm":
+        h = ctypes.c_void_p()
+        _check(load_library().sdns_comm_nccl_init(uid, size, rank, device, ctypes.byref(h)))
+        return Comm(h)
+
+    @property
+    def rank(self) -> int:
+        return self._lib.sdns_comm_rank(self._h)
+
+    @property
+    def size(self) -> int:
+        return self._lib.sdns_comm_size(self._h)
+
+    def barrier(self):
+        _check(self._lib.sdns_comm_barrier(self._h))
+
+    def allreduce(self, values, op: str = "sum") -> np.ndarray:
+        v = np.ascontiguousarray(values, dtype=np.float64).copy()
+        _check(self._lib.sdns_comm_allreduce(self._h, _ptr(v), v.size,
+                                             {"sum": 0, "max": 1, "min": 2}[op]))
+        return v
+
+    def close(self):
+        if self._h:
+            self._lib.sdns_comm_destroy(self._h)
+            self._h = None
+
+
+def run_group(size: int, body: Callable[[int, Comm], object], device: int = 0,
+              timeout_s: float = 600.0) -> list:
+    """run_group, proj/core/src/transport.cpp:397-424: runs body(rank, comm)
+    on one host thread per rank over an in-process group sharing `device`;
+    rethrows the lowest-rank exception."""
+    comms = [Comm.loopback()] if size == 1 else Comm.inprocess_group(size, device, timeout_s)
+    results: list = [None] * size
+    errors: list = [None] * size
+
+    def worker(r):
+        try:
+            results[r] = body(r, comms[r])
+        except BaseException as e:  # noqa: BLE001
+            errors[r] = e
+
+    if size == 1:
+        worker(0)
+    else:
+        ts = [threading.Thread(target=worker, args=(r,)) for r in range(size)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    for c in comms:
+        c.close()
+    for e in errors:
+        if e is not None:
+            raise e
+    return results
+
+
+# --- context and fields -----------------------------------------------------------
+
+class Context:
+    """One rank's device context: DistributedFFT + WavenumberMesh + RhsWorkspace
+    (proj/core/src/fft.cpp:15-57, mesh.cpp:23-72, navier_stokes.hpp:32-41)."""
+
+    def __init__(self, cfg: SolverConfig, rank: int = 0, device: int = 0,
+                 comm: Optional[Comm] = None, stream: Optional[int] = None):
+        self.cfg = cfg
+        self._lib = load_library()
+        self._own_comm = comm is None
+        self.comm = comm if comm is not None else Comm.loopback()
+        c = cfg.to_c()
+        h = ctypes.c_void_p()
+        _check(self._lib.sdns_ctx_create(ctypes.byref(c), rank, device, self.comm._h,
+                                         ctypes.c_void_p(stream) if stream else None,
+                                         ctypes.byref(h)))
+        self._h = h
+        lo = _Layout()
+        self._lib.sdns_ctx_layout(h, ctypes.byref(lo))
+        self.layout = Layout._from_c(lo)
+
+    @property
+    def stream(self) -> int:
+        return self._lib.sdns_ctx_stream(self._h) or 0
+
+    @property
+    def device_bytes(self) -> int:
+        return self._lib.sdns_ctx_device_bytes(self._h)
+
+    def sync(self):
+        _check(self._lib.sdns_ctx_sync(self._h))
+
+    def timing(self, enable: bool = True):
+        """Enables (and resets) CUDA-event timing of every pipeline launch."""
+        _check(self._lib.sdns_ctx_timing(self._h, 1 if enable else 0))
+
+    def timing_read(self):
+        """Returns {pass: (total_ms, launches)} since the last enable/read."""
+        ms = np.zeros(NPASS)
+        cnt = np.zeros(NPASS, dtype=np.int64)
+        _check(self._lib.sdns_ctx_timing_read(self._h, _ptr(ms), _ptr(cnt)))
+        return {PASS_NAMES[i]: (float(ms[i]), int(cnt[i])) for i in range(NPASS)}
+
+    def real_field(self, ncomp: int = 3) -> "Field":
+        return Field(self, 0, ncomp)
+
+    def spectral_field(self, ncomp: int = 3) -> "Field":
+        return Field(self, 1, ncomp)
+
+    def close(self):
+        if self._h:
+            self._lib.sdns_ctx_destroy(self._h)
+            self._h = None
+        if self._own_comm:
+            self.comm.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class Field:
+    """Device-resident field (Field3d / VectorField3, fields.hpp:10-49)."""
+
+    def __init__(self, ctx: Context, kind: int, ncomp: int, handle=None, owned=True):
+        self.ctx = ctx
+        self.kind = kind
+        self.ncomp = ncomp
+        self._owned = owned
+        if handle is None:
+            h = ctypes.c_void_p()
+            _check(ctx._lib.sdns_field_alloc(ctx._h, kind, ncomp, ctypes.byref(h)))
+            handle = h
+        self._h = handle
+
+    @property
+    def shape(self) -> tuple:
+        lo = self.ctx.layout
+        return (self.ncomp,) + tuple(lo.real_shape if self.kind == 0 else lo.spec_shape)
+
+    @property
+    def dtype(self):
+        return np.float64 if self.kind == 0 else np.complex128
+
+    def upload(self, host: np.ndarray) -> "Field":
+        a = np.ascontiguousarray(host, dtype=self.dtype).reshape(self.shape)
+        _check(self.ctx._lib.sdns_field_upload(self.ctx._h, self._h, _ptr(a)))
+        return self
+
+    def download(self) -> np.ndarray:
+        out = np.empty(self.shape, dtype=self.dtype)
+        _check(self.ctx._lib.sdns_field_download(self.ctx._h, self._h, _ptr(out)))
+        return out
+
+    def copy_from(self, other: "Field"):
+        _check(self.ctx._lib.sdns_field_copy(self.ctx._h, other._h, self._h))
+
+    def free(self):
+        if self._h and self._owned:
+            self.ctx._lib.sdns_field_free(self._h)
+        self._h = None
+
+
+# --- operators ---------------------------------------------------------------------
+
+class DistributedFFT:
+    """DistributedFFT, proj/core/include/sdns/fft.hpp:26-62 (collective)."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+
+    def forward(self, u: Field, fu: Field):
+        _check(self.ctx._lib.sdns_fft_forward(self.ctx._h, u._h, fu._h))
+
+    def inverse(self, fu: Field, u: Field):
+        _check(self.ctx._lib.sdns_fft_inverse(self.ctx._h, fu._h, u._h))
+
+
+def curl_hat(ctx: Context, u_hat: Field, omega_hat: Field):
+    """navier_stokes.cpp:52-72."""
+    _check(ctx._lib.sdns_curl_hat(ctx._h, u_hat._h, omega_hat._h))
+
+
+def cross(ctx: Context, a: Field, b: Field, out: Field):
+    """navier_stokes.cpp:34-50."""
+    _check(ctx._lib.sdns_cross(ctx._h, a._h, b._h, out._h))
+
+
+def project(ctx: Context, u_hat: Field):
+    """navier_stokes.cpp:85-102 (in place)."""
+    _check(ctx._lib.sdns_project(ctx._h, u_hat._h))
+
+
+def pressure_hat(ctx: Context, nl_hat: Field, p_hat: Field):
+    """navier_stokes.cpp:74-83."""
+    _check(ctx._lib.sdns_pressure_hat(ctx._h, nl_hat._h, p_hat._h))
+
+
+def compute_rhs(ctx: Context, u_hat: Field, nu: float, du_hat: Field):
+    """navier_stokes.cpp:104-139."""
+    _check(ctx._lib.sdns_compute_rhs(ctx._h, u_hat._h, nu, du_hat._h))
+
+
+class Rk4State:
+    """Rk4State + rk4_step + advance (proj/core/include/sdns/rk4.hpp:18-62)."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+        h = ctypes.c_void_p()
+        _check(ctx._lib.sdns_state_create(ctx._h, ctypes.byref(h)))
+        self._h = h
+        self.u_hat = Field(ctx, 1, 3, handle=ctypes.c_void_p(ctx._lib.sdns_state_u_hat(h)),
+                           owned=False)
+
+    def set(self, u_hat: Field, t: float = 0.0, step: int = 0):
+        _check(self.ctx._lib.sdns_state_set(self.ctx._h, self._h, u_hat._h, t, step))
+
+    def get(self, out: Field):
+        _check(self.ctx._lib.sdns_state_get(self.ctx._h, self._h, out._h))
+
+    @property
+    def t(self) -> float:
+        t = ctypes.c_double()
+        s = ctypes.c_int64()
+        self.ctx._lib.sdns_state_time(self._h, ctypes.byref(t), ctypes.byref(s))
+        return t.value
+
+    @property
+    def step(self) -> int:
+        t = ctypes.c_double()
+        s = ctypes.c_int64()
+        self.ctx._lib.sdns_state_time(self._h, ctypes.byref(t), ctypes.byref(s))
+        return s.value
+
+    def rk4_step(self, dt: float, post_project: bool = True, check: bool = True) -> bool:
+        """rk4_step (rk4.cpp:73-77) with the runner's post-step projection
+        fused in; raises DivergenceError on a non-finite update if check."""
+        fin = ctypes.c_int(1)
+        _check(self.ctx._lib.sdns_rk4_step(self.ctx._h, self._h, dt, 1 if post_project else 0,
+                                            ctypes.byref(fin) if check else None))
+        if check and not fin.value:
+            raise DivergenceError(f"non-finite values in solution update at step {self.step}",
+                                  self.step)
+        return bool(fin.value)
+
+    def advance(self, sample: Optional[Callable[[int, float], None]] = None):
+        """advance, rk4.cpp:86-107 (post_step = project, runner.cpp:107)."""
+        err: list = []
+
+        def cb(step, t, _user):
+            try:
+                sample(int(step), float(t))
+            except BaseException as e:  # noqa: BLE001
+                err.append(e)
+
+        fn = SAMPLE_FN(cb) if sample else SAMPLE_FN()
+        fail = ctypes.c_int64(0)
+        rc = self.ctx._lib.sdns_advance(self.ctx._h, self._h, fn, None, ctypes.byref(fail))
+        if err:
+            raise err[0]
+        _check(rc, fail.value)
+
+    def step_host(self, host_u_hat: np.ndarray, dt: float, steps: int = 1):
+        """Host-buffer tier: upload, `steps` fused steps, download (in place)."""
+        _check(self.ctx._lib.sdns_rk4_step_host(self.ctx._h, self._h, _ptr(host_u_hat), dt,
+                                                 steps))
+
+    def close(self):
+        if self._h:
+            self.ctx._lib.sdns_state_destroy(self._h)
+            self._h = None
+
+
+@dataclass
+class FlowStats:
+    """FlowStats, proj/core/include/sdns/diagnostics.hpp:12-19."""
+    t: float
+    energy: float
+    enstrophy: float
+    dissipation: float
+    divergence_max: float
+    spectrum: np.ndarray
+
+
+def collect_stats(ctx: Context, u_hat: Field, nu: float, t: float = 0.0) -> FlowStats:
+    """diagnostics.cpp:71-91 (deterministic device reduction + rank-order fold)."""
+    shells = spectrum_shells(ctx.cfg.n)
+    row = np.zeros(5 + shells)
+    _check(ctx._lib.sdns_collect_stats(ctx._h, u_hat._h, nu, t, _ptr(row)))
+    return FlowStats(row[0], row[1], row[2], row[3], row[4], row[5:].copy())
+
+
+def l2_diff(ctx: Context, a: Field, b: Field) -> float:
+    """diagnostics.cpp:113-127."""
+    out = ctypes.c_double()
+    _check(ctx._lib.sdns_l2_diff(ctx._h, a._h, b._h, ctypes.byref(out)))
+    return out.value

@@ -1,0 +1,403 @@
+// Communication backends for the transposes of the distributed FFT
+// (Communicator contract, proj/core/include/sdns/transport.hpp:39-94):
+//  - loopback (p = 1): all-to-all is one device copy per block;
+//  - in-process group: threads-as-ranks sharing ONE device, the analogue of
+//    the reference's InProcessBackend (transport.cpp:80-368). Exchanges are
+//    stream-ordered cudaMemcpyAsync between the ranks' buffers, fenced with
+//    events; no kernel ever waits on another. Used to run and test the
+//    multi-rank decomposition on a single GPU;
+//  - NCCL (one process per GPU, NVLink / NVSwitch): grouped ncclSend /
+//    ncclRecv all-to-all (NCCL 2.27 has no ncclAlltoAll), ncclCommSplit for
+//    pencil row / column groups. NCCL is loaded with dlopen so the library
+//    shares whichever libnccl.so.2 the process (e.g. torch) already uses.
+// Reductions gather every rank's values and fold them in ascending rank
+// order (transport.cpp:319-329), so results are bit-identical on every rank.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <map>
+#include <mutex>
+
+#include "host.h"
+
+namespace sdns_host {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(SDNS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+void fold(double* acc, const double* v, int n, int op) {
+  for (int i = 0; i < n; ++i) {
+    if (op == 0) acc[i] += v[i];
+    else if (op == 1) acc[i] = acc[i] > v[i] ? acc[i] : v[i];
+    else acc[i] = acc[i] < v[i] ? acc[i] : v[i];
+  }
+}
+
+// --------------------------------------------------------------------------
+class LoopbackComm final : public Comm {
+ public:
+  LoopbackComm() : Comm(0, 1) {}
+  void alltoall(const std::vector<Xfer>& xs, cudaStream_t s) override {
+    for (const Xfer& x : xs) {
+      if (x.peer != 0 || x.send_bytes != x.recv_bytes) protocol_error("loopback: bad block table");
+      if (x.send != x.recv && x.send_bytes)
+        SDNS_CUDA(cudaMemcpyAsync(x.recv, x.send, x.send_bytes, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  void allreduce(double*, int, int) override {}
+  void barrier() override {}
+  std::shared_ptr<Comm> split(int, int) override { return std::make_shared<LoopbackComm>(); }
+  int device() const override {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+  }
+};
+
+// --------------------------------------------------------------------------
+// Shared bulletin board of an in-process group.
+struct Board {
+  int size;
+  int device;
+  double timeout_s;
+  std::mutex mu;
+  std::condition_variable cv;
+  long long gen = 0;
+  int arrived = 0;
+  bool poisoned = false;
+  std::string reason;
+  std::vector<std::vector<Xfer>> posted;
+  std::vector<std::vector<double>> values;
+  std::vector<cudaEvent_t> ready, done;
+  std::vector<std::pair<int, int>> split_req;
+  std::map<std::pair<long long, int>, std::shared_ptr<Board>> children;
+
+  Board(int n, int dev, double to) : size(n), device(dev), timeout_s(to) {
+    posted.resize(n);
+    values.resize(n);
+    split_req.resize(n);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    SDNS_CUDA(cudaSetDevice(dev));
+    ready.resize(n);
+    done.resize(n);
+    for (int i = 0; i < n; ++i) {
+      SDNS_CUDA(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
+      SDNS_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+    cudaSetDevice(prev);
+  }
+  ~Board() {
+    for (auto e : ready) cudaEventDestroy(e);
+    for (auto e : done) cudaEventDestroy(e);
+  }
+
+  // Generation-counted barrier; throws on poison or timeout.
+  void wait_all(std::unique_lock<std::mutex>& lk) {
+    if (poisoned) protocol_error("group poisoned: " + reason);
+    const long long my = gen;
+    if (++arrived == size) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    const auto deadline = std::chrono::steady_clock::now() +
+                          std::chrono::duration<double>(timeout_s);
+    while (gen == my && !poisoned) {
+      if (cv.wait_until(lk, deadline) == std::cv_status::timeout && gen == my && !poisoned) {
+        poisoned = true;
+        reason = "collective timed out";
+        cv.notify_all();
+        timeout_error("in-process collective timed out after " + std::to_string(timeout_s) + " s");
+      }
+    }
+    if (poisoned && gen == my) protocol_error("group poisoned: " + reason);
+  }
+};
+
+class InProcessComm final : public Comm {
+ public:
+  InProcessComm(std::shared_ptr<Board> b, int rank) : Comm(rank, b->size), b_(std::move(b)) {}
+
+  int device() const override { return b_->device; }
+
+  void alltoall(const std::vector<Xfer>& xs, cudaStream_t s) override {
+    Board& b = *b_;
+    SDNS_CUDA(cudaEventRecord(b.ready[rank_], s));
+    {
+      std::unique_lock<std::mutex> lk(b.mu);
+      b.posted[rank_] = xs;
+      b.wait_all(lk);
+    }
+    // Validate tables and copy every block destined to me from its sender.
+    std::vector<int> waited(size_, 0);
+    std::vector<int> nth_from(size_, 0);
+    for (const Xfer& x : xs) {
+      const int q = x.peer;
+      if (q < 0 || q >= size_) protocol_error("all_to_all: peer out of range");
+      // k-th block I receive from q = k-th block q sends to me
+      int k = nth_from[q]++;
+      const Xfer* match = nullptr;
+      for (const Xfer& y : b.posted[q]) {
+        if (y.peer != rank_) continue;
+        if (k-- == 0) {
+          match = &y;
+          break;
+        }
+      }
+      if (!match) protocol_error("all_to_all: peer " + std::to_string(q) + " sent fewer blocks");
+      if (match->send_bytes != x.recv_bytes)
+        protocol_error("all_to_all: inconsistent block tables between ranks " +
+                       std::to_string(q) + " and " + std::to_string(rank_));
+      if (!waited[q]) {
+        SDNS_CUDA(cudaStreamWaitEvent(s, b.ready[q], 0));
+        waited[q] = 1;
+      }
+      if (x.recv_bytes && match->send != x.recv)
+        SDNS_CUDA(cudaMemcpyAsync(x.recv, match->send, x.recv_bytes, cudaMemcpyDeviceToDevice, s));
+    }
+    SDNS_CUDA(cudaEventRecord(b.done[rank_], s));
+    {
+      std::unique_lock<std::mutex> lk(b.mu);
+      b.wait_all(lk);
+    }
+    // My send buffers may be reused only after every peer copied from them.
+    for (int q = 0; q < size_; ++q)
+      if (q != rank_) SDNS_CUDA(cudaStreamWaitEvent(s, b.done[q], 0));
+    {
+      std::unique_lock<std::mutex> lk(b.mu);
+      b.wait_all(lk);
+    }
+  }
+
+  void allreduce(double* v, int n, int op) override {
+    Board& b = *b_;
+    std::unique_lock<std::mutex> lk(b.mu);
+    b.values[rank_].assign(v, v + n);
+    b.wait_all(lk);
+    for (int q = 0; q < size_; ++q)
+      if (static_cast<int>(b.values[q].size()) != n)
+        protocol_error("allreduce: mismatched lengths across ranks");
+    std::vector<double> acc = b.values[0];
+    for (int q = 1; q < size_; ++q) fold(acc.data(), b.values[q].data(), n, op);
+    b.wait_all(lk);
+    std::memcpy(v, acc.data(), sizeof(double) * n);
+  }
+
+  void barrier() override {
+    std::unique_lock<std::mutex> lk(b_->mu);
+    b_->wait_all(lk);
+  }
+
+  std::shared_ptr<Comm> split(int color, int key) override {
+    Board& b = *b_;
+    std::unique_lock<std::mutex> lk(b.mu);
+    b.split_req[rank_] = {color, key};
+    const long long g = b.gen;
+    b.wait_all(lk);
+    std::vector<std::pair<int, int>> members;  // (key, rank)
+    for (int q = 0; q < size_; ++q)
+      if (b.split_req[q].first == color) members.push_back({b.split_req[q].second, q});
+    std::sort(members.begin(), members.end());
+    int my = 0;
+    for (size_t i = 0; i < members.size(); ++i)
+      if (members[i].second == rank_) my = static_cast<int>(i);
+    auto kk = std::make_pair(g, color);
+    auto it = b.children.find(kk);
+    std::shared_ptr<Board> child;
+    if (it == b.children.end()) {
+      child = std::make_shared<Board>(static_cast<int>(members.size()), b.device, b.timeout_s);
+      b.children[kk] = child;
+    } else {
+      child = it->second;
+    }
+    b.wait_all(lk);
+    return std::make_shared<InProcessComm>(child, my);
+  }
+
+ private:
+  std::shared_ptr<Board> b_;
+};
+
+// --------------------------------------------------------------------------
+// NCCL through dlopen (the subset we call; ABI per /usr/include/nccl.h).
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclInt8 = 0, ncclFloat64 = 8 };
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+  static NcclApi& get() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      const char* names[] = {"libnccl.so.2", "libnccl.so"};
+      for (const char* nm : names) {
+        api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+        if (api.h) break;
+      }
+      if (!api.h) return;
+      auto sym = [](const char* s) { return dlsym(api.h, s); };
+      api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+      api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+      api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+      api.CommSplit = reinterpret_cast<decltype(api.CommSplit)>(sym("ncclCommSplit"));
+      api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+      api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+      api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+      api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+      api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+      api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    });
+    if (!api.h || !api.GetUniqueId || !api.Send || !api.CommSplit)
+      throw Error(SDNS_CUDA_ERROR, "NCCL (libnccl.so.2) could not be loaded");
+    return api;
+  }
+};
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != 0) {
+    auto& api = NcclApi::get();
+    throw Error(SDNS_PROTOCOL_ERROR,
+                std::string(what) + ": " + (api.GetErrorString ? api.GetErrorString(r) : "nccl error"));
+  }
+}
+
+class NcclComm final : public Comm {
+ public:
+  NcclComm(ncclComm_t c, int rank, int size, int device)
+      : Comm(rank, size), comm_(c), device_(device) {
+    SDNS_CUDA(cudaSetDevice(device_));
+    SDNS_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    SDNS_CUDA(cudaMalloc(&dbuf_, sizeof(double) * kMaxVals * (size + 1)));
+  }
+  ~NcclComm() override {
+    if (dbuf_) cudaFree(dbuf_);
+    if (side_) cudaStreamDestroy(side_);
+    if (comm_) NcclApi::get().CommDestroy(comm_);
+  }
+  int device() const override { return device_; }
+
+  void alltoall(const std::vector<Xfer>& xs, cudaStream_t s) override {
+    auto& api = NcclApi::get();
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (const Xfer& x : xs) {
+      if (x.peer == rank_) {
+        if (x.send_bytes != x.recv_bytes) protocol_error("all_to_all: self block size mismatch");
+        if (x.send_bytes && x.send != x.recv)
+          SDNS_CUDA(cudaMemcpyAsync(x.recv, x.send, x.send_bytes, cudaMemcpyDeviceToDevice, s));
+        continue;
+      }
+      if (x.send_bytes) nccl_check(api.Send(x.send, x.send_bytes, ncclInt8, x.peer, comm_, s), "ncclSend");
+      if (x.recv_bytes) nccl_check(api.Recv(x.recv, x.recv_bytes, ncclInt8, x.peer, comm_, s), "ncclRecv");
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+  }
+
+  void allreduce(double* v, int n, int op) override {
+    if (n > kMaxVals) {
+      for (int off = 0; off < n; off += kMaxVals)
+        allreduce(v + off, std::min(kMaxVals, n - off), op);
+      return;
+    }
+    auto& api = NcclApi::get();
+    double* mine = dbuf_ + static_cast<size_t>(kMaxVals) * size_;
+    SDNS_CUDA(cudaMemcpyAsync(mine, v, sizeof(double) * n, cudaMemcpyHostToDevice, side_));
+    nccl_check(api.AllGather(mine, dbuf_, static_cast<size_t>(n), ncclFloat64, comm_, side_),
+               "ncclAllGather");
+    std::vector<double> all(static_cast<size_t>(n) * size_);
+    SDNS_CUDA(cudaMemcpyAsync(all.data(), dbuf_, sizeof(double) * n * size_,
+                              cudaMemcpyDeviceToHost, side_));
+    SDNS_CUDA(cudaStreamSynchronize(side_));
+    std::vector<double> acc(all.begin(), all.begin() + n);
+    for (int q = 1; q < size_; ++q) fold(acc.data(), all.data() + static_cast<size_t>(q) * n, n, op);
+    std::memcpy(v, acc.data(), sizeof(double) * n);
+  }
+
+  void barrier() override {
+    double x = 0.0;
+    allreduce(&x, 1, 0);
+  }
+
+  std::shared_ptr<Comm> split(int color, int key) override {
+    auto& api = NcclApi::get();
+    ncclComm_t nc = nullptr;
+    nccl_check(api.CommSplit(comm_, color, key, &nc, nullptr), "ncclCommSplit");
+    // rank within the new group: order by (key, rank) like the reference
+    double mine[2] = {static_cast<double>(color), static_cast<double>(key)};
+    std::vector<double> all(2 * static_cast<size_t>(size_));
+    gather2(mine, all.data());
+    int my = 0, cnt = 0;
+    for (int q = 0; q < size_; ++q) {
+      if (static_cast<int>(all[2 * q]) != color) continue;
+      ++cnt;
+      const int kq = static_cast<int>(all[2 * q + 1]);
+      if (kq < key || (kq == key && q < rank_)) ++my;
+    }
+    return std::make_shared<NcclComm>(nc, my, cnt, device_);
+  }
+
+ private:
+  static constexpr int kMaxVals = 4096;
+  void gather2(const double* mine, double* all) {
+    auto& api = NcclApi::get();
+    double* d_mine = dbuf_ + static_cast<size_t>(kMaxVals) * size_;
+    SDNS_CUDA(cudaMemcpyAsync(d_mine, mine, sizeof(double) * 2, cudaMemcpyHostToDevice, side_));
+    nccl_check(api.AllGather(d_mine, dbuf_, 2, ncclFloat64, comm_, side_), "ncclAllGather");
+    SDNS_CUDA(cudaMemcpyAsync(all, dbuf_, sizeof(double) * 2 * size_, cudaMemcpyDeviceToHost, side_));
+    SDNS_CUDA(cudaStreamSynchronize(side_));
+  }
+  ncclComm_t comm_ = nullptr;
+  int device_ = 0;
+  cudaStream_t side_ = nullptr;
+  double* dbuf_ = nullptr;
+};
+
+}  // namespace
+
+std::shared_ptr<Comm> make_loopback_comm() { return std::make_shared<LoopbackComm>(); }
+
+std::vector<std::shared_ptr<Comm>> make_inprocess_group(int size, int device, double timeout_s) {
+  if (size < 1) config_error("in-process group size must be >= 1");
+  auto b = std::make_shared<Board>(size, device, timeout_s);
+  std::vector<std::shared_ptr<Comm>> out;
+  for (int r = 0; r < size; ++r) out.push_back(std::make_shared<InProcessComm>(b, r));
+  return out;
+}
+
+void nccl_unique_id(unsigned char id[128]) {
+  ncclUniqueId u;
+  nccl_check(NcclApi::get().GetUniqueId(&u), "ncclGetUniqueId");
+  std::memcpy(id, u.internal, 128);
+}
+
+std::shared_ptr<Comm> make_nccl_comm(const unsigned char id[128], int size, int rank, int device) {
+  ncclUniqueId u;
+  std::memcpy(u.internal, id, 128);
+  SDNS_CUDA(cudaSetDevice(device));
+  ncclComm_t c = nullptr;
+  nccl_check(NcclApi::get().CommInitRank(&c, size, u, rank), "ncclCommInitRank");
+  return std::make_shared<NcclComm>(c, rank, size, device);
+}
+
+}  // namespace sdns_host

@@ -1,0 +1,811 @@
+// Host orchestration of the device pipeline and the C ABI (include/sdns_cuda.h).
+//
+// One sdns_ctx is one rank: its layout (build_layout), wavenumber geometry
+// (computed in-register by the kernels, mesh.cpp:23-89), the twiddle table,
+// the transpose work buffers and the communicator(s). It replaces the
+// reference's DistributedFFT + WavenumberMesh + RhsWorkspace
+// (fft.cpp:15-57, mesh.cpp:23-72, navier_stokes.hpp:32-41).
+//
+// Device layout: spectral components are (s0, s1, pitch)
+// complex with pitch = round_up(s2, 8); real components are (r0, r1, r2)
+// doubles. Slab work buffers:
+//   wa  "x layout"  (n, np, pitch) x 6 comps  -- send buffer of the inverse
+//        transpose / receive buffer of the forward one
+//   wb  "y layout"  [peer][x_l][y_l][pitch] x 6 comps -- the receive layout,
+//        read directly by the y pass (no unpack pass); aliases wa at p = 1.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "host.h"
+#include "kernels.cuh"
+
+using namespace sdns_host;
+using sdns_dev::ColGeom;
+using sdns_dev::RowMap;
+using sdns_dev::SpecGeom;
+using sdns_dev::WaveGeom;
+using sdns_dev::XfArgs;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SDNS_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SDNS_INTERNAL_ERROR;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return SDNS_INTERNAL_ERROR;
+  }
+}
+
+int ilog2(long long v) {
+  int s = 0;
+  while ((1LL << s) < v) ++s;
+  return s;
+}
+
+bool is_pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
+
+}  // namespace
+
+struct sdns_field;
+
+struct sdns_ctx {
+  sdns_config cfg{};
+  sdns_layout lo{};
+  int device = 0;
+  std::shared_ptr<Comm> world;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double2* tw = nullptr;
+  double2* wa = nullptr;
+  double2* wb = nullptr;
+  long long spec_cs = 0;   // complex elements per spectral component (padded)
+  long long real_cs = 0;   // doubles per real component
+  int pitch = 0;
+  int np = 0;              // slab block (n / p)
+  double norm = 1.0;
+  double* d_partial = nullptr;
+  double* d_out = nullptr;
+  double* h_out = nullptr;  // pinned
+  int* d_flag = nullptr;
+  int* h_flag = nullptr;    // pinned
+  int shells = 0;
+  int64_t dev_bytes = 0;
+  // Optional per-pass CUDA-event timing (bench.py's live roofline). Events
+  // are created when timing is enabled, never inside a step.
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_tag;
+  size_t ev_used = 0;
+
+  int tick(int tag) {
+    if (!timing) return -1;
+    if (ev_used + 2 > ev.size()) return -1;
+    const int i = static_cast<int>(ev_used);
+    ev_used += 2;
+    ev_tag[static_cast<size_t>(i)] = tag;
+    cudaEventRecord(ev[static_cast<size_t>(i)], stream);
+    return i;
+  }
+  void tock(int i) {
+    if (i >= 0) cudaEventRecord(ev[static_cast<size_t>(i) + 1], stream);
+  }
+
+  SpecGeom sgeom() const {
+    SpecGeom g;
+    g.n = cfg.n;
+    g.s0 = static_cast<int>(lo.spec_shape[0]);
+    g.s1 = static_cast<int>(lo.spec_shape[1]);
+    g.s2 = static_cast<int>(lo.spec_shape[2]);
+    g.o0 = static_cast<int>(lo.spec_offset[0]);
+    g.o1 = static_cast<int>(lo.spec_offset[1]);
+    g.o2 = static_cast<int>(lo.spec_offset[2]);
+    g.pitch = pitch;
+    g.cs = spec_cs;
+    return g;
+  }
+  // x pass over the x layout: rows = local y, positions = x (full axis)
+  ColGeom xgeom() const {
+    ColGeom g;
+    g.rs = pitch;
+    g.ps0 = static_cast<long long>(np) * pitch;
+    g.ps1 = 0;
+    g.pb_shift = 30;
+    g.nrows = np;
+    g.n2 = static_cast<int>(lo.spec_shape[2]);
+    g.pitch = pitch;
+    return g;
+  }
+  WaveGeom xwave() const {
+    WaveGeom w;
+    w.n = cfg.n;
+    w.row_is_y = 1;
+    w.row_off = static_cast<int>(lo.spec_offset[1]);
+    w.kz_off = static_cast<int>(lo.spec_offset[2]);
+    return w;
+  }
+  // y pass over the receive layout: rows = local x, positions = y
+  ColGeom ygeom() const {
+    ColGeom g;
+    g.rs = static_cast<long long>(np) * pitch;
+    g.ps0 = pitch;
+    g.ps1 = static_cast<long long>(np) * np * pitch;
+    g.pb_shift = ilog2(np);
+    g.nrows = np;
+    g.n2 = static_cast<int>(lo.spec_shape[2]);
+    g.pitch = pitch;
+    return g;
+  }
+  RowMap zmap(bool by_xy) const {
+    RowMap r;
+    r.nrows = np * cfg.n;
+    r.ny = cfg.n;
+    r.blk = (by_xy && cfg.p > 1) ? np : 0;
+    r.pitch = pitch;
+    r.n2 = static_cast<int>(lo.nf);
+    return r;
+  }
+  // transpose between wa (x layout) and wb (receive layout)
+  void exchange(bool inverse_dir, int nfields) {
+    if (cfg.p == 1) return;
+    const int tk = tick(inverse_dir ? SDNS_PASS_A2A_INV : SDNS_PASS_A2A_FWD);
+    const long long blk = static_cast<long long>(np) * np * pitch;
+    std::vector<Xfer> xs;
+    xs.reserve(static_cast<size_t>(nfields) * cfg.p);
+    for (int f = 0; f < nfields; ++f)
+      for (int q = 0; q < cfg.p; ++q) {
+        double2* a = wa + f * spec_cs + q * blk;
+        double2* b = wb + f * spec_cs + q * blk;
+        const size_t bytes = sizeof(double2) * static_cast<size_t>(blk);
+        if (inverse_dir) xs.push_back({q, a, b, bytes, bytes});
+        else xs.push_back({q, b, a, bytes, bytes});
+      }
+    world->alltoall(xs, stream);
+    tock(tk);
+  }
+};
+
+struct sdns_field {
+  sdns_ctx* ctx = nullptr;
+  int kind = SDNS_SPECTRAL;
+  int ncomp = 0;
+  void* data = nullptr;
+  bool owned = true;
+  double2* spec() const { return static_cast<double2*>(data); }
+  double* real() const { return static_cast<double*>(data); }
+};
+
+struct sdns_state {
+  sdns_ctx* ctx = nullptr;
+  sdns_field u;        // current state (the reference's u_hat / base)
+  double2* nxt = nullptr;    // stage value
+  double2* accum = nullptr;
+  double2* carry = nullptr;
+  double t = 0.0;
+  int64_t step = 0;
+};
+
+namespace {
+
+void set_device(sdns_ctx* c) { SDNS_CUDA(cudaSetDevice(c->device)); }
+
+void require_spec(const sdns_field* f, int ncomp, const char* what) {
+  if (!f || f->kind != SDNS_SPECTRAL || f->ncomp < ncomp)
+    config_error(std::string(what) + ": expected a spectral field with " + std::to_string(ncomp) +
+                 " components");
+}
+void require_real(const sdns_field* f, int ncomp, const char* what) {
+  if (!f || f->kind != SDNS_REAL || f->ncomp < ncomp)
+    config_error(std::string(what) + ": expected a real field with " + std::to_string(ncomp) +
+                 " components");
+}
+
+void post_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(SDNS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// One fused RHS evaluation: P1 .. P5 (kernels.cu) with the transposes.
+void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args_in) {
+  const int n = c->cfg.n;
+  cudaStream_t s = c->stream;
+  int tk = c->tick(SDNS_PASS_X_INV_CURL);
+  sdns_dev::x_inverse_curl(n, u_in, c->spec_cs, c->wa, c->spec_cs, c->xgeom(), c->xwave(), c->tw, s);
+  c->tock(tk);
+  c->exchange(true, 6);
+  tk = c->tick(SDNS_PASS_Y_INV);
+  sdns_dev::col_plain(n, +1, c->wb, c->wb, c->spec_cs, c->spec_cs, 6, c->ygeom(), c->tw, s);
+  c->tock(tk);
+  tk = c->tick(SDNS_PASS_Z_FUSED);
+  sdns_dev::z_fused(n, c->wb, c->spec_cs, c->zmap(false), c->norm, c->tw, s);
+  c->tock(tk);
+  tk = c->tick(SDNS_PASS_Y_FWD);
+  sdns_dev::col_plain(n, -1, c->wb, c->wb, c->spec_cs, c->spec_cs, 3, c->ygeom(), c->tw, s);
+  c->tock(tk);
+  c->exchange(false, 3);
+  XfArgs a = args_in;
+  a.nl = c->wa;
+  a.nl_cs = c->spec_cs;
+  a.cs = c->spec_cs;
+  a.dealias = c->cfg.dealias;
+  tk = c->tick(SDNS_PASS_X_FWD_TAIL + mode);
+  sdns_dev::x_forward_fused(n, mode, a, c->xgeom(), c->xwave(), c->tw, s);
+  c->tock(tk);
+  post_launch("rhs pipeline");
+}
+
+void fft_forward_impl(sdns_ctx* c, const sdns_field* real, sdns_field* spec) {
+  const int n = c->cfg.n;
+  cudaStream_t s = c->stream;
+  const int nc = std::min(real->ncomp, spec->ncomp);
+  for (int f = 0; f < nc; ++f)
+    sdns_dev::z_r2c(n, real->real() + f * c->real_cs, c->wb + f * c->spec_cs, c->zmap(true), c->tw, s);
+  sdns_dev::col_plain(n, -1, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw, s);
+  c->exchange(false, nc);
+  sdns_dev::col_plain(n, -1, c->wa, spec->spec(), c->spec_cs, c->spec_cs, nc, c->xgeom(), c->tw, s);
+  post_launch("fft forward");
+}
+
+void fft_inverse_impl(sdns_ctx* c, const sdns_field* spec, sdns_field* real) {
+  const int n = c->cfg.n;
+  cudaStream_t s = c->stream;
+  const int nc = std::min(real->ncomp, spec->ncomp);
+  sdns_dev::col_plain(n, +1, spec->spec(), c->wa, c->spec_cs, c->spec_cs, nc, c->xgeom(), c->tw, s);
+  c->exchange(true, nc);
+  sdns_dev::col_plain(n, +1, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw, s);
+  for (int f = 0; f < nc; ++f)
+    sdns_dev::z_c2r(n, c->wb + f * c->spec_cs, real->real() + f * c->real_cs, c->zmap(true), c->norm,
+                    c->tw, s);
+  post_launch("fft inverse");
+}
+
+bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool want_flag) {
+  static const double kW[3] = {1.0, 2.0, 2.0};
+  static const double kB[3] = {0.5, 0.5, 1.0};
+  double2* u = st->u.spec();
+  for (int stage = 0; stage < 4; ++stage) {
+    XfArgs a{};
+    a.nu = c->cfg.nu;
+    a.base = u;
+    a.cs = c->spec_cs;
+    if (stage < 3) {
+      a.u = stage == 0 ? u : st->nxt;
+      a.out = st->nxt;
+      a.accum = st->accum;
+      a.w = kW[stage];
+      a.bdt = kB[stage] * dt;
+      rhs_pipeline(c, a.u, stage == 0 ? sdns_dev::XF_RK0 : sdns_dev::XF_RK12, a);
+    } else {
+      a.u = st->nxt;
+      a.accum = st->accum;
+      a.carry = st->carry;
+      a.base_out = u;
+      a.sixth = dt / 6.0;
+      a.project = post_project;
+      a.finite = c->d_flag;
+      SDNS_CUDA(cudaMemsetAsync(c->d_flag, 0xff, sizeof(int), c->stream));
+      rhs_pipeline(c, st->nxt, sdns_dev::XF_RK3, a);
+    }
+  }
+  st->t += dt;
+  st->step += 1;
+  if (!want_flag) return true;
+  SDNS_CUDA(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  SDNS_CUDA(cudaStreamSynchronize(c->stream));
+  double ok = *c->h_flag != 0 ? 1.0 : 0.0;
+  c->world->allreduce(&ok, 1, 2);
+  return ok > 0.5;
+}
+
+void stats_impl(sdns_ctx* c, const sdns_field* u, double nu, double t, double* row) {
+  const SpecGeom g = c->sgeom();
+  sdns_dev::stats_local(u->spec(), g, c->shells, c->d_partial, c->d_out, c->stream);
+  post_launch("collect_stats");
+  const int stride = c->shells + 3;
+  SDNS_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(double) * stride, cudaMemcpyDeviceToHost,
+                            c->stream));
+  SDNS_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<double> sums(static_cast<size_t>(2 + c->shells));
+  sums[0] = c->h_out[0];
+  sums[1] = c->h_out[1];
+  for (int i = 0; i < c->shells; ++i) sums[2 + i] = c->h_out[3 + i];
+  double dmax = c->h_out[2];
+  c->world->allreduce(sums.data(), static_cast<int>(sums.size()), 0);
+  c->world->allreduce(&dmax, 1, 1);
+  const double n3 = static_cast<double>(c->cfg.n) * c->cfg.n * c->cfg.n;
+  const double n6 = n3 * n3;
+  row[0] = t;
+  row[1] = 0.5 * sums[0] / n6;
+  row[2] = 0.5 * sums[1] / n6;
+  row[3] = 2.0 * nu * row[2];
+  row[4] = dmax;
+  for (int i = 0; i < c->shells; ++i) row[5 + i] = sums[2 + i] / n6;
+}
+
+void* dev_alloc(sdns_ctx* c, size_t bytes) {
+  void* p = nullptr;
+  SDNS_CUDA(cudaMalloc(&p, bytes));
+  SDNS_CUDA(cudaMemsetAsync(p, 0, bytes, c->stream));
+  c->dev_bytes += static_cast<int64_t>(bytes);
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sdns_last_error(void) { return g_last_error.c_str(); }
+
+const char* sdns_version(void) { return "sdns-b200 0.1 (sm_100a)"; }
+
+int sdns_config_validate(const sdns_config* cfg) {
+  return guarded([&] { validate(*cfg); });
+}
+
+int sdns_build_layout(const sdns_config* cfg, int rank, sdns_layout* out) {
+  return guarded([&] { *out = build_layout(*cfg, rank); });
+}
+
+int64_t sdns_block_size(int64_t total, int parts, int index) { return block_size(total, parts, index); }
+int64_t sdns_block_start(int64_t total, int parts, int index) { return block_start(total, parts, index); }
+int64_t sdns_step_count(double t_end, double dt) { return step_count(t_end, dt); }
+int sdns_spectrum_shells(int64_t n) { return spectrum_shells(n); }
+
+int sdns_iso_init_host(int64_t n, uint64_t seed, double k0, double energy, const sdns_layout* lo,
+                       double* out) {
+  return guarded([&] {
+    if (n < 4 || n % 2) config_error("iso init: n must be even and >= 4");
+    iso_init(n, seed, k0, energy, *lo, out);
+  });
+}
+
+int sdns_comm_loopback(sdns_comm** out) {
+  return guarded([&] { *out = new sdns_comm{make_loopback_comm()}; });
+}
+
+int sdns_comm_inprocess_group(int size, int device, double timeout_s, sdns_comm** out) {
+  return guarded([&] {
+    auto g = make_inprocess_group(size, device, timeout_s);
+    for (int r = 0; r < size; ++r) out[r] = new sdns_comm{g[static_cast<size_t>(r)]};
+  });
+}
+
+int sdns_comm_nccl_unique_id(unsigned char id[128]) {
+  return guarded([&] { nccl_unique_id(id); });
+}
+
+int sdns_comm_nccl_init(const unsigned char id[128], int size, int rank, int device, sdns_comm** out) {
+  return guarded([&] { *out = new sdns_comm{make_nccl_comm(id, size, rank, device)}; });
+}
+
+int sdns_comm_rank(const sdns_comm* c) { return c->c->rank(); }
+int sdns_comm_size(const sdns_comm* c) { return c->c->size(); }
+int sdns_comm_barrier(sdns_comm* c) {
+  return guarded([&] { c->c->barrier(); });
+}
+int sdns_comm_allreduce(sdns_comm* c, double* v, int n, int op) {
+  return guarded([&] {
+    if (op < 0 || op > 2) config_error("allreduce: unknown op");
+    c->c->allreduce(v, n, op);
+  });
+}
+int sdns_comm_destroy(sdns_comm* c) {
+  return guarded([&] { delete c; });
+}
+
+int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* comm, void* stream,
+                    sdns_ctx** out) {
+  return guarded([&] {
+    validate(*cfg);
+    if (!comm) config_error("ctx: communicator is NULL");
+    if (comm->c->size() != cfg->p)
+      config_error("communicator size " + std::to_string(comm->c->size()) +
+                   " does not match configured p=" + std::to_string(cfg->p));
+    if (comm->c->rank() != rank) config_error("communicator rank does not match layout rank");
+    if (!is_pow2(cfg->n) || cfg->n < 8 || cfg->n > 1024)
+      config_error("the sm_100a path supports power-of-two n in [8, 1024], got n=" +
+                   std::to_string(cfg->n));
+    if (cfg->decomp != SDNS_SLAB)
+      config_error("the sm_100a path implements the slab decomposition; pencil is not built yet");
+    auto c = std::make_unique<sdns_ctx>();
+    c->cfg = *cfg;
+    c->lo = build_layout(*cfg, rank);
+    c->device = device;
+    c->world = comm->c;
+    SDNS_CUDA(cudaSetDevice(device));
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      SDNS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    const long long n = cfg->n;
+    c->np = static_cast<int>(n / cfg->p);
+    c->pitch = static_cast<int>((c->lo.spec_shape[2] + 7) / 8 * 8);
+    c->spec_cs = c->lo.spec_shape[0] * c->lo.spec_shape[1] * c->pitch;
+    c->real_cs = c->lo.real_shape[0] * c->lo.real_shape[1] * c->lo.real_shape[2];
+    c->norm = 1.0 / (static_cast<double>(n) * static_cast<double>(n) * static_cast<double>(n));
+    c->shells = spectrum_shells(n);
+    c->tw = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * n));
+    sdns_dev::make_twiddles(static_cast<int>(n), c->tw, c->stream);
+    const size_t wbytes = sizeof(double2) * static_cast<size_t>(c->spec_cs) * 6;
+    c->wa = static_cast<double2*>(dev_alloc(c.get(), wbytes));
+    c->wb = cfg->p == 1 ? c->wa : static_cast<double2*>(dev_alloc(c.get(), wbytes));
+    const int stride = c->shells + 3;
+    const int nblk = std::max<int>(static_cast<int>(c->lo.spec_shape[0]), 592);
+    c->d_partial = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride * nblk));
+    c->d_out = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride));
+    c->d_flag = static_cast<int*>(dev_alloc(c.get(), sizeof(int)));
+    SDNS_CUDA(cudaMallocHost(&c->h_out, sizeof(double) * stride));
+    SDNS_CUDA(cudaMallocHost(&c->h_flag, sizeof(int)));
+    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    post_launch("ctx create");
+    *out = c.release();
+  });
+}
+
+int sdns_ctx_destroy(sdns_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->tw);
+    if (c->wb != c->wa) cudaFree(c->wb);
+    cudaFree(c->wa);
+    cudaFree(c->d_partial);
+    cudaFree(c->d_out);
+    cudaFree(c->d_flag);
+    cudaFreeHost(c->h_out);
+    cudaFreeHost(c->h_flag);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+  });
+}
+
+int sdns_ctx_layout(const sdns_ctx* c, sdns_layout* out) {
+  *out = c->lo;
+  return SDNS_OK;
+}
+void* sdns_ctx_stream(const sdns_ctx* c) { return c->stream; }
+int sdns_ctx_sync(sdns_ctx* c) {
+  return guarded([&] {
+    set_device(c);
+    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+int64_t sdns_ctx_device_bytes(const sdns_ctx* c) { return c->dev_bytes; }
+
+int sdns_field_alloc(sdns_ctx* c, int kind, int ncomp, sdns_field** out) {
+  return guarded([&] {
+    if (ncomp < 1) config_error("field: ncomp must be >= 1");
+    if (kind != SDNS_REAL && kind != SDNS_SPECTRAL) config_error("field: unknown kind");
+    set_device(c);
+    auto f = std::make_unique<sdns_field>();
+    f->ctx = c;
+    f->kind = kind;
+    f->ncomp = ncomp;
+    const size_t bytes = kind == SDNS_REAL ? sizeof(double) * c->real_cs * ncomp
+                                           : sizeof(double2) * c->spec_cs * ncomp;
+    SDNS_CUDA(cudaMalloc(&f->data, bytes));
+    SDNS_CUDA(cudaMemsetAsync(f->data, 0, bytes, c->stream));
+    *out = f.release();
+  });
+}
+
+int sdns_field_free(sdns_field* f) {
+  return guarded([&] {
+    if (!f) return;
+    if (f->owned) {
+      cudaSetDevice(f->ctx->device);
+      cudaFree(f->data);
+    }
+    delete f;
+  });
+}
+
+int sdns_field_upload(sdns_ctx* c, sdns_field* f, const double* host) {
+  return guarded([&] {
+    set_device(c);
+    if (f->kind == SDNS_REAL) {
+      SDNS_CUDA(cudaMemcpyAsync(f->data, host, sizeof(double) * c->real_cs * f->ncomp,
+                                cudaMemcpyHostToDevice, c->stream));
+    } else {
+      const size_t s2 = static_cast<size_t>(c->lo.spec_shape[2]);
+      const size_t rows = static_cast<size_t>(c->lo.spec_shape[0] * c->lo.spec_shape[1]);
+      for (int q = 0; q < f->ncomp; ++q)
+        SDNS_CUDA(cudaMemcpy2DAsync(f->spec() + q * c->spec_cs, sizeof(double2) * c->pitch,
+                                    host + 2 * q * s2 * rows, sizeof(double2) * s2,
+                                    sizeof(double2) * s2, rows, cudaMemcpyHostToDevice, c->stream));
+    }
+    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int sdns_field_download(sdns_ctx* c, const sdns_field* f, double* host) {
+  return guarded([&] {
+    set_device(c);
+    if (f->kind == SDNS_REAL) {
+      SDNS_CUDA(cudaMemcpyAsync(host, f->data, sizeof(double) * c->real_cs * f->ncomp,
+                                cudaMemcpyDeviceToHost, c->stream));
+    } else {
+      const size_t s2 = static_cast<size_t>(c->lo.spec_shape[2]);
+      const size_t rows = static_cast<size_t>(c->lo.spec_shape[0] * c->lo.spec_shape[1]);
+      for (int q = 0; q < f->ncomp; ++q)
+        SDNS_CUDA(cudaMemcpy2DAsync(host + 2 * q * s2 * rows, sizeof(double2) * s2,
+                                    f->spec() + q * c->spec_cs, sizeof(double2) * c->pitch,
+                                    sizeof(double2) * s2, rows, cudaMemcpyDeviceToHost, c->stream));
+    }
+    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int sdns_field_copy(sdns_ctx* c, const sdns_field* src, sdns_field* dst) {
+  return guarded([&] {
+    if (src->kind != dst->kind || src->ncomp != dst->ncomp) config_error("field copy: shape mismatch");
+    set_device(c);
+    const size_t bytes = src->kind == SDNS_REAL ? sizeof(double) * c->real_cs * src->ncomp
+                                                : sizeof(double2) * c->spec_cs * src->ncomp;
+    SDNS_CUDA(cudaMemcpyAsync(dst->data, src->data, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  });
+}
+
+int sdns_fft_forward(sdns_ctx* c, const sdns_field* real, sdns_field* spec) {
+  return guarded([&] {
+    require_real(real, 1, "forward");
+    require_spec(spec, real->ncomp, "forward");
+    if (real->ncomp > 6) config_error("forward: at most 6 components per call");
+    set_device(c);
+    fft_forward_impl(c, real, spec);
+  });
+}
+
+int sdns_fft_inverse(sdns_ctx* c, const sdns_field* spec, sdns_field* real) {
+  return guarded([&] {
+    require_spec(spec, 1, "inverse");
+    require_real(real, spec->ncomp, "inverse");
+    if (spec->ncomp > 6) config_error("inverse: at most 6 components per call");
+    set_device(c);
+    fft_inverse_impl(c, spec, real);
+  });
+}
+
+int sdns_curl_hat(sdns_ctx* c, const sdns_field* u, sdns_field* w) {
+  return guarded([&] {
+    require_spec(u, 3, "curl_hat");
+    require_spec(w, 3, "curl_hat");
+    set_device(c);
+    sdns_dev::pw_curl(u->spec(), w->spec(), c->sgeom(), c->stream);
+    post_launch("curl_hat");
+  });
+}
+
+int sdns_cross(sdns_ctx* c, const sdns_field* a, const sdns_field* b, sdns_field* o) {
+  return guarded([&] {
+    require_real(a, 3, "cross");
+    require_real(b, 3, "cross");
+    require_real(o, 3, "cross");
+    set_device(c);
+    sdns_dev::pw_cross(a->real(), b->real(), o->real(), c->real_cs, c->real_cs, c->stream);
+    post_launch("cross");
+  });
+}
+
+int sdns_project(sdns_ctx* c, sdns_field* u) {
+  return guarded([&] {
+    require_spec(u, 3, "project");
+    set_device(c);
+    sdns_dev::pw_project(u->spec(), c->sgeom(), c->stream);
+    post_launch("project");
+  });
+}
+
+int sdns_pressure_hat(sdns_ctx* c, const sdns_field* nl, sdns_field* p) {
+  return guarded([&] {
+    require_spec(nl, 3, "pressure_hat");
+    require_spec(p, 1, "pressure_hat");
+    set_device(c);
+    sdns_dev::pw_pressure(nl->spec(), p->spec(), c->sgeom(), c->stream);
+    post_launch("pressure_hat");
+  });
+}
+
+int sdns_compute_rhs(sdns_ctx* c, const sdns_field* u, double nu, sdns_field* du) {
+  return guarded([&] {
+    require_spec(u, 3, "compute_rhs");
+    require_spec(du, 3, "compute_rhs");
+    if (u->data == du->data) config_error("compute_rhs: u_hat and du_hat must not alias");
+    set_device(c);
+    XfArgs a{};
+    a.u = u->spec();
+    a.out = du->spec();
+    a.nu = nu;
+    rhs_pipeline(c, u->spec(), sdns_dev::XF_TAIL, a);
+  });
+}
+
+int sdns_state_create(sdns_ctx* c, sdns_state** out) {
+  return guarded([&] {
+    set_device(c);
+    auto st = std::make_unique<sdns_state>();
+    st->ctx = c;
+    st->u.ctx = c;
+    st->u.kind = SDNS_SPECTRAL;
+    st->u.ncomp = 3;
+    st->u.owned = false;
+    const size_t bytes = sizeof(double2) * static_cast<size_t>(c->spec_cs) * 3;
+    st->u.data = dev_alloc(c, bytes);
+    st->nxt = static_cast<double2*>(dev_alloc(c, bytes));
+    st->accum = static_cast<double2*>(dev_alloc(c, bytes));
+    st->carry = static_cast<double2*>(dev_alloc(c, bytes));
+    *out = st.release();
+  });
+}
+
+int sdns_state_destroy(sdns_state* st) {
+  return guarded([&] {
+    if (!st) return;
+    cudaSetDevice(st->ctx->device);
+    cudaStreamSynchronize(st->ctx->stream);
+    cudaFree(st->u.data);
+    cudaFree(st->nxt);
+    cudaFree(st->accum);
+    cudaFree(st->carry);
+    delete st;
+  });
+}
+
+int sdns_state_set(sdns_ctx* c, sdns_state* st, const sdns_field* u, double t, int64_t step) {
+  return guarded([&] {
+    require_spec(u, 3, "state_set");
+    set_device(c);
+    const size_t bytes = sizeof(double2) * static_cast<size_t>(c->spec_cs) * 3;
+    SDNS_CUDA(cudaMemcpyAsync(st->u.data, u->data, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    SDNS_CUDA(cudaMemsetAsync(st->carry, 0, bytes, c->stream));
+    st->t = t;
+    st->step = step;
+  });
+}
+
+int sdns_state_get(sdns_ctx* c, const sdns_state* st, sdns_field* u) {
+  return guarded([&] {
+    require_spec(u, 3, "state_get");
+    set_device(c);
+    const size_t bytes = sizeof(double2) * static_cast<size_t>(c->spec_cs) * 3;
+    SDNS_CUDA(cudaMemcpyAsync(u->data, st->u.data, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  });
+}
+
+sdns_field* sdns_state_u_hat(sdns_state* st) { return &st->u; }
+
+int sdns_state_time(const sdns_state* st, double* t, int64_t* step) {
+  if (t) *t = st->t;
+  if (step) *step = st->step;
+  return SDNS_OK;
+}
+
+int sdns_rk4_step(sdns_ctx* c, sdns_state* st, double dt, int post_project, int* finite) {
+  return guarded([&] {
+    set_device(c);
+    const bool ok = step_impl(c, st, dt, post_project, finite != nullptr);
+    if (finite) *finite = ok ? 1 : 0;
+  });
+}
+
+int sdns_advance(sdns_ctx* c, sdns_state* st, sdns_sample_fn sample, void* user, int64_t* fail_step) {
+  return guarded([&] {
+    set_device(c);
+    const sdns_config& cfg = c->cfg;
+    const int64_t n_steps = step_count(cfg.t_end, cfg.dt);
+    if (sample) sample(0, st->t, user);
+    for (int64_t k = 1; k <= n_steps; ++k) {
+      const bool last = k == n_steps;
+      const double target = last ? cfg.t_end : static_cast<double>(k) * cfg.dt;
+      const double dt = target - st->t;
+      const bool ok = step_impl(c, st, dt, 1, true);
+      st->t = target;
+      if (!ok) {
+        if (fail_step) *fail_step = k;
+        throw Error(SDNS_DIVERGENCE_ERROR,
+                    "non-finite values in solution update at step " + std::to_string(k));
+      }
+      if (sample && (k % cfg.out_every == 0 || last)) sample(k, st->t, user);
+    }
+  });
+}
+
+int sdns_rk4_step_host(sdns_ctx* c, sdns_state* st, double* host, double dt, int steps) {
+  return guarded([&] {
+    set_device(c);
+    const size_t s2 = static_cast<size_t>(c->lo.spec_shape[2]);
+    const size_t rows = static_cast<size_t>(c->lo.spec_shape[0] * c->lo.spec_shape[1]);
+    for (int q = 0; q < 3; ++q)
+      SDNS_CUDA(cudaMemcpy2DAsync(st->u.spec() + q * c->spec_cs, sizeof(double2) * c->pitch,
+                                  host + 2 * q * s2 * rows, sizeof(double2) * s2,
+                                  sizeof(double2) * s2, rows, cudaMemcpyHostToDevice, c->stream));
+    for (int k = 0; k < steps; ++k) step_impl(c, st, dt, 1, false);
+    for (int q = 0; q < 3; ++q)
+      SDNS_CUDA(cudaMemcpy2DAsync(host + 2 * q * s2 * rows, sizeof(double2) * s2,
+                                  st->u.spec() + q * c->spec_cs, sizeof(double2) * c->pitch,
+                                  sizeof(double2) * s2, rows, cudaMemcpyDeviceToHost, c->stream));
+    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int sdns_collect_stats(sdns_ctx* c, const sdns_field* u, double nu, double t, double* row) {
+  return guarded([&] {
+    require_spec(u, 3, "collect_stats");
+    set_device(c);
+    stats_impl(c, u, nu, t, row);
+  });
+}
+
+int sdns_l2_diff(sdns_ctx* c, const sdns_field* a, const sdns_field* b, double* out) {
+  return guarded([&] {
+    require_real(a, 1, "l2_diff");
+    require_real(b, a->ncomp, "l2_diff");
+    set_device(c);
+    sdns_dev::l2_local(a->real(), b->real(), c->real_cs * a->ncomp, c->d_partial, c->d_out, c->stream);
+    post_launch("l2_diff");
+    SDNS_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    double v = c->h_out[0];
+    c->world->allreduce(&v, 1, 0);
+    const double n3 = static_cast<double>(c->cfg.n) * c->cfg.n * c->cfg.n;
+    *out = std::sqrt(v / n3);
+  });
+}
+
+int sdns_ctx_timing(sdns_ctx* c, int enable) {
+  return guarded([&] {
+    set_device(c);
+    if (enable && c->ev.empty()) {
+      const size_t nev = 16384;
+      c->ev.resize(nev);
+      c->ev_tag.assign(nev, 0);
+      for (auto& e : c->ev) SDNS_CUDA(cudaEventCreate(&e));
+    }
+    c->timing = enable != 0;
+    c->ev_used = 0;
+  });
+}
+
+int sdns_ctx_timing_read(sdns_ctx* c, double* ms, int64_t* launches) {
+  return guarded([&] {
+    set_device(c);
+    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    for (int t = 0; t < SDNS_NPASS; ++t) {
+      ms[t] = 0.0;
+      launches[t] = 0;
+    }
+    for (size_t i = 0; i + 1 < c->ev_used + 1 && i < c->ev_used; i += 2) {
+      float f = 0.0f;
+      SDNS_CUDA(cudaEventElapsedTime(&f, c->ev[i], c->ev[i + 1]));
+      const int t = c->ev_tag[i];
+      ms[t] += static_cast<double>(f);
+      launches[t] += 1;
+    }
+    c->ev_used = 0;
+  });
+}
+
+void* sdns_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+  return p;
+}
+void sdns_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,184 @@
+// Device-side fp64 FFT building blocks for sm_100a.
+//
+// A length-N complex transform of one "column" is computed cooperatively by
+// TPC = N/E threads, each holding E elements in registers. Thread t holds
+// element m at position t + m*TPC both on entry and on exit (natural order),
+// so the first stage reads and the last stage writes in exactly the pattern a
+// coalesced global load/store wants. Between stages the data is exchanged
+// through shared memory with a Stockham autosort step (no bit reversal):
+//   stage radix R, sub-length NS: butterfly j in [0, N/R) reads positions
+//   j + r*N/R, twiddles by W_{NS*R}^{(j mod NS)*r}, and writes
+//   (j/NS)*NS*R + (j mod NS) + r*NS.
+// Radices are E (8 or 16) until the remainder, which is a smaller power of
+// two. Twiddles come from a per-length table tw[q] = exp(-2*pi*i*q/N) in
+// global memory (L1-resident), conjugated for the inverse direction.
+// Unnormalised in both directions (FFTW convention, SerialFFT,
+// proj/core/include/sdns/serial_fft.hpp:13-14).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace sdns_dev {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// multiply by S*i (S = -1 forward, +1 inverse)
+template <int S>
+__device__ __forceinline__ double2 mul_si(double2 a) {
+  return S < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+}
+
+template <int S>
+__device__ __forceinline__ double2 twiddle(const double2* __restrict__ tw, int q) {
+  const double2 w = __ldg(tw + q);
+  return S < 0 ? w : make_double2(w.x, -w.y);
+}
+
+// In-place DFT of R register values, output in natural order.
+template <int R, int S>
+struct Dft;
+
+template <int S>
+struct Dft<1, S> {
+  __device__ __forceinline__ static void run(double2*) {}
+};
+
+template <int S>
+struct Dft<2, S> {
+  __device__ __forceinline__ static void run(double2* a) {
+    const double2 t = a[1];
+    a[1] = csub(a[0], t);
+    a[0] = cadd(a[0], t);
+  }
+};
+
+template <int S>
+struct Dft<4, S> {
+  __device__ __forceinline__ static void run(double2* a) {
+    const double2 s02 = cadd(a[0], a[2]), d02 = csub(a[0], a[2]);
+    const double2 s13 = cadd(a[1], a[3]), d13 = mul_si<S>(csub(a[1], a[3]));
+    a[0] = cadd(s02, s13);
+    a[2] = csub(s02, s13);
+    a[1] = cadd(d02, d13);
+    a[3] = csub(d02, d13);
+  }
+};
+
+template <int S>
+struct Dft<8, S> {
+  __device__ __forceinline__ static void run(double2* a) {
+    constexpr double H = 0.70710678118654752440;  // sqrt(1/2)
+    double2 e[4] = {a[0], a[2], a[4], a[6]};
+    double2 o[4] = {a[1], a[3], a[5], a[7]};
+    Dft<4, S>::run(e);
+    Dft<4, S>::run(o);
+    // W8^1 = H(1 + S i), W8^2 = S i, W8^3 = H(-1 + S i)
+    const double2 o1 = make_double2(H * (o[1].x - S * o[1].y), H * (o[1].y + S * o[1].x));
+    const double2 o2 = mul_si<S>(o[2]);
+    const double2 o3 = make_double2(H * (-o[3].x - S * o[3].y), H * (-o[3].y + S * o[3].x));
+    a[0] = cadd(e[0], o[0]);
+    a[4] = csub(e[0], o[0]);
+    a[1] = cadd(e[1], o1);
+    a[5] = csub(e[1], o1);
+    a[2] = cadd(e[2], o2);
+    a[6] = csub(e[2], o2);
+    a[3] = cadd(e[3], o3);
+    a[7] = csub(e[3], o3);
+  }
+};
+
+template <int S>
+struct Dft<16, S> {
+  __device__ __forceinline__ static void run(double2* a) {
+    // 16 = 2 x 8 decimation in time with W16^k = exp(S*2*pi*i*k/16).
+    constexpr double C1 = 0.92387953251128675613;  // cos(pi/8)
+    constexpr double S1 = 0.38268343236508977173;  // sin(pi/8)
+    constexpr double H = 0.70710678118654752440;
+    double2 e[8], o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      e[i] = a[2 * i];
+      o[i] = a[2 * i + 1];
+    }
+    Dft<8, S>::run(e);
+    Dft<8, S>::run(o);
+    const double wr[8] = {1.0, C1, H, S1, 0.0, -S1, -H, -C1};
+    const double wi[8] = {0.0, S1, H, C1, 1.0, C1, H, S1};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double2 w = make_double2(wr[k], S * wi[k]);
+      const double2 t = (k == 0) ? o[0] : cmul(o[k], w);
+      a[k] = cadd(e[k], t);
+      a[k + 8] = csub(e[k], t);
+    }
+  }
+};
+
+// Elements held per thread for a transform of length N.
+__host__ __device__ constexpr int fft_elems(int n) { return n >= 1024 ? 16 : (n >= 8 ? 8 : n); }
+
+// Shared-memory placement of a column: element x at sm[x * cs].
+struct ColIdx {
+  int cs;
+  __device__ __forceinline__ int operator()(int x) const { return x * cs; }
+};
+// Placement of a contiguous line with an XOR swizzle on 16-byte slots so the
+// stride-R writes of the first Stockham stage do not serialise on one bank.
+struct SwzIdx {
+  __device__ __forceinline__ int operator()(int x) const { return x ^ ((x >> 3) & 7); }
+};
+
+// One Stockham stage (and the rest, recursively). `sm` points at this
+// column's element 0 in shared memory; element x lives at sm[idx(x)].
+template <int N, int E, int S, int NS, class IDX>
+__device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx, int t,
+                                           const double2* __restrict__ tw) {
+  constexpr int REM = N / NS;
+  constexpr int R = REM >= E ? E : REM;
+  constexpr int NB = E / R;
+  constexpr int TPC = N / E;
+  constexpr bool LAST = (NS * R == N);
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    double2 a[R];
+    const int j = t + b * TPC;
+    const int k = j & (NS - 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) a[r] = v[b + r * NB];
+    if (NS > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) a[r] = cmul(a[r], twiddle<S>(tw, k * r * (N / (NS * R))));
+    }
+    Dft<R, S>::run(a);
+    if (LAST) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[b + r * NB] = a[r];
+    } else {
+      const int base = (j - k) * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm[idx(base + r * NS)] = a[r];
+    }
+  }
+  if constexpr (!LAST) {
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = sm[idx(t + m * TPC)];
+    __syncthreads();
+    fft_stages<N, E, S, NS * R>(v, sm, idx, t, tw);
+  }
+}
+
+// Full transform: v[m] = x[t + m*TPC] on entry, X[t + m*TPC] on exit.
+// Must be called by every thread of the block (contains __syncthreads).
+template <int N, int S, class IDX>
+__device__ __forceinline__ void block_fft(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
+                                          const double2* __restrict__ tw) {
+  fft_stages<N, fft_elems(N), S, 1>(v, sm, idx, t, tw);
+}
+
+}  // namespace sdns_dev

@@ -1,0 +1,83 @@
+// Host-side (C++) internals behind include/sdns_cuda.h.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/sdns_cuda.h"
+
+namespace sdns_host {
+
+// Exception types mirroring proj/core/include/sdns/types.hpp:28-62; the
+// C ABI maps them onto status codes.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void config_error(const std::string& m) { throw Error(SDNS_CONFIG_ERROR, m); }
+[[noreturn]] inline void protocol_error(const std::string& m) { throw Error(SDNS_PROTOCOL_ERROR, m); }
+[[noreturn]] inline void timeout_error(const std::string& m) { throw Error(SDNS_TIMEOUT_ERROR, m); }
+
+void cuda_check(cudaError_t e, const char* what);
+#define SDNS_CUDA(call) ::sdns_host::cuda_check((call), #call)
+
+// layout.cpp
+void validate(const sdns_config& cfg);
+sdns_layout build_layout(const sdns_config& cfg, int rank);
+int64_t block_size(int64_t total, int parts, int index);
+int64_t block_start(int64_t total, int parts, int index);
+int64_t step_count(double t_end, double dt);
+int spectrum_shells(int64_t n);
+
+// comm.cpp --------------------------------------------------------------------
+// One point-to-point block of an all-to-all: `bytes` from my `send` to
+// group peer `peer` and `bytes` from that peer into my `recv`.
+struct Xfer {
+  int peer;
+  const void* send;
+  void* recv;
+  size_t send_bytes;
+  size_t recv_bytes;
+};
+
+class Comm {
+ public:
+  virtual ~Comm() = default;
+  int rank() const { return rank_; }
+  int size() const { return size_; }
+  // Collective variable all-to-all of device buffers, enqueued on `s`.
+  // The k-th block sent to peer q matches the k-th block q receives from me.
+  virtual void alltoall(const std::vector<Xfer>& xs, cudaStream_t s) = 0;
+  // In-place host reduction, folded in ascending rank order (op 0 sum,
+  // 1 max, 2 min) like InProcessComm (transport.cpp:319-329).
+  virtual void allreduce(double* v, int n, int op) = 0;
+  virtual void barrier() = 0;
+  // Split by color, ordered by (key, rank) (transport.hpp:66-67).
+  virtual std::shared_ptr<Comm> split(int color, int key) = 0;
+  virtual int device() const = 0;
+
+ protected:
+  Comm(int r, int s) : rank_(r), size_(s) {}
+  int rank_, size_;
+};
+
+std::shared_ptr<Comm> make_loopback_comm();
+std::vector<std::shared_ptr<Comm>> make_inprocess_group(int size, int device, double timeout_s);
+void nccl_unique_id(unsigned char id[128]);
+std::shared_ptr<Comm> make_nccl_comm(const unsigned char id[128], int size, int rank, int device);
+
+// iso_init.cpp
+void iso_init(int64_t n, uint64_t seed, double k0, double energy, const sdns_layout& lo,
+              double* out);
+
+}  // namespace sdns_host
+
+// Opaque handle wrappers (C ABI types)
+struct sdns_comm {
+  std::shared_ptr<sdns_host::Comm> c;
+};

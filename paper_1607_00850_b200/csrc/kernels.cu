@@ -1,0 +1,895 @@
+// sm_100a kernels of the spectral-DNS right-hand-side pipeline.
+//
+// Pass structure of one RHS evaluation (reference
+// compute_rhs, proj/core/src/navier_stokes.cpp:104-139, and DistributedFFT,
+// proj/core/src/fft.cpp:81-126):
+//   P1 k_x_inv_curl   x-axis inverse c2c of u_hat and of omega_hat = i k x u_hat
+//   P2 k_col_plain    y-axis inverse c2c of the 6 fields (in place)
+//   P3 k_z_fused      z-axis c2r of the 6 fields, 1/n^3, u x omega, z r2c of 3
+//   P4 k_col_plain    y-axis forward c2c of the 3 fields (in place)
+//   P5 k_x_fwd_fused  x-axis forward c2c + dealias + projection + viscous term
+//                     + RK4 stage update (+ Neumaier carry, projection, finite)
+// Pointwise parts follow the reference operation order with explicit
+// round-to-nearest intrinsics (no FMA contraction), so the standalone
+// pointwise kernels are bitwise equal to the reference CPU functions.
+#include <cstdio>
+#include <vector>
+
+#include "fft_core.cuh"
+#include "kernels.cuh"
+
+namespace sdns_dev {
+
+namespace {
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// axis_wavenumber, proj/core/include/sdns/mesh.hpp:19-21
+__device__ __forceinline__ double wavenum(int j, int n) {
+  return static_cast<double>(j <= n / 2 - 1 ? j : j - n);
+}
+
+__device__ __forceinline__ long long col_off(const ColGeom& g, int row, int pos, int kz) {
+  return static_cast<long long>(row) * g.rs +
+         static_cast<long long>(pos >> g.pb_shift) * g.ps1 +
+         static_cast<long long>(pos & ((1 << g.pb_shift) - 1)) * g.ps0 + kz;
+}
+
+// i * (a*x - b*y) for complex x, y and real a, b (curl component).
+__device__ __forceinline__ double2 i_cross(double a, double2 x, double b, double2 y) {
+  const double re = dsub(dmul(a, x.x), dmul(b, y.x));
+  const double im = dsub(dmul(a, x.y), dmul(b, y.y));
+  return make_double2(-im, re);
+}
+
+// Launch shape of the column passes.
+template <int N>
+struct ColCfg {
+  static constexpr int E = fft_elems(N);
+  static constexpr int TPC = N / E;
+  // columns per CTA: fill ~256-512 threads, 8-column (128 B) tiles at least
+  static constexpr int CS = TPC >= 64 ? 8 : (256 / TPC < 8 ? 8 : 256 / TPC);
+  static constexpr int THREADS = TPC * CS;
+  // fused forward x-pass keeps 3 components in shared memory
+  static constexpr int CSF = N >= 512 ? 4 : (CS > 16 ? 16 : CS);
+  static constexpr int THREADSF = TPC * CSF;
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Twiddles
+
+__global__ void k_twiddles(int n, double2* tw) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  double s, c;
+  // sincospi is accurate to ~1 ulp and exact at the symmetry points
+  sincospi(-2.0 * static_cast<double>(q) / static_cast<double>(n), &s, &c);
+  tw[q] = make_double2(c, s);
+}
+
+void make_twiddles(int n, double2* d_tw, cudaStream_t s) {
+  k_twiddles<<<(n + 255) / 256, 256, 0, s>>>(n, d_tw);
+}
+
+// ---------------------------------------------------------------------------
+// Plain column transforms (x or y axis), nfields fields, in -> out (may alias)
+
+template <int N, int S>
+__global__ void __launch_bounds__(ColCfg<N>::THREADS)
+k_col_plain(const double2* in, double2* out, long long in_cs, long long out_cs, int nfields,
+            ColGeom g, const double2* __restrict__ tw) {
+  constexpr int E = ColCfg<N>::E, TPC = ColCfg<N>::TPC, CS = ColCfg<N>::CS;
+  extern __shared__ double2 smem[];
+  const int col = threadIdx.x % CS, t = threadIdx.x / CS;
+  const long long gc = static_cast<long long>(blockIdx.x) * CS + col;
+  const int row = static_cast<int>(gc / g.pitch), kz = static_cast<int>(gc % g.pitch);
+  const bool valid = row < g.nrows && kz < g.n2;
+#pragma unroll 1
+  for (int f = 0; f < nfields; ++f) {
+    double2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m)
+      v[m] = valid ? in[f * in_cs + col_off(g, row, t + m * TPC, kz)] : make_double2(0.0, 0.0);
+    block_fft<N, S>(v, smem + col, ColIdx{CS}, t, tw);
+    if (valid) {
+#pragma unroll
+      for (int m = 0; m < E; ++m) out[f * out_cs + col_off(g, row, t + m * TPC, kz)] = v[m];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// P1: x-axis inverse transform of u_hat and of omega_hat = i k x u_hat.
+// Outputs 0..2 = u, 3..5 = omega (curl_hat, navier_stokes.cpp:52-72). The
+// curl needs kx, which is only known before this transform, so omega is
+// formed in the prologue; inputs are re-read per output (L2 hits).
+
+template <int N>
+__global__ void __launch_bounds__(ColCfg<N>::THREADS)
+k_x_inv_curl(const double2* __restrict__ u, long long u_cs, double2* __restrict__ out,
+             long long out_cs, ColGeom g, WaveGeom w, const double2* __restrict__ tw) {
+  constexpr int E = ColCfg<N>::E, TPC = ColCfg<N>::TPC, CS = ColCfg<N>::CS;
+  extern __shared__ double2 smem[];
+  const int col = threadIdx.x % CS, t = threadIdx.x / CS;
+  const long long gc = static_cast<long long>(blockIdx.x) * CS + col;
+  const int row = static_cast<int>(gc / g.pitch), kz = static_cast<int>(gc % g.pitch);
+  const bool valid = row < g.nrows && kz < g.n2;
+  const double ky = wavenum(w.row_off + row, N);
+  const double kzd = static_cast<double>(w.kz_off + kz);
+  const double2* u0 = u;
+  const double2* u1 = u + u_cs;
+  const double2* u2 = u + 2 * u_cs;
+  const double2 z = make_double2(0.0, 0.0);
+#pragma unroll 1
+  for (int o = 0; o < 6; ++o) {
+    double2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int pos = t + m * TPC;
+      const long long off = col_off(g, row, pos, kz);
+      const double kx = wavenum(pos, N);
+      double2 r = z;
+      if (valid) {
+        switch (o) {
+          case 0: r = u0[off]; break;
+          case 1: r = u1[off]; break;
+          case 2: r = u2[off]; break;
+          case 3: r = i_cross(ky, u2[off], kzd, u1[off]); break;
+          case 4: r = i_cross(kzd, u0[off], kx, u2[off]); break;
+          default: r = i_cross(kx, u1[off], ky, u0[off]); break;
+        }
+      }
+      v[m] = r;
+    }
+    block_fft<N, +1>(v, smem + col, ColIdx{CS}, t, tw);
+    if (valid) {
+#pragma unroll
+      for (int m = 0; m < E; ++m) out[o * out_cs + col_off(g, row, t + m * TPC, kz)] = v[m];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// P5: x-axis forward transform of the 3 nonlinear components, then per mode
+// the compute_rhs tail (navier_stokes.cpp:114-138) and the RK4 stage update
+// (rk4.cpp:44-65), the post-step projection (runner.cpp:107) and the finite
+// check (rk4.cpp:13-18, evaluated before the projection like the reference).
+
+__device__ __forceinline__ double two_sum_err(double a, double b, double s) {
+  // Neumaier branch of TwoSum, rk4.cpp:21-23
+  return fabs(a) >= fabs(b) ? dadd(dsub(a, s), b) : dadd(dsub(b, s), a);
+}
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(ColCfg<N>::THREADSF)
+k_x_fwd_fused(XfArgs a, ColGeom g, WaveGeom w, const double2* __restrict__ tw) {
+  constexpr int E = ColCfg<N>::E, TPC = ColCfg<N>::TPC, CS = ColCfg<N>::CSF;
+  extern __shared__ double2 smem[];
+  const int col = threadIdx.x % CS, t = threadIdx.x / CS;
+  const long long gc = static_cast<long long>(blockIdx.x) * CS + col;
+  const int row = static_cast<int>(gc / g.pitch), kz = static_cast<int>(gc % g.pitch);
+  const bool valid = row < g.nrows && kz < g.n2;
+  double2 v[E];
+#pragma unroll 1
+  for (int c = 0; c < 3; ++c) {
+    double2* reg = smem + c * N * CS + col;
+#pragma unroll
+    for (int m = 0; m < E; ++m)
+      v[m] = valid ? a.nl[c * a.nl_cs + col_off(g, row, t + m * TPC, kz)]
+                   : make_double2(0.0, 0.0);
+    block_fft<N, -1>(v, reg, ColIdx{CS}, t, tw);
+    if (c < 2) {
+#pragma unroll
+      for (int m = 0; m < E; ++m) reg[(t + m * TPC) * CS] = v[m];
+    }
+  }
+  if (!valid) return;
+  const double ky = wavenum(w.row_off + row, N);
+  const double kzd = static_cast<double>(w.kz_off + kz);
+  const double kmax = static_cast<double>(N) / 3.0;
+  const bool keep_yz = fabs(ky) < kmax && fabs(kzd) < kmax;
+  bool finite = true;
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int pos = t + m * TPC;
+    const double kx = wavenum(pos, N);
+    const long long off = col_off(g, row, pos, kz);
+    double2 c0 = smem[(pos)*CS + col];
+    double2 c1 = smem[N * CS + pos * CS + col];
+    double2 c2 = v[m];
+    if (a.dealias && !(fabs(kx) < kmax && keep_yz)) {
+      c0 = c1 = c2 = make_double2(0.0, 0.0);
+    }
+    // wavenumbers(), mesh.cpp:56-60
+    const double k2 = dadd(dadd(dmul(kx, kx), dmul(ky, ky)), dmul(kzd, kzd));
+    const double inv = k2 > 0.0 ? 1.0 / k2 : 0.0;
+    const double kxk = dmul(kx, inv), kyk = dmul(ky, inv), kzk = dmul(kzd, inv);
+    // kd = kx c0 + ky c1 + kz c2; c -= (k/k^2) kd
+    const double kdr = dadd(dadd(dmul(kx, c0.x), dmul(ky, c1.x)), dmul(kzd, c2.x));
+    const double kdi = dadd(dadd(dmul(kx, c0.y), dmul(ky, c1.y)), dmul(kzd, c2.y));
+    c0 = make_double2(dsub(c0.x, dmul(kxk, kdr)), dsub(c0.y, dmul(kxk, kdi)));
+    c1 = make_double2(dsub(c1.x, dmul(kyk, kdr)), dsub(c1.y, dmul(kyk, kdi)));
+    c2 = make_double2(dsub(c2.x, dmul(kzk, kdr)), dsub(c2.y, dmul(kzk, kdi)));
+    const double visc = dmul(a.nu, k2);
+    double2 du[3];
+    const double2 cc[3] = {c0, c1, c2};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double2 uq = a.u[q * a.cs + off];
+      du[q] = make_double2(dsub(cc[q].x, dmul(visc, uq.x)), dsub(cc[q].y, dmul(visc, uq.y)));
+    }
+    if (MODE == XF_TAIL) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) a.out[q * a.cs + off] = du[q];
+    } else if (MODE == XF_RK0 || MODE == XF_RK12) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const long long o = q * a.cs + off;
+        double2 s = make_double2(dmul(a.w, du[q].x), dmul(a.w, du[q].y));
+        if (MODE == XF_RK12) {
+          const double2 s0 = a.accum[o];
+          s = make_double2(dadd(s0.x, s.x), dadd(s0.y, s.y));
+        }
+        a.accum[o] = s;
+        const double2 b = a.base[o];
+        a.out[o] = make_double2(dadd(b.x, dmul(a.bdt, du[q].x)), dadd(b.y, dmul(a.bdt, du[q].y)));
+      }
+    } else {  // XF_RK3
+      double2 un[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const long long o = q * a.cs + off;
+        const double2 s = a.accum[o];
+        const double2 cr = a.carry[o];
+        const double2 b = a.base[o];
+        const double dr = dadd(dmul(a.sixth, dadd(s.x, du[q].x)), cr.x);
+        const double di = dadd(dmul(a.sixth, dadd(s.y, du[q].y)), cr.y);
+        const double nr = dadd(b.x, dr), ni = dadd(b.y, di);
+        a.carry[o] = make_double2(two_sum_err(b.x, dr, nr), two_sum_err(b.y, di, ni));
+        un[q] = make_double2(nr, ni);
+        finite = finite && isfinite(nr) && isfinite(ni);
+      }
+      if (a.project) {
+        // project(), navier_stokes.cpp:85-102
+        const double pr = dadd(dadd(dmul(kx, un[0].x), dmul(ky, un[1].x)), dmul(kzd, un[2].x));
+        const double pi = dadd(dadd(dmul(kx, un[0].y), dmul(ky, un[1].y)), dmul(kzd, un[2].y));
+        un[0] = make_double2(dsub(un[0].x, dmul(kxk, pr)), dsub(un[0].y, dmul(kxk, pi)));
+        un[1] = make_double2(dsub(un[1].x, dmul(kyk, pr)), dsub(un[1].y, dmul(kyk, pi)));
+        un[2] = make_double2(dsub(un[2].x, dmul(kzk, pr)), dsub(un[2].y, dmul(kzk, pi)));
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) a.base_out[q * a.cs + off] = un[q];
+    }
+  }
+  if (MODE == XF_RK3 && !finite) atomicAnd(a.finite, 0);
+}
+
+// ---------------------------------------------------------------------------
+// P3: per z-line (row) of the 6 fields after the y pass:
+//   3 complex inverse FFTs of length n carry the 6 real lines in pairs
+//   (u0,u1), (u2,w0), (w1,w2) -- c2r with the imaginary parts of the kz = 0
+//   and kz = n/2 bins ignored, as FFTW's c2r does -- then the 1/n^3 scale
+//   (fft.cpp:125), the cross product u x omega (navier_stokes.cpp:45-49), and
+//   forward r2c of the 3 products, two in one complex FFT. Real data never
+//   leaves shared memory. Results overwrite fields 0..2 of the row.
+
+template <int N>
+struct ZCfg {
+  static constexpr int E = fft_elems(N);
+  static constexpr int TPC = N / E;
+  static constexpr int RPC = TPC >= 128 ? 1 : (TPC >= 32 ? 128 / TPC : 128 / TPC);
+  static constexpr int THREADS = TPC * RPC;
+};
+
+__device__ __forceinline__ long long zrow_off(const RowMap& rm, int ri) {
+  if (rm.blk == 0) return static_cast<long long>(ri) * rm.pitch;
+  const int xl = ri / rm.ny, y = ri - xl * rm.ny;
+  const int q = y / rm.blk, yl = y - q * rm.blk;
+  return (static_cast<long long>(q * rm.blk + xl) * rm.blk + yl) * rm.pitch;
+}
+
+// Full-length spectrum sample at position pos of A + iB from half spectra.
+template <int N>
+__device__ __forceinline__ double2 pair_sample(const double2* A, const double2* B, int pos) {
+  double2 a, b;
+  if (pos <= N / 2) {
+    a = A[pos];
+    b = B[pos];
+    if (pos == 0 || pos == N / 2) {
+      a.y = 0.0;
+      b.y = 0.0;
+    }
+  } else {
+    a = cconj(A[N - pos]);
+    b = cconj(B[N - pos]);
+  }
+  return make_double2(a.x - b.y, a.y + b.x);
+}
+
+template <int N>
+__global__ void __launch_bounds__(ZCfg<N>::THREADS)
+k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __restrict__ tw) {
+  constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x % TPC, r = threadIdx.x / TPC;
+  const int ri = blockIdx.x * ZCfg<N>::RPC + r;
+  const bool valid = ri < rm.nrows;
+  const long long ro = valid ? zrow_off(rm, ri) : 0;
+  double2* reg = smem + r * 3 * N;
+  const SwzIdx sw;
+  double2 v[E];
+#pragma unroll 1
+  for (int p = 0; p < 3; ++p) {
+    const double2* A = f + (2 * p) * cs + ro;
+    const double2* B = f + (2 * p + 1) * cs + ro;
+#pragma unroll
+    for (int m = 0; m < E; ++m)
+      v[m] = valid ? pair_sample<N>(A, B, t + m * TPC) : make_double2(0.0, 0.0);
+    block_fft<N, +1>(v, reg + p * N, sw, t, tw);
+#pragma unroll
+    for (int m = 0; m < E; ++m) reg[p * N + sw(t + m * TPC)] = v[m];
+  }
+  double n2r[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int x = sw(t + m * TPC);
+    const double2 p0 = reg[x], p1 = reg[N + x], p2 = reg[2 * N + x];
+    const double ua = dmul(p0.x, norm), ub = dmul(p0.y, norm), uc = dmul(p1.x, norm);
+    const double wa = dmul(p1.y, norm), wb = dmul(p2.x, norm), wc = dmul(p2.y, norm);
+    const double n0 = dsub(dmul(ub, wc), dmul(uc, wb));
+    const double n1 = dsub(dmul(uc, wa), dmul(ua, wc));
+    n2r[m] = dsub(dmul(ua, wb), dmul(ub, wa));
+    v[m] = make_double2(n0, n1);
+  }
+  __syncthreads();
+  block_fft<N, -1>(v, reg, sw, t, tw);
+#pragma unroll
+  for (int m = 0; m < E; ++m) reg[sw(t + m * TPC)] = v[m];
+  __syncthreads();
+  if (valid) {
+    double2* o0 = f + ro;
+    double2* o1 = f + cs + ro;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int k = t + m * TPC;
+      if (k <= N / 2) {
+        const double2 d = reg[sw(k)];
+        const double2 e = cconj(reg[sw((N - k) & (N - 1))]);
+        o0[k] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
+        const double2 dd = csub(d, e);
+        o1[k] = make_double2(0.5 * dd.y, -0.5 * dd.x);
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < E; ++m) v[m] = make_double2(n2r[m], 0.0);
+  block_fft<N, -1>(v, reg + N, sw, t, tw);
+  if (valid) {
+    double2* o2 = f + 2 * cs + ro;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int k = t + m * TPC;
+      if (k <= N / 2) o2[k] = v[m];
+    }
+  }
+}
+
+// Standalone c2r along z (DistributedFFT::inverse tail, fft.cpp:124-125):
+// rows 2i and 2i+1 of one field share one complex inverse FFT.
+template <int N>
+__global__ void __launch_bounds__(ZCfg<N>::THREADS)
+k_z_c2r(const double2* __restrict__ spec, double* __restrict__ real, RowMap rm, double norm,
+        const double2* __restrict__ tw) {
+  constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x % TPC, r = threadIdx.x / TPC;
+  const int pr = blockIdx.x * ZCfg<N>::RPC + r;
+  const int ri = 2 * pr;
+  const bool valid = ri < rm.nrows;
+  double2 v[E];
+  if (valid) {
+    const double2* A = spec + zrow_off(rm, ri);
+    const double2* B = spec + zrow_off(rm, ri + 1);
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = pair_sample<N>(A, B, t + m * TPC);
+  } else {
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = make_double2(0.0, 0.0);
+  }
+  block_fft<N, +1>(v, smem + r * N, SwzIdx{}, t, tw);
+  if (valid) {
+    double* a = real + static_cast<long long>(ri) * N;
+    double* b = a + N;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      a[t + m * TPC] = dmul(v[m].x, norm);
+      b[t + m * TPC] = dmul(v[m].y, norm);
+    }
+  }
+}
+
+// Standalone r2c along z (DistributedFFT::forward head, fft.cpp:87).
+template <int N>
+__global__ void __launch_bounds__(ZCfg<N>::THREADS)
+k_z_r2c(const double* __restrict__ real, double2* __restrict__ spec, RowMap rm,
+        const double2* __restrict__ tw) {
+  constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x % TPC, r = threadIdx.x / TPC;
+  const int pr = blockIdx.x * ZCfg<N>::RPC + r;
+  const int ri = 2 * pr;
+  const bool valid = ri < rm.nrows;
+  double2* reg = smem + r * N;
+  const SwzIdx sw;
+  double2 v[E];
+  if (valid) {
+    const double* a = real + static_cast<long long>(ri) * N;
+    const double* b = a + N;
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = make_double2(a[t + m * TPC], b[t + m * TPC]);
+  } else {
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = make_double2(0.0, 0.0);
+  }
+  block_fft<N, -1>(v, reg, sw, t, tw);
+#pragma unroll
+  for (int m = 0; m < E; ++m) reg[sw(t + m * TPC)] = v[m];
+  __syncthreads();
+  if (valid) {
+    double2* oa = spec + zrow_off(rm, ri);
+    double2* ob = spec + zrow_off(rm, ri + 1);
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int k = t + m * TPC;
+      if (k <= N / 2) {
+        const double2 d = reg[sw(k)];
+        const double2 e = cconj(reg[sw((N - k) & (N - 1))]);
+        oa[k] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
+        const double2 dd = csub(d, e);
+        ob[k] = make_double2(0.5 * dd.y, -0.5 * dd.x);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pointwise spectral kernels (reference op order, no contraction)
+
+struct ModeIdx {
+  int i, j, k;
+  bool ok;
+  long long off;
+};
+
+__device__ __forceinline__ ModeIdx mode_of(const SpecGeom& g, long long e) {
+  ModeIdx m;
+  const long long row = e / g.pitch;
+  m.k = static_cast<int>(e - row * g.pitch);
+  m.j = static_cast<int>(row % g.s1);
+  m.i = static_cast<int>(row / g.s1);
+  m.ok = m.i < g.s0 && m.k < g.s2;
+  m.off = e;
+  return m;
+}
+
+__global__ void k_curl(const double2* __restrict__ u, double2* __restrict__ w, SpecGeom g) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const ModeIdx m = mode_of(g, e);
+  if (!m.ok) return;
+  const double kx = wavenum(g.o0 + m.i, g.n), ky = wavenum(g.o1 + m.j, g.n);
+  const double kz = static_cast<double>(g.o2 + m.k);
+  const double2 u0 = u[e], u1 = u[g.cs + e], u2 = u[2 * g.cs + e];
+  w[e] = i_cross(ky, u2, kz, u1);
+  w[g.cs + e] = i_cross(kz, u0, kx, u2);
+  w[2 * g.cs + e] = i_cross(kx, u1, ky, u0);
+}
+
+__device__ __forceinline__ void k_over_k2(double kx, double ky, double kz, double& a, double& b,
+                                          double& c) {
+  const double k2 = dadd(dadd(dmul(kx, kx), dmul(ky, ky)), dmul(kz, kz));
+  const double inv = k2 > 0.0 ? 1.0 / k2 : 0.0;
+  a = dmul(kx, inv);
+  b = dmul(ky, inv);
+  c = dmul(kz, inv);
+}
+
+__global__ void k_project(double2* u, SpecGeom g) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const ModeIdx m = mode_of(g, e);
+  if (!m.ok) return;
+  const double kx = wavenum(g.o0 + m.i, g.n), ky = wavenum(g.o1 + m.j, g.n);
+  const double kz = static_cast<double>(g.o2 + m.k);
+  double a, b, c;
+  k_over_k2(kx, ky, kz, a, b, c);
+  double2 u0 = u[e], u1 = u[g.cs + e], u2 = u[2 * g.cs + e];
+  const double kr = dadd(dadd(dmul(kx, u0.x), dmul(ky, u1.x)), dmul(kz, u2.x));
+  const double ki = dadd(dadd(dmul(kx, u0.y), dmul(ky, u1.y)), dmul(kz, u2.y));
+  u[e] = make_double2(dsub(u0.x, dmul(a, kr)), dsub(u0.y, dmul(a, ki)));
+  u[g.cs + e] = make_double2(dsub(u1.x, dmul(b, kr)), dsub(u1.y, dmul(b, ki)));
+  u[2 * g.cs + e] = make_double2(dsub(u2.x, dmul(c, kr)), dsub(u2.y, dmul(c, ki)));
+}
+
+__global__ void k_pressure(const double2* __restrict__ nl, double2* __restrict__ p, SpecGeom g) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const ModeIdx m = mode_of(g, e);
+  if (!m.ok) return;
+  const double kx = wavenum(g.o0 + m.i, g.n), ky = wavenum(g.o1 + m.j, g.n);
+  const double kz = static_cast<double>(g.o2 + m.k);
+  double a, b, c;
+  k_over_k2(kx, ky, kz, a, b, c);
+  const double2 n0 = nl[e], n1 = nl[g.cs + e], n2 = nl[2 * g.cs + e];
+  const double kr = dadd(dadd(dmul(a, n0.x), dmul(b, n1.x)), dmul(c, n2.x));
+  const double ki = dadd(dadd(dmul(a, n0.y), dmul(b, n1.y)), dmul(c, n2.y));
+  p[e] = make_double2(ki, -kr);  // Complex(0,-1) * kd
+}
+
+__global__ void k_cross(const double* __restrict__ a, const double* __restrict__ b,
+                        double* __restrict__ o, long long count, long long cs) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  const double a0 = a[e], a1 = a[cs + e], a2 = a[2 * cs + e];
+  const double b0 = b[e], b1 = b[cs + e], b2 = b[2 * cs + e];
+  o[e] = dsub(dmul(a1, b2), dmul(a2, b1));
+  o[cs + e] = dsub(dmul(a2, b0), dmul(a0, b2));
+  o[2 * cs + e] = dsub(dmul(a0, b1), dmul(a1, b0));
+}
+
+__global__ void k_finite(const double2* __restrict__ u, SpecGeom g, int* flag) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const ModeIdx m = mode_of(g, e);
+  if (!m.ok) return;
+  bool ok = true;
+  for (int c = 0; c < 3; ++c) {
+    const double2 v = u[c * g.cs + e];
+    ok = ok && isfinite(v.x) && isfinite(v.y);
+  }
+  if (!ok) atomicAnd(flag, 0);
+}
+
+static unsigned grid_for(long long n, int threads) {
+  return static_cast<unsigned>((n + threads - 1) / threads);
+}
+
+void pw_curl(const double2* u, double2* w, const SpecGeom& g, cudaStream_t s) {
+  const long long tot = static_cast<long long>(g.s0) * g.s1 * g.pitch;
+  k_curl<<<grid_for(tot, 256), 256, 0, s>>>(u, w, g);
+}
+void pw_project(double2* u, const SpecGeom& g, cudaStream_t s) {
+  const long long tot = static_cast<long long>(g.s0) * g.s1 * g.pitch;
+  k_project<<<grid_for(tot, 256), 256, 0, s>>>(u, g);
+}
+void pw_pressure(const double2* nl, double2* p, const SpecGeom& g, cudaStream_t s) {
+  const long long tot = static_cast<long long>(g.s0) * g.s1 * g.pitch;
+  k_pressure<<<grid_for(tot, 256), 256, 0, s>>>(nl, p, g);
+}
+void pw_cross(const double* a, const double* b, double* o, long long count, long long cs,
+              cudaStream_t s) {
+  k_cross<<<grid_for(count, 256), 256, 0, s>>>(a, b, o, count, cs);
+}
+void pw_finite(const double2* u, const SpecGeom& g, int* flag, cudaStream_t s) {
+  const long long tot = static_cast<long long>(g.s0) * g.s1 * g.pitch;
+  k_finite<<<grid_for(tot, 256), 256, 0, s>>>(u, g, flag);
+}
+__global__ void k_fill_pad(double2* f, SpecGeom g, int ncomp) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const ModeIdx m = mode_of(g, e);
+  if (m.i >= g.s0 || m.k < g.s2) return;
+  for (int c = 0; c < ncomp; ++c) f[c * g.cs + e] = make_double2(0.0, 0.0);
+}
+void pw_fill_pad(double2* f, int ncomp, const SpecGeom& g, cudaStream_t s) {
+  const long long tot = static_cast<long long>(g.s0) * g.s1 * g.pitch;
+  k_fill_pad<<<grid_for(tot, 256), 256, 0, s>>>(f, g, ncomp);
+}
+
+// ---------------------------------------------------------------------------
+// Diagnostics (collect_stats, diagnostics.cpp:24-91) with a fixed reduction
+// order: one CTA per local x plane, each warp walks y rows and kz chunks in
+// order; the spectrum uses per-warp shared-memory histograms fed by a
+// segmented scan (|k| and hence the shell index is nondecreasing in kz along
+// a row); a second kernel folds the per-plane partials in plane order.
+
+constexpr int kStatsWarps = 8;
+
+__global__ void __launch_bounds__(kStatsWarps * 32)
+k_stats_partial(const double2* __restrict__ u, SpecGeom g, int shells, double* partial) {
+  extern __shared__ double sh[];  // [kStatsWarps][shells] + reductions
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* hist = sh + warp * shells;
+  for (int s = lane; s < shells; s += 32) hist[s] = 0.0;
+  __syncwarp();
+  const int i = blockIdx.x;
+  const double kx = wavenum(g.o0 + i, g.n);
+  const double eps = 2.220446049250313e-16;
+  const double half = static_cast<double>(g.n / 2);
+  double se = 0.0, sz = 0.0, dmax = 0.0;
+  for (int j = warp; j < g.s1; j += kStatsWarps) {
+    const double ky = wavenum(g.o1 + j, g.n);
+    const long long rowoff = (static_cast<long long>(i) * g.s1 + j) * g.pitch;
+    for (int k0 = 0; k0 < g.s2; k0 += 32) {
+      const int k = k0 + lane;
+      const bool ok = k < g.s2;
+      double we = 0.0;
+      int shell = -1;
+      if (ok) {
+        const double kz = static_cast<double>(g.o2 + k);
+        const double w = (kz == 0.0 || kz == half) ? 1.0 : 2.0;
+        const long long e = rowoff + k;
+        const double2 u0 = u[e], u1 = u[g.cs + e], u2 = u[2 * g.cs + e];
+        const double ee = (u0.x * u0.x + u0.y * u0.y) + (u1.x * u1.x + u1.y * u1.y) +
+                          (u2.x * u2.x + u2.y * u2.y);
+        const double2 c0 = make_double2(ky * u2.x - kz * u1.x, ky * u2.y - kz * u1.y);
+        const double2 c1 = make_double2(kz * u0.x - kx * u2.x, kz * u0.y - kx * u2.y);
+        const double2 c2 = make_double2(kx * u1.x - ky * u0.x, kx * u1.y - ky * u0.y);
+        const double zz = (c0.x * c0.x + c0.y * c0.y) + (c1.x * c1.x + c1.y * c1.y) +
+                          (c2.x * c2.x + c2.y * c2.y);
+        se += w * ee;
+        sz += w * zz;
+        const double k2 = (kx * kx + ky * ky) + kz * kz;
+        const double kn = sqrt(k2);
+        shell = static_cast<int>(llround(kn));
+        we = 0.5 * w * ee;
+        const double kdr = (kx * u0.x + ky * u1.x) + kz * u2.x;
+        const double kdi = (kx * u0.y + ky * u1.y) + kz * u2.y;
+        const double ratio = hypot(kdr, kdi) / (kn * sqrt(ee) + eps);
+        dmax = fmax(dmax, ratio);
+      }
+      // segmented inclusive scan over lanes with equal shell (fixed order)
+      double acc = we;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double o = __shfl_up_sync(0xffffffffu, acc, d);
+        const int os = __shfl_up_sync(0xffffffffu, shell, d);
+        if (lane >= d && os == shell) acc += o;
+      }
+      const int nxt = __shfl_down_sync(0xffffffffu, shell, 1);
+      const bool tail = ok && (lane == 31 || nxt != shell);
+      if (tail && shell < shells) hist[shell] += acc;
+      __syncwarp();
+    }
+  }
+  // fixed-order warp reductions
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    se += __shfl_xor_sync(0xffffffffu, se, d);
+    sz += __shfl_xor_sync(0xffffffffu, sz, d);
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, d));
+  }
+  double* red = sh + kStatsWarps * shells;
+  if (lane == 0) {
+    red[warp * 3 + 0] = se;
+    red[warp * 3 + 1] = sz;
+    red[warp * 3 + 2] = dmax;
+  }
+  __syncthreads();
+  const int stride = shells + 3;
+  double* out = partial + static_cast<long long>(blockIdx.x) * stride;
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int w = 0; w < kStatsWarps; ++w) {
+      a += red[w * 3 + 0];
+      b += red[w * 3 + 1];
+      c = fmax(c, red[w * 3 + 2]);
+    }
+    out[0] = a;
+    out[1] = b;
+    out[2] = c;
+  }
+  for (int s = threadIdx.x; s < shells; s += blockDim.x) {
+    double acc = 0.0;
+    for (int w = 0; w < kStatsWarps; ++w) acc += sh[w * shells + s];
+    out[3 + s] = acc;
+  }
+}
+
+__global__ void k_fold_partials(const double* partial, int nblocks, int stride, double* out) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= stride) return;
+  double acc = 0.0;
+  if (v == 2) {
+    for (int b = 0; b < nblocks; ++b) acc = fmax(acc, partial[static_cast<long long>(b) * stride + v]);
+  } else {
+    for (int b = 0; b < nblocks; ++b) acc += partial[static_cast<long long>(b) * stride + v];
+  }
+  out[v] = acc;
+}
+
+int stats_blocks(const SpecGeom& g) { return g.s0; }
+
+void stats_local(const double2* u, const SpecGeom& g, int shells, double* d_partial,
+                 double* d_out, cudaStream_t s) {
+  const size_t shm = sizeof(double) * (kStatsWarps * shells + kStatsWarps * 3);
+  k_stats_partial<<<g.s0, kStatsWarps * 32, shm, s>>>(u, g, shells, d_partial);
+  const int stride = shells + 3;
+  k_fold_partials<<<(stride + 127) / 128, 128, 0, s>>>(d_partial, g.s0, stride, d_out);
+}
+
+constexpr int kL2Blocks = 592;
+
+__global__ void k_l2_partial(const double* __restrict__ a, const double* __restrict__ b,
+                             long long count, double* partial) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < count;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double d = a[e] - b[e];
+    acc += d * d;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+void l2_local(const double* a, const double* b, long long count, double* d_partial,
+              double* d_out, cudaStream_t s) {
+  k_l2_partial<<<kL2Blocks, 256, 0, s>>>(a, b, count, d_partial);
+  k_fold_partials<<<1, 32, 0, s>>>(d_partial, kL2Blocks, 1, d_out);
+}
+
+// ---------------------------------------------------------------------------
+// Dispatch over the (power-of-two) transform length
+
+#define SDNS_FOR_N(X) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
+
+// Opt in to >48 KB dynamic shared memory once per kernel instantiation (the
+// call sites below are templates, so each static flag is per kernel).
+#define SDNS_SET_SMEM(kernel, bytes)                                              \
+  do {                                                                           \
+    static bool sdns_smem_done_ = false;                                          \
+    if (!sdns_smem_done_) {                                                       \
+      if ((bytes) > 48 * 1024)                                                    \
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             static_cast<int>(bytes));                            \
+      sdns_smem_done_ = true;                                                     \
+    }                                                                            \
+  } while (0)
+
+template <int N>
+static void col_plain_n(int dir, const double2* in, double2* out, long long in_cs, long long out_cs,
+                        int nfields, const ColGeom& g, const double2* tw, cudaStream_t s) {
+  using C = ColCfg<N>;
+  const long long cols = static_cast<long long>(g.nrows) * g.pitch;
+  const unsigned grid = static_cast<unsigned>((cols + C::CS - 1) / C::CS);
+  const size_t shm = sizeof(double2) * N * C::CS;
+  if (dir < 0) {
+    SDNS_SET_SMEM((k_col_plain<N, -1>), shm);
+    k_col_plain<N, -1><<<grid, C::THREADS, shm, s>>>(in, out, in_cs, out_cs, nfields, g, tw);
+  } else {
+    SDNS_SET_SMEM((k_col_plain<N, +1>), shm);
+    k_col_plain<N, +1><<<grid, C::THREADS, shm, s>>>(in, out, in_cs, out_cs, nfields, g, tw);
+  }
+}
+
+void col_plain(int n, int dir, const double2* in, double2* out, long long in_cs, long long out_cs,
+               int nfields, const ColGeom& g, const double2* tw, cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: col_plain_n<NN>(dir, in, out, in_cs, out_cs, nfields, g, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+template <int N>
+static void x_inv_curl_n(const double2* u, long long u_cs, double2* out, long long out_cs,
+                         const ColGeom& g, const WaveGeom& w, const double2* tw, cudaStream_t s) {
+  using C = ColCfg<N>;
+  const long long cols = static_cast<long long>(g.nrows) * g.pitch;
+  const unsigned grid = static_cast<unsigned>((cols + C::CS - 1) / C::CS);
+  const size_t shm = sizeof(double2) * N * C::CS;
+  SDNS_SET_SMEM((k_x_inv_curl<N>), shm);
+  k_x_inv_curl<N><<<grid, C::THREADS, shm, s>>>(u, u_cs, out, out_cs, g, w, tw);
+}
+
+void x_inverse_curl(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
+                    const ColGeom& g, const WaveGeom& w, const double2* tw, cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: x_inv_curl_n<NN>(u, u_cs, out, out_cs, g, w, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+template <int N, int MODE>
+static void x_fwd_mode(const XfArgs& a, const ColGeom& g, const WaveGeom& w, const double2* tw,
+                       cudaStream_t s) {
+  using C = ColCfg<N>;
+  const long long cols = static_cast<long long>(g.nrows) * g.pitch;
+  const unsigned grid = static_cast<unsigned>((cols + C::CSF - 1) / C::CSF);
+  const size_t shm = sizeof(double2) * 3 * N * C::CSF;
+  SDNS_SET_SMEM((k_x_fwd_fused<N, MODE>), shm);
+  k_x_fwd_fused<N, MODE><<<grid, C::THREADSF, shm, s>>>(a, g, w, tw);
+}
+
+template <int N>
+static void x_fwd_n(int mode, const XfArgs& a, const ColGeom& g, const WaveGeom& w,
+                    const double2* tw, cudaStream_t s) {
+  switch (mode) {
+    case XF_TAIL: x_fwd_mode<N, XF_TAIL>(a, g, w, tw, s); return;
+    case XF_RK0: x_fwd_mode<N, XF_RK0>(a, g, w, tw, s); return;
+    case XF_RK12: x_fwd_mode<N, XF_RK12>(a, g, w, tw, s); return;
+    default: x_fwd_mode<N, XF_RK3>(a, g, w, tw, s); return;
+  }
+}
+
+void x_forward_fused(int n, int mode, const XfArgs& a, const ColGeom& g, const WaveGeom& w,
+                     const double2* tw, cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: x_fwd_n<NN>(mode, a, g, w, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+template <int N>
+static void z_fused_n(double2* rows, long long cs, const RowMap& rm, double norm,
+                      const double2* tw, cudaStream_t s) {
+  using C = ZCfg<N>;
+  const unsigned grid = static_cast<unsigned>((rm.nrows + C::RPC - 1) / C::RPC);
+  const size_t shm = sizeof(double2) * 3 * N * C::RPC;
+  SDNS_SET_SMEM((k_z_fused<N>), shm);
+  k_z_fused<N><<<grid, C::THREADS, shm, s>>>(rows, cs, rm, norm, tw);
+}
+
+void z_fused(int n, double2* rows, long long cs, const RowMap& rm, double norm,
+             const double2* tw, cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: z_fused_n<NN>(rows, cs, rm, norm, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+template <int N>
+static void z_c2r_n(const double2* spec, double* real, const RowMap& rm, double norm,
+                    const double2* tw, cudaStream_t s) {
+  using C = ZCfg<N>;
+  const int pairs = rm.nrows / 2;
+  const unsigned grid = static_cast<unsigned>((pairs + C::RPC - 1) / C::RPC);
+  const size_t shm = sizeof(double2) * N * C::RPC;
+  SDNS_SET_SMEM((k_z_c2r<N>), shm);
+  k_z_c2r<N><<<grid, C::THREADS, shm, s>>>(spec, real, rm, norm, tw);
+}
+
+void z_c2r(int n, const double2* spec, double* real, const RowMap& rm, double norm,
+           const double2* tw, cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: z_c2r_n<NN>(spec, real, rm, norm, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+template <int N>
+static void z_r2c_n(const double* real, double2* spec, const RowMap& rm, const double2* tw,
+                    cudaStream_t s) {
+  using C = ZCfg<N>;
+  const int pairs = rm.nrows / 2;
+  const unsigned grid = static_cast<unsigned>((pairs + C::RPC - 1) / C::RPC);
+  const size_t shm = sizeof(double2) * N * C::RPC;
+  SDNS_SET_SMEM((k_z_r2c<N>), shm);
+  k_z_r2c<N><<<grid, C::THREADS, shm, s>>>(real, spec, rm, tw);
+}
+
+void z_r2c(int n, const double* real, double2* spec, const RowMap& rm, const double2* tw,
+           cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: z_r2c_n<NN>(real, spec, rm, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+}  // namespace sdns_dev

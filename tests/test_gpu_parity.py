@@ -1,0 +1,369 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracles.
+
+Bars (BASELINE.json north_star): FFT vs reference <= 1e-11 * max|X| and
+round trip <= 1e-13 relative L2; pointwise operators bitwise; velocity field
+relative L2 <= 1e-11 after 10 RK4 steps; energy and enstrophy <= 1e-12
+relative per sampled step.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_1607_00850_b200 as S
+from oracle import sdns_np as O
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = np.load(os.path.join(ROOT, "tests", "golden", "golden_ref.npz"))
+
+
+def rel(a, b):
+    return np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(np.asarray(b).ravel()), 1e-300)
+
+
+def ctx_for(n, nu=0.01, dt=0.01, steps=10, out_every=1, dealias=True):
+    cfg = S.SolverConfig(n=n, nu=nu, dt=dt, t_end=steps * dt, dealias=dealias,
+                         out_every=out_every)
+    return S.Context(cfg)
+
+
+# --- transforms ------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [8, 16, 32, 64, 128, 256])
+def test_fft_forward_inverse_vs_numpy(n):
+    rng = np.random.default_rng(42 + n)
+    u = rng.uniform(-1, 1, (3, n, n, n))
+    with ctx_for(n) as c:
+        fft = S.DistributedFFT(c)
+        fu_d, u_d = c.spectral_field(), c.real_field()
+        u_d.upload(u)
+        fft.forward(u_d, fu_d)
+        fu = fu_d.download()
+        ref = O.forward(u)
+        assert np.abs(fu - ref).max() <= 1e-11 * np.abs(ref).max()
+        back = c.real_field()
+        fft.inverse(fu_d, back)
+        assert rel(back.download(), u) <= 1e-13
+
+
+def test_fft_matches_reference_golden():
+    u = GOLD["fft8_u"]
+    with ctx_for(8) as c:
+        fft = S.DistributedFFT(c)
+        ud, fd = c.real_field().upload(u), c.spectral_field()
+        fft.forward(ud, fd)
+        fu = fd.download()
+        g = GOLD["fft8_slab1"]
+        assert np.abs(fu - g).max() <= 1e-11 * np.abs(g).max()
+
+
+def test_fft_constant_field_and_cosine_spike():
+    """proj/tests/test_fft.cpp:112-175: DC of a constant = 2.5 n^3, cos(x)
+    spike = n^3/2, inverse of the DC spike recovers 2.5 everywhere."""
+    n = 16
+    with ctx_for(n) as c:
+        fft = S.DistributedFFT(c)
+        u = np.full((3, n, n, n), 2.5)
+        fd = c.spectral_field()
+        fft.forward(c.real_field().upload(u), fd)
+        fu = fd.download()
+        assert abs(fu[0, 0, 0, 0] - 2.5 * n**3) <= 1e-9
+        fu0 = fu.copy()
+        fu0[:, 0, 0, 0] = 0
+        assert np.abs(fu0).max() <= 1e-9
+        back = c.real_field()
+        fft.inverse(fd, back)
+        assert np.allclose(back.download(), 2.5, rtol=0, atol=1e-13)
+        x = O.physical_axis(n)
+        u = np.broadcast_to(np.cos(x)[:, None, None], (3, n, n, n)).copy()
+        fft.forward(c.real_field().upload(u), fd)
+        fu = fd.download()
+        assert abs(fu[0, 1, 0, 0] - n**3 / 2) <= 1e-9
+        assert abs(fu[0, n - 1, 0, 0] - n**3 / 2) <= 1e-9
+
+
+def test_c2r_ignores_imaginary_dc_and_nyquist():
+    """FFTW c2r semantics: Im of the kz = 0 and kz = n/2
+    bins does not reach the real output, exactly as the reference."""
+    n = 16
+    rng = np.random.default_rng(7)
+    u = rng.uniform(-1, 1, (3, n, n, n))
+    uh = O.forward(u)
+    bad = uh.copy()
+    bad[:, 3, 5, 0] += 0.25j
+    bad[:, 2, 1, n // 2] -= 0.5j
+    with ctx_for(n) as c:
+        fft = S.DistributedFFT(c)
+        out = c.real_field()
+        fft.inverse(c.spectral_field().upload(bad), out)
+        got = out.download()
+    expect = O.inverse(bad, n)  # pocketfft c2r also drops them
+    assert np.abs(got - expect).max() <= 1e-14 * max(1.0, np.abs(expect).max())
+
+
+# --- pointwise operators: bitwise ---------------------------------------------------
+
+def test_pointwise_ops_bitwise_vs_reference():
+    uh = GOLD["pw8_uh"]
+    with ctx_for(8) as c:
+        u = c.spectral_field().upload(uh)
+        w = c.spectral_field()
+        S.curl_hat(c, u, w)
+        assert np.array_equal(w.download(), GOLD["pw8_curl"])
+        p = c.spectral_field(1)
+        S.pressure_hat(c, u, p)
+        assert np.array_equal(p.download()[0], GOLD["pw8_pressure"])
+        S.project(c, u)
+        assert np.array_equal(u.download(), GOLD["pw8_project"])
+        a = c.real_field().upload(GOLD["pw8_a"])
+        b = c.real_field().upload(GOLD["pw8_b"])
+        o = c.real_field()
+        S.cross(c, a, b, o)
+        assert np.array_equal(o.download(), GOLD["pw8_cross"])
+
+
+# --- compute_rhs -------------------------------------------------------------------
+
+def test_compute_rhs_matches_reference_golden():
+    for key_in, key_out, n, nu in (("rnd16_uh", "rnd16_rhs", 16, 1e-3),):
+        with ctx_for(n) as c:
+            u = c.spectral_field().upload(GOLD[key_in])
+            du = c.spectral_field()
+            S.compute_rhs(c, u, nu, du)
+            assert rel(du.download(), GOLD[key_out]) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [16, 32, 64])
+def test_compute_rhs_vs_numpy_oracle(n):
+    rng = np.random.default_rng(n)
+    wm = O.Wavenumbers(n)
+    uh = O.project(O.forward(rng.uniform(-1, 1, (3, n, n, n))), wm) / n**3
+    expect = O.compute_rhs(uh, wm, 0.01)
+    with ctx_for(n) as c:
+        du = c.spectral_field()
+        S.compute_rhs(c, c.spectral_field().upload(uh), 0.01, du)
+        assert rel(du.download(), expect) <= 1e-12
+
+
+def test_compute_rhs_solenoidal_and_linear_in_nu():
+    """proj/tests/test_ns.cpp:170-214: k . du = 0, d(du)/d(nu) = -k^2 u."""
+    n = 16
+    wm = O.Wavenumbers(n)
+    uh = O.project(O.forward(O.taylor_green_baseline(n)), wm)
+    with ctx_for(n) as c:
+        u = c.spectral_field().upload(uh)
+        d0, d1 = c.spectral_field(), c.spectral_field()
+        S.compute_rhs(c, u, 0.0, d0)
+        S.compute_rhs(c, u, 0.1, d1)
+        a, b = d0.download(), d1.download()
+    kd = (wm.KX * a[0] + wm.KY * a[1]) + wm.KZ * a[2]
+    assert np.abs(kd).max() <= 1e-9 * max(1.0, np.abs(a).max())
+    assert np.abs((b - a) / 0.1 + wm.k2[None] * uh).max() <= 1e-10 * np.abs(wm.k2[None] * uh).max()
+
+
+# --- RK4 trajectories -----------------------------------------------------------
+
+def run_gpu(n, uh0, nu, dt, steps, out_every=1, project_init=True):
+    cfg = S.SolverConfig(n=n, nu=nu, dt=dt, t_end=steps * dt, out_every=out_every)
+    with S.Context(cfg) as c:
+        u = c.spectral_field().upload(uh0)
+        if project_init:
+            S.project(c, u)
+        st = S.Rk4State(c)
+        st.set(u)
+        rows = []
+        st.advance(lambda k, t: rows.append(S.collect_stats(c, st.u_hat, nu, t)))
+        final = st.u_hat.download()
+        st.close()
+    return rows, final
+
+
+def test_taylor_green_16_matches_reference_golden():
+    rows, final = run_gpu(16, GOLD["tg16_uh0"], 0.01, 0.01, 10)
+    g = GOLD["tg16_stats"]
+    assert len(rows) == g.shape[0]
+    for r, gr in zip(rows, g):
+        assert r.t == gr[0]
+        assert abs(r.energy - gr[1]) <= 1e-12 * gr[1]
+        assert abs(r.enstrophy - gr[2]) <= 1e-12 * gr[2]
+        assert np.allclose(r.spectrum, gr[5:], rtol=1e-11, atol=1e-30)
+    assert rel(final, GOLD["tg16_final"]) <= 1e-11
+
+
+def test_config1_taylor_green_64_100_steps_vs_reference(ref):
+    """BASELINE config 1: TG n=64, nu=0.01, dt=0.01, 100 steps, E and Z every step."""
+    n, nu, dt, steps = 64, 0.01, 0.01, 100
+    uh0 = ref.forward(O.taylor_green_baseline(n), n)
+    gs, gf = ref.run(uh0, n, nu, dt, steps, out_every=1, decomp="slab", p=8)
+    rows, final = run_gpu(n, uh0, nu, dt, steps)
+    assert len(rows) == gs.shape[0] == steps + 1
+    for r, gr in zip(rows, gs):
+        assert abs(r.energy - gr[1]) <= 1e-12 * gr[1]
+        assert abs(r.enstrophy - gr[2]) <= 1e-12 * gr[2]
+        assert r.divergence_max <= 1e-10
+    assert rel(final, gf) <= 1e-11
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_iso_10_steps_vs_reference(ref, n):
+    """Configs 2-4 construction at test size: iso field, 10 RK4 steps."""
+    cfg = S.SolverConfig(n=n)
+    lo = S.build_layout(cfg, 0)
+    uh0 = S.iso_init(n, lo, seed=1607)
+    nu, dt = 1e-3, 1e-3
+    gs, gf = ref.run(uh0, n, nu, dt, 10, out_every=1, init_project=False, p=8)
+    rows, final = run_gpu(n, uh0, nu, dt, 10, project_init=False)
+    assert abs(rows[0].energy - 0.5) <= 1e-13
+    for r, gr in zip(rows, gs):
+        assert abs(r.energy - gr[1]) <= 1e-12 * gr[1]
+        assert abs(r.enstrophy - gr[2]) <= 1e-12 * gr[2]
+    assert rel(final, gf) <= 1e-11
+
+
+def test_rk4_steps_match_reference_golden():
+    n = 16
+    cfg = S.SolverConfig(n=n, nu=1e-3, dt=1e-3)
+    with S.Context(cfg) as c:
+        st = S.Rk4State(c)
+        st.set(c.spectral_field().upload(GOLD["rnd16_uh"]))
+        for _ in range(3):
+            st.rk4_step(1e-3, post_project=True)
+        assert rel(st.u_hat.download(), GOLD["rnd16_rk3"]) <= 1e-12
+        assert st.step == 3
+        st.close()
+
+
+def test_stats_match_reference():
+    n = 16
+    with ctx_for(n) as c:
+        s = S.collect_stats(c, c.spectral_field().upload(GOLD["rnd16_uh"]), 1e-3)
+    g = GOLD["rnd16_stats"]
+    assert abs(s.energy - g[1]) <= 1e-13 * g[1]
+    assert abs(s.enstrophy - g[2]) <= 1e-13 * g[2]
+    assert abs(s.dissipation - g[3]) <= 1e-13 * g[3]
+    assert abs(s.divergence_max - g[4]) <= 1e-12 * max(g[4], 1e-300) + 1e-15
+    assert np.allclose(s.spectrum, g[5:], rtol=1e-12, atol=1e-300)
+
+
+def test_stats_deterministic_bitwise():
+    n = 32
+    lo = S.build_layout(S.SolverConfig(n=n), 0)
+    uh = S.iso_init(n, lo)
+    with ctx_for(n) as c:
+        u = c.spectral_field().upload(uh)
+        a = S.collect_stats(c, u, 1e-3)
+        b = S.collect_stats(c, u, 1e-3)
+    assert a.energy == b.energy and a.enstrophy == b.enstrophy
+    assert np.array_equal(a.spectrum, b.spectrum)
+
+
+# --- advance semantics and errors ------------------------------------------------
+
+def test_advance_schedule_and_shortened_last_step():
+    """rk4.cpp:86-107: t_end = 0.1, dt = 0.03 -> 4 steps, last dt = 0.01."""
+    n = 8
+    cfg = S.SolverConfig(n=n, nu=0.01, dt=0.03, t_end=0.1, out_every=2)
+    with S.Context(cfg) as c:
+        u = c.spectral_field().upload(GOLD["pw8_uh"] * 1e-3)
+        S.project(c, u)
+        st = S.Rk4State(c)
+        st.set(u)
+        seen = []
+        st.advance(lambda k, t: seen.append((k, t)))
+        assert seen == [(0, 0.0), (2, 0.06), (4, 0.1)]
+        assert st.t == 0.1 and st.step == 4
+        st.close()
+
+
+def test_divergence_error_on_nonfinite():
+    n = 8
+    cfg = S.SolverConfig(n=n, nu=0.01, dt=0.01, t_end=0.02)
+    with S.Context(cfg) as c:
+        uh = GOLD["pw8_uh"].copy()
+        uh[0, 1, 1, 1] = np.nan
+        st = S.Rk4State(c)
+        st.set(c.spectral_field().upload(uh))
+        with pytest.raises(S.DivergenceError) as ei:
+            st.advance()
+        assert ei.value.step == 1
+        st.close()
+
+
+def test_config_errors():
+    with pytest.raises(S.ConfigError):
+        S.Context(S.SolverConfig(n=12))  # not a power of two on the GPU path
+    with pytest.raises(S.ConfigError):
+        S.Context(S.SolverConfig(n=7))
+    with ctx_for(8) as c:
+        u = c.spectral_field()
+        with pytest.raises(S.ConfigError):
+            S.compute_rhs(c, u, 0.01, u)
+
+
+# --- multi-rank decomposition on one GPU (threads-as-ranks) ------------------------
+
+def _scatter_spec(g, lo):
+    (s0, s1, s2), (o0, o1, o2) = lo.spec_shape, lo.spec_offset
+    return g[:, o0:o0 + s0, o1:o1 + s1, o2:o2 + s2]
+
+
+def _scatter_real(g, lo):
+    (s0, s1, s2), (o0, o1, o2) = lo.real_shape, lo.real_offset
+    return g[:, o0:o0 + s0, o1:o1 + s1, o2:o2 + s2]
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_inprocess_slab_fft_matches_single_rank(p):
+    n = 32
+    rng = np.random.default_rng(3)
+    u = rng.uniform(-1, 1, (3, n, n, n))
+    expect = O.forward(u)
+    cfg = S.SolverConfig(n=n, p=p)
+
+    def body(rank, comm):
+        with S.Context(cfg, rank=rank, comm=comm) as c:
+            fft = S.DistributedFFT(c)
+            lo = c.layout
+            ud = c.real_field().upload(_scatter_real(u, lo))
+            fd = c.spectral_field()
+            fft.forward(ud, fd)
+            back = c.real_field()
+            fft.inverse(fd, back)
+            return lo, fd.download(), back.download()
+
+    out = S.run_group(p, body)
+    for lo, fu, back in out:
+        e = _scatter_spec(expect, lo)
+        assert np.abs(fu - e).max() <= 1e-11 * np.abs(expect).max()
+        assert rel(back, _scatter_real(u, lo)) <= 1e-13
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_inprocess_slab_rk4_matches_single_rank(p):
+    n = 32
+    lo1 = S.build_layout(S.SolverConfig(n=n), 0)
+    uh0 = S.iso_init(n, lo1)
+    _, f1 = run_gpu(n, uh0, 1e-3, 1e-3, 5, project_init=False)
+    cfg = S.SolverConfig(n=n, p=p, nu=1e-3, dt=1e-3, t_end=5e-3, out_every=1)
+
+    def body(rank, comm):
+        with S.Context(cfg, rank=rank, comm=comm) as c:
+            lo = c.layout
+            uh = S.iso_init(n, lo)
+            assert np.array_equal(uh, _scatter_spec(uh0, lo))
+            st = S.Rk4State(c)
+            st.set(c.spectral_field().upload(uh))
+            rows = []
+            st.advance(lambda k, t: rows.append(S.collect_stats(c, st.u_hat, 1e-3, t)))
+            out = (lo, st.u_hat.download(), rows)
+            st.close()
+            return out
+
+    res = S.run_group(p, body)
+    for lo, f, rows in res:
+        assert rel(f, _scatter_spec(f1, lo)) <= 1e-12
+    for r in range(1, p):
+        for a, b in zip(res[0][2], res[r][2]):
+            assert a.energy == b.energy and a.enstrophy == b.enstrophy
