@@ -187,13 +187,14 @@ enum {
   SDNS_PASS_Y_INV = 1,      /* P2 */
   SDNS_PASS_Z_FUSED = 2,    /* P3 */
   SDNS_PASS_Y_FWD = 3,      /* P4 */
-  SDNS_PASS_X_FWD_TAIL = 4, /* P5, compute_rhs tail */
-  SDNS_PASS_X_FWD_RK0 = 5,  /* P5, RK4 stage 0 */
-  SDNS_PASS_X_FWD_RK12 = 6, /* P5, RK4 stages 1-2 */
-  SDNS_PASS_X_FWD_RK3 = 7,  /* P5, RK4 stage 3 + projection */
+  SDNS_PASS_X_FWD_TAIL = 4, /* P5b, compute_rhs tail */
+  SDNS_PASS_X_FWD_RK0 = 5,  /* P5b, RK4 stage 0 */
+  SDNS_PASS_X_FWD_RK12 = 6, /* P5b, RK4 stages 1-2 */
+  SDNS_PASS_X_FWD_RK3 = 7,  /* P5b, RK4 stage 3 + projection */
   SDNS_PASS_A2A_INV = 8,
   SDNS_PASS_A2A_FWD = 9,
-  SDNS_NPASS = 10
+  SDNS_PASS_X_FWD_FFT = 10, /* P5a, x-axis forward FFT of the nonlinear term */
+  SDNS_NPASS = 11
 };
 /* Enables (and resets) event timing of every pipeline launch. */
 int sdns_ctx_timing(sdns_ctx* ctx, int enable);

@@ -29,7 +29,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsdns_cuda.so")
+LIB_PATH = os.environ.get("SDNS_LIB", os.path.join(_HERE, "libsdns_cuda.so"))
 
 
 # --- errors (proj/core/include/sdns/types.hpp:28-62) ------------------------
@@ -94,7 +94,7 @@ class _Layout(ctypes.Structure):
 
 
 PASS_NAMES = ["x_inv_curl", "y_inv", "z_fused", "y_fwd", "x_fwd_tail", "x_fwd_rk0",
-              "x_fwd_rk12", "x_fwd_rk3", "a2a_inv", "a2a_fwd"]
+              "x_fwd_rk12", "x_fwd_rk3", "a2a_inv", "a2a_fwd", "x_fwd_fft"]
 NPASS = len(PASS_NAMES)
 
 SAMPLE_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p)

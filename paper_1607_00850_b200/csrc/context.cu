@@ -71,6 +71,7 @@ struct sdns_ctx {
   double2* wa = nullptr;
   double2* wb = nullptr;
   long long spec_cs = 0;   // complex elements per spectral component (padded)
+  int prow = 0;            // rows per x plane incl. one pad row (s1 + 1)
   long long real_cs = 0;   // doubles per real component
   int pitch = 0;
   int np = 0;              // slab block (n / p)
@@ -112,14 +113,16 @@ struct sdns_ctx {
     g.o1 = static_cast<int>(lo.spec_offset[1]);
     g.o2 = static_cast<int>(lo.spec_offset[2]);
     g.pitch = pitch;
+    g.prow = prow;
     g.cs = spec_cs;
     return g;
   }
+  long long plane() const { return static_cast<long long>(prow) * pitch; }
   // x pass over the x layout: rows = local y, positions = x (full axis)
   ColGeom xgeom() const {
     ColGeom g;
     g.rs = pitch;
-    g.ps0 = static_cast<long long>(np) * pitch;
+    g.ps0 = plane();
     g.ps1 = 0;
     g.pb_shift = 30;
     g.nrows = np;
@@ -138,29 +141,79 @@ struct sdns_ctx {
   // y pass over the receive layout: rows = local x, positions = y
   ColGeom ygeom() const {
     ColGeom g;
-    g.rs = static_cast<long long>(np) * pitch;
+    g.rs = plane();
     g.ps0 = pitch;
-    g.ps1 = static_cast<long long>(np) * np * pitch;
+    g.ps1 = np * plane();
     g.pb_shift = ilog2(np);
     g.nrows = np;
     g.n2 = static_cast<int>(lo.spec_shape[2]);
     g.pitch = pitch;
     return g;
   }
+  // Largest kept |k| of the 2/3 rule: |k| < n/3  <=>  |k| <= (n-1)/3
+  // (dealias_mask, mesh.cpp:74-89).
+  int keep_k() const { return (cfg.n - 1) / 3; }
+  // Forward y pass: only kz < n/3 columns, only |ky| < n/3 outputs stored.
+  ColGeom ygeom_fwd() const {
+    ColGeom g = ygeom();
+    if (!cfg.dealias) return g;
+    const int K = keep_k();
+    const int kzk = std::max(0, std::min(g.n2, K + 1 - static_cast<int>(lo.spec_offset[2])));
+    g.n2 = kzk;
+    g.pitch = std::max(8, (kzk + 7) / 8 * 8);
+    g.keep_k = K;
+    return g;
+  }
+  // Forward x pass: only (ky, kz) columns inside the 2/3 band, only |kx| < n/3
+  // outputs stored. Local y rows form up to two kept bands.
+  ColGeom xgeom_fwd() const {
+    ColGeom g = xgeom();
+    if (!cfg.dealias) return g;
+    const int K = keep_k(), n = cfg.n;
+    const int kzk = std::max(0, std::min(g.n2, K + 1 - static_cast<int>(lo.spec_offset[2])));
+    g.n2 = kzk;
+    g.pitch = std::max(8, (kzk + 7) / 8 * 8);
+    g.keep_k = K;
+    const int o1 = static_cast<int>(lo.spec_offset[1]), e1 = o1 + np;  // [o1, e1)
+    const int a0 = std::max(o1, 0), a1 = std::min(e1, K + 1);             // [0, K]
+    const int b0 = std::max(o1, n - K), b1 = std::min(e1, n);             // [n-K, n)
+    const int na = std::max(0, a1 - a0), nb = std::max(0, b1 - b0);
+    g.nrows = na + nb;
+    g.seg_a = na;
+    g.off0 = a0 - o1;
+    g.off1 = b0 - o1;
+    return g;
+  }
   RowMap zmap(bool by_xy) const {
     RowMap r;
     r.nrows = np * cfg.n;
+    r.rpp = np;
     r.ny = cfg.n;
-    r.blk = (by_xy && cfg.p > 1) ? np : 0;
+    r.blk = by_xy ? np : 0;
+    r.prow = prow;
     r.pitch = pitch;
     r.n2 = static_cast<int>(lo.nf);
     return r;
+  }
+  // Host block (s0, s1, s2) <-> device planes (s0, prow, pitch) copy.
+  void copy_spec(void* dst, const void* src, bool to_device) const {
+    cudaMemcpy3DParms p{};
+    const size_t s2b = sizeof(double2) * static_cast<size_t>(lo.spec_shape[2]);
+    const size_t s1 = static_cast<size_t>(lo.spec_shape[1]);
+    cudaPitchedPtr host = make_cudaPitchedPtr(const_cast<void*>(to_device ? src : dst), s2b, s2b, s1);
+    cudaPitchedPtr dev = make_cudaPitchedPtr(const_cast<void*>(to_device ? dst : src),
+                                             sizeof(double2) * pitch, s2b, prow);
+    p.srcPtr = to_device ? host : dev;
+    p.dstPtr = to_device ? dev : host;
+    p.extent = make_cudaExtent(s2b, s1, static_cast<size_t>(lo.spec_shape[0]));
+    p.kind = to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    SDNS_CUDA(cudaMemcpy3DAsync(&p, stream));
   }
   // transpose between wa (x layout) and wb (receive layout)
   void exchange(bool inverse_dir, int nfields) {
     if (cfg.p == 1) return;
     const int tk = tick(inverse_dir ? SDNS_PASS_A2A_INV : SDNS_PASS_A2A_FWD);
-    const long long blk = static_cast<long long>(np) * np * pitch;
+    const long long blk = np * plane();
     std::vector<Xfer> xs;
     xs.reserve(static_cast<size_t>(nfields) * cfg.p);
     for (int f = 0; f < nfields; ++f)
@@ -221,17 +274,22 @@ void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args
   const int n = c->cfg.n;
   cudaStream_t s = c->stream;
   int tk = c->tick(SDNS_PASS_X_INV_CURL);
-  sdns_dev::x_inverse_curl(n, u_in, c->spec_cs, c->wa, c->spec_cs, c->xgeom(), c->xwave(), c->tw, s);
+  sdns_dev::x_inverse_split(n, u_in, c->spec_cs, c->wa, c->spec_cs, c->xgeom(), c->tw, s);
   c->tock(tk);
-  c->exchange(true, 6);
+  c->exchange(true, 5);
   tk = c->tick(SDNS_PASS_Y_INV);
-  sdns_dev::col_plain(n, +1, c->wb, c->wb, c->spec_cs, c->spec_cs, 6, c->ygeom(), c->tw, s);
+  sdns_dev::y_inverse_curl(n, c->wb, c->spec_cs, c->ygeom(), c->tw, s);
   c->tock(tk);
+  // Forward direction: with the 2/3 rule on, modes the mask zeroes are never
+  // computed or stored (kept modes are computed by identical transforms).
+  RowMap zm = c->zmap(false);
+  if (c->cfg.dealias) zm.kz_keep = c->keep_k() + 1;
   tk = c->tick(SDNS_PASS_Z_FUSED);
-  sdns_dev::z_fused(n, c->wb, c->spec_cs, c->zmap(false), c->norm, c->tw, s);
+  sdns_dev::z_fused(n, c->wb, c->spec_cs, zm, c->norm, c->tw, s);
   c->tock(tk);
   tk = c->tick(SDNS_PASS_Y_FWD);
-  sdns_dev::col_plain(n, -1, c->wb, c->wb, c->spec_cs, c->spec_cs, 3, c->ygeom(), c->tw, s);
+  sdns_dev::col_plain(n, -1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, 3, c->ygeom_fwd(),
+                      c->tw, s);
   c->tock(tk);
   c->exchange(false, 3);
   XfArgs a = args_in;
@@ -239,8 +297,12 @@ void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args
   a.nl_cs = c->spec_cs;
   a.cs = c->spec_cs;
   a.dealias = c->cfg.dealias;
+  tk = c->tick(SDNS_PASS_X_FWD_FFT);
+  sdns_dev::col_plain(n, -1, true, c->wa, c->wa, c->spec_cs, c->spec_cs, 3, c->xgeom_fwd(),
+                      c->tw, s);
+  c->tock(tk);
   tk = c->tick(SDNS_PASS_X_FWD_TAIL + mode);
-  sdns_dev::x_forward_fused(n, mode, a, c->xgeom(), c->xwave(), c->tw, s);
+  sdns_dev::rk_update(mode, a, c->sgeom(), s);
   c->tock(tk);
   post_launch("rhs pipeline");
 }
@@ -251,9 +313,10 @@ void fft_forward_impl(sdns_ctx* c, const sdns_field* real, sdns_field* spec) {
   const int nc = std::min(real->ncomp, spec->ncomp);
   for (int f = 0; f < nc; ++f)
     sdns_dev::z_r2c(n, real->real() + f * c->real_cs, c->wb + f * c->spec_cs, c->zmap(true), c->tw, s);
-  sdns_dev::col_plain(n, -1, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw, s);
+  sdns_dev::col_plain(n, -1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw, s);
   c->exchange(false, nc);
-  sdns_dev::col_plain(n, -1, c->wa, spec->spec(), c->spec_cs, c->spec_cs, nc, c->xgeom(), c->tw, s);
+  sdns_dev::col_plain(n, -1, true, c->wa, spec->spec(), c->spec_cs, c->spec_cs, nc, c->xgeom(),
+                      c->tw, s);
   post_launch("fft forward");
 }
 
@@ -261,9 +324,10 @@ void fft_inverse_impl(sdns_ctx* c, const sdns_field* spec, sdns_field* real) {
   const int n = c->cfg.n;
   cudaStream_t s = c->stream;
   const int nc = std::min(real->ncomp, spec->ncomp);
-  sdns_dev::col_plain(n, +1, spec->spec(), c->wa, c->spec_cs, c->spec_cs, nc, c->xgeom(), c->tw, s);
+  sdns_dev::col_plain(n, +1, true, spec->spec(), c->wa, c->spec_cs, c->spec_cs, nc, c->xgeom(),
+                      c->tw, s);
   c->exchange(true, nc);
-  sdns_dev::col_plain(n, +1, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw, s);
+  sdns_dev::col_plain(n, +1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw, s);
   for (int f = 0; f < nc; ++f)
     sdns_dev::z_c2r(n, c->wb + f * c->spec_cs, real->real() + f * c->real_cs, c->zmap(true), c->norm,
                     c->tw, s);
@@ -433,7 +497,8 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
     const long long n = cfg->n;
     c->np = static_cast<int>(n / cfg->p);
     c->pitch = static_cast<int>((c->lo.spec_shape[2] + 7) / 8 * 8);
-    c->spec_cs = c->lo.spec_shape[0] * c->lo.spec_shape[1] * c->pitch;
+    c->prow = static_cast<int>(c->lo.spec_shape[1]) + 1;
+    c->spec_cs = c->lo.spec_shape[0] * c->prow * c->pitch;
     c->real_cs = c->lo.real_shape[0] * c->lo.real_shape[1] * c->lo.real_shape[2];
     c->norm = 1.0 / (static_cast<double>(n) * static_cast<double>(n) * static_cast<double>(n));
     c->shells = spectrum_shells(n);
@@ -524,9 +589,7 @@ int sdns_field_upload(sdns_ctx* c, sdns_field* f, const double* host) {
       const size_t s2 = static_cast<size_t>(c->lo.spec_shape[2]);
       const size_t rows = static_cast<size_t>(c->lo.spec_shape[0] * c->lo.spec_shape[1]);
       for (int q = 0; q < f->ncomp; ++q)
-        SDNS_CUDA(cudaMemcpy2DAsync(f->spec() + q * c->spec_cs, sizeof(double2) * c->pitch,
-                                    host + 2 * q * s2 * rows, sizeof(double2) * s2,
-                                    sizeof(double2) * s2, rows, cudaMemcpyHostToDevice, c->stream));
+        c->copy_spec(f->spec() + q * c->spec_cs, host + 2 * q * s2 * rows, true);
     }
     SDNS_CUDA(cudaStreamSynchronize(c->stream));
   });
@@ -542,9 +605,7 @@ int sdns_field_download(sdns_ctx* c, const sdns_field* f, double* host) {
       const size_t s2 = static_cast<size_t>(c->lo.spec_shape[2]);
       const size_t rows = static_cast<size_t>(c->lo.spec_shape[0] * c->lo.spec_shape[1]);
       for (int q = 0; q < f->ncomp; ++q)
-        SDNS_CUDA(cudaMemcpy2DAsync(host + 2 * q * s2 * rows, sizeof(double2) * s2,
-                                    f->spec() + q * c->spec_cs, sizeof(double2) * c->pitch,
-                                    sizeof(double2) * s2, rows, cudaMemcpyDeviceToHost, c->stream));
+        c->copy_spec(host + 2 * q * s2 * rows, f->spec() + q * c->spec_cs, false);
     }
     SDNS_CUDA(cudaStreamSynchronize(c->stream));
   });
@@ -730,14 +791,10 @@ int sdns_rk4_step_host(sdns_ctx* c, sdns_state* st, double* host, double dt, int
     const size_t s2 = static_cast<size_t>(c->lo.spec_shape[2]);
     const size_t rows = static_cast<size_t>(c->lo.spec_shape[0] * c->lo.spec_shape[1]);
     for (int q = 0; q < 3; ++q)
-      SDNS_CUDA(cudaMemcpy2DAsync(st->u.spec() + q * c->spec_cs, sizeof(double2) * c->pitch,
-                                  host + 2 * q * s2 * rows, sizeof(double2) * s2,
-                                  sizeof(double2) * s2, rows, cudaMemcpyHostToDevice, c->stream));
+      c->copy_spec(st->u.spec() + q * c->spec_cs, host + 2 * q * s2 * rows, true);
     for (int k = 0; k < steps; ++k) step_impl(c, st, dt, 1, false);
     for (int q = 0; q < 3; ++q)
-      SDNS_CUDA(cudaMemcpy2DAsync(host + 2 * q * s2 * rows, sizeof(double2) * s2,
-                                  st->u.spec() + q * c->spec_cs, sizeof(double2) * c->pitch,
-                                  sizeof(double2) * s2, rows, cudaMemcpyDeviceToHost, c->stream));
+      c->copy_spec(host + 2 * q * s2 * rows, st->u.spec() + q * c->spec_cs, false);
     SDNS_CUDA(cudaStreamSynchronize(c->stream));
   });
 }

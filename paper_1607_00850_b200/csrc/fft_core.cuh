@@ -10,8 +10,8 @@
 //   j + r*N/R, twiddles by W_{NS*R}^{(j mod NS)*r}, and writes
 //   (j/NS)*NS*R + (j mod NS) + r*NS.
 // Radices are E (8 or 16) until the remainder, which is a smaller power of
-// two. Twiddles come from a per-length table tw[q] = exp(-2*pi*i*q/N) in
-// global memory (L1-resident), conjugated for the inverse direction.
+// two. Twiddles come from a per-length table tw[q] = exp(-2*pi*i*q/N) that
+// each CTA copies to shared memory once, conjugated for the inverse.
 // Unnormalised in both directions (FFTW convention, SerialFFT,
 // proj/core/include/sdns/serial_fft.hpp:13-14).
 #pragma once
@@ -35,7 +35,8 @@ __device__ __forceinline__ double2 mul_si(double2 a) {
 
 template <int S>
 __device__ __forceinline__ double2 twiddle(const double2* __restrict__ tw, int q) {
-  const double2 w = __ldg(tw + q);
+  // tw is the shared-memory copy of the table (LDS, no LSU global traffic)
+  const double2 w = tw[q];
   return S < 0 ? w : make_double2(w.x, -w.y);
 }
 
@@ -179,6 +180,11 @@ template <int N, int S, class IDX>
 __device__ __forceinline__ void block_fft(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
                                           const double2* __restrict__ tw) {
   fft_stages<N, fft_elems(N), S, 1>(v, sm, idx, t, tw);
+}
+
+// Copies the n-entry twiddle table to shared memory (caller syncs).
+__device__ __forceinline__ void load_twiddles(double2* dst, const double2* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
 }
 
 }  // namespace sdns_dev

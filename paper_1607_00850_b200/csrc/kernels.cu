@@ -3,10 +3,12 @@
 // Pass structure of one RHS evaluation (reference
 // compute_rhs, proj/core/src/navier_stokes.cpp:104-139, and DistributedFFT,
 // proj/core/src/fft.cpp:81-126):
-//   P1 k_x_inv_curl   x-axis inverse c2c of u_hat and of omega_hat = i k x u_hat
-//   P2 k_col_plain    y-axis inverse c2c of the 6 fields (in place)
-//   P3 k_z_fused      z-axis c2r of the 6 fields, 1/n^3, u x omega, z r2c of 3
-//   P4 k_col_plain    y-axis forward c2c of the 3 fields (in place)
+//   P1 k_pipe_xinv    x-axis inverse c2c of u_hat (+ kx u_hat for the curl)
+//   P2 k_pipe_yinv    y-axis inverse c2c, completing the x/y parts of the curl
+//   P3 k_z_fused      z-axis c2r of the 6 fields (+ the kz part of the curl),
+//                     1/n^3, u x omega, z r2c of 3
+//   P4 k_pipe_plain   y-axis forward c2c of the 3 fields (in place)
+// (P1, P2, P4 live in kernels_col.cu.)
 //   P5 k_x_fwd_fused  x-axis forward c2c + dealias + projection + viscous term
 //                     + RK4 stage update (+ Neumaier carry, projection, finite)
 // Pointwise parts follow the reference operation order with explicit
@@ -50,8 +52,7 @@ struct ColCfg {
   static constexpr int E = fft_elems(N);
   static constexpr int TPC = N / E;
   // columns per CTA: fill ~256-512 threads, 8-column (128 B) tiles at least
-  static constexpr int CS = TPC >= 64 ? 8 : (256 / TPC < 8 ? 8 : 256 / TPC);
-  static constexpr int THREADS = TPC * CS;
+  static constexpr int CS = TPC >= 64 ? 4 : (256 / TPC < 8 ? 8 : 256 / TPC);
   // fused forward x-pass keeps 3 components in shared memory
   static constexpr int CSF = N >= 512 ? 4 : (CS > 16 ? 16 : CS);
   static constexpr int THREADSF = TPC * CSF;
@@ -76,84 +77,6 @@ void make_twiddles(int n, double2* d_tw, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// Plain column transforms (x or y axis), nfields fields, in -> out (may alias)
-
-template <int N, int S>
-__global__ void __launch_bounds__(ColCfg<N>::THREADS)
-k_col_plain(const double2* in, double2* out, long long in_cs, long long out_cs, int nfields,
-            ColGeom g, const double2* __restrict__ tw) {
-  constexpr int E = ColCfg<N>::E, TPC = ColCfg<N>::TPC, CS = ColCfg<N>::CS;
-  extern __shared__ double2 smem[];
-  const int col = threadIdx.x % CS, t = threadIdx.x / CS;
-  const long long gc = static_cast<long long>(blockIdx.x) * CS + col;
-  const int row = static_cast<int>(gc / g.pitch), kz = static_cast<int>(gc % g.pitch);
-  const bool valid = row < g.nrows && kz < g.n2;
-#pragma unroll 1
-  for (int f = 0; f < nfields; ++f) {
-    double2 v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m)
-      v[m] = valid ? in[f * in_cs + col_off(g, row, t + m * TPC, kz)] : make_double2(0.0, 0.0);
-    block_fft<N, S>(v, smem + col, ColIdx{CS}, t, tw);
-    if (valid) {
-#pragma unroll
-      for (int m = 0; m < E; ++m) out[f * out_cs + col_off(g, row, t + m * TPC, kz)] = v[m];
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// P1: x-axis inverse transform of u_hat and of omega_hat = i k x u_hat.
-// Outputs 0..2 = u, 3..5 = omega (curl_hat, navier_stokes.cpp:52-72). The
-// curl needs kx, which is only known before this transform, so omega is
-// formed in the prologue; inputs are re-read per output (L2 hits).
-
-template <int N>
-__global__ void __launch_bounds__(ColCfg<N>::THREADS)
-k_x_inv_curl(const double2* __restrict__ u, long long u_cs, double2* __restrict__ out,
-             long long out_cs, ColGeom g, WaveGeom w, const double2* __restrict__ tw) {
-  constexpr int E = ColCfg<N>::E, TPC = ColCfg<N>::TPC, CS = ColCfg<N>::CS;
-  extern __shared__ double2 smem[];
-  const int col = threadIdx.x % CS, t = threadIdx.x / CS;
-  const long long gc = static_cast<long long>(blockIdx.x) * CS + col;
-  const int row = static_cast<int>(gc / g.pitch), kz = static_cast<int>(gc % g.pitch);
-  const bool valid = row < g.nrows && kz < g.n2;
-  const double ky = wavenum(w.row_off + row, N);
-  const double kzd = static_cast<double>(w.kz_off + kz);
-  const double2* u0 = u;
-  const double2* u1 = u + u_cs;
-  const double2* u2 = u + 2 * u_cs;
-  const double2 z = make_double2(0.0, 0.0);
-#pragma unroll 1
-  for (int o = 0; o < 6; ++o) {
-    double2 v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-      const int pos = t + m * TPC;
-      const long long off = col_off(g, row, pos, kz);
-      const double kx = wavenum(pos, N);
-      double2 r = z;
-      if (valid) {
-        switch (o) {
-          case 0: r = u0[off]; break;
-          case 1: r = u1[off]; break;
-          case 2: r = u2[off]; break;
-          case 3: r = i_cross(ky, u2[off], kzd, u1[off]); break;
-          case 4: r = i_cross(kzd, u0[off], kx, u2[off]); break;
-          default: r = i_cross(kx, u1[off], ky, u0[off]); break;
-        }
-      }
-      v[m] = r;
-    }
-    block_fft<N, +1>(v, smem + col, ColIdx{CS}, t, tw);
-    if (valid) {
-#pragma unroll
-      for (int m = 0; m < E; ++m) out[o * out_cs + col_off(g, row, t + m * TPC, kz)] = v[m];
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // P5: x-axis forward transform of the 3 nonlinear components, then per mode
 // the compute_rhs tail (navier_stokes.cpp:114-138) and the RK4 stage update
 // (rk4.cpp:44-65), the post-step projection (runner.cpp:107) and the finite
@@ -164,51 +87,48 @@ __device__ __forceinline__ double two_sum_err(double a, double b, double s) {
   return fabs(a) >= fabs(b) ? dadd(dsub(a, s), b) : dadd(dsub(b, s), a);
 }
 
-template <int N, int MODE>
-__global__ void __launch_bounds__(ColCfg<N>::THREADSF)
-k_x_fwd_fused(XfArgs a, ColGeom g, WaveGeom w, const double2* __restrict__ tw) {
-  constexpr int E = ColCfg<N>::E, TPC = ColCfg<N>::TPC, CS = ColCfg<N>::CSF;
-  extern __shared__ double2 smem[];
-  const int col = threadIdx.x % CS, t = threadIdx.x / CS;
-  const long long gc = static_cast<long long>(blockIdx.x) * CS + col;
-  const int row = static_cast<int>(gc / g.pitch), kz = static_cast<int>(gc % g.pitch);
-  const bool valid = row < g.nrows && kz < g.n2;
-  double2 v[E];
-#pragma unroll 1
-  for (int c = 0; c < 3; ++c) {
-    double2* reg = smem + c * N * CS + col;
-#pragma unroll
-    for (int m = 0; m < E; ++m)
-      v[m] = valid ? a.nl[c * a.nl_cs + col_off(g, row, t + m * TPC, kz)]
-                   : make_double2(0.0, 0.0);
-    block_fft<N, -1>(v, reg, ColIdx{CS}, t, tw);
-    if (c < 2) {
-#pragma unroll
-      for (int m = 0; m < E; ++m) reg[(t + m * TPC) * CS] = v[m];
-    }
-  }
-  if (!valid) return;
-  const double ky = wavenum(w.row_off + row, N);
-  const double kzd = static_cast<double>(w.kz_off + kz);
-  const double kmax = static_cast<double>(N) / 3.0;
-  const bool keep_yz = fabs(ky) < kmax && fabs(kzd) < kmax;
+// P5b: the per-mode tail as a streaming kernel over the x layout, after the
+// x-axis forward FFT of the nonlinear term has run in place (P5a,
+// k_pipe_plain): dealias mask, projection, viscous term and the RK4 stage
+// update (+ Neumaier carry, post-step projection, finite flag). Bitwise the
+// reference operation order.
+template <int MODE>
+__global__ void __launch_bounds__(256)
+k_rk_update(XfArgs a, SpecGeom g) {
+  const long long total = static_cast<long long>(g.s0) * g.prow * g.pitch;
+  const double kmax = static_cast<double>(g.n) / 3.0;
   bool finite = true;
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long row = e / g.pitch;
+    const int k = static_cast<int>(e - row * g.pitch);
+    const int j = static_cast<int>(row % g.prow);
+    const int i = static_cast<int>(row / g.prow);
+    if (k >= g.s2 || j >= g.s1) continue;
+    const double kx = wavenum(g.o0 + i, g.n), ky = wavenum(g.o1 + j, g.n);
+    const double kzd = static_cast<double>(g.o2 + k);
+    // dealias mask (navier_stokes.cpp:123-125): masked modes of the nonlinear
+    // term are zero and were never computed by the pruned forward passes
+    const bool keep = !a.dealias || (fabs(kx) < kmax && fabs(ky) < kmax && fabs(kzd) < kmax);
+    double2 c0 = make_double2(0.0, 0.0), c1 = c0, c2 = c0;
+    if (keep) {
+      c0 = a.nl[e];
+      c1 = a.nl[a.nl_cs + e];
+      c2 = a.nl[2 * a.nl_cs + e];
+    }
+    double2 uq[3], bq[3], sq[3], cr[3];
 #pragma unroll
-  for (int m = 0; m < E; ++m) {
-    const int pos = t + m * TPC;
-    const double kx = wavenum(pos, N);
-    const long long off = col_off(g, row, pos, kz);
-    double2 c0 = smem[(pos)*CS + col];
-    double2 c1 = smem[N * CS + pos * CS + col];
-    double2 c2 = v[m];
-    if (a.dealias && !(fabs(kx) < kmax && keep_yz)) {
-      c0 = c1 = c2 = make_double2(0.0, 0.0);
+    for (int q = 0; q < 3; ++q) {
+      uq[q] = a.u[q * a.cs + e];
+      if (MODE != XF_TAIL) bq[q] = a.base[q * a.cs + e];
+      if (MODE == XF_RK12 || MODE == XF_RK3) sq[q] = a.accum[q * a.cs + e];
+      if (MODE == XF_RK3) cr[q] = a.carry[q * a.cs + e];
     }
     // wavenumbers(), mesh.cpp:56-60
     const double k2 = dadd(dadd(dmul(kx, kx), dmul(ky, ky)), dmul(kzd, kzd));
     const double inv = k2 > 0.0 ? 1.0 / k2 : 0.0;
     const double kxk = dmul(kx, inv), kyk = dmul(ky, inv), kzk = dmul(kzd, inv);
-    // kd = kx c0 + ky c1 + kz c2; c -= (k/k^2) kd
+    // kd = kx c0 + ky c1 + kz c2; c -= (k/k^2) kd  (navier_stokes.cpp:128-133)
     const double kdr = dadd(dadd(dmul(kx, c0.x), dmul(ky, c1.x)), dmul(kzd, c2.x));
     const double kdi = dadd(dadd(dmul(kx, c0.y), dmul(ky, c1.y)), dmul(kzd, c2.y));
     c0 = make_double2(dsub(c0.x, dmul(kxk, kdr)), dsub(c0.y, dmul(kxk, kdi)));
@@ -218,38 +138,29 @@ k_x_fwd_fused(XfArgs a, ColGeom g, WaveGeom w, const double2* __restrict__ tw) {
     double2 du[3];
     const double2 cc[3] = {c0, c1, c2};
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const double2 uq = a.u[q * a.cs + off];
-      du[q] = make_double2(dsub(cc[q].x, dmul(visc, uq.x)), dsub(cc[q].y, dmul(visc, uq.y)));
-    }
+    for (int q = 0; q < 3; ++q)
+      du[q] = make_double2(dsub(cc[q].x, dmul(visc, uq[q].x)), dsub(cc[q].y, dmul(visc, uq[q].y)));
     if (MODE == XF_TAIL) {
 #pragma unroll
-      for (int q = 0; q < 3; ++q) a.out[q * a.cs + off] = du[q];
+      for (int q = 0; q < 3; ++q) a.out[q * a.cs + e] = du[q];
     } else if (MODE == XF_RK0 || MODE == XF_RK12) {
+      // rk4.cpp:47-50
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        const long long o = q * a.cs + off;
         double2 s = make_double2(dmul(a.w, du[q].x), dmul(a.w, du[q].y));
-        if (MODE == XF_RK12) {
-          const double2 s0 = a.accum[o];
-          s = make_double2(dadd(s0.x, s.x), dadd(s0.y, s.y));
-        }
-        a.accum[o] = s;
-        const double2 b = a.base[o];
-        a.out[o] = make_double2(dadd(b.x, dmul(a.bdt, du[q].x)), dadd(b.y, dmul(a.bdt, du[q].y)));
+        if (MODE == XF_RK12) s = make_double2(dadd(sq[q].x, s.x), dadd(sq[q].y, s.y));
+        a.accum[q * a.cs + e] = s;
+        a.out[q * a.cs + e] = make_double2(dadd(bq[q].x, dmul(a.bdt, du[q].x)),
+                                           dadd(bq[q].y, dmul(a.bdt, du[q].y)));
       }
-    } else {  // XF_RK3
+    } else {  // XF_RK3, rk4.cpp:55-64
       double2 un[3];
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        const long long o = q * a.cs + off;
-        const double2 s = a.accum[o];
-        const double2 cr = a.carry[o];
-        const double2 b = a.base[o];
-        const double dr = dadd(dmul(a.sixth, dadd(s.x, du[q].x)), cr.x);
-        const double di = dadd(dmul(a.sixth, dadd(s.y, du[q].y)), cr.y);
-        const double nr = dadd(b.x, dr), ni = dadd(b.y, di);
-        a.carry[o] = make_double2(two_sum_err(b.x, dr, nr), two_sum_err(b.y, di, ni));
+        const double dr = dadd(dmul(a.sixth, dadd(sq[q].x, du[q].x)), cr[q].x);
+        const double di = dadd(dmul(a.sixth, dadd(sq[q].y, du[q].y)), cr[q].y);
+        const double nr = dadd(bq[q].x, dr), ni = dadd(bq[q].y, di);
+        a.carry[q * a.cs + e] = make_double2(two_sum_err(bq[q].x, dr, nr), two_sum_err(bq[q].y, di, ni));
         un[q] = make_double2(nr, ni);
         finite = finite && isfinite(nr) && isfinite(ni);
       }
@@ -262,7 +173,7 @@ k_x_fwd_fused(XfArgs a, ColGeom g, WaveGeom w, const double2* __restrict__ tw) {
         un[2] = make_double2(dsub(un[2].x, dmul(kzk, pr)), dsub(un[2].y, dmul(kzk, pi)));
       }
 #pragma unroll
-      for (int q = 0; q < 3; ++q) a.base_out[q * a.cs + off] = un[q];
+      for (int q = 0; q < 3; ++q) a.base_out[q * a.cs + e] = un[q];
     }
   }
   if (MODE == XF_RK3 && !finite) atomicAnd(a.finite, 0);
@@ -281,15 +192,19 @@ template <int N>
 struct ZCfg {
   static constexpr int E = fft_elems(N);
   static constexpr int TPC = N / E;
-  static constexpr int RPC = TPC >= 128 ? 1 : (TPC >= 32 ? 128 / TPC : 128 / TPC);
+  static constexpr int RPC = TPC >= 128 ? 1 : (128 / TPC > 32 ? 32 : 128 / TPC);
   static constexpr int THREADS = TPC * RPC;
+  static constexpr int HP = N / 2 + 8;  // padded half-row (n/2+1 modes)
 };
 
 __device__ __forceinline__ long long zrow_off(const RowMap& rm, int ri) {
-  if (rm.blk == 0) return static_cast<long long>(ri) * rm.pitch;
+  if (rm.blk == 0) {
+    const int pl = ri / rm.rpp, r = ri - pl * rm.rpp;
+    return (static_cast<long long>(pl) * rm.prow + r) * rm.pitch;
+  }
   const int xl = ri / rm.ny, y = ri - xl * rm.ny;
   const int q = y / rm.blk, yl = y - q * rm.blk;
-  return (static_cast<long long>(q * rm.blk + xl) * rm.blk + yl) * rm.pitch;
+  return (static_cast<long long>(q * rm.blk + xl) * rm.prow + yl) * rm.pitch;
 }
 
 // Full-length spectrum sample at position pos of A + iB from half spectra.
@@ -311,7 +226,7 @@ __device__ __forceinline__ double2 pair_sample(const double2* A, const double2* 
 }
 
 template <int N>
-__global__ void __launch_bounds__(ZCfg<N>::THREADS)
+__global__ void __launch_bounds__(ZCfg<N>::THREADS, 4)
 k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __restrict__ tw) {
   constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC;
   extern __shared__ double2 smem[];
@@ -319,25 +234,51 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   const int ri = blockIdx.x * ZCfg<N>::RPC + r;
   const bool valid = ri < rm.nrows;
   const long long ro = valid ? zrow_off(rm, ri) : 0;
-  double2* reg = smem + r * 3 * N;
+  // Stage the 6 half-rows once (coalesced, each element read once); the
+  // staging area of pair p (2 half-rows, 2*HP >= n entries) then serves as
+  // that pair's FFT exchange buffer and result store.
+  constexpr int HP = ZCfg<N>::HP;
+  double2* S = smem + r * 6 * HP;
+  double2* tws = smem + ZCfg<N>::RPC * 6 * HP;
+  load_twiddles(tws, tw, N);
   const SwzIdx sw;
+  if (valid) {
+    // fields: 0..2 = u, 3 = w0', 4 = w1', 5 = w2. The z part of the curl:
+    // w0 = w0' - i kz u1, w1 = w1' + i kz u0 (kz = global index on a full line)
+#pragma unroll
+    for (int k0 = 0; k0 <= N / 2; k0 += TPC) {
+      const int k = k0 + t;
+      if (k <= N / 2) {
+        const double kz = static_cast<double>(k);
+        const double2 u0 = f[ro + k], u1 = f[cs + ro + k], u2 = f[2 * cs + ro + k];
+        const double2 a = f[3 * cs + ro + k], b = f[4 * cs + ro + k], c = f[5 * cs + ro + k];
+        S[k] = u0;
+        S[HP + k] = u1;
+        S[2 * HP + k] = u2;
+        S[3 * HP + k] = make_double2(a.x + kz * u1.y, a.y - kz * u1.x);
+        S[4 * HP + k] = make_double2(b.x - kz * u0.y, b.y + kz * u0.x);
+        S[5 * HP + k] = c;
+      }
+    }
+  }
+  __syncthreads();
   double2 v[E];
 #pragma unroll 1
   for (int p = 0; p < 3; ++p) {
-    const double2* A = f + (2 * p) * cs + ro;
-    const double2* B = f + (2 * p + 1) * cs + ro;
+    double2* reg = S + 2 * p * HP;
 #pragma unroll
-    for (int m = 0; m < E; ++m)
-      v[m] = valid ? pair_sample<N>(A, B, t + m * TPC) : make_double2(0.0, 0.0);
-    block_fft<N, +1>(v, reg + p * N, sw, t, tw);
+    for (int m = 0; m < E; ++m) v[m] = pair_sample<N>(reg, reg + HP, t + m * TPC);
+    __syncthreads();
+    block_fft<N, +1>(v, reg, sw, t, tws);
 #pragma unroll
-    for (int m = 0; m < E; ++m) reg[p * N + sw(t + m * TPC)] = v[m];
+    for (int m = 0; m < E; ++m) reg[sw(t + m * TPC)] = v[m];
   }
+  double2* reg = S;  // pair 0 region (forward FFT of n0 + i n1)
   double n2r[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const int x = sw(t + m * TPC);
-    const double2 p0 = reg[x], p1 = reg[N + x], p2 = reg[2 * N + x];
+    const double2 p0 = S[x], p1 = S[2 * HP + x], p2 = S[4 * HP + x];
     const double ua = dmul(p0.x, norm), ub = dmul(p0.y, norm), uc = dmul(p1.x, norm);
     const double wa = dmul(p1.y, norm), wb = dmul(p2.x, norm), wc = dmul(p2.y, norm);
     const double n0 = dsub(dmul(ub, wc), dmul(uc, wb));
@@ -346,7 +287,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
     v[m] = make_double2(n0, n1);
   }
   __syncthreads();
-  block_fft<N, -1>(v, reg, sw, t, tw);
+  block_fft<N, -1>(v, reg, sw, t, tws);
 #pragma unroll
   for (int m = 0; m < E; ++m) reg[sw(t + m * TPC)] = v[m];
   __syncthreads();
@@ -356,7 +297,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
 #pragma unroll
     for (int m = 0; m < E; ++m) {
       const int k = t + m * TPC;
-      if (k <= N / 2) {
+      if (k <= N / 2 && k < rm.kz_keep) {  // kz >= n/3 is dealiased away
         const double2 d = reg[sw(k)];
         const double2 e = cconj(reg[sw((N - k) & (N - 1))]);
         o0[k] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
@@ -367,13 +308,13 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   }
 #pragma unroll
   for (int m = 0; m < E; ++m) v[m] = make_double2(n2r[m], 0.0);
-  block_fft<N, -1>(v, reg + N, sw, t, tw);
+  block_fft<N, -1>(v, S + 2 * HP, sw, t, tws);
   if (valid) {
     double2* o2 = f + 2 * cs + ro;
 #pragma unroll
     for (int m = 0; m < E; ++m) {
       const int k = t + m * TPC;
-      if (k <= N / 2) o2[k] = v[m];
+      if (k <= N / 2 && k < rm.kz_keep) o2[k] = v[m];
     }
   }
 }
@@ -400,7 +341,10 @@ k_z_c2r(const double2* __restrict__ spec, double* __restrict__ real, RowMap rm, 
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = make_double2(0.0, 0.0);
   }
-  block_fft<N, +1>(v, smem + r * N, SwzIdx{}, t, tw);
+  double2* tws = smem + ZCfg<N>::RPC * N;
+  load_twiddles(tws, tw, N);
+  __syncthreads();
+  block_fft<N, +1>(v, smem + r * N, SwzIdx{}, t, tws);
   if (valid) {
     double* a = real + static_cast<long long>(ri) * N;
     double* b = a + N;
@@ -435,7 +379,10 @@ k_z_r2c(const double* __restrict__ real, double2* __restrict__ spec, RowMap rm,
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = make_double2(0.0, 0.0);
   }
-  block_fft<N, -1>(v, reg, sw, t, tw);
+  double2* tws = smem + ZCfg<N>::RPC * N;
+  load_twiddles(tws, tw, N);
+  __syncthreads();
+  block_fft<N, -1>(v, reg, sw, t, tws);
 #pragma unroll
   for (int m = 0; m < E; ++m) reg[sw(t + m * TPC)] = v[m];
   __syncthreads();
@@ -469,9 +416,9 @@ __device__ __forceinline__ ModeIdx mode_of(const SpecGeom& g, long long e) {
   ModeIdx m;
   const long long row = e / g.pitch;
   m.k = static_cast<int>(e - row * g.pitch);
-  m.j = static_cast<int>(row % g.s1);
-  m.i = static_cast<int>(row / g.s1);
-  m.ok = m.i < g.s0 && m.k < g.s2;
+  m.j = static_cast<int>(row % g.prow);
+  m.i = static_cast<int>(row / g.prow);
+  m.ok = m.i < g.s0 && m.j < g.s1 && m.k < g.s2;
   m.off = e;
   return m;
 }
@@ -555,15 +502,15 @@ static unsigned grid_for(long long n, int threads) {
 }
 
 void pw_curl(const double2* u, double2* w, const SpecGeom& g, cudaStream_t s) {
-  const long long tot = static_cast<long long>(g.s0) * g.s1 * g.pitch;
+  const long long tot = static_cast<long long>(g.s0) * g.prow * g.pitch;
   k_curl<<<grid_for(tot, 256), 256, 0, s>>>(u, w, g);
 }
 void pw_project(double2* u, const SpecGeom& g, cudaStream_t s) {
-  const long long tot = static_cast<long long>(g.s0) * g.s1 * g.pitch;
+  const long long tot = static_cast<long long>(g.s0) * g.prow * g.pitch;
   k_project<<<grid_for(tot, 256), 256, 0, s>>>(u, g);
 }
 void pw_pressure(const double2* nl, double2* p, const SpecGeom& g, cudaStream_t s) {
-  const long long tot = static_cast<long long>(g.s0) * g.s1 * g.pitch;
+  const long long tot = static_cast<long long>(g.s0) * g.prow * g.pitch;
   k_pressure<<<grid_for(tot, 256), 256, 0, s>>>(nl, p, g);
 }
 void pw_cross(const double* a, const double* b, double* o, long long count, long long cs,
@@ -571,7 +518,7 @@ void pw_cross(const double* a, const double* b, double* o, long long count, long
   k_cross<<<grid_for(count, 256), 256, 0, s>>>(a, b, o, count, cs);
 }
 void pw_finite(const double2* u, const SpecGeom& g, int* flag, cudaStream_t s) {
-  const long long tot = static_cast<long long>(g.s0) * g.s1 * g.pitch;
+  const long long tot = static_cast<long long>(g.s0) * g.prow * g.pitch;
   k_finite<<<grid_for(tot, 256), 256, 0, s>>>(u, g, flag);
 }
 __global__ void k_fill_pad(double2* f, SpecGeom g, int ncomp) {
@@ -581,7 +528,7 @@ __global__ void k_fill_pad(double2* f, SpecGeom g, int ncomp) {
   for (int c = 0; c < ncomp; ++c) f[c * g.cs + e] = make_double2(0.0, 0.0);
 }
 void pw_fill_pad(double2* f, int ncomp, const SpecGeom& g, cudaStream_t s) {
-  const long long tot = static_cast<long long>(g.s0) * g.s1 * g.pitch;
+  const long long tot = static_cast<long long>(g.s0) * g.prow * g.pitch;
   k_fill_pad<<<grid_for(tot, 256), 256, 0, s>>>(f, g, ncomp);
 }
 
@@ -608,7 +555,7 @@ k_stats_partial(const double2* __restrict__ u, SpecGeom g, int shells, double* p
   double se = 0.0, sz = 0.0, dmax = 0.0;
   for (int j = warp; j < g.s1; j += kStatsWarps) {
     const double ky = wavenum(g.o1 + j, g.n);
-    const long long rowoff = (static_cast<long long>(i) * g.s1 + j) * g.pitch;
+    const long long rowoff = (static_cast<long long>(i) * g.prow + j) * g.pitch;
     for (int k0 = 0; k0 < g.s2; k0 += 32) {
       const int k = k0 + lane;
       const bool ok = k < g.s2;
@@ -747,86 +694,33 @@ void l2_local(const double* a, const double* b, long long count, double* d_parti
       if ((bytes) > 48 * 1024)                                                    \
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              static_cast<int>(bytes));                            \
+      cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, \
+                           100);                                                  \
       sdns_smem_done_ = true;                                                     \
     }                                                                            \
   } while (0)
 
-template <int N>
-static void col_plain_n(int dir, const double2* in, double2* out, long long in_cs, long long out_cs,
-                        int nfields, const ColGeom& g, const double2* tw, cudaStream_t s) {
-  using C = ColCfg<N>;
-  const long long cols = static_cast<long long>(g.nrows) * g.pitch;
-  const unsigned grid = static_cast<unsigned>((cols + C::CS - 1) / C::CS);
-  const size_t shm = sizeof(double2) * N * C::CS;
-  if (dir < 0) {
-    SDNS_SET_SMEM((k_col_plain<N, -1>), shm);
-    k_col_plain<N, -1><<<grid, C::THREADS, shm, s>>>(in, out, in_cs, out_cs, nfields, g, tw);
-  } else {
-    SDNS_SET_SMEM((k_col_plain<N, +1>), shm);
-    k_col_plain<N, +1><<<grid, C::THREADS, shm, s>>>(in, out, in_cs, out_cs, nfields, g, tw);
+template <int MODE>
+static void rk_update_mode(const XfArgs& a, const SpecGeom& g, cudaStream_t s) {
+  static int grid = 0;
+  if (!grid) {
+    int occ = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rk_update<MODE>, 256, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 148);
   }
+  const long long total = static_cast<long long>(g.s0) * g.prow * g.pitch;
+  const long long need = (total + 255) / 256;
+  k_rk_update<MODE><<<static_cast<unsigned>(need < grid ? need : grid), 256, 0, s>>>(a, g);
 }
 
-void col_plain(int n, int dir, const double2* in, double2* out, long long in_cs, long long out_cs,
-               int nfields, const ColGeom& g, const double2* tw, cudaStream_t s) {
-  switch (n) {
-#define X(NN) \
-  case NN: col_plain_n<NN>(dir, in, out, in_cs, out_cs, nfields, g, tw, s); return;
-    SDNS_FOR_N(X)
-#undef X
-  }
-}
-
-template <int N>
-static void x_inv_curl_n(const double2* u, long long u_cs, double2* out, long long out_cs,
-                         const ColGeom& g, const WaveGeom& w, const double2* tw, cudaStream_t s) {
-  using C = ColCfg<N>;
-  const long long cols = static_cast<long long>(g.nrows) * g.pitch;
-  const unsigned grid = static_cast<unsigned>((cols + C::CS - 1) / C::CS);
-  const size_t shm = sizeof(double2) * N * C::CS;
-  SDNS_SET_SMEM((k_x_inv_curl<N>), shm);
-  k_x_inv_curl<N><<<grid, C::THREADS, shm, s>>>(u, u_cs, out, out_cs, g, w, tw);
-}
-
-void x_inverse_curl(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
-                    const ColGeom& g, const WaveGeom& w, const double2* tw, cudaStream_t s) {
-  switch (n) {
-#define X(NN) \
-  case NN: x_inv_curl_n<NN>(u, u_cs, out, out_cs, g, w, tw, s); return;
-    SDNS_FOR_N(X)
-#undef X
-  }
-}
-
-template <int N, int MODE>
-static void x_fwd_mode(const XfArgs& a, const ColGeom& g, const WaveGeom& w, const double2* tw,
-                       cudaStream_t s) {
-  using C = ColCfg<N>;
-  const long long cols = static_cast<long long>(g.nrows) * g.pitch;
-  const unsigned grid = static_cast<unsigned>((cols + C::CSF - 1) / C::CSF);
-  const size_t shm = sizeof(double2) * 3 * N * C::CSF;
-  SDNS_SET_SMEM((k_x_fwd_fused<N, MODE>), shm);
-  k_x_fwd_fused<N, MODE><<<grid, C::THREADSF, shm, s>>>(a, g, w, tw);
-}
-
-template <int N>
-static void x_fwd_n(int mode, const XfArgs& a, const ColGeom& g, const WaveGeom& w,
-                    const double2* tw, cudaStream_t s) {
+void rk_update(int mode, const XfArgs& a, const SpecGeom& g, cudaStream_t s) {
   switch (mode) {
-    case XF_TAIL: x_fwd_mode<N, XF_TAIL>(a, g, w, tw, s); return;
-    case XF_RK0: x_fwd_mode<N, XF_RK0>(a, g, w, tw, s); return;
-    case XF_RK12: x_fwd_mode<N, XF_RK12>(a, g, w, tw, s); return;
-    default: x_fwd_mode<N, XF_RK3>(a, g, w, tw, s); return;
-  }
-}
-
-void x_forward_fused(int n, int mode, const XfArgs& a, const ColGeom& g, const WaveGeom& w,
-                     const double2* tw, cudaStream_t s) {
-  switch (n) {
-#define X(NN) \
-  case NN: x_fwd_n<NN>(mode, a, g, w, tw, s); return;
-    SDNS_FOR_N(X)
-#undef X
+    case XF_TAIL: rk_update_mode<XF_TAIL>(a, g, s); return;
+    case XF_RK0: rk_update_mode<XF_RK0>(a, g, s); return;
+    case XF_RK12: rk_update_mode<XF_RK12>(a, g, s); return;
+    default: rk_update_mode<XF_RK3>(a, g, s); return;
   }
 }
 
@@ -835,7 +729,7 @@ static void z_fused_n(double2* rows, long long cs, const RowMap& rm, double norm
                       const double2* tw, cudaStream_t s) {
   using C = ZCfg<N>;
   const unsigned grid = static_cast<unsigned>((rm.nrows + C::RPC - 1) / C::RPC);
-  const size_t shm = sizeof(double2) * 3 * N * C::RPC;
+  const size_t shm = sizeof(double2) * (6 * C::HP * C::RPC + N);
   SDNS_SET_SMEM((k_z_fused<N>), shm);
   k_z_fused<N><<<grid, C::THREADS, shm, s>>>(rows, cs, rm, norm, tw);
 }
@@ -856,7 +750,7 @@ static void z_c2r_n(const double2* spec, double* real, const RowMap& rm, double 
   using C = ZCfg<N>;
   const int pairs = rm.nrows / 2;
   const unsigned grid = static_cast<unsigned>((pairs + C::RPC - 1) / C::RPC);
-  const size_t shm = sizeof(double2) * N * C::RPC;
+  const size_t shm = sizeof(double2) * (N * C::RPC + N);
   SDNS_SET_SMEM((k_z_c2r<N>), shm);
   k_z_c2r<N><<<grid, C::THREADS, shm, s>>>(spec, real, rm, norm, tw);
 }
@@ -877,7 +771,7 @@ static void z_r2c_n(const double* real, double2* spec, const RowMap& rm, const d
   using C = ZCfg<N>;
   const int pairs = rm.nrows / 2;
   const unsigned grid = static_cast<unsigned>((pairs + C::RPC - 1) / C::RPC);
-  const size_t shm = sizeof(double2) * N * C::RPC;
+  const size_t shm = sizeof(double2) * (N * C::RPC + N);
   SDNS_SET_SMEM((k_z_r2c<N>), shm);
   k_z_r2c<N><<<grid, C::THREADS, shm, s>>>(real, spec, rm, tw);
 }

@@ -15,12 +15,20 @@ namespace sdns_dev {
 // at (row, pos, kz) lives at row*rs + (pos >> pb_shift)*ps1 +
 // (pos & ((1<<pb_shift)-1))*ps0 + kz. This covers the natural layouts and the
 // slab receive layout [peer][x_l][y_l][kz] with one formula.
+//
+// Work enumeration (forward dealias pruning): tiles walk
+// `nrows` enumerated rows x `pitch` kz slots, of which the first n2 are
+// transformed; enumerated row r maps to storage row r + off0 for r < seg_a,
+// else r - seg_a + off1 (the two kept |k| < n/3 bands). keep_k >= 0 limits
+// the stored output positions to |wavenumber| <= keep_k.
 struct ColGeom {
   long long rs = 0, ps0 = 0, ps1 = 0;
   int pb_shift = 30;
   int nrows = 0;
-  int n2 = 0;     // valid kz entries per row
-  int pitch = 0;  // padded kz entries per row (multiple of 8)
+  int n2 = 0;     // transformed kz entries per row
+  int pitch = 0;  // kz slots per enumerated row (multiple of the tile width)
+  int seg_a = 1 << 30, off0 = 0, off1 = 0;
+  int keep_k = -1;
 };
 
 // Wavenumbers of a column pass: which physical axis the transform runs
@@ -32,13 +40,21 @@ struct WaveGeom {
   int kz_off = 0;    // global kz offset of kz index 0
 };
 
-// Row mapping for the z passes: real row ri = (x_l, y) -> spectral row.
+// Row mapping for the z passes. Spectral rows live in planes of `prow`
+// rows (the last row of each plane is padding, so that the plane stride is
+// an odd multiple of 128 B and strided x-pass accesses spread over all HBM
+// channels). Memory order (blk == 0): row ri = (plane ri / rpp, ri % rpp).
+// By (x_l, y) (blk = np): ri = x_l*ny + y lives in plane (y/np)*np + x_l,
+// row y % np -- the slab receive layout; at p = 1 simply plane x, row y.
 struct RowMap {
-  int nrows = 0;     // number of (x_l, y) rows
-  int ny = 0;        // real y extent
-  int blk = 0;       // 0: spectral row = ri; else slab recv layout block (np)
-  int pitch = 0;     // spectral row pitch
+  int nrows = 0;     // number of rows
+  int rpp = 0;       // real rows per plane (memory order)
+  int ny = 0;        // real y extent (by-(x_l, y) order)
+  int blk = 0;       // 0: memory order; else slab block np
+  int prow = 0;      // rows per plane including the pad row
+  int pitch = 0;     // spectral row pitch (complex)
   int n2 = 0;        // valid kz entries (n/2+1 for a full z line)
+  int kz_keep = 1 << 30;  // forward outputs stored only for kz < kz_keep
 };
 
 // Fused x-pass forward epilogue variants.
@@ -71,13 +87,20 @@ struct XfArgs {
 // twiddle table exp(-2 pi i q / n), q in [0, n)
 void make_twiddles(int n, double2* d_tw, cudaStream_t s);
 
-void col_plain(int n, int dir, const double2* in, double2* out, long long in_cs,
+// xaxis selects the tile shape tuned for the large-stride (x) axis.
+void col_plain(int n, int dir, bool xaxis, const double2* in, double2* out, long long in_cs,
                long long out_cs, int nfields, const ColGeom& g, const double2* tw,
                cudaStream_t s);
-void x_inverse_curl(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
-                    const ColGeom& g, const WaveGeom& w, const double2* tw, cudaStream_t s);
-void x_forward_fused(int n, int mode, const XfArgs& a, const ColGeom& g, const WaveGeom& w,
-                     const double2* tw, cudaStream_t s);
+// P1: u_hat (3 comps) -> [U0, U1, U2, K1, K2] (5 comps of `out`)
+void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
+                     const ColGeom& g, const double2* tw, cudaStream_t s);
+// P2: in place, fields [U0, U1, U2, K1, K2] -> [u0, u1, u2, w0', w1', w2]
+void y_inverse_curl(int n, double2* f, long long cs, const ColGeom& g, const double2* tw,
+                    cudaStream_t s);
+struct SpecGeom;
+// P5b: mask + projection + viscous + RK4 stage update, streaming over the
+// x layout (a.nl holds the x-forward-transformed nonlinear term).
+void rk_update(int mode, const XfArgs& a, const SpecGeom& g, cudaStream_t s);
 
 void z_fused(int n, double2* rows, long long cs, const RowMap& rm, double norm,
              const double2* tw, cudaStream_t s);
@@ -92,7 +115,8 @@ struct SpecGeom {
   int s0 = 0, s1 = 0, s2 = 0;    // local shape
   int o0 = 0, o1 = 0, o2 = 0;    // global offsets
   int pitch = 0;
-  long long cs = 0;              // component stride (s0*s1*pitch)
+  int prow = 0;                  // rows per x plane incl. the pad row (s1 + 1)
+  long long cs = 0;              // component stride (s0*prow*pitch)
 };
 
 void pw_curl(const double2* u, double2* w, const SpecGeom& g, cudaStream_t s);

@@ -1,0 +1,385 @@
+// Column passes (FFTs along x or y) as persistent, cp.async-fed tile
+// pipelines for sm_100a.
+//
+// A tile is CS consecutive kz columns of one row (CS*16 B contiguous per
+// position) over all N positions of the transformed axis. Each CTA walks a
+// strided list of work items; tiles are copied global->shared with cp.async
+// (LDGSTS, zero-filled outside the valid kz range) -- with two buffers the
+// copy of item i+1 overlaps the transform of item i -- then transformed in
+// place and written back with coalesced 16-byte stores. Every item reads
+// exactly one input tile, which is what the linearity restructuring of the
+// curl allows:
+//   P1 x inverse:  U_c = F_x^-1(u_c),  K_c = F_x^-1(kx u_c)   (c = 1, 2)
+//   P2 y inverse:  u_c = F_y^-1(U_c),  w0' = F_y^-1(i ky U2),
+//                  w1' = F_y^-1(-i K2), w2 = i(F_y^-1(K1) - F_y^-1(ky U0))
+//   P3 (z pass) then completes w0 = w0' - i kz u1 and w1 = w1' + i kz u0,
+// which is omega_hat = i k x u_hat (curl_hat, navier_stokes.cpp:52-72)
+// distributed over the three axes.
+//
+// Tile shapes (measured on B200 at n = 512): x passes (2 MB
+// position stride) prefer 8-column / 128 B tiles with one buffer and two
+// 512-thread CTAs per SM; y passes (4 KB stride) prefer 4-column tiles, two
+// buffers, three 256-thread CTAs per SM.
+#include "fft_core.cuh"
+#include "kernels.cuh"
+
+namespace sdns_dev {
+
+namespace {
+
+enum : int { VX = 3, VY = 1, VYI = 0 };
+
+template <int N, int V>
+struct PipeCfg {
+  static constexpr int E = fft_elems(N);
+  static constexpr int TPC = N / E;
+  static constexpr int CSW = (V == 1 || V == 2) ? 4 : 8;  // columns at TPC >= 64
+  static constexpr int CS0 = TPC >= 64 ? CSW : (512 / TPC > 64 ? 64 : 512 / TPC);
+  static constexpr int CS = N >= 1024 ? 4 : CS0;
+  static constexpr int THREADS = TPC * CS;
+  static constexpr int NBUF = (V == 2 || V == 3) ? 1 : 2;
+  static constexpr int MINB = V == 1 ? 3 : (V == 2 ? 4 : (V == 3 ? 2 : 1));
+  static constexpr int TILE = N * CS;  // complex elements per tile buffer
+  // tile buffers + the twiddle table
+  static constexpr size_t SMEM = sizeof(double2) * (NBUF * TILE + N);
+};
+
+__device__ __forceinline__ long long col_off(const ColGeom& g, int row, int pos, int kz) {
+  return static_cast<long long>(row) * g.rs +
+         static_cast<long long>(pos >> g.pb_shift) * g.ps1 +
+         static_cast<long long>(pos & ((1 << g.pb_shift) - 1)) * g.ps0 + kz;
+}
+
+__device__ __forceinline__ double wavenum(int j, int n) {
+  return static_cast<double>(j <= n / 2 - 1 ? j : j - n);
+}
+
+__device__ __forceinline__ void cp_async16(double2* dst, const double2* src, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(sz)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+struct Tile {
+  int row, kz;
+  bool valid;
+};
+
+// Shared-memory placement of a tile: position x of column c at
+// tpos(x)*CS + c. With 4-column (64 B) rows, positions are swizzled in pairs
+// of 8 so that the stride-8 writes of the first Stockham stage alternate
+// between the two 64 B halves of a bank row.
+template <int CS>
+struct TileIdx {
+  __device__ __forceinline__ int operator()(int x) const {
+    return (CS == 4 ? (x ^ ((x >> 3) & 1)) : x) * CS;
+  }
+};
+
+template <int CS>
+__device__ __forceinline__ Tile tile_of(int tile, int col, const ColGeom& g) {
+  const long long gc = static_cast<long long>(tile) * CS + col;
+  Tile t;
+  const int re = static_cast<int>(gc / g.pitch);
+  t.kz = static_cast<int>(gc - static_cast<long long>(re) * g.pitch);
+  t.valid = re < g.nrows && t.kz < g.n2;
+  t.row = re < g.seg_a ? re + g.off0 : re - g.seg_a + g.off1;
+  return t;
+}
+
+template <int N, int CS>
+__device__ __forceinline__ void issue_tile(double2* buf, const double2* src, const ColGeom& g,
+                                           const Tile& tl, int col, int t) {
+  constexpr int E = fft_elems(N), TPC = N / E;
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int pos = t + m * TPC;
+    const double2* p = tl.valid ? src + col_off(g, tl.row, pos, tl.kz) : src;
+    cp_async16(buf + TileIdx<CS>{}(pos) + col, p, tl.valid);
+  }
+}
+
+template <int N, int CS>
+__device__ __forceinline__ void read_own(double2 (&v)[fft_elems(N)], const double2* buf, int col,
+                                         int t) {
+  constexpr int E = fft_elems(N), TPC = N / E;
+#pragma unroll
+  for (int m = 0; m < E; ++m) v[m] = buf[TileIdx<CS>{}(t + m * TPC) + col];
+}
+
+template <int N>
+__device__ __forceinline__ void store_own(double2* dst, const double2 (&v)[fft_elems(N)],
+                                          const ColGeom& g, const Tile& tl, int t) {
+  constexpr int E = fft_elems(N), TPC = N / E;
+  if (!tl.valid) return;
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int pos = t + m * TPC;
+    if (g.keep_k >= 0 && pos > g.keep_k && pos < N - g.keep_k) continue;  // masked mode
+    dst[col_off(g, tl.row, pos, tl.kz)] = v[m];
+  }
+}
+
+__device__ __forceinline__ double2 times_i(double2 a) { return make_double2(-a.y, a.x); }
+__device__ __forceinline__ double2 times_mi(double2 a) { return make_double2(a.y, -a.x); }
+
+// Generic persistent pipeline driver: `items` items per tile; src(f) gives
+// the input field of item f; body(f, buf, tile, col, t, twiddles) transforms.
+template <int N, int V, class SrcF, class BodyF>
+__device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g, SrcF src,
+                                         const double2* __restrict__ tw_global, BodyF body) {
+  extern __shared__ double2 smem[];
+  constexpr int CS = PipeCfg<N, V>::CS, NBUF = PipeCfg<N, V>::NBUF;
+  const int col = threadIdx.x % CS, t = threadIdx.x / CS;
+  double2* buf[2] = {smem, smem + (NBUF - 1) * N * CS};
+  double2* tws = smem + NBUF * N * CS;
+  load_twiddles(tws, tw_global, N);  // visible after the first __syncthreads below
+  const int G = gridDim.x;
+  auto tile_at = [&](long long i) { return static_cast<int>(blockIdx.x + (i / items) * G); };
+  if (NBUF == 1) {
+    for (long long i = 0; tile_at(i) < ntiles; ++i) {
+      const Tile tl = tile_of<CS>(tile_at(i), col, g);
+      issue_tile<N, CS>(buf[0], src(static_cast<int>(i % items)), g, tl, col, t);
+      cp_commit();
+      cp_wait0();
+      __syncthreads();
+      body(static_cast<int>(i % items), buf[0], tl, col, t, static_cast<const double2*>(tws));
+      __syncthreads();
+    }
+    return;
+  }
+  if (tile_at(0) < ntiles)
+    issue_tile<N, CS>(buf[0], src(0), g, tile_of<CS>(tile_at(0), col, g), col, t);
+  cp_commit();
+  for (long long i = 0; tile_at(i) < ntiles; ++i) {
+    const long long j = i + 1;
+    const int tj = tile_at(j);
+    if (tj < ntiles)
+      issue_tile<N, CS>(buf[j & 1], src(static_cast<int>(j % items)), g, tile_of<CS>(tj, col, g),
+                        col, t);
+    cp_commit();
+    cp_wait1();
+    __syncthreads();
+    body(static_cast<int>(i % items), buf[i & 1], tile_of<CS>(tile_at(i), col, g), col, t,
+         static_cast<const double2*>(tws));
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Plain multi-field column transform (y passes, x-forward, API passes).
+
+template <int N, int S, int V>
+__global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
+k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs, int nfields,
+             ColGeom g, int ntiles, const double2* __restrict__ tw) {
+  constexpr int CS = PipeCfg<N, V>::CS;
+  pipeline<N, V>(ntiles, nfields, g, [&](int f) { return in + f * in_cs; }, tw,
+                 [&](int f, double2* buf, const Tile& tl, int col, int t, const double2* tws) {
+                   double2 v[fft_elems(N)];
+                   read_own<N, CS>(v, buf, col, t);
+                   __syncthreads();
+                   block_fft<N, S>(v, buf + col, TileIdx<CS>{}, t, tws);
+                   store_own<N>(out + f * out_cs, v, g, tl, t);
+                 });
+}
+
+// ---------------------------------------------------------------------------
+// P1: x inverse of u_hat -> [U0, U1, U2, K1, K2] (fields 0..4 of `out`).
+
+template <int N, int V>
+__global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
+k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, ColGeom g,
+            int ntiles, const double2* __restrict__ tw) {
+  constexpr int CS = PipeCfg<N, V>::CS, E = fft_elems(N), TPC = N / E;
+  pipeline<N, V>(ntiles, 3, g, [&](int f) { return u + f * u_cs; }, tw,
+                 [&](int f, double2* buf, const Tile& tl, int col, int t, const double2* tws) {
+                   double2 vin[E], v[E];
+                   read_own<N, CS>(vin, buf, col, t);
+                   __syncthreads();
+                   if (f > 0) {
+#pragma unroll
+                     for (int m = 0; m < E; ++m) {
+                       const double kx = wavenum(t + m * TPC, N);
+                       v[m] = make_double2(kx * vin[m].x, kx * vin[m].y);
+                     }
+                     block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                     store_own<N>(out + (2 + f) * out_cs, v, g, tl, t);
+                   }
+#pragma unroll
+                   for (int m = 0; m < E; ++m) v[m] = vin[m];
+                   block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                   store_own<N>(out + f * out_cs, v, g, tl, t);
+                 });
+}
+
+// ---------------------------------------------------------------------------
+// P2: y inverse, in place on fields 0..4 = [U0, U1, U2, K1, K2] of `f`,
+// producing [u0, u1, u2, w0', w1', w2] in fields 0..5. Items per tile in the
+// order U0, K1, U1, U2, K2 so that no field is overwritten before it is read;
+// F_y(ky U0) parks in field 5 (re-read by the same thread in the next item
+// while the tile is still L2-resident).
+
+template <int N, int V>
+__global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
+k_pipe_yinv(double2* f, long long cs, ColGeom g, int ntiles, const double2* __restrict__ tw) {
+  constexpr int CS = PipeCfg<N, V>::CS, E = fft_elems(N), TPC = N / E;
+  const int order[5] = {0, 3, 1, 2, 4};
+  pipeline<N, V>(ntiles, 5, g, [&](int it) { return f + order[it] * cs; }, tw,
+                 [&](int it, double2* buf, const Tile& tl, int col, int t, const double2* tws) {
+                   double2 vin[E], v[E];
+                   read_own<N, CS>(vin, buf, col, t);
+                   __syncthreads();
+                   if (it == 0 || it == 3) {  // U0 -> D = F(ky U0); U2 -> w0' = F(i ky U2)
+#pragma unroll
+                     for (int m = 0; m < E; ++m) {
+                       const double ky = wavenum(t + m * TPC, N);
+                       const double2 a = make_double2(ky * vin[m].x, ky * vin[m].y);
+                       v[m] = it == 0 ? a : times_i(a);
+                     }
+                     block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                     store_own<N>(f + (it == 0 ? 5 : 3) * cs, v, g, tl, t);
+                   }
+                   if (it == 1) {  // K1 -> w2 = i (F(K1) - D)
+                     block_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
+                     if (tl.valid) {
+                       double2* w2 = f + 5 * cs;
+#pragma unroll
+                       for (int m = 0; m < E; ++m) {
+                         const long long o = col_off(g, tl.row, t + m * TPC, tl.kz);
+                         const double2 d = w2[o];
+                         w2[o] = times_i(make_double2(vin[m].x - d.x, vin[m].y - d.y));
+                       }
+                     }
+                   } else if (it == 4) {  // K2 -> w1' = F(-i K2)
+#pragma unroll
+                     for (int m = 0; m < E; ++m) v[m] = times_mi(vin[m]);
+                     block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                     store_own<N>(f + 4 * cs, v, g, tl, t);
+                   } else {  // U0, U1, U2 -> u_c
+                     block_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
+                     store_own<N>(f + order[it] * cs, vin, g, tl, t);
+                   }
+                 });
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+
+#define SDNS_FOR_N(X) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
+
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <class K>
+static unsigned persistent_grid(K kernel, int threads, size_t smem, long long ntiles,
+                                int* cache) {
+  if (*cache == 0) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
+    *cache = occ > 0 ? occ : 1;
+  }
+  const long long g = static_cast<long long>(*cache) * num_sms();
+  return static_cast<unsigned>(ntiles < g ? ntiles : g);
+}
+
+template <int N, int V>
+static long long ntiles_of(const ColGeom& g) {
+  const long long cols = static_cast<long long>(g.nrows) * g.pitch;
+  return (cols + PipeCfg<N, V>::CS - 1) / PipeCfg<N, V>::CS;
+}
+
+template <int N, int S, int V>
+static void plain_launch(const double2* in, double2* out, long long in_cs, long long out_cs,
+                         int nfields, const ColGeom& g, const double2* tw, cudaStream_t s) {
+  using C = PipeCfg<N, V>;
+  const long long nt = ntiles_of<N, V>(g);
+  if (nt <= 0) return;
+  static int occ = 0;
+  const unsigned grid = persistent_grid(k_pipe_plain<N, S, V>, C::THREADS, C::SMEM, nt, &occ);
+  k_pipe_plain<N, S, V><<<grid, C::THREADS, C::SMEM, s>>>(in, out, in_cs, out_cs, nfields, g,
+                                                          static_cast<int>(nt), tw);
+}
+
+template <int N>
+static void col_plain_n(int dir, bool xaxis, const double2* in, double2* out, long long in_cs,
+                        long long out_cs, int nfields, const ColGeom& g, const double2* tw,
+                        cudaStream_t s) {
+  if (dir < 0) {
+    if (xaxis) plain_launch<N, -1, VX>(in, out, in_cs, out_cs, nfields, g, tw, s);
+    else plain_launch<N, -1, VY>(in, out, in_cs, out_cs, nfields, g, tw, s);
+  } else {
+    if (xaxis) plain_launch<N, +1, VX>(in, out, in_cs, out_cs, nfields, g, tw, s);
+    else plain_launch<N, +1, VY>(in, out, in_cs, out_cs, nfields, g, tw, s);
+  }
+}
+
+void col_plain(int n, int dir, bool xaxis, const double2* in, double2* out, long long in_cs,
+               long long out_cs, int nfields, const ColGeom& g, const double2* tw,
+               cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: col_plain_n<NN>(dir, xaxis, in, out, in_cs, out_cs, nfields, g, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+template <int N>
+static void x_inv_n(const double2* u, long long u_cs, double2* out, long long out_cs,
+                    const ColGeom& g, const double2* tw, cudaStream_t s) {
+  using C = PipeCfg<N, VX>;
+  const long long nt = ntiles_of<N, VX>(g);
+  static int occ = 0;
+  const unsigned grid = persistent_grid(k_pipe_xinv<N, VX>, C::THREADS, C::SMEM, nt, &occ);
+  k_pipe_xinv<N, VX><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, g,
+                                                       static_cast<int>(nt), tw);
+}
+
+void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
+                     const ColGeom& g, const double2* tw, cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: x_inv_n<NN>(u, u_cs, out, out_cs, g, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+template <int N>
+static void y_inv_n(double2* f, long long cs, const ColGeom& g, const double2* tw, cudaStream_t s) {
+  using C = PipeCfg<N, VYI>;
+  const long long nt = ntiles_of<N, VYI>(g);
+  static int occ = 0;
+  const unsigned grid = persistent_grid(k_pipe_yinv<N, VYI>, C::THREADS, C::SMEM, nt, &occ);
+  k_pipe_yinv<N, VYI><<<grid, C::THREADS, C::SMEM, s>>>(f, cs, g, static_cast<int>(nt), tw);
+}
+
+void y_inverse_curl(int n, double2* f, long long cs, const ColGeom& g, const double2* tw,
+                    cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: y_inv_n<NN>(f, cs, g, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+}  // namespace sdns_dev

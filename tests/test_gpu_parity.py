@@ -147,6 +147,24 @@ def test_compute_rhs_vs_numpy_oracle(n):
         assert rel(du.download(), expect) <= 1e-12
 
 
+@pytest.mark.parametrize("dealias", [False, True])
+def test_compute_rhs_dealias_switch(dealias):
+    """dealias = false disables the 2/3 rule (and the forward pruning)."""
+    n = 32
+    rng = np.random.default_rng(5)
+    wm = O.Wavenumbers(n, dealias=dealias)
+    uh = O.project(O.forward(rng.uniform(-1, 1, (3, n, n, n))), wm) / n**3
+    expect = O.compute_rhs(uh, wm, 0.02)
+    with ctx_for(n, dealias=dealias) as c:
+        du = c.spectral_field()
+        S.compute_rhs(c, c.spectral_field().upload(uh), 0.02, du)
+        got = du.download()
+    assert rel(got, expect) <= 1e-12
+    if not dealias:  # the masked band carries the nonlinear term when the rule is off
+        band = ~O.Wavenumbers(n, dealias=True).mask
+        assert np.abs(got[:, band]).max() > 1e-6
+
+
 def test_compute_rhs_solenoidal_and_linear_in_nu():
     """proj/tests/test_ns.cpp:170-214: k . du = 0, d(du)/d(nu) = -k^2 u."""
     n = 16

@@ -1,0 +1,23 @@
+import csv, subprocess, sys
+rep = sys.argv[1]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+hdr = rows[0]
+want = ['Kernel Name','gpu__time_duration.sum','dram__bytes_read.sum','dram__bytes_write.sum',
+ 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed','sm__warps_active.avg.pct_of_peak_sustained_active',
+ 'launch__registers_per_thread','launch__occupancy_limit_registers','launch__occupancy_limit_shared_mem',
+ 'launch__shared_mem_per_block_dynamic','sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
+ 'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum','lts__t_sectors_srcunit_tex_op_read.sum',
+ 'smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio',
+ 'smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio',
+ 'smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio',
+ 'smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio',
+ 'smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio',
+ 'smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio',
+ 'smsp__issue_active.avg.pct_of_peak_sustained_active','launch__grid_size','launch__block_size']
+idx = [hdr.index(w) if w in hdr else -1 for w in want]
+for r in rows[2:]:
+    print('----')
+    for w, i in zip(want, idx):
+        if i >= 0:
+            print(f'  {w}: {r[i]}')
