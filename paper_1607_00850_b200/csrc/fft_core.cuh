@@ -123,6 +123,24 @@ struct Dft<16, S> {
 // Elements held per thread for a transform of length N.
 __host__ __device__ constexpr int fft_elems(int n) { return n >= 1024 ? 16 : (n >= 8 ? 8 : n); }
 
+// Stage-ordered twiddle table. Stage NS (> 1) of radix R stores
+// W_{NS*R}^{k*r} at off(NS) + (r-1)*NS + k, k in [0, NS), r in [1, R), so the
+// lanes of a warp read consecutive (or identical) 16-byte entries: no bank
+// conflicts, unlike strided reads of a single exp(-2 pi i q / n) table.
+__host__ __device__ constexpr int tw_stage_off(int n, int e, int ns_target) {
+  int off = 0;
+  for (int ns = 1; ns < ns_target;) {
+    const int rem = n / ns;
+    const int r = rem >= e ? e : rem;
+    if (ns > 1) off += ns * (r - 1);
+    ns *= r;
+  }
+  return off;
+}
+__host__ __device__ constexpr int tw_stage_total(int n) {
+  return tw_stage_off(n, fft_elems(n), n);
+}
+
 // Shared-memory placement of a column: element x at sm[x * cs].
 struct ColIdx {
   int cs;
@@ -134,11 +152,23 @@ struct SwzIdx {
   __device__ __forceinline__ int operator()(int x) const { return x ^ ((x >> 3) & 7); }
 };
 
+// Barrier policies: the whole CTA, or a named barrier over the threads that
+// own one transform (lets independent transforms in a CTA drift apart).
+struct CtaBar {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct NamedBar {
+  int id, nthreads;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+  }
+};
+
 // One Stockham stage (and the rest, recursively). `sm` points at this
 // column's element 0 in shared memory; element x lives at sm[idx(x)].
-template <int N, int E, int S, int NS, class IDX>
+template <int N, int E, int S, int NS, class IDX, class BAR = CtaBar>
 __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx, int t,
-                                           const double2* __restrict__ tw) {
+                                           const double2* __restrict__ tw, BAR bar = BAR{}) {
   constexpr int REM = N / NS;
   constexpr int R = REM >= E ? E : REM;
   constexpr int NB = E / R;
@@ -152,8 +182,9 @@ __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx
 #pragma unroll
     for (int r = 0; r < R; ++r) a[r] = v[b + r * NB];
     if (NS > 1) {
+      constexpr int TOFF = tw_stage_off(N, E, NS);
 #pragma unroll
-      for (int r = 1; r < R; ++r) a[r] = cmul(a[r], twiddle<S>(tw, k * r * (N / (NS * R))));
+      for (int r = 1; r < R; ++r) a[r] = cmul(a[r], twiddle<S>(tw, TOFF + (r - 1) * NS + k));
     }
     Dft<R, S>::run(a);
     if (LAST) {
@@ -166,25 +197,27 @@ __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx
     }
   }
   if constexpr (!LAST) {
-    __syncthreads();
+    bar();
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = sm[idx(t + m * TPC)];
-    __syncthreads();
-    fft_stages<N, E, S, NS * R>(v, sm, idx, t, tw);
+    bar();
+    fft_stages<N, E, S, NS * R, IDX, BAR>(v, sm, idx, t, tw, bar);
   }
 }
 
 // Full transform: v[m] = x[t + m*TPC] on entry, X[t + m*TPC] on exit.
-// Must be called by every thread of the block (contains __syncthreads).
-template <int N, int S, class IDX>
+// Must be called by every thread the barrier policy covers.
+template <int N, int S, class IDX, class BAR = CtaBar>
 __device__ __forceinline__ void block_fft(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
-                                          const double2* __restrict__ tw) {
-  fft_stages<N, fft_elems(N), S, 1>(v, sm, idx, t, tw);
+                                          const double2* __restrict__ tw, BAR bar = BAR{}) {
+  fft_stages<N, fft_elems(N), S, 1, IDX, BAR>(v, sm, idx, t, tw, bar);
 }
 
-// Copies the n-entry twiddle table to shared memory (caller syncs).
+// Copies the stage-ordered twiddle table of length-n transforms to shared
+// memory (tw_stage_total(n) <= n entries; caller syncs).
 __device__ __forceinline__ void load_twiddles(double2* dst, const double2* __restrict__ src, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
+  const int total = tw_stage_total(n);
+  for (int i = threadIdx.x; i < total; i += blockDim.x) dst[i] = __ldg(src + i);
 }
 
 }  // namespace sdns_dev

@@ -15,6 +15,7 @@
 // round-to-nearest intrinsics (no FMA contraction), so the standalone
 // pointwise kernels are bitwise equal to the reference CPU functions.
 #include <cstdio>
+#include <type_traits>
 #include <vector>
 
 #include "fft_core.cuh"
@@ -63,17 +64,34 @@ struct ColCfg {
 // ---------------------------------------------------------------------------
 // Twiddles
 
-__global__ void k_twiddles(int n, double2* tw) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= n) return;
-  double s, c;
-  // sincospi is accurate to ~1 ulp and exact at the symmetry points
-  sincospi(-2.0 * static_cast<double>(q) / static_cast<double>(n), &s, &c);
-  tw[q] = make_double2(c, s);
+// Stage-ordered table (fft_core.cuh tw_stage_off): entry (NS, r, k) holds
+// W_{NS*R}^{k r} = exp(-2 pi i q / n), q = k r n / (NS R).
+__global__ void k_twiddles(int n, int e, double2* tw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int off = 0;
+  for (int ns = 1; ns < n;) {
+    const int rem = n / ns;
+    const int r = rem >= e ? e : rem;
+    if (ns > 1) {
+      const int cnt = ns * (r - 1);
+      if (i >= off && i < off + cnt) {
+        const int rr = (i - off) / ns + 1, k = (i - off) % ns;
+        const int q = k * rr * (n / (ns * r));
+        double s, c;
+        // sincospi is accurate to ~1 ulp and exact at the symmetry points
+        sincospi(-2.0 * static_cast<double>(q) / static_cast<double>(n), &s, &c);
+        tw[i] = make_double2(c, s);
+        return;
+      }
+      off += cnt;
+    }
+    ns *= r;
+  }
 }
 
 void make_twiddles(int n, double2* d_tw, cudaStream_t s) {
-  k_twiddles<<<(n + 255) / 256, 256, 0, s>>>(n, d_tw);
+  const int total = tw_stage_total(n);
+  if (total > 0) k_twiddles<<<(total + 255) / 256, 256, 0, s>>>(n, fft_elems(n), d_tw);
 }
 
 // ---------------------------------------------------------------------------
@@ -225,22 +243,40 @@ __device__ __forceinline__ double2 pair_sample(const double2* A, const double2* 
   return make_double2(a.x - b.y, a.y + b.x);
 }
 
+struct WarpBar {
+  __device__ __forceinline__ void operator()() const { __syncwarp(); }
+};
+
+// Launch shape of the fused z pass: 4 rows of 64 threads at n >= 512 (each
+// row synchronises on its own named barrier), else whole rows per warp.
 template <int N>
-__global__ void __launch_bounds__(ZCfg<N>::THREADS, 4)
+struct ZFCfg {
+  static constexpr int E = fft_elems(N);
+  static constexpr int TPC = N / E;
+  static constexpr int RPC = TPC >= 64 ? 4 : (256 / TPC > 64 ? 64 : 256 / TPC);
+  static constexpr int THREADS = TPC * RPC;
+  static constexpr int HP = N / 2 + 8;  // padded half-row (n/2+1 modes)
+  static constexpr size_t SMEM = sizeof(double2) * (static_cast<size_t>(RPC) * 6 * HP + N);
+};
+
+template <int N>
+__global__ void __launch_bounds__(ZFCfg<N>::THREADS, 2)
 k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __restrict__ tw) {
-  constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC;
+  constexpr int E = ZFCfg<N>::E, TPC = ZFCfg<N>::TPC, HP = ZFCfg<N>::HP, RPC = ZFCfg<N>::RPC;
+  using Bar = typename std::conditional<(TPC >= 64), NamedBar, WarpBar>::type;
   extern __shared__ double2 smem[];
   const int t = threadIdx.x % TPC, r = threadIdx.x / TPC;
-  const int ri = blockIdx.x * ZCfg<N>::RPC + r;
+  const int ri = blockIdx.x * RPC + r;
   const bool valid = ri < rm.nrows;
   const long long ro = valid ? zrow_off(rm, ri) : 0;
   // Stage the 6 half-rows once (coalesced, each element read once); the
   // staging area of pair p (2 half-rows, 2*HP >= n entries) then serves as
-  // that pair's FFT exchange buffer and result store.
-  constexpr int HP = ZCfg<N>::HP;
+  // that pair's FFT exchange buffer. Pair results stay in registers.
   double2* S = smem + r * 6 * HP;
-  double2* tws = smem + ZCfg<N>::RPC * 6 * HP;
+  double2* tws = smem + RPC * 6 * HP;
   load_twiddles(tws, tw, N);
+  Bar bar;
+  if constexpr (TPC >= 64) bar = Bar{1 + r, TPC};
   const SwzIdx sw;
   if (valid) {
     // fields: 0..2 = u, 3 = w0', 4 = w1', 5 = w2. The z part of the curl:
@@ -261,36 +297,44 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
       }
     }
   }
-  __syncthreads();
-  double2 v[E];
-#pragma unroll 1
-  for (int p = 0; p < 3; ++p) {
-    double2* reg = S + 2 * p * HP;
+  __syncthreads();  // twiddles + staging
+  double2 p1[E], v[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = pair_sample<N>(reg, reg + HP, t + m * TPC);
-    __syncthreads();
-    block_fft<N, +1>(v, reg, sw, t, tws);
+  for (int m = 0; m < E; ++m) v[m] = pair_sample<N>(S, S + HP, t + m * TPC);
+  bar();
+  block_fft<N, +1>(v, S, sw, t, tws, bar);
+  // pair 0 result parks in its own (now free) region at this thread's positions
 #pragma unroll
-    for (int m = 0; m < E; ++m) reg[sw(t + m * TPC)] = v[m];
+  for (int m = 0; m < E; ++m) {
+    S[sw(t + m * TPC)] = v[m];
+    v[m] = pair_sample<N>(S + 2 * HP, S + 3 * HP, t + m * TPC);
   }
-  double2* reg = S;  // pair 0 region (forward FFT of n0 + i n1)
+  bar();
+  block_fft<N, +1>(v, S + 2 * HP, sw, t, tws, bar);
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    p1[m] = v[m];
+    v[m] = pair_sample<N>(S + 4 * HP, S + 5 * HP, t + m * TPC);
+  }
+  bar();
+  block_fft<N, +1>(v, S + 4 * HP, sw, t, tws, bar);
+  // (u0,u1) = p0, (u2,w0) = p1, (w1,w2) = v; 1/n^3 then u x omega
   double n2r[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) {
-    const int x = sw(t + m * TPC);
-    const double2 p0 = S[x], p1 = S[2 * HP + x], p2 = S[4 * HP + x];
-    const double ua = dmul(p0.x, norm), ub = dmul(p0.y, norm), uc = dmul(p1.x, norm);
-    const double wa = dmul(p1.y, norm), wb = dmul(p2.x, norm), wc = dmul(p2.y, norm);
+    const double2 q0 = S[sw(t + m * TPC)];
+    const double ua = dmul(q0.x, norm), ub = dmul(q0.y, norm), uc = dmul(p1[m].x, norm);
+    const double wa = dmul(p1[m].y, norm), wb = dmul(v[m].x, norm), wc = dmul(v[m].y, norm);
     const double n0 = dsub(dmul(ub, wc), dmul(uc, wb));
     const double n1 = dsub(dmul(uc, wa), dmul(ua, wc));
     n2r[m] = dsub(dmul(ua, wb), dmul(ub, wa));
     v[m] = make_double2(n0, n1);
   }
-  __syncthreads();
-  block_fft<N, -1>(v, reg, sw, t, tws);
+  bar();  // every thread has read its parked pair-0 values
+  block_fft<N, -1>(v, S, sw, t, tws, bar);
 #pragma unroll
-  for (int m = 0; m < E; ++m) reg[sw(t + m * TPC)] = v[m];
-  __syncthreads();
+  for (int m = 0; m < E; ++m) S[sw(t + m * TPC)] = v[m];
+  bar();
   if (valid) {
     double2* o0 = f + ro;
     double2* o1 = f + cs + ro;
@@ -298,8 +342,8 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
     for (int m = 0; m < E; ++m) {
       const int k = t + m * TPC;
       if (k <= N / 2 && k < rm.kz_keep) {  // kz >= n/3 is dealiased away
-        const double2 d = reg[sw(k)];
-        const double2 e = cconj(reg[sw((N - k) & (N - 1))]);
+        const double2 d = S[sw(k)];
+        const double2 e = cconj(S[sw((N - k) & (N - 1))]);
         o0[k] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
         const double2 dd = csub(d, e);
         o1[k] = make_double2(0.5 * dd.y, -0.5 * dd.x);
@@ -308,7 +352,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   }
 #pragma unroll
   for (int m = 0; m < E; ++m) v[m] = make_double2(n2r[m], 0.0);
-  block_fft<N, -1>(v, S + 2 * HP, sw, t, tws);
+  block_fft<N, -1>(v, S + 2 * HP, sw, t, tws, bar);
   if (valid) {
     double2* o2 = f + 2 * cs + ro;
 #pragma unroll
@@ -727,9 +771,9 @@ void rk_update(int mode, const XfArgs& a, const SpecGeom& g, cudaStream_t s) {
 template <int N>
 static void z_fused_n(double2* rows, long long cs, const RowMap& rm, double norm,
                       const double2* tw, cudaStream_t s) {
-  using C = ZCfg<N>;
+  using C = ZFCfg<N>;
   const unsigned grid = static_cast<unsigned>((rm.nrows + C::RPC - 1) / C::RPC);
-  const size_t shm = sizeof(double2) * (6 * C::HP * C::RPC + N);
+  const size_t shm = C::SMEM;
   SDNS_SET_SMEM((k_z_fused<N>), shm);
   k_z_fused<N><<<grid, C::THREADS, shm, s>>>(rows, cs, rm, norm, tw);
 }

@@ -27,7 +27,7 @@ namespace sdns_dev {
 
 namespace {
 
-enum : int { VX = 3, VY = 1, VYI = 0 };
+enum : int { VX = 3, VY = 1, VYI = 0, VXI = 4 };
 
 template <int N, int V>
 struct PipeCfg {
@@ -37,7 +37,7 @@ struct PipeCfg {
   static constexpr int CS0 = TPC >= 64 ? CSW : (512 / TPC > 64 ? 64 : 512 / TPC);
   static constexpr int CS = N >= 1024 ? 4 : CS0;
   static constexpr int THREADS = TPC * CS;
-  static constexpr int NBUF = (V == 2 || V == 3) ? 1 : 2;
+  static constexpr int NBUF = (V == 2 || V == 3 || V == 4) ? 1 : 2;
   static constexpr int MINB = V == 1 ? 3 : (V == 2 ? 4 : (V == 3 ? 2 : 1));
   static constexpr int TILE = N * CS;  // complex elements per tile buffer
   // tile buffers + the twiddle table
@@ -65,7 +65,7 @@ __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 struct Tile {
-  int row, kz;
+  long long base;  // row*rs + kz of this thread's column
   bool valid;
 };
 
@@ -82,24 +82,40 @@ struct TileIdx {
 
 template <int CS>
 __device__ __forceinline__ Tile tile_of(int tile, int col, const ColGeom& g) {
-  const long long gc = static_cast<long long>(tile) * CS + col;
+  const int gc = tile * CS + col;
+  const int re = gc / g.pitch;
+  const int kz = gc - re * g.pitch;
+  const int row = re < g.seg_a ? re + g.off0 : re - g.seg_a + g.off1;
   Tile t;
-  const int re = static_cast<int>(gc / g.pitch);
-  t.kz = static_cast<int>(gc - static_cast<long long>(re) * g.pitch);
-  t.valid = re < g.nrows && t.kz < g.n2;
-  t.row = re < g.seg_a ? re + g.off0 : re - g.seg_a + g.off1;
+  t.valid = re < g.nrows && kz < g.n2;
+  t.base = static_cast<long long>(row) * g.rs + kz;
   return t;
 }
 
+// Per-thread element offsets of positions t + m*TPC (fixed for the kernel).
+template <int N>
+struct PosOff {
+  int o[fft_elems(N)];
+  __device__ __forceinline__ PosOff(const ColGeom& g, int t) {
+    constexpr int E = fft_elems(N), TPC = N / E;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int pos = t + m * TPC;
+      o[m] = static_cast<int>(static_cast<long long>(pos >> g.pb_shift) * g.ps1 +
+                              static_cast<long long>(pos & ((1 << g.pb_shift) - 1)) * g.ps0);
+    }
+  }
+};
+
 template <int N, int CS>
-__device__ __forceinline__ void issue_tile(double2* buf, const double2* src, const ColGeom& g,
-                                           const Tile& tl, int col, int t) {
+__device__ __forceinline__ void issue_tile(double2* buf, const double2* src, const Tile& tl,
+                                           const PosOff<N>& po, int col, int t) {
   constexpr int E = fft_elems(N), TPC = N / E;
+  const double2* b = src + tl.base;
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const int pos = t + m * TPC;
-    const double2* p = tl.valid ? src + col_off(g, tl.row, pos, tl.kz) : src;
-    cp_async16(buf + TileIdx<CS>{}(pos) + col, p, tl.valid);
+    cp_async16(buf + TileIdx<CS>{}(pos) + col, tl.valid ? b + po.o[m] : src, tl.valid);
   }
 }
 
@@ -113,14 +129,16 @@ __device__ __forceinline__ void read_own(double2 (&v)[fft_elems(N)], const doubl
 
 template <int N>
 __device__ __forceinline__ void store_own(double2* dst, const double2 (&v)[fft_elems(N)],
-                                          const ColGeom& g, const Tile& tl, int t) {
+                                          const ColGeom& g, const Tile& tl, const PosOff<N>& po,
+                                          int t) {
   constexpr int E = fft_elems(N), TPC = N / E;
   if (!tl.valid) return;
+  double2* b = dst + tl.base;
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const int pos = t + m * TPC;
     if (g.keep_k >= 0 && pos > g.keep_k && pos < N - g.keep_k) continue;  // masked mode
-    dst[col_off(g, tl.row, pos, tl.kz)] = v[m];
+    b[po.o[m]] = v[m];
   }
 }
 
@@ -128,44 +146,54 @@ __device__ __forceinline__ double2 times_i(double2 a) { return make_double2(-a.y
 __device__ __forceinline__ double2 times_mi(double2 a) { return make_double2(a.y, -a.x); }
 
 // Generic persistent pipeline driver: `items` items per tile; src(f) gives
-// the input field of item f; body(f, buf, tile, col, t, twiddles) transforms.
+// the input field of item f; body(f, buf, tile, pos_offsets, col, t,
+// twiddles) transforms.
 template <int N, int V, class SrcF, class BodyF>
 __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g, SrcF src,
                                          const double2* __restrict__ tw_global, BodyF body) {
   extern __shared__ double2 smem[];
   constexpr int CS = PipeCfg<N, V>::CS, NBUF = PipeCfg<N, V>::NBUF;
   const int col = threadIdx.x % CS, t = threadIdx.x / CS;
+  const PosOff<N> po(g, t);
   double2* buf[2] = {smem, smem + (NBUF - 1) * N * CS};
   double2* tws = smem + NBUF * N * CS;
   load_twiddles(tws, tw_global, N);  // visible after the first __syncthreads below
   const int G = gridDim.x;
-  auto tile_at = [&](long long i) { return static_cast<int>(blockIdx.x + (i / items) * G); };
+  int f = 0, tile = blockIdx.x;
   if (NBUF == 1) {
-    for (long long i = 0; tile_at(i) < ntiles; ++i) {
-      const Tile tl = tile_of<CS>(tile_at(i), col, g);
-      issue_tile<N, CS>(buf[0], src(static_cast<int>(i % items)), g, tl, col, t);
+    for (; tile < ntiles;) {
+      const Tile tl = tile_of<CS>(tile, col, g);
+      issue_tile<N, CS>(buf[0], src(f), tl, po, col, t);
       cp_commit();
       cp_wait0();
       __syncthreads();
-      body(static_cast<int>(i % items), buf[0], tl, col, t, static_cast<const double2*>(tws));
+      body(f, buf[0], tl, po, col, t, static_cast<const double2*>(tws));
       __syncthreads();
+      if (++f == items) {
+        f = 0;
+        tile += G;
+      }
     }
     return;
   }
-  if (tile_at(0) < ntiles)
-    issue_tile<N, CS>(buf[0], src(0), g, tile_of<CS>(tile_at(0), col, g), col, t);
+  Tile cur = tile_of<CS>(tile, col, g);
+  if (tile < ntiles) issue_tile<N, CS>(buf[0], src(0), cur, po, col, t);
   cp_commit();
-  for (long long i = 0; tile_at(i) < ntiles; ++i) {
-    const long long j = i + 1;
-    const int tj = tile_at(j);
-    if (tj < ntiles)
-      issue_tile<N, CS>(buf[j & 1], src(static_cast<int>(j % items)), g, tile_of<CS>(tj, col, g),
-                        col, t);
+  for (int i = 0; tile < ntiles; ++i) {
+    int fn = f + 1, tn = tile;
+    if (fn == items) {
+      fn = 0;
+      tn += G;
+    }
+    const Tile nxt = tile_of<CS>(tn, col, g);
+    if (tn < ntiles) issue_tile<N, CS>(buf[(i + 1) & 1], src(fn), nxt, po, col, t);
     cp_commit();
     cp_wait1();
     __syncthreads();
-    body(static_cast<int>(i % items), buf[i & 1], tile_of<CS>(tile_at(i), col, g), col, t,
-         static_cast<const double2*>(tws));
+    body(f, buf[i & 1], cur, po, col, t, static_cast<const double2*>(tws));
+    f = fn;
+    tile = tn;
+    cur = nxt;
   }
 }
 
@@ -180,12 +208,13 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
              ColGeom g, int ntiles, const double2* __restrict__ tw) {
   constexpr int CS = PipeCfg<N, V>::CS;
   pipeline<N, V>(ntiles, nfields, g, [&](int f) { return in + f * in_cs; }, tw,
-                 [&](int f, double2* buf, const Tile& tl, int col, int t, const double2* tws) {
+                 [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po, int col,
+                     int t, const double2* tws) {
                    double2 v[fft_elems(N)];
                    read_own<N, CS>(v, buf, col, t);
                    __syncthreads();
                    block_fft<N, S>(v, buf + col, TileIdx<CS>{}, t, tws);
-                   store_own<N>(out + f * out_cs, v, g, tl, t);
+                   store_own<N>(out + f * out_cs, v, g, tl, po, t);
                  });
 }
 
@@ -198,7 +227,8 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
             int ntiles, const double2* __restrict__ tw) {
   constexpr int CS = PipeCfg<N, V>::CS, E = fft_elems(N), TPC = N / E;
   pipeline<N, V>(ntiles, 3, g, [&](int f) { return u + f * u_cs; }, tw,
-                 [&](int f, double2* buf, const Tile& tl, int col, int t, const double2* tws) {
+                 [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po, int col,
+                     int t, const double2* tws) {
                    double2 vin[E], v[E];
                    read_own<N, CS>(vin, buf, col, t);
                    __syncthreads();
@@ -209,12 +239,12 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                        v[m] = make_double2(kx * vin[m].x, kx * vin[m].y);
                      }
                      block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(out + (2 + f) * out_cs, v, g, tl, t);
+                     store_own<N>(out + (2 + f) * out_cs, v, g, tl, po, t);
                    }
 #pragma unroll
                    for (int m = 0; m < E; ++m) v[m] = vin[m];
                    block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
-                   store_own<N>(out + f * out_cs, v, g, tl, t);
+                   store_own<N>(out + f * out_cs, v, g, tl, po, t);
                  });
 }
 
@@ -231,7 +261,8 @@ k_pipe_yinv(double2* f, long long cs, ColGeom g, int ntiles, const double2* __re
   constexpr int CS = PipeCfg<N, V>::CS, E = fft_elems(N), TPC = N / E;
   const int order[5] = {0, 3, 1, 2, 4};
   pipeline<N, V>(ntiles, 5, g, [&](int it) { return f + order[it] * cs; }, tw,
-                 [&](int it, double2* buf, const Tile& tl, int col, int t, const double2* tws) {
+                 [&](int it, double2* buf, const Tile& tl, const PosOff<N>& po, int col,
+                     int t, const double2* tws) {
                    double2 vin[E], v[E];
                    read_own<N, CS>(vin, buf, col, t);
                    __syncthreads();
@@ -243,27 +274,26 @@ k_pipe_yinv(double2* f, long long cs, ColGeom g, int ntiles, const double2* __re
                        v[m] = it == 0 ? a : times_i(a);
                      }
                      block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(f + (it == 0 ? 5 : 3) * cs, v, g, tl, t);
+                     store_own<N>(f + (it == 0 ? 5 : 3) * cs, v, g, tl, po, t);
                    }
                    if (it == 1) {  // K1 -> w2 = i (F(K1) - D)
                      block_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
                      if (tl.valid) {
-                       double2* w2 = f + 5 * cs;
+                       double2* w2 = f + 5 * cs + tl.base;
 #pragma unroll
                        for (int m = 0; m < E; ++m) {
-                         const long long o = col_off(g, tl.row, t + m * TPC, tl.kz);
-                         const double2 d = w2[o];
-                         w2[o] = times_i(make_double2(vin[m].x - d.x, vin[m].y - d.y));
+                         const double2 d = w2[po.o[m]];
+                         w2[po.o[m]] = times_i(make_double2(vin[m].x - d.x, vin[m].y - d.y));
                        }
                      }
                    } else if (it == 4) {  // K2 -> w1' = F(-i K2)
 #pragma unroll
                      for (int m = 0; m < E; ++m) v[m] = times_mi(vin[m]);
                      block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(f + 4 * cs, v, g, tl, t);
+                     store_own<N>(f + 4 * cs, v, g, tl, po, t);
                    } else {  // U0, U1, U2 -> u_c
                      block_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(f + order[it] * cs, vin, g, tl, t);
+                     store_own<N>(f + order[it] * cs, vin, g, tl, po, t);
                    }
                  });
 }
@@ -345,12 +375,12 @@ void col_plain(int n, int dir, bool xaxis, const double2* in, double2* out, long
 template <int N>
 static void x_inv_n(const double2* u, long long u_cs, double2* out, long long out_cs,
                     const ColGeom& g, const double2* tw, cudaStream_t s) {
-  using C = PipeCfg<N, VX>;
-  const long long nt = ntiles_of<N, VX>(g);
+  using C = PipeCfg<N, VXI>;
+  const long long nt = ntiles_of<N, VXI>(g);
   static int occ = 0;
-  const unsigned grid = persistent_grid(k_pipe_xinv<N, VX>, C::THREADS, C::SMEM, nt, &occ);
-  k_pipe_xinv<N, VX><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, g,
-                                                       static_cast<int>(nt), tw);
+  const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI>, C::THREADS, C::SMEM, nt, &occ);
+  k_pipe_xinv<N, VXI><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, g,
+                                                        static_cast<int>(nt), tw);
 }
 
 void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
