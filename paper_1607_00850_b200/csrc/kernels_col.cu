@@ -16,10 +16,10 @@
 // which is omega_hat = i k x u_hat (curl_hat, navier_stokes.cpp:52-72)
 // distributed over the three axes.
 //
-// Tile shapes (measured on B200 at n = 512): x passes (2 MB
-// position stride) prefer 8-column / 128 B tiles with one buffer and two
-// 512-thread CTAs per SM; y passes (4 KB stride) prefer 4-column tiles, two
-// buffers, three 256-thread CTAs per SM.
+// Tile shapes (measured on B200 at n = 512): 8-column / 128 B
+// tiles throughout; the two-FFT-per-item inverse passes run one 512-thread
+// CTA per SM with two buffers, the plain forward passes one buffer and two
+// CTAs per SM.
 #include "fft_core.cuh"
 #include "kernels.cuh"
 
@@ -27,7 +27,19 @@ namespace sdns_dev {
 
 namespace {
 
-enum : int { VX = 3, VY = 1, VYI = 0, VXI = 4 };
+#ifndef SDNS_VX
+#define SDNS_VX 3
+#endif
+#ifndef SDNS_VY
+#define SDNS_VY 3
+#endif
+#ifndef SDNS_VYI
+#define SDNS_VYI 0
+#endif
+#ifndef SDNS_VXI
+#define SDNS_VXI 0
+#endif
+enum : int { VX = SDNS_VX, VY = SDNS_VY, VYI = SDNS_VYI, VXI = SDNS_VXI };
 
 template <int N, int V>
 struct PipeCfg {
@@ -43,12 +55,6 @@ struct PipeCfg {
   // tile buffers + the twiddle table
   static constexpr size_t SMEM = sizeof(double2) * (NBUF * TILE + N);
 };
-
-__device__ __forceinline__ long long col_off(const ColGeom& g, int row, int pos, int kz) {
-  return static_cast<long long>(row) * g.rs +
-         static_cast<long long>(pos >> g.pb_shift) * g.ps1 +
-         static_cast<long long>(pos & ((1 << g.pb_shift) - 1)) * g.ps0 + kz;
-}
 
 __device__ __forceinline__ double wavenum(int j, int n) {
   return static_cast<double>(j <= n / 2 - 1 ? j : j - n);
