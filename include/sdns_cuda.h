@@ -98,6 +98,22 @@ int sdns_iso_init_host(int64_t n, uint64_t seed, double k0, double energy,
 /* Library build string. */
 const char* sdns_version(void);
 
+/* Device layout of a rank's fields: spectral components are
+ * s0 x planes of `prow` = s1 + 1 rows (one pad row) of `pitch` =
+ * round_up(s2, 8) complex; `np` = n / p; element counts per component. */
+typedef struct sdns_dev_layout {
+  int pitch, prow, np;
+  int64_t spec_cs, real_cs;
+} sdns_dev_layout;
+int sdns_device_layout(const sdns_config* cfg, int rank, sdns_dev_layout* out);
+/* The transpose plan the context executes for `nfields` fields: *count
+ * entries of (peer, source offset, destination offset, complex count),
+ * offsets relative to the x-layout / receive-layout work buffers. Replaces
+ * the pack -> all_to_all -> unpack of fft.cpp:89-122 (slab). out may be NULL
+ * to query the count. */
+int sdns_exchange_plan(const sdns_config* cfg, int rank, int inverse, int nfields,
+                       int64_t* out, int* count);
+
 /* ---- communicators (Communicator, transport.hpp:46-94) ------------------ */
 int sdns_comm_loopback(sdns_comm** out);                            /* transport.hpp:96-98 */
 /* Threads-as-ranks on ONE device (InProcessBackend, transport.hpp:109-131):

@@ -22,7 +22,7 @@ import numpy as np
 __all__ = [
     "SolverConfig", "Layout", "ConfigError", "ProtocolError", "CollectiveTimeout",
     "DivergenceError", "IoError", "CudaError", "SdnsError", "load_library", "validate",
-    "build_layout", "block_size", "block_start", "step_count", "spectrum_shells",
+    "build_layout", "device_layout", "exchange_plan", "block_size", "block_start", "step_count", "spectrum_shells",
     "iso_init", "Comm", "Context", "Field", "DistributedFFT", "curl_hat", "cross",
     "project", "pressure_hat", "compute_rhs", "Rk4State", "FlowStats", "collect_stats",
     "l2_diff", "run_group",
@@ -91,6 +91,11 @@ class _Layout(ctypes.Structure):
                 ("nstages", ctypes.c_int), ("stage_peers", ctypes.c_int * 2),
                 ("send_counts", (ctypes.c_int64 * MAX_PEERS) * 2),
                 ("recv_counts", (ctypes.c_int64 * MAX_PEERS) * 2)]
+
+
+class _DevLayout(ctypes.Structure):
+    _fields_ = [("pitch", ctypes.c_int), ("prow", ctypes.c_int), ("np", ctypes.c_int),
+                ("spec_cs", ctypes.c_int64), ("real_cs", ctypes.c_int64)]
 
 
 PASS_NAMES = ["x_inv_curl", "y_inv", "z_fused", "y_fwd", "x_fwd_tail", "x_fwd_rk0",
@@ -164,6 +169,8 @@ def load_library(path: str = LIB_PATH):
             "sdns_l2_diff": (I, [P, P, P, ctypes.POINTER(D)]),
             "sdns_ctx_timing": (I, [P, I]),
             "sdns_ctx_timing_read": (I, [P, P, P]),
+            "sdns_device_layout": (I, [ctypes.POINTER(_Config), I, ctypes.POINTER(_DevLayout)]),
+            "sdns_exchange_plan": (I, [ctypes.POINTER(_Config), I, I, I, P, ctypes.POINTER(I)]),
             "sdns_host_alloc": (P, [ctypes.c_size_t]),
             "sdns_host_free": (V, [P]),
         }
@@ -276,6 +283,28 @@ def build_layout(cfg: SolverConfig, rank: int) -> Layout:
     out = _Layout()
     _check(load_library().sdns_build_layout(ctypes.byref(c), rank, ctypes.byref(out)))
     return Layout._from_c(out)
+
+
+def device_layout(cfg: SolverConfig, rank: int) -> dict:
+    """Device field layout of a rank (include/sdns_cuda.h sdns_device_layout)."""
+    c = cfg.to_c()
+    out = _DevLayout()
+    _check(load_library().sdns_device_layout(ctypes.byref(c), rank, ctypes.byref(out)))
+    return {"pitch": out.pitch, "prow": out.prow, "np": out.np, "spec_cs": out.spec_cs,
+            "real_cs": out.real_cs}
+
+
+def exchange_plan(cfg: SolverConfig, rank: int, inverse: bool, nfields: int) -> np.ndarray:
+    """The transpose plan a context executes: rows (peer, src_off, dst_off, count)."""
+    c = cfg.to_c()
+    cnt = ctypes.c_int(0)
+    lib = load_library()
+    _check(lib.sdns_exchange_plan(ctypes.byref(c), rank, int(inverse), nfields, None,
+                                  ctypes.byref(cnt)))
+    out = np.zeros((cnt.value, 4), dtype=np.int64)
+    _check(lib.sdns_exchange_plan(ctypes.byref(c), rank, int(inverse), nfields, _ptr(out),
+                                  ctypes.byref(cnt)))
+    return out
 
 
 def block_size(total: int, parts: int, index: int) -> int:

@@ -13,6 +13,7 @@
 //        transpose / receive buffer of the forward one
 //   wb  "y layout"  [peer][x_l][y_l][pitch] x 6 comps -- the receive layout,
 //        read directly by the y pass (no unpack pass); aliases wa at p = 1.
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -55,6 +56,38 @@ int ilog2(long long v) {
 }
 
 bool is_pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// Device layout of one rank: spectral components are x planes
+// of `prow` = s1 + 1 rows (one pad row) of `pitch` = round_up(s2, 8) complex.
+sdns_dev_layout dev_layout(const sdns_config& cfg, const sdns_layout& lo) {
+  sdns_dev_layout d{};
+  d.pitch = static_cast<int>((lo.spec_shape[2] + 7) / 8 * 8);
+  d.prow = static_cast<int>(lo.spec_shape[1]) + 1;
+  d.np = cfg.n / cfg.p;
+  d.spec_cs = lo.spec_shape[0] * d.prow * d.pitch;
+  d.real_cs = lo.real_shape[0] * lo.real_shape[1] * lo.real_shape[2];
+  return d;
+}
+
+// Slab transpose plan: per field and peer q, the x planes [q np, (q+1) np)
+// of the x layout (wa) are one contiguous block; received blocks land back to
+// back as [q][x_l][y_l] planes -- the receive layout the y pass reads
+// directly (no pack/unpack pass; replaces fft.cpp:89-95 and :116-122).
+// Entries: (peer, offset in source, offset in destination, complex count);
+// inverse: wa -> wb, forward: wb -> wa.
+std::vector<std::array<long long, 4>> exchange_plan(const sdns_config& cfg, const sdns_layout& lo,
+                                                     bool inverse_dir, int nfields) {
+  const sdns_dev_layout d = dev_layout(cfg, lo);
+  const long long blk = static_cast<long long>(d.np) * d.prow * d.pitch;
+  std::vector<std::array<long long, 4>> plan;
+  for (int f = 0; f < nfields; ++f)
+    for (int q = 0; q < cfg.p; ++q) {
+      const long long off = f * d.spec_cs + q * blk;
+      plan.push_back({q, off, off, blk});
+    }
+  (void)inverse_dir;  // the slab plan is symmetric
+  return plan;
+}
 
 }  // namespace
 
@@ -213,17 +246,15 @@ struct sdns_ctx {
   void exchange(bool inverse_dir, int nfields) {
     if (cfg.p == 1) return;
     const int tk = tick(inverse_dir ? SDNS_PASS_A2A_INV : SDNS_PASS_A2A_FWD);
-    const long long blk = np * plane();
+    const auto plan = exchange_plan(cfg, lo, inverse_dir, nfields);
     std::vector<Xfer> xs;
-    xs.reserve(static_cast<size_t>(nfields) * cfg.p);
-    for (int f = 0; f < nfields; ++f)
-      for (int q = 0; q < cfg.p; ++q) {
-        double2* a = wa + f * spec_cs + q * blk;
-        double2* b = wb + f * spec_cs + q * blk;
-        const size_t bytes = sizeof(double2) * static_cast<size_t>(blk);
-        if (inverse_dir) xs.push_back({q, a, b, bytes, bytes});
-        else xs.push_back({q, b, a, bytes, bytes});
-      }
+    xs.reserve(plan.size());
+    double2* src = inverse_dir ? wa : wb;
+    double2* dst = inverse_dir ? wb : wa;
+    for (const auto& e : plan) {
+      const size_t bytes = sizeof(double2) * static_cast<size_t>(e[3]);
+      xs.push_back({static_cast<int>(e[0]), src + e[1], dst + e[2], bytes, bytes});
+    }
     world->alltoall(xs, stream);
     tock(tk);
   }
@@ -421,6 +452,21 @@ int sdns_build_layout(const sdns_config* cfg, int rank, sdns_layout* out) {
   return guarded([&] { *out = build_layout(*cfg, rank); });
 }
 
+int sdns_device_layout(const sdns_config* cfg, int rank, sdns_dev_layout* out) {
+  return guarded([&] { *out = dev_layout(*cfg, build_layout(*cfg, rank)); });
+}
+
+int sdns_exchange_plan(const sdns_config* cfg, int rank, int inverse, int nfields, int64_t* out,
+                       int* count) {
+  return guarded([&] {
+    const auto plan = exchange_plan(*cfg, build_layout(*cfg, rank), inverse != 0, nfields);
+    if (out)
+      for (size_t i = 0; i < plan.size(); ++i)
+        for (int j = 0; j < 4; ++j) out[4 * i + j] = plan[i][j];
+    if (count) *count = static_cast<int>(plan.size());
+  });
+}
+
 int64_t sdns_block_size(int64_t total, int parts, int index) { return block_size(total, parts, index); }
 int64_t sdns_block_start(int64_t total, int parts, int index) { return block_start(total, parts, index); }
 int64_t sdns_step_count(double t_end, double dt) { return step_count(t_end, dt); }
@@ -495,11 +541,12 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
       c->own_stream = true;
     }
     const long long n = cfg->n;
-    c->np = static_cast<int>(n / cfg->p);
-    c->pitch = static_cast<int>((c->lo.spec_shape[2] + 7) / 8 * 8);
-    c->prow = static_cast<int>(c->lo.spec_shape[1]) + 1;
-    c->spec_cs = c->lo.spec_shape[0] * c->prow * c->pitch;
-    c->real_cs = c->lo.real_shape[0] * c->lo.real_shape[1] * c->lo.real_shape[2];
+    const sdns_dev_layout dl = dev_layout(*cfg, c->lo);
+    c->np = dl.np;
+    c->pitch = dl.pitch;
+    c->prow = dl.prow;
+    c->spec_cs = dl.spec_cs;
+    c->real_cs = dl.real_cs;
     c->norm = 1.0 / (static_cast<double>(n) * static_cast<double>(n) * static_cast<double>(n));
     c->shells = spectrum_shells(n);
     c->tw = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * n));
