@@ -63,7 +63,7 @@ sdns_dev_layout dev_layout(const sdns_config& cfg, const sdns_layout& lo) {
   sdns_dev_layout d{};
   d.pitch = static_cast<int>((lo.spec_shape[2] + 7) / 8 * 8);
   d.prow = static_cast<int>(lo.spec_shape[1]) + 1;
-  d.np = cfg.n / cfg.p;
+  d.np = cfg.decomp == SDNS_PENCIL ? cfg.n / cfg.p1 : cfg.n / cfg.p;
   d.spec_cs = lo.spec_shape[0] * d.prow * d.pitch;
   d.real_cs = lo.real_shape[0] * lo.real_shape[1] * lo.real_shape[2];
   return d;
@@ -107,8 +107,20 @@ struct sdns_ctx {
   int prow = 0;            // rows per x plane incl. one pad row (s1 + 1)
   long long real_cs = 0;   // doubles per real component
   int pitch = 0;
-  int np = 0;              // slab block (n / p)
+  int np = 0;              // slab block n/p; pencil n/p1 (= x_l = y_l2)
   double norm = 1.0;
+  // Pencil (p = p1 x p2, fft.cpp:130-227): row group (same coord1, size p2,
+  // trades kz for y) and column group (same coord2, size p1, trades y for
+  // x). wc: row-send/receive layout [q][x_l][y_l][pitch]; wd: z lines as p2
+  // kz segments [q][x_l][y_l][pitch_q].
+  bool pencil = false;
+  std::shared_ptr<Comm> row, col;
+  double2* wc = nullptr;
+  double2* wd = nullptr;
+  long long cs_c = 0, cs_d = 0;
+  int yl = 0;  // real y block n/p2
+  std::vector<long long> seg_base;
+  std::vector<int> seg_pitch, seg_k0, seg_b;
   double* d_partial = nullptr;
   double* d_out = nullptr;
   double* h_out = nullptr;  // pinned
@@ -219,14 +231,74 @@ struct sdns_ctx {
   }
   RowMap zmap(bool by_xy) const {
     RowMap r;
+    r.n2 = static_cast<int>(lo.nf);
+    if (pencil) {  // z lines (x_l, y_l) spread over the p2 kz segments of wd
+      r.nrows = np * yl;
+      r.nseg = static_cast<int>(seg_base.size());
+      for (int q = 0; q < r.nseg; ++q) {
+        r.seg_base[q] = seg_base[static_cast<size_t>(q)];
+        r.seg_pitch[q] = seg_pitch[static_cast<size_t>(q)];
+        r.seg_k0[q] = seg_k0[static_cast<size_t>(q)];
+      }
+      r.seg_k0[r.nseg] = r.n2;
+      return r;
+    }
     r.nrows = np * cfg.n;
     r.rpp = np;
     r.ny = cfg.n;
     r.blk = by_xy ? np : 0;
     r.prow = prow;
     r.pitch = pitch;
-    r.n2 = static_cast<int>(lo.nf);
     return r;
+  }
+  // Pencil y pass over the row layout wc: element (x_l, y) at
+  // ((y/yl)*np + x_l)*yl*pitch + (y%yl)*pitch.
+  ColGeom ygeom_row() const {
+    ColGeom g;
+    g.rs = static_cast<long long>(yl) * pitch;
+    g.ps0 = pitch;
+    g.ps1 = static_cast<long long>(np) * yl * pitch;
+    g.pb_shift = ilog2(yl);
+    g.nrows = np;
+    g.n2 = static_cast<int>(lo.spec_shape[2]);
+    g.pitch = pitch;
+    return g;
+  }
+  // Pencil column-group transpose, wa <-> wb (x blocks <-> y2 blocks),
+  // fft.cpp:166-173 / :191-199 without the pack/unpack passes.
+  void exchange_col(bool inverse_dir, int nfields) {
+    const int tk = tick(inverse_dir ? SDNS_PASS_A2A_INV : SDNS_PASS_A2A_FWD);
+    const long long blk = np * plane();
+    std::vector<Xfer> xs;
+    double2* src = inverse_dir ? wa : wb;
+    double2* dst = inverse_dir ? wb : wa;
+    for (int f = 0; f < nfields; ++f)
+      for (int s = 0; s < cfg.p1; ++s) {
+        const long long off = f * spec_cs + s * blk;
+        const size_t bytes = sizeof(double2) * static_cast<size_t>(blk);
+        xs.push_back({s, src + off, dst + off, bytes, bytes});
+      }
+    col->alltoall(xs, stream);
+    tock(tk);
+  }
+  // Pencil row-group transpose, wc <-> wd: my kz block of every row peer's
+  // y slice <-> every peer's kz block of my y slice (unequal blocks when
+  // p2 does not divide n/2+1), fft.cpp:141-160 / :203-223.
+  void exchange_row(bool inverse_dir, int nfields) {
+    const int tk = tick(inverse_dir ? SDNS_PASS_A2A_INV : SDNS_PASS_A2A_FWD);
+    const long long rows = static_cast<long long>(np) * yl;
+    std::vector<Xfer> xs;
+    for (int f = 0; f < nfields; ++f)
+      for (int q = 0; q < cfg.p2; ++q) {
+        double2* c = wc + f * cs_c + q * rows * pitch;
+        double2* d = wd + f * cs_d + seg_base[static_cast<size_t>(q)];
+        const size_t cb = sizeof(double2) * static_cast<size_t>(rows * pitch);
+        const size_t db = sizeof(double2) * static_cast<size_t>(rows * seg_pitch[static_cast<size_t>(q)]);
+        if (inverse_dir) xs.push_back({q, c, d, cb, db});
+        else xs.push_back({q, d, c, db, cb});
+      }
+    row->alltoall(xs, stream);
+    tock(tk);
   }
   // Host block (s0, s1, s2) <-> device planes (s0, prow, pitch) copy.
   void copy_spec(void* dst, const void* src, bool to_device) const {
@@ -301,28 +373,62 @@ void post_launch(const char* what) {
 }
 
 // One fused RHS evaluation: P1 .. P5 (kernels.cu) with the transposes.
+// Pencil forward y pass geometry: reads the row layout (wc), writes the
+// column-send layout (wb); with the 2/3 rule on only kz < n/3 columns are
+// transformed and only |ky| < n/3 outputs stored.
+void pencil_yfwd_geoms(const sdns_ctx* c, bool prune, ColGeom& gi, ColGeom& go) {
+  gi = c->ygeom_row();
+  go = c->ygeom();
+  if (!prune || !c->cfg.dealias) return;
+  const int K = c->keep_k();
+  const int kzk = std::max(0, std::min(gi.n2, K + 1 - static_cast<int>(c->lo.spec_offset[2])));
+  gi.n2 = kzk;
+  gi.pitch = std::max(8, (kzk + 7) / 8 * 8);
+  go.keep_k = K;
+}
+
+// One fused RHS evaluation: P1 .. P5 (kernels*.cu) with the transposes.
 void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args_in) {
   const int n = c->cfg.n;
   cudaStream_t s = c->stream;
   int tk = c->tick(SDNS_PASS_X_INV_CURL);
   sdns_dev::x_inverse_split(n, u_in, c->spec_cs, c->wa, c->spec_cs, c->xgeom(), c->tw, s);
   c->tock(tk);
-  c->exchange(true, 5);
-  tk = c->tick(SDNS_PASS_Y_INV);
-  sdns_dev::y_inverse_curl(n, c->wb, c->spec_cs, c->ygeom(), c->tw, s);
-  c->tock(tk);
   // Forward direction: with the 2/3 rule on, modes the mask zeroes are never
   // computed or stored (kept modes are computed by identical transforms).
   RowMap zm = c->zmap(false);
   if (c->cfg.dealias) zm.kz_keep = c->keep_k() + 1;
-  tk = c->tick(SDNS_PASS_Z_FUSED);
-  sdns_dev::z_fused(n, c->wb, c->spec_cs, zm, c->norm, c->tw, s);
-  c->tock(tk);
-  tk = c->tick(SDNS_PASS_Y_FWD);
-  sdns_dev::col_plain(n, -1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, 3, c->ygeom_fwd(),
-                      c->tw, s);
-  c->tock(tk);
-  c->exchange(false, 3);
+  if (!c->pencil) {
+    c->exchange(true, 5);
+    tk = c->tick(SDNS_PASS_Y_INV);
+    sdns_dev::y_inverse_curl(n, c->wb, c->spec_cs, c->ygeom(), c->tw, s);
+    c->tock(tk);
+    tk = c->tick(SDNS_PASS_Z_FUSED);
+    sdns_dev::z_fused(n, c->wb, c->spec_cs, zm, c->norm, c->tw, s);
+    c->tock(tk);
+    tk = c->tick(SDNS_PASS_Y_FWD);
+    sdns_dev::col_plain(n, -1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, 3, c->ygeom_fwd(),
+                        c->tw, s);
+    c->tock(tk);
+    c->exchange(false, 3);
+  } else {
+    c->exchange_col(true, 5);
+    tk = c->tick(SDNS_PASS_Y_INV);
+    sdns_dev::y_inverse_curl_to(n, c->wb, c->wc, c->spec_cs, c->cs_c, c->ygeom(), c->ygeom_row(),
+                                c->tw, s);
+    c->tock(tk);
+    c->exchange_row(true, 6);
+    tk = c->tick(SDNS_PASS_Z_FUSED);
+    sdns_dev::z_fused(n, c->wd, c->cs_d, zm, c->norm, c->tw, s);
+    c->tock(tk);
+    c->exchange_row(false, 3);
+    ColGeom gi, go;
+    pencil_yfwd_geoms(c, true, gi, go);
+    tk = c->tick(SDNS_PASS_Y_FWD);
+    sdns_dev::col_plain_to(n, -1, c->wc, c->wb, c->cs_c, c->spec_cs, 3, gi, go, c->tw, s);
+    c->tock(tk);
+    c->exchange_col(false, 3);
+  }
   XfArgs a = args_in;
   a.nl = c->wa;
   a.nl_cs = c->spec_cs;
@@ -342,10 +448,23 @@ void fft_forward_impl(sdns_ctx* c, const sdns_field* real, sdns_field* spec) {
   const int n = c->cfg.n;
   cudaStream_t s = c->stream;
   const int nc = std::min(real->ncomp, spec->ncomp);
-  for (int f = 0; f < nc; ++f)
-    sdns_dev::z_r2c(n, real->real() + f * c->real_cs, c->wb + f * c->spec_cs, c->zmap(true), c->tw, s);
-  sdns_dev::col_plain(n, -1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw, s);
-  c->exchange(false, nc);
+  if (!c->pencil) {
+    for (int f = 0; f < nc; ++f)
+      sdns_dev::z_r2c(n, real->real() + f * c->real_cs, c->wb + f * c->spec_cs, c->zmap(true),
+                      c->tw, s);
+    sdns_dev::col_plain(n, -1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw,
+                        s);
+    c->exchange(false, nc);
+  } else {
+    for (int f = 0; f < nc; ++f)
+      sdns_dev::z_r2c(n, real->real() + f * c->real_cs, c->wd + f * c->cs_d, c->zmap(true), c->tw,
+                      s);
+    c->exchange_row(false, nc);
+    ColGeom gi, go;
+    pencil_yfwd_geoms(c, false, gi, go);
+    sdns_dev::col_plain_to(n, -1, c->wc, c->wb, c->cs_c, c->spec_cs, nc, gi, go, c->tw, s);
+    c->exchange_col(false, nc);
+  }
   sdns_dev::col_plain(n, -1, true, c->wa, spec->spec(), c->spec_cs, c->spec_cs, nc, c->xgeom(),
                       c->tw, s);
   post_launch("fft forward");
@@ -357,11 +476,22 @@ void fft_inverse_impl(sdns_ctx* c, const sdns_field* spec, sdns_field* real) {
   const int nc = std::min(real->ncomp, spec->ncomp);
   sdns_dev::col_plain(n, +1, true, spec->spec(), c->wa, c->spec_cs, c->spec_cs, nc, c->xgeom(),
                       c->tw, s);
-  c->exchange(true, nc);
-  sdns_dev::col_plain(n, +1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw, s);
-  for (int f = 0; f < nc; ++f)
-    sdns_dev::z_c2r(n, c->wb + f * c->spec_cs, real->real() + f * c->real_cs, c->zmap(true), c->norm,
-                    c->tw, s);
+  if (!c->pencil) {
+    c->exchange(true, nc);
+    sdns_dev::col_plain(n, +1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw,
+                        s);
+    for (int f = 0; f < nc; ++f)
+      sdns_dev::z_c2r(n, c->wb + f * c->spec_cs, real->real() + f * c->real_cs, c->zmap(true),
+                      c->norm, c->tw, s);
+  } else {
+    c->exchange_col(true, nc);
+    sdns_dev::col_plain_to(n, +1, c->wb, c->wc, c->spec_cs, c->cs_c, nc, c->ygeom(),
+                           c->ygeom_row(), c->tw, s);
+    c->exchange_row(true, nc);
+    for (int f = 0; f < nc; ++f)
+      sdns_dev::z_c2r(n, c->wd + f * c->cs_d, real->real() + f * c->real_cs, c->zmap(true),
+                      c->norm, c->tw, s);
+  }
   post_launch("fft inverse");
 }
 
@@ -526,8 +656,9 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
     if (!is_pow2(cfg->n) || cfg->n < 8 || cfg->n > 1024)
       config_error("the sm_100a path supports power-of-two n in [8, 1024], got n=" +
                    std::to_string(cfg->n));
-    if (cfg->decomp != SDNS_SLAB)
-      config_error("the sm_100a path implements the slab decomposition; pencil is not built yet");
+    if (cfg->decomp == SDNS_PENCIL && (!is_pow2(cfg->p1) || !is_pow2(cfg->p2) ||
+                                       cfg->p2 > sdns_dev::kMaxSeg))
+      config_error("the sm_100a pencil path needs power-of-two p1, p2 (p2 <= 16)");
     auto c = std::make_unique<sdns_ctx>();
     c->cfg = *cfg;
     c->lo = build_layout(*cfg, rank);
@@ -553,7 +684,31 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
     sdns_dev::make_twiddles(static_cast<int>(n), c->tw, c->stream);
     const size_t wbytes = sizeof(double2) * static_cast<size_t>(c->spec_cs) * 6;
     c->wa = static_cast<double2*>(dev_alloc(c.get(), wbytes));
-    c->wb = cfg->p == 1 ? c->wa : static_cast<double2*>(dev_alloc(c.get(), wbytes));
+    c->pencil = cfg->decomp == SDNS_PENCIL;
+    if (c->pencil) {
+      // collective: row group = same coord1 ordered by coord2, column group =
+      // same coord2 ordered by coord1 (fft.cpp:39-40)
+      c->row = c->world->split(c->lo.coord1, c->lo.coord2);
+      c->col = c->world->split(c->lo.coord2, c->lo.coord1);
+      c->yl = cfg->n / cfg->p2;
+      const long long rows = static_cast<long long>(c->np) * c->yl;
+      c->cs_c = rows * cfg->p2 * c->pitch;
+      long long base = 0;
+      for (int q = 0; q < cfg->p2; ++q) {
+        const int b = static_cast<int>(block_size(c->lo.nf, cfg->p2, q));
+        c->seg_b.push_back(b);
+        c->seg_k0.push_back(static_cast<int>(block_start(c->lo.nf, cfg->p2, q)));
+        c->seg_pitch.push_back((b + 7) / 8 * 8);
+        c->seg_base.push_back(base);
+        base += rows * c->seg_pitch.back();
+      }
+      c->cs_d = base;
+      c->wb = static_cast<double2*>(dev_alloc(c.get(), wbytes));
+      c->wc = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * static_cast<size_t>(c->cs_c) * 6));
+      c->wd = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * static_cast<size_t>(c->cs_d) * 6));
+    } else {
+      c->wb = cfg->p == 1 ? c->wa : static_cast<double2*>(dev_alloc(c.get(), wbytes));
+    }
     const int stride = c->shells + 3;
     const int nblk = std::max<int>(static_cast<int>(c->lo.spec_shape[0]), 592);
     c->d_partial = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride * nblk));
@@ -574,6 +729,8 @@ int sdns_ctx_destroy(sdns_ctx* c) {
     cudaStreamSynchronize(c->stream);
     cudaFree(c->tw);
     if (c->wb != c->wa) cudaFree(c->wb);
+    if (c->wc) cudaFree(c->wc);
+    if (c->wd) cudaFree(c->wd);
     cudaFree(c->wa);
     cudaFree(c->d_partial);
     cudaFree(c->d_out);

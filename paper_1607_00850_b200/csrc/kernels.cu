@@ -215,6 +215,14 @@ struct ZCfg {
   static constexpr int HP = N / 2 + 8;  // padded half-row (n/2+1 modes)
 };
 
+// Offset of element kz of z line ri: `ro` = zrow_off for unsegmented maps.
+__device__ __forceinline__ long long zel(const RowMap& rm, long long ro, int ri, int k) {
+  if (rm.nseg == 0) return ro + k;
+  int sg = 0;
+  while (sg + 1 < rm.nseg && k >= rm.seg_k0[sg + 1]) ++sg;
+  return rm.seg_base[sg] + static_cast<long long>(ri) * rm.seg_pitch[sg] + (k - rm.seg_k0[sg]);
+}
+
 __device__ __forceinline__ long long zrow_off(const RowMap& rm, int ri) {
   if (rm.blk == 0) {
     const int pl = ri / rm.rpp, r = ri - pl * rm.rpp;
@@ -268,7 +276,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   const int t = threadIdx.x % TPC, r = threadIdx.x / TPC;
   const int ri = blockIdx.x * RPC + r;
   const bool valid = ri < rm.nrows;
-  const long long ro = valid ? zrow_off(rm, ri) : 0;
+  const long long ro = (valid && rm.nseg == 0) ? zrow_off(rm, ri) : 0;
   // Stage the 6 half-rows once (coalesced, each element read once); the
   // staging area of pair p (2 half-rows, 2*HP >= n entries) then serves as
   // that pair's FFT exchange buffer. Pair results stay in registers.
@@ -286,8 +294,9 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
       const int k = k0 + t;
       if (k <= N / 2) {
         const double kz = static_cast<double>(k);
-        const double2 u0 = f[ro + k], u1 = f[cs + ro + k], u2 = f[2 * cs + ro + k];
-        const double2 a = f[3 * cs + ro + k], b = f[4 * cs + ro + k], c = f[5 * cs + ro + k];
+        const long long e = zel(rm, ro, ri, k);
+        const double2 u0 = f[e], u1 = f[cs + e], u2 = f[2 * cs + e];
+        const double2 a = f[3 * cs + e], b = f[4 * cs + e], c = f[5 * cs + e];
         S[k] = u0;
         S[HP + k] = u1;
         S[2 * HP + k] = u2;
@@ -336,17 +345,18 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   for (int m = 0; m < E; ++m) S[sw(t + m * TPC)] = v[m];
   bar();
   if (valid) {
-    double2* o0 = f + ro;
-    double2* o1 = f + cs + ro;
+    double2* o0 = f;
+    double2* o1 = f + cs;
 #pragma unroll
     for (int m = 0; m < E; ++m) {
       const int k = t + m * TPC;
       if (k <= N / 2 && k < rm.kz_keep) {  // kz >= n/3 is dealiased away
         const double2 d = S[sw(k)];
         const double2 e = cconj(S[sw((N - k) & (N - 1))]);
-        o0[k] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
+        const long long el = zel(rm, ro, ri, k);
+        o0[el] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
         const double2 dd = csub(d, e);
-        o1[k] = make_double2(0.5 * dd.y, -0.5 * dd.x);
+        o1[el] = make_double2(0.5 * dd.y, -0.5 * dd.x);
       }
     }
   }
@@ -354,11 +364,11 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   for (int m = 0; m < E; ++m) v[m] = make_double2(n2r[m], 0.0);
   block_fft<N, -1>(v, S + 2 * HP, sw, t, tws, bar);
   if (valid) {
-    double2* o2 = f + 2 * cs + ro;
+    double2* o2 = f + 2 * cs;
 #pragma unroll
     for (int m = 0; m < E; ++m) {
       const int k = t + m * TPC;
-      if (k <= N / 2 && k < rm.kz_keep) o2[k] = v[m];
+      if (k <= N / 2 && k < rm.kz_keep) o2[zel(rm, ro, ri, k)] = v[m];
     }
   }
 }
@@ -369,26 +379,31 @@ template <int N>
 __global__ void __launch_bounds__(ZCfg<N>::THREADS)
 k_z_c2r(const double2* __restrict__ spec, double* __restrict__ real, RowMap rm, double norm,
         const double2* __restrict__ tw) {
-  constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC;
+  constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC, HP = ZCfg<N>::HP;
   extern __shared__ double2 smem[];
   const int t = threadIdx.x % TPC, r = threadIdx.x / TPC;
   const int pr = blockIdx.x * ZCfg<N>::RPC + r;
   const int ri = 2 * pr;
   const bool valid = ri < rm.nrows;
-  double2 v[E];
-  if (valid) {
-    const double2* A = spec + zrow_off(rm, ri);
-    const double2* B = spec + zrow_off(rm, ri + 1);
-#pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = pair_sample<N>(A, B, t + m * TPC);
-  } else {
-#pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = make_double2(0.0, 0.0);
-  }
-  double2* tws = smem + ZCfg<N>::RPC * N;
+  // stage both half-rows (a pencil z line is spread over kz blocks)
+  double2* S = smem + r * 2 * HP;
+  double2* tws = smem + ZCfg<N>::RPC * 2 * HP;
   load_twiddles(tws, tw, N);
+  if (valid) {
+    const long long ra = rm.nseg ? 0 : zrow_off(rm, ri);
+    const long long rb = rm.nseg ? 0 : zrow_off(rm, ri + 1);
+    for (int k = t; k <= N / 2; k += TPC) {
+      S[k] = spec[zel(rm, ra, ri, k)];
+      S[HP + k] = spec[zel(rm, rb, ri + 1, k)];
+    }
+  }
   __syncthreads();
-  block_fft<N, +1>(v, smem + r * N, SwzIdx{}, t, tws);
+  double2 v[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m)
+    v[m] = valid ? pair_sample<N>(S, S + HP, t + m * TPC) : make_double2(0.0, 0.0);
+  __syncthreads();
+  block_fft<N, +1>(v, S, SwzIdx{}, t, tws);
   if (valid) {
     double* a = real + static_cast<long long>(ri) * N;
     double* b = a + N;
@@ -431,17 +446,17 @@ k_z_r2c(const double* __restrict__ real, double2* __restrict__ spec, RowMap rm,
   for (int m = 0; m < E; ++m) reg[sw(t + m * TPC)] = v[m];
   __syncthreads();
   if (valid) {
-    double2* oa = spec + zrow_off(rm, ri);
-    double2* ob = spec + zrow_off(rm, ri + 1);
+    const long long ra = rm.nseg ? 0 : zrow_off(rm, ri);
+    const long long rb = rm.nseg ? 0 : zrow_off(rm, ri + 1);
 #pragma unroll
     for (int m = 0; m < E; ++m) {
       const int k = t + m * TPC;
       if (k <= N / 2) {
         const double2 d = reg[sw(k)];
         const double2 e = cconj(reg[sw((N - k) & (N - 1))]);
-        oa[k] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
+        spec[zel(rm, ra, ri, k)] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
         const double2 dd = csub(d, e);
-        ob[k] = make_double2(0.5 * dd.y, -0.5 * dd.x);
+        spec[zel(rm, rb, ri + 1, k)] = make_double2(0.5 * dd.y, -0.5 * dd.x);
       }
     }
   }
@@ -794,7 +809,7 @@ static void z_c2r_n(const double2* spec, double* real, const RowMap& rm, double 
   using C = ZCfg<N>;
   const int pairs = rm.nrows / 2;
   const unsigned grid = static_cast<unsigned>((pairs + C::RPC - 1) / C::RPC);
-  const size_t shm = sizeof(double2) * (N * C::RPC + N);
+  const size_t shm = sizeof(double2) * (2 * C::HP * C::RPC + N);
   SDNS_SET_SMEM((k_z_c2r<N>), shm);
   k_z_c2r<N><<<grid, C::THREADS, shm, s>>>(spec, real, rm, norm, tw);
 }

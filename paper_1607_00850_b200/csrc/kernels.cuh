@@ -40,6 +40,8 @@ struct WaveGeom {
   int kz_off = 0;    // global kz offset of kz index 0
 };
 
+constexpr int kMaxSeg = 16;  // max pencil p2
+
 // Row mapping for the z passes. Spectral rows live in planes of `prow`
 // rows (the last row of each plane is padding, so that the plane stride is
 // an odd multiple of 128 B and strided x-pass accesses spread over all HBM
@@ -55,6 +57,13 @@ struct RowMap {
   int pitch = 0;     // spectral row pitch (complex)
   int n2 = 0;        // valid kz entries (n/2+1 for a full z line)
   int kz_keep = 1 << 30;  // forward outputs stored only for kz < kz_keep
+  // Pencil: a z line is assembled from nseg kz blocks (one per row peer,
+  // fft.cpp:141-160); block q holds rows ri at seg_base[q] + ri*seg_pitch[q]
+  // for kz in [seg_k0[q], seg_k0[q+1]). nseg == 0: the row maps above.
+  int nseg = 0;
+  long long seg_base[kMaxSeg] = {};
+  int seg_pitch[kMaxSeg] = {};
+  int seg_k0[kMaxSeg + 1] = {};
 };
 
 // Fused x-pass forward epilogue variants.
@@ -97,6 +106,14 @@ void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long
 // P2: in place, fields [U0, U1, U2, K1, K2] -> [u0, u1, u2, w0', w1', w2]
 void y_inverse_curl(int n, double2* f, long long cs, const ColGeom& g, const double2* tw,
                     cudaStream_t s);
+// Same, reading geometry g of `fin` and writing geometry go of `fout`
+// (pencil: col-receive layout in, row-send layout out).
+void y_inverse_curl_to(int n, const double2* fin, double2* fout, long long cs_in, long long cs_out,
+                       const ColGeom& g, const ColGeom& go, const double2* tw, cudaStream_t s);
+// Plain column transform with a separate output geometry (pencil y passes).
+void col_plain_to(int n, int dir, const double2* in, double2* out, long long in_cs,
+                  long long out_cs, int nfields, const ColGeom& g, const ColGeom& go,
+                  const double2* tw, cudaStream_t s);
 struct SpecGeom;
 // P5b: mask + projection + viscous + RK4 stage update, streaming over the
 // x layout (a.nl holds the x-forward-transformed nonlinear term).

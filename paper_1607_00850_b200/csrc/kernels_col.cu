@@ -72,6 +72,7 @@ __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0
 
 struct Tile {
   long long base;  // row*rs + kz of this thread's column
+  int row, kz;
   bool valid;
 };
 
@@ -94,6 +95,8 @@ __device__ __forceinline__ Tile tile_of(int tile, int col, const ColGeom& g) {
   const int row = re < g.seg_a ? re + g.off0 : re - g.seg_a + g.off1;
   Tile t;
   t.valid = re < g.nrows && kz < g.n2;
+  t.row = row;
+  t.kz = kz;
   t.base = static_cast<long long>(row) * g.rs + kz;
   return t;
 }
@@ -147,6 +150,28 @@ __device__ __forceinline__ void store_own(double2* dst, const double2 (&v)[fft_e
     b[po.o[m]] = v[m];
   }
 }
+
+// Output placement: the input geometry (in-place passes) or a separate one
+// (pencil y passes write the next transpose's send layout directly).
+template <int N, bool SEP>
+struct OutSel;
+template <int N>
+struct OutSel<N, false> {
+  __device__ __forceinline__ OutSel(const ColGeom&, int) {}
+  __device__ __forceinline__ Tile tile(const Tile& t, const ColGeom&) const { return t; }
+  __device__ __forceinline__ const PosOff<N>& po(const PosOff<N>& in) const { return in; }
+};
+template <int N>
+struct OutSel<N, true> {
+  PosOff<N> p;
+  __device__ __forceinline__ OutSel(const ColGeom& go, int t) : p(go, t) {}
+  __device__ __forceinline__ Tile tile(const Tile& t, const ColGeom& go) const {
+    Tile o = t;
+    o.base = static_cast<long long>(t.row) * go.rs + t.kz;
+    return o;
+  }
+  __device__ __forceinline__ const PosOff<N>& po(const PosOff<N>&) const { return p; }
+};
 
 __device__ __forceinline__ double2 times_i(double2 a) { return make_double2(-a.y, a.x); }
 __device__ __forceinline__ double2 times_mi(double2 a) { return make_double2(a.y, -a.x); }
@@ -208,11 +233,12 @@ __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g
 // ---------------------------------------------------------------------------
 // Plain multi-field column transform (y passes, x-forward, API passes).
 
-template <int N, int S, int V>
+template <int N, int S, int V, bool SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs, int nfields,
-             ColGeom g, int ntiles, const double2* __restrict__ tw) {
+             ColGeom g, ColGeom go, int ntiles, const double2* __restrict__ tw) {
   constexpr int CS = PipeCfg<N, V>::CS;
+  const OutSel<N, SEP> os(go, threadIdx.x / CS);
   pipeline<N, V>(ntiles, nfields, g, [&](int f) { return in + f * in_cs; }, tw,
                  [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po, int col,
                      int t, const double2* tws) {
@@ -220,7 +246,7 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
                    read_own<N, CS>(v, buf, col, t);
                    __syncthreads();
                    block_fft<N, S>(v, buf + col, TileIdx<CS>{}, t, tws);
-                   store_own<N>(out + f * out_cs, v, g, tl, po, t);
+                   store_own<N>(out + f * out_cs, v, go, os.tile(tl, go), os.po(po), t);
                  });
 }
 
@@ -261,12 +287,14 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
 // F_y(ky U0) parks in field 5 (re-read by the same thread in the next item
 // while the tile is still L2-resident).
 
-template <int N, int V>
+template <int N, int V, bool SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
-k_pipe_yinv(double2* f, long long cs, ColGeom g, int ntiles, const double2* __restrict__ tw) {
+k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGeom g, ColGeom go,
+            int ntiles, const double2* __restrict__ tw) {
   constexpr int CS = PipeCfg<N, V>::CS, E = fft_elems(N), TPC = N / E;
   const int order[5] = {0, 3, 1, 2, 4};
-  pipeline<N, V>(ntiles, 5, g, [&](int it) { return f + order[it] * cs; }, tw,
+  const OutSel<N, SEP> os(go, threadIdx.x / CS);
+  pipeline<N, V>(ntiles, 5, g, [&](int it) { return fin + order[it] * cs_in; }, tw,
                  [&](int it, double2* buf, const Tile& tl, const PosOff<N>& po, int col,
                      int t, const double2* tws) {
                    double2 vin[E], v[E];
@@ -280,26 +308,27 @@ k_pipe_yinv(double2* f, long long cs, ColGeom g, int ntiles, const double2* __re
                        v[m] = it == 0 ? a : times_i(a);
                      }
                      block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(f + (it == 0 ? 5 : 3) * cs, v, g, tl, po, t);
+                     store_own<N>(f + (it == 0 ? 5 : 3) * cs, v, go, os.tile(tl, go), os.po(po), t);
                    }
                    if (it == 1) {  // K1 -> w2 = i (F(K1) - D)
                      block_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
                      if (tl.valid) {
-                       double2* w2 = f + 5 * cs + tl.base;
+                       double2* w2 = f + 5 * cs + os.tile(tl, go).base;
+                       const PosOff<N>& p2 = os.po(po);
 #pragma unroll
                        for (int m = 0; m < E; ++m) {
-                         const double2 d = w2[po.o[m]];
-                         w2[po.o[m]] = times_i(make_double2(vin[m].x - d.x, vin[m].y - d.y));
+                         const double2 d = w2[p2.o[m]];
+                         w2[p2.o[m]] = times_i(make_double2(vin[m].x - d.x, vin[m].y - d.y));
                        }
                      }
                    } else if (it == 4) {  // K2 -> w1' = F(-i K2)
 #pragma unroll
                      for (int m = 0; m < E; ++m) v[m] = times_mi(vin[m]);
                      block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(f + 4 * cs, v, g, tl, po, t);
+                     store_own<N>(f + 4 * cs, v, go, os.tile(tl, go), os.po(po), t);
                    } else {  // U0, U1, U2 -> u_c
                      block_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(f + order[it] * cs, vin, g, tl, po, t);
+                     store_own<N>(f + order[it] * cs, vin, go, os.tile(tl, go), os.po(po), t);
                    }
                  });
 }
@@ -342,28 +371,35 @@ static long long ntiles_of(const ColGeom& g) {
   return (cols + PipeCfg<N, V>::CS - 1) / PipeCfg<N, V>::CS;
 }
 
-template <int N, int S, int V>
+template <int N, int S, int V, bool SEP>
 static void plain_launch(const double2* in, double2* out, long long in_cs, long long out_cs,
-                         int nfields, const ColGeom& g, const double2* tw, cudaStream_t s) {
+                         int nfields, const ColGeom& g, const ColGeom& go, const double2* tw,
+                         cudaStream_t s) {
   using C = PipeCfg<N, V>;
   const long long nt = ntiles_of<N, V>(g);
   if (nt <= 0) return;
   static int occ = 0;
-  const unsigned grid = persistent_grid(k_pipe_plain<N, S, V>, C::THREADS, C::SMEM, nt, &occ);
-  k_pipe_plain<N, S, V><<<grid, C::THREADS, C::SMEM, s>>>(in, out, in_cs, out_cs, nfields, g,
-                                                          static_cast<int>(nt), tw);
+  const unsigned grid =
+      persistent_grid(k_pipe_plain<N, S, V, SEP>, C::THREADS, C::SMEM, nt, &occ);
+  k_pipe_plain<N, S, V, SEP><<<grid, C::THREADS, C::SMEM, s>>>(in, out, in_cs, out_cs, nfields,
+                                                               g, go, static_cast<int>(nt), tw);
 }
 
 template <int N>
 static void col_plain_n(int dir, bool xaxis, const double2* in, double2* out, long long in_cs,
-                        long long out_cs, int nfields, const ColGeom& g, const double2* tw,
-                        cudaStream_t s) {
+                        long long out_cs, int nfields, const ColGeom& g, const ColGeom* go,
+                        const double2* tw, cudaStream_t s) {
+  if (go) {  // separate output layout (pencil y passes; y-shaped tiles)
+    if (dir < 0) plain_launch<N, -1, VY, true>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+    else plain_launch<N, +1, VY, true>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+    return;
+  }
   if (dir < 0) {
-    if (xaxis) plain_launch<N, -1, VX>(in, out, in_cs, out_cs, nfields, g, tw, s);
-    else plain_launch<N, -1, VY>(in, out, in_cs, out_cs, nfields, g, tw, s);
+    if (xaxis) plain_launch<N, -1, VX, false>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
+    else plain_launch<N, -1, VY, false>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
   } else {
-    if (xaxis) plain_launch<N, +1, VX>(in, out, in_cs, out_cs, nfields, g, tw, s);
-    else plain_launch<N, +1, VY>(in, out, in_cs, out_cs, nfields, g, tw, s);
+    if (xaxis) plain_launch<N, +1, VX, false>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
+    else plain_launch<N, +1, VY, false>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
   }
 }
 
@@ -372,7 +408,18 @@ void col_plain(int n, int dir, bool xaxis, const double2* in, double2* out, long
                cudaStream_t s) {
   switch (n) {
 #define X(NN) \
-  case NN: col_plain_n<NN>(dir, xaxis, in, out, in_cs, out_cs, nfields, g, tw, s); return;
+  case NN: col_plain_n<NN>(dir, xaxis, in, out, in_cs, out_cs, nfields, g, nullptr, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+void col_plain_to(int n, int dir, const double2* in, double2* out, long long in_cs,
+                  long long out_cs, int nfields, const ColGeom& g, const ColGeom& go,
+                  const double2* tw, cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: col_plain_n<NN>(dir, false, in, out, in_cs, out_cs, nfields, g, &go, tw, s); return;
     SDNS_FOR_N(X)
 #undef X
   }
@@ -400,19 +447,40 @@ void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long
 }
 
 template <int N>
-static void y_inv_n(double2* f, long long cs, const ColGeom& g, const double2* tw, cudaStream_t s) {
+static void y_inv_n(const double2* fin, double2* f, long long cs_in, long long cs,
+                    const ColGeom& g, const ColGeom* go, const double2* tw, cudaStream_t s) {
   using C = PipeCfg<N, VYI>;
   const long long nt = ntiles_of<N, VYI>(g);
-  static int occ = 0;
-  const unsigned grid = persistent_grid(k_pipe_yinv<N, VYI>, C::THREADS, C::SMEM, nt, &occ);
-  k_pipe_yinv<N, VYI><<<grid, C::THREADS, C::SMEM, s>>>(f, cs, g, static_cast<int>(nt), tw);
+  if (go) {
+    static int occ = 0;
+    const unsigned grid =
+        persistent_grid(k_pipe_yinv<N, VYI, true>, C::THREADS, C::SMEM, nt, &occ);
+    k_pipe_yinv<N, VYI, true><<<grid, C::THREADS, C::SMEM, s>>>(fin, f, cs_in, cs, g, *go,
+                                                                static_cast<int>(nt), tw);
+  } else {
+    static int occ = 0;
+    const unsigned grid =
+        persistent_grid(k_pipe_yinv<N, VYI, false>, C::THREADS, C::SMEM, nt, &occ);
+    k_pipe_yinv<N, VYI, false><<<grid, C::THREADS, C::SMEM, s>>>(fin, f, cs_in, cs, g, g,
+                                                                 static_cast<int>(nt), tw);
+  }
 }
 
 void y_inverse_curl(int n, double2* f, long long cs, const ColGeom& g, const double2* tw,
                     cudaStream_t s) {
   switch (n) {
 #define X(NN) \
-  case NN: y_inv_n<NN>(f, cs, g, tw, s); return;
+  case NN: y_inv_n<NN>(f, f, cs, cs, g, nullptr, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+void y_inverse_curl_to(int n, const double2* fin, double2* fout, long long cs_in, long long cs_out,
+                       const ColGeom& g, const ColGeom& go, const double2* tw, cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: y_inv_n<NN>(fin, fout, cs_in, cs_out, g, &go, tw, s); return;
     SDNS_FOR_N(X)
 #undef X
   }

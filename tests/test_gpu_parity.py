@@ -385,3 +385,97 @@ def test_inprocess_slab_rk4_matches_single_rank(p):
     for r in range(1, p):
         for a, b in zip(res[0][2], res[r][2]):
             assert a.energy == b.energy and a.enstrophy == b.enstrophy
+
+
+# --- pencil decomposition (fft.cpp:130-227) on one GPU ---------------------------
+
+PENCILS = [(2, 1), (1, 2), (2, 2), (2, 4), (4, 2)]
+
+
+@pytest.mark.parametrize("p1,p2", PENCILS)
+def test_inprocess_pencil_fft_matches_reference_golden_rule(p1, p2):
+    """Distributed forward/inverse on a p1 x p2 pencil grid vs the global FFT
+    (proj/tests/test_fft.cpp:73-110 runs pencil 1, 2x2, 2x4 at n = 8)."""
+    n = 16
+    rng = np.random.default_rng(9)
+    u = rng.uniform(-1, 1, (3, n, n, n))
+    expect = O.forward(u)
+    cfg = S.SolverConfig(n=n, decomp="pencil", p=p1 * p2, p1=p1, p2=p2)
+
+    def body(rank, comm):
+        with S.Context(cfg, rank=rank, comm=comm) as c:
+            fft = S.DistributedFFT(c)
+            lo = c.layout
+            fd = c.spectral_field()
+            fft.forward(c.real_field().upload(_scatter_real(u, lo)), fd)
+            back = c.real_field()
+            fft.inverse(fd, back)
+            return lo, fd.download(), back.download()
+
+    for lo, fu, back in S.run_group(p1 * p2, body):
+        assert np.abs(fu - _scatter_spec(expect, lo)).max() <= 1e-11 * np.abs(expect).max()
+        assert rel(back, _scatter_real(u, lo)) <= 1e-13
+
+
+def test_pencil_fft_golden_n8_2x4():
+    """The reference's own pencil 2x4 result at n = 8 (tests/golden)."""
+    n = 8
+    u = GOLD["fft8_u"]
+    cfg = S.SolverConfig(n=n, decomp="pencil", p=8, p1=2, p2=4)
+
+    def body(rank, comm):
+        with S.Context(cfg, rank=rank, comm=comm) as c:
+            fd = c.spectral_field()
+            S.DistributedFFT(c).forward(c.real_field().upload(_scatter_real(u, c.layout)), fd)
+            return c.layout, fd.download()
+
+    g = GOLD["fft8_pencil24"]
+    for lo, fu in S.run_group(8, body):
+        assert np.abs(fu - _scatter_spec(g, lo)).max() <= 1e-11 * np.abs(g).max()
+
+
+@pytest.mark.parametrize("p1,p2", [(2, 2), (2, 4)])
+def test_inprocess_pencil_rk4_matches_single_rank(p1, p2):
+    """Configs 4 construction at test size: iso field, pencil p1 x p2 vs p = 1."""
+    n = 32
+    lo1 = S.build_layout(S.SolverConfig(n=n), 0)
+    uh0 = S.iso_init(n, lo1)
+    _, f1 = run_gpu(n, uh0, 1e-3, 1e-3, 4, project_init=False)
+    cfg = S.SolverConfig(n=n, decomp="pencil", p=p1 * p2, p1=p1, p2=p2, nu=1e-3, dt=1e-3,
+                         t_end=4e-3, out_every=1)
+
+    def body(rank, comm):
+        with S.Context(cfg, rank=rank, comm=comm) as c:
+            lo = c.layout
+            st = S.Rk4State(c)
+            st.set(c.spectral_field().upload(S.iso_init(n, lo)))
+            rows = []
+            st.advance(lambda k, t: rows.append(S.collect_stats(c, st.u_hat, 1e-3, t)))
+            out = (lo, st.u_hat.download(), rows)
+            st.close()
+            return out
+
+    res = S.run_group(p1 * p2, body)
+    for lo, f, rows in res:
+        assert rel(f, _scatter_spec(f1, lo)) <= 1e-12
+    for r in range(1, p1 * p2):
+        for a, b in zip(res[0][2], res[r][2]):
+            assert a.energy == b.energy and a.enstrophy == b.enstrophy
+
+
+def test_pencil_compute_rhs_vs_reference_pencil(ref):
+    """compute_rhs on the reference's own pencil 2x2 decomposition."""
+    n = 16
+    uh = GOLD["rnd16_uh"]
+    expect = ref.compute_rhs(uh, n, 1e-3, decomp="pencil", p=4, p1=2, p2=2)
+    cfg = S.SolverConfig(n=n, decomp="pencil", p=4, p1=2, p2=2)
+
+    def body(rank, comm):
+        with S.Context(cfg, rank=rank, comm=comm) as c:
+            du = c.spectral_field()
+            S.compute_rhs(c, c.spectral_field().upload(_scatter_spec(uh, c.layout)), 1e-3, du)
+            return c.layout, du.download()
+
+    for lo, du in S.run_group(4, body):
+        e = _scatter_spec(expect, lo)
+        assert np.linalg.norm(du - e) <= 1e-12 * np.linalg.norm(expect)
