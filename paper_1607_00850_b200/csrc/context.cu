@@ -173,6 +173,7 @@ struct sdns_ctx {
     g.nrows = np;
     g.n2 = static_cast<int>(lo.spec_shape[2]);
     g.pitch = pitch;
+    g.row_off = static_cast<int>(lo.spec_offset[1]);
     return g;
   }
   WaveGeom xwave() const {

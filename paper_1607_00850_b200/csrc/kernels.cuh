@@ -29,6 +29,7 @@ struct ColGeom {
   int pitch = 0;  // kz slots per enumerated row (multiple of the tile width)
   int seg_a = 1 << 30, off0 = 0, off1 = 0;
   int keep_k = -1;
+  int row_off = 0;  // global index of storage row 0 (x pass: the y offset)
 };
 
 // Wavenumbers of a column pass: which physical axis the transform runs

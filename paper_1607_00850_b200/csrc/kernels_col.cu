@@ -271,6 +271,17 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                        v[m] = make_double2(kx * vin[m].x, kx * vin[m].y);
                      }
                      block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                     if (f == 1 && tl.valid) {
+                       // w2' = i (K1 - ky U0): ky is constant along an x column and
+                       // U0 was stored by this thread in item 0 (L2-resident)
+                       const double ky = wavenum(g.row_off + tl.row, N);
+                       const double2* u0 = out + tl.base;
+#pragma unroll
+                       for (int m = 0; m < E; ++m) {
+                         const double2 a = u0[po.o[m]];
+                         v[m] = times_i(make_double2(v[m].x - ky * a.x, v[m].y - ky * a.y));
+                       }
+                     }
                      store_own<N>(out + (2 + f) * out_cs, v, g, tl, po, t);
                    }
 #pragma unroll
@@ -292,7 +303,9 @@ __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGeom g, ColGeom go,
             int ntiles, const double2* __restrict__ tw) {
   constexpr int CS = PipeCfg<N, V>::CS, E = fft_elems(N), TPC = N / E;
-  const int order[5] = {0, 3, 1, 2, 4};
+  // items: U0, U1, w2' (field 3), U2, K2 -- field 3 is consumed before the U2
+  // item writes w0' over it
+  const int order[5] = {0, 1, 3, 2, 4};
   const OutSel<N, SEP> os(go, threadIdx.x / CS);
   pipeline<N, V>(ntiles, 5, g, [&](int it) { return fin + order[it] * cs_in; }, tw,
                  [&](int it, double2* buf, const Tile& tl, const PosOff<N>& po, int col,
@@ -300,27 +313,18 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
                    double2 vin[E], v[E];
                    read_own<N, CS>(vin, buf, col, t);
                    __syncthreads();
-                   if (it == 0 || it == 3) {  // U0 -> D = F(ky U0); U2 -> w0' = F(i ky U2)
+                   if (it == 3) {  // U2 -> w0' = F(i ky U2) (and u2 below)
 #pragma unroll
                      for (int m = 0; m < E; ++m) {
                        const double ky = wavenum(t + m * TPC, N);
-                       const double2 a = make_double2(ky * vin[m].x, ky * vin[m].y);
-                       v[m] = it == 0 ? a : times_i(a);
+                       v[m] = times_i(make_double2(ky * vin[m].x, ky * vin[m].y));
                      }
                      block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(f + (it == 0 ? 5 : 3) * cs, v, go, os.tile(tl, go), os.po(po), t);
+                     store_own<N>(f + 3 * cs, v, go, os.tile(tl, go), os.po(po), t);
                    }
-                   if (it == 1) {  // K1 -> w2 = i (F(K1) - D)
+                   if (it == 2) {  // w2' -> w2 = F(w2')
                      block_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
-                     if (tl.valid) {
-                       double2* w2 = f + 5 * cs + os.tile(tl, go).base;
-                       const PosOff<N>& p2 = os.po(po);
-#pragma unroll
-                       for (int m = 0; m < E; ++m) {
-                         const double2 d = w2[p2.o[m]];
-                         w2[p2.o[m]] = times_i(make_double2(vin[m].x - d.x, vin[m].y - d.y));
-                       }
-                     }
+                     store_own<N>(f + 5 * cs, vin, go, os.tile(tl, go), os.po(po), t);
                    } else if (it == 4) {  // K2 -> w1' = F(-i K2)
 #pragma unroll
                      for (int m = 0; m < E; ++m) v[m] = times_mi(vin[m]);
