@@ -251,6 +251,28 @@ __device__ __forceinline__ double2 pair_sample(const double2* A, const double2* 
   return make_double2(a.x - b.y, a.y + b.x);
 }
 
+// Same for A + iB with B = B' + SG i kz A (kz = the half-spectrum index):
+// the z part of the curl folded into the sampling.
+template <int N, int SG>
+__device__ __forceinline__ double2 pair_sample_kz(const double2* A, const double2* B, int pos) {
+  const int k = pos <= N / 2 ? pos : N - pos;
+  double2 a = A[k], b = B[k];
+  const double kz = static_cast<double>(k);
+  if (SG > 0)
+    b = make_double2(b.x - kz * a.y, b.y + kz * a.x);
+  else
+    b = make_double2(b.x + kz * a.y, b.y - kz * a.x);
+  if (pos == 0 || pos == N / 2) {
+    a.y = 0.0;
+    b.y = 0.0;
+  }
+  if (pos > N / 2) {
+    a = cconj(a);
+    b = cconj(b);
+  }
+  return make_double2(a.x - b.y, a.y + b.x);
+}
+
 struct WarpBar {
   __device__ __forceinline__ void operator()() const { __syncwarp(); }
 };
@@ -287,36 +309,37 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   if constexpr (TPC >= 64) bar = Bar{1 + r, TPC};
   const SwzIdx sw;
   if (valid) {
-    // fields: 0..2 = u, 3 = w0', 4 = w1', 5 = w2. The z part of the curl:
-    // w0 = w0' - i kz u1, w1 = w1' + i kz u0 (kz = global index on a full line)
+    // fields: 0..2 = u, 3 = w0', 4 = w1', 5 = w2, staged as the pairs
+    // (u0, w1') (u1, w0') (u2, w2): LDGSTS straight to shared memory, all of
+    // the row in flight at once. The z part of the curl (w0 = w0' - i kz u1,
+    // w1 = w1' + i kz u0) is applied when the pair is sampled.
 #pragma unroll
     for (int k0 = 0; k0 <= N / 2; k0 += TPC) {
       const int k = k0 + t;
       if (k <= N / 2) {
-        const double kz = static_cast<double>(k);
         const long long e = zel(rm, ro, ri, k);
-        const double2 u0 = f[e], u1 = f[cs + e], u2 = f[2 * cs + e];
-        const double2 a = f[3 * cs + e], b = f[4 * cs + e], c = f[5 * cs + e];
-        S[k] = u0;
-        S[HP + k] = u1;
-        S[2 * HP + k] = u2;
-        S[3 * HP + k] = make_double2(a.x + kz * u1.y, a.y - kz * u1.x);
-        S[4 * HP + k] = make_double2(b.x - kz * u0.y, b.y + kz * u0.x);
-        S[5 * HP + k] = c;
+        cp_async16(S + k, f + e, true);
+        cp_async16(S + HP + k, f + 4 * cs + e, true);
+        cp_async16(S + 2 * HP + k, f + cs + e, true);
+        cp_async16(S + 3 * HP + k, f + 3 * cs + e, true);
+        cp_async16(S + 4 * HP + k, f + 2 * cs + e, true);
+        cp_async16(S + 5 * HP + k, f + 5 * cs + e, true);
       }
     }
   }
+  cp_commit();
+  cp_wait0();
   __syncthreads();  // twiddles + staging
   double2 p1[E], v[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = pair_sample<N>(S, S + HP, t + m * TPC);
+  for (int m = 0; m < E; ++m) v[m] = pair_sample_kz<N, +1>(S, S + HP, t + m * TPC);
   bar();
   block_fft<N, +1>(v, S, sw, t, tws, bar);
   // pair 0 result parks in its own (now free) region at this thread's positions
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     S[sw(t + m * TPC)] = v[m];
-    v[m] = pair_sample<N>(S + 2 * HP, S + 3 * HP, t + m * TPC);
+    v[m] = pair_sample_kz<N, -1>(S + 2 * HP, S + 3 * HP, t + m * TPC);
   }
   bar();
   block_fft<N, +1>(v, S + 2 * HP, sw, t, tws, bar);
@@ -327,13 +350,13 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   }
   bar();
   block_fft<N, +1>(v, S + 4 * HP, sw, t, tws, bar);
-  // (u0,u1) = p0, (u2,w0) = p1, (w1,w2) = v; 1/n^3 then u x omega
+  // (u0,w1) = p0, (u1,w0) = p1, (u2,w2) = v; 1/n^3 then u x omega
   double n2r[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const double2 q0 = S[sw(t + m * TPC)];
-    const double ua = dmul(q0.x, norm), ub = dmul(q0.y, norm), uc = dmul(p1[m].x, norm);
-    const double wa = dmul(p1[m].y, norm), wb = dmul(v[m].x, norm), wc = dmul(v[m].y, norm);
+    const double ua = dmul(q0.x, norm), ub = dmul(p1[m].x, norm), uc = dmul(v[m].x, norm);
+    const double wa = dmul(p1[m].y, norm), wb = dmul(q0.y, norm), wc = dmul(v[m].y, norm);
     const double n0 = dsub(dmul(ub, wc), dmul(uc, wb));
     const double n1 = dsub(dmul(uc, wa), dmul(ua, wc));
     n2r[m] = dsub(dmul(ua, wb), dmul(ub, wa));

@@ -60,16 +60,6 @@ __device__ __forceinline__ double wavenum(int j, int n) {
   return static_cast<double>(j <= n / 2 - 1 ? j : j - n);
 }
 
-__device__ __forceinline__ void cp_async16(double2* dst, const double2* src, bool valid) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(sz)
-               : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
 struct Tile {
   long long base;  // row*rs + kz of this thread's column
   int row, kz;

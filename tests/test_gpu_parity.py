@@ -183,6 +183,16 @@ def test_compute_rhs_solenoidal_and_linear_in_nu():
 
 # --- RK4 trajectories -----------------------------------------------------------
 
+def spectrum_close(a, b, energy, rtol=1e-11, eps=1e-15):
+    """Shell spectra agree to rtol, or to the roundoff of the shell's modes:
+    a velocity error of eps * sqrt(E) moves a shell holding E_k by at most
+    2 sqrt(E_k) eps sqrt(E) (deep cascade shells, E_k / E ~ 1e-18, sit at
+    that level after a few steps whatever the FFT's rounding)."""
+    a, b = np.asarray(a), np.asarray(b)
+    tol = rtol * np.abs(b) + 2.0 * np.sqrt(np.abs(b)) * eps * np.sqrt(energy) + 1e-300
+    return bool(np.all(np.abs(a - b) <= tol))
+
+
 def run_gpu(n, uh0, nu, dt, steps, out_every=1, project_init=True):
     cfg = S.SolverConfig(n=n, nu=nu, dt=dt, t_end=steps * dt, out_every=out_every)
     with S.Context(cfg) as c:
@@ -206,7 +216,7 @@ def test_taylor_green_16_matches_reference_golden():
         assert r.t == gr[0]
         assert abs(r.energy - gr[1]) <= 1e-12 * gr[1]
         assert abs(r.enstrophy - gr[2]) <= 1e-12 * gr[2]
-        assert np.allclose(r.spectrum, gr[5:], rtol=1e-11, atol=1e-30)
+        assert spectrum_close(r.spectrum, gr[5:], gr[1])
     assert rel(final, GOLD["tg16_final"]) <= 1e-11
 
 

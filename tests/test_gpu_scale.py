@@ -17,6 +17,7 @@ import pytest
 
 import paper_1607_00850_b200 as S
 from oracle import sdns_np as O
+from test_gpu_parity import spectrum_close
 
 pytestmark = pytest.mark.gpu
 
@@ -89,7 +90,7 @@ def test_config2_256_ten_steps_vs_reference(ref):
     for r, g in zip(rows, gs):
         assert abs(r.energy - g[1]) <= 1e-12 * g[1]
         assert abs(r.enstrophy - g[2]) <= 1e-12 * g[2]
-        assert np.allclose(r.spectrum, g[5:], rtol=1e-10, atol=1e-30)
+        assert spectrum_close(r.spectrum, g[5:], g[1], rtol=1e-10)
     assert rel(final, gf) <= 1e-11
 
 
