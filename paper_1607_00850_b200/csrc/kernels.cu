@@ -34,12 +34,6 @@ __device__ __forceinline__ double wavenum(int j, int n) {
   return static_cast<double>(j <= n / 2 - 1 ? j : j - n);
 }
 
-__device__ __forceinline__ long long col_off(const ColGeom& g, int row, int pos, int kz) {
-  return static_cast<long long>(row) * g.rs +
-         static_cast<long long>(pos >> g.pb_shift) * g.ps1 +
-         static_cast<long long>(pos & ((1 << g.pb_shift) - 1)) * g.ps0 + kz;
-}
-
 // i * (a*x - b*y) for complex x, y and real a, b (curl component).
 __device__ __forceinline__ double2 i_cross(double a, double2 x, double b, double2 y) {
   const double re = dsub(dmul(a, x.x), dmul(b, y.x));

@@ -39,6 +39,9 @@ namespace {
 #ifndef SDNS_VXI
 #define SDNS_VXI 0
 #endif
+#ifndef SDNS_NB0
+#define SDNS_NB0 3
+#endif
 enum : int { VX = SDNS_VX, VY = SDNS_VY, VYI = SDNS_VYI, VXI = SDNS_VXI };
 
 template <int N, int V>
@@ -49,7 +52,8 @@ struct PipeCfg {
   static constexpr int CS0 = TPC >= 64 ? CSW : (512 / TPC > 64 ? 64 : 512 / TPC);
   static constexpr int CS = N >= 1024 ? 4 : CS0;
   static constexpr int THREADS = TPC * CS;
-  static constexpr int NBUF = (V == 2 || V == 3 || V == 4) ? 1 : 2;
+  static constexpr int NBUF = (V == 2 || V == 3 || V == 4) ? 1
+                             : (V == 0 && N == 512) ? SDNS_NB0 : 2;
   static constexpr int MINB = V == 1 ? 3 : (V == 2 ? 4 : (V == 3 ? 2 : 1));
   static constexpr int TILE = N * CS;  // complex elements per tile buffer
   // tile buffers + the twiddle table
@@ -163,6 +167,18 @@ struct OutSel<N, true> {
   __device__ __forceinline__ const PosOff<N>& po(const PosOff<N>&) const { return p; }
 };
 
+// Column transform; SDNS_NOFFT builds a memory-only variant (wrong results)
+// for A/B measurements of the pipelines' memory ceiling.
+template <int N, int S, class IDX>
+__device__ __forceinline__ void col_fft(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
+                                        const double2* __restrict__ tw) {
+#ifdef SDNS_NOFFT
+  __syncthreads();
+#else
+  block_fft<N, S>(v, sm, idx, t, tw);
+#endif
+}
+
 __device__ __forceinline__ double2 times_i(double2 a) { return make_double2(-a.y, a.x); }
 __device__ __forceinline__ double2 times_mi(double2 a) { return make_double2(a.y, -a.x); }
 
@@ -176,7 +192,6 @@ __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g
   constexpr int CS = PipeCfg<N, V>::CS, NBUF = PipeCfg<N, V>::NBUF;
   const int col = threadIdx.x % CS, t = threadIdx.x / CS;
   const PosOff<N> po(g, t);
-  double2* buf[2] = {smem, smem + (NBUF - 1) * N * CS};
   double2* tws = smem + NBUF * N * CS;
   load_twiddles(tws, tw_global, N);  // visible after the first __syncthreads below
   const int G = gridDim.x;
@@ -184,11 +199,11 @@ __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g
   if (NBUF == 1) {
     for (; tile < ntiles;) {
       const Tile tl = tile_of<CS>(tile, col, g);
-      issue_tile<N, CS>(buf[0], src(f), tl, po, col, t);
+      issue_tile<N, CS>(smem, src(f), tl, po, col, t);
       cp_commit();
       cp_wait0();
       __syncthreads();
-      body(f, buf[0], tl, po, col, t, static_cast<const double2*>(tws));
+      body(f, smem, tl, po, col, t, static_cast<const double2*>(tws));
       __syncthreads();
       if (++f == items) {
         f = 0;
@@ -197,24 +212,58 @@ __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g
     }
     return;
   }
-  Tile cur = tile_of<CS>(tile, col, g);
-  if (tile < ntiles) issue_tile<N, CS>(buf[0], src(0), cur, po, col, t);
-  cp_commit();
-  for (int i = 0; tile < ntiles; ++i) {
-    int fn = f + 1, tn = tile;
-    if (fn == items) {
-      fn = 0;
-      tn += G;
+  // NBUF-deep ring: items i+1 .. i+NBUF-1 are in flight while item i is
+  // transformed. The buffer refilled at step i is the one item i-1 used;
+  // block_fft ends with a barrier after its last shared-memory read, so no
+  // thread still reads it. Items run field-inner: the tiles in flight are one
+  // kz chunk of consecutive fields, and at any time the grid covers one
+  // contiguous range of tiles (measured better on the x axis than walking
+  // groups of adjacent tiles per CTA).
+  struct Item {
+    int t0, f;
+  };
+  auto adv = [&](Item it) {
+    if (++it.f == items) {
+      it.f = 0;
+      it.t0 += G;
     }
-    const Tile nxt = tile_of<CS>(tn, col, g);
-    if (tn < ntiles) issue_tile<N, CS>(buf[(i + 1) & 1], src(fn), nxt, po, col, t);
+    return it;
+  };
+  double2* ring[3] = {smem, smem + N * CS, smem + (NBUF > 2 ? 2 : 0) * N * CS};
+  Item cur{static_cast<int>(blockIdx.x), 0};
+  Tile tc = tile_of<CS>(cur.t0, col, g);
+  if (cur.t0 < ntiles) issue_tile<N, CS>(ring[0], src(0), tc, po, col, t);
+  cp_commit();
+  Item n1 = adv(cur);
+  Tile tn1 = tile_of<CS>(n1.t0, col, g);
+  if (NBUF > 2) {
+    if (n1.t0 < ntiles) issue_tile<N, CS>(ring[1], src(n1.f), tn1, po, col, t);
     cp_commit();
-    cp_wait1();
-    __syncthreads();
-    body(f, buf[i & 1], cur, po, col, t, static_cast<const double2*>(tws));
-    f = fn;
-    tile = tn;
-    cur = nxt;
+  }
+  for (int i = 0; cur.t0 < ntiles; ++i) {
+    if (NBUF > 2) {
+      const Item n2 = adv(n1);
+      const Tile tn2 = tile_of<CS>(n2.t0, col, g);
+      if (n2.t0 < ntiles) issue_tile<N, CS>(ring[(i + 2) % 3], src(n2.f), tn2, po, col, t);
+      cp_commit();
+      cp_wait2();
+      __syncthreads();
+      body(cur.f, ring[i % 3], tc, po, col, t, static_cast<const double2*>(tws));
+      cur = n1;
+      tc = tn1;
+      n1 = n2;
+      tn1 = tn2;
+    } else {
+      if (n1.t0 < ntiles) issue_tile<N, CS>(ring[(i + 1) & 1], src(n1.f), tn1, po, col, t);
+      cp_commit();
+      cp_wait1();
+      __syncthreads();
+      body(cur.f, ring[i & 1], tc, po, col, t, static_cast<const double2*>(tws));
+      cur = n1;
+      tc = tn1;
+      n1 = adv(n1);
+      tn1 = tile_of<CS>(n1.t0, col, g);
+    }
   }
 }
 
@@ -235,13 +284,14 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
                    double2 v[fft_elems(N)];
                    read_own<N, CS>(v, buf, col, t);
                    __syncthreads();
-                   block_fft<N, S>(v, buf + col, TileIdx<CS>{}, t, tws);
+                   col_fft<N, S>(v, buf + col, TileIdx<CS>{}, t, tws);
                    store_own<N>(out + f * out_cs, v, go, os.tile(tl, go), os.po(po), t);
                  });
 }
 
 // ---------------------------------------------------------------------------
-// P1: x inverse of u_hat -> [U0, U1, U2, K1, K2] (fields 0..4 of `out`).
+// P1: x inverse of u_hat -> [U0, U1, U2, w2', K2] (fields 0..4 of `out`),
+// w2' = i (F(kx u1) - ky U0).
 
 template <int N, int V>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
@@ -260,43 +310,45 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                        const double kx = wavenum(t + m * TPC, N);
                        v[m] = make_double2(kx * vin[m].x, kx * vin[m].y);
                      }
-                     block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
-                     if (f == 1 && tl.valid) {
+                     col_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                     if (f == 1) {
                        // w2' = i (K1 - ky U0): ky is constant along an x column and
-                       // U0 was stored by this thread in item 0 (L2-resident)
-                       const double ky = wavenum(g.row_off + tl.row, N);
-                       const double2* u0 = out + tl.base;
+                       // U0 of this tile was stored by item 0 (L2-resident)
+                       if (tl.valid) {
+                         const double ky = wavenum(g.row_off + tl.row, N);
+                         const double2* u0 = out + tl.base;
 #pragma unroll
-                       for (int m = 0; m < E; ++m) {
-                         const double2 a = u0[po.o[m]];
-                         v[m] = times_i(make_double2(v[m].x - ky * a.x, v[m].y - ky * a.y));
+                         for (int m = 0; m < E; ++m) {
+                           const double2 a = u0[po.o[m]];
+                           v[m] = times_i(make_double2(v[m].x - ky * a.x, v[m].y - ky * a.y));
+                         }
                        }
                      }
                      store_own<N>(out + (2 + f) * out_cs, v, g, tl, po, t);
                    }
 #pragma unroll
                    for (int m = 0; m < E; ++m) v[m] = vin[m];
-                   block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                   col_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
                    store_own<N>(out + f * out_cs, v, g, tl, po, t);
                  });
 }
 
 // ---------------------------------------------------------------------------
-// P2: y inverse, in place on fields 0..4 = [U0, U1, U2, K1, K2] of `f`,
-// producing [u0, u1, u2, w0', w1', w2] in fields 0..5. Items per tile in the
-// order U0, K1, U1, U2, K2 so that no field is overwritten before it is read;
-// F_y(ky U0) parks in field 5 (re-read by the same thread in the next item
-// while the tile is still L2-resident).
+// P2: y inverse of fields 0..4 = [U0, U1, U2, w2', K2] of `fin`, producing
+// [u0, u1, u2, w0', w1', w2] in fields 0..5 of `f` (in place for the slab
+// layouts). Items per tile in the order U0, U1, w2', U2, K2: field 3 (w2') is
+// consumed before the U2 item writes w0' over it.
 
 template <int N, int V, bool SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGeom g, ColGeom go,
             int ntiles, const double2* __restrict__ tw) {
   constexpr int CS = PipeCfg<N, V>::CS, E = fft_elems(N), TPC = N / E;
-  // items: U0, U1, w2' (field 3), U2, K2 -- field 3 is consumed before the U2
-  // item writes w0' over it
   const int order[5] = {0, 1, 3, 2, 4};
   const OutSel<N, SEP> os(go, threadIdx.x / CS);
+  auto put = [&](int field, const double2(&r)[E], const Tile& tl, const PosOff<N>& po, int t) {
+    store_own<N>(f + field * cs, r, go, os.tile(tl, go), os.po(po), t);
+  };
   pipeline<N, V>(ntiles, 5, g, [&](int it) { return fin + order[it] * cs_in; }, tw,
                  [&](int it, double2* buf, const Tile& tl, const PosOff<N>& po, int col,
                      int t, const double2* tws) {
@@ -309,20 +361,20 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
                        const double ky = wavenum(t + m * TPC, N);
                        v[m] = times_i(make_double2(ky * vin[m].x, ky * vin[m].y));
                      }
-                     block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(f + 3 * cs, v, go, os.tile(tl, go), os.po(po), t);
+                     col_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                     put(3, v, tl, po, t);
                    }
                    if (it == 2) {  // w2' -> w2 = F(w2')
-                     block_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(f + 5 * cs, vin, go, os.tile(tl, go), os.po(po), t);
+                     col_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
+                     put(5, vin, tl, po, t);
                    } else if (it == 4) {  // K2 -> w1' = F(-i K2)
 #pragma unroll
                      for (int m = 0; m < E; ++m) v[m] = times_mi(vin[m]);
-                     block_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(f + 4 * cs, v, go, os.tile(tl, go), os.po(po), t);
+                     col_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                     put(4, v, tl, po, t);
                    } else {  // U0, U1, U2 -> u_c
-                     block_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
-                     store_own<N>(f + order[it] * cs, vin, go, os.tile(tl, go), os.po(po), t);
+                     col_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
+                     put(order[it], vin, tl, po, t);
                    }
                  });
 }
