@@ -180,9 +180,19 @@ struct NamedBar {
 
 // One Stockham stage (and the rest, recursively). `sm` points at this
 // column's element 0 in shared memory; element x lives at sm[idx(x)].
-template <int N, int E, int S, int NS, class IDX, class BAR = CtaBar>
+// Final-stage twiddles held in registers by kernels that run several
+// transforms per thread (the z pass): W^k and W^{4k} of a last radix-8 stage
+// (k = the thread's butterfly index, forward sign); the other powers follow
+// by complex products (at most three roundings), replacing seven
+// shared-memory reads per butterfly.
+struct LastTw {
+  double2 w1, w4;
+};
+
+template <int N, int E, int S, int NS, class IDX, class BAR = CtaBar, bool LREG = false>
 __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx, int t,
-                                           const double2* __restrict__ tw, BAR bar = BAR{}) {
+                                           const double2* __restrict__ tw, BAR bar = BAR{},
+                                           LastTw lt = LastTw{}) {
   constexpr int REM = N / NS;
   constexpr int R = REM >= E ? E : REM;
   constexpr int NB = E / R;
@@ -195,7 +205,18 @@ __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx
     const int k = j & (NS - 1);
 #pragma unroll
     for (int r = 0; r < R; ++r) a[r] = v[b + r * NB];
-    if (NS > 1) {
+    if constexpr (LREG && LAST && NS > 1 && R == 8 && NB == 1) {
+      const double2 w1 = S < 0 ? lt.w1 : make_double2(lt.w1.x, -lt.w1.y);
+      const double2 w4 = S < 0 ? lt.w4 : make_double2(lt.w4.x, -lt.w4.y);
+      const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+      a[1] = cmul(a[1], w1);
+      a[2] = cmul(a[2], w2);
+      a[3] = cmul(a[3], w3);
+      a[4] = cmul(a[4], w4);
+      a[5] = cmul(a[5], cmul(w4, w1));
+      a[6] = cmul(a[6], cmul(w4, w2));
+      a[7] = cmul(a[7], cmul(w4, w3));
+    } else if (NS > 1) {
       constexpr int TOFF = tw_stage_off(N, E, NS);
 #pragma unroll
       for (int r = 1; r < R; ++r) a[r] = cmul(a[r], twiddle<S>(tw, TOFF + (r - 1) * NS + k));
@@ -215,7 +236,7 @@ __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = sm[idx(t + m * TPC)];
     bar();
-    fft_stages<N, E, S, NS * R, IDX, BAR>(v, sm, idx, t, tw, bar);
+    fft_stages<N, E, S, NS * R, IDX, BAR, LREG>(v, sm, idx, t, tw, bar, lt);
   }
 }
 
@@ -225,6 +246,24 @@ template <int N, int S, class IDX, class BAR = CtaBar>
 __device__ __forceinline__ void block_fft(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
                                           const double2* __restrict__ tw, BAR bar = BAR{}) {
   fft_stages<N, fft_elems(N), S, 1, IDX, BAR>(v, sm, idx, t, tw, bar);
+}
+
+// Same with the final-stage twiddles from registers (see LastTw).
+template <int N, int S, class IDX, class BAR>
+__device__ __forceinline__ void block_fft_lt(double2 (&v)[fft_elems(N)], double2* sm, IDX idx,
+                                             int t, const double2* __restrict__ tw, BAR bar,
+                                             const LastTw& lt) {
+  fft_stages<N, fft_elems(N), S, 1, IDX, BAR, true>(v, sm, idx, t, tw, bar, lt);
+}
+
+// LastTw of thread t for length-N transforms whose last stage is radix 8
+// with one butterfly per thread (tw = the stage-ordered table).
+template <int N>
+__device__ __forceinline__ LastTw last_twiddles(const double2* tw, int t) {
+  constexpr int NS = N / 8;
+  constexpr int TOFF = tw_stage_off(N, fft_elems(N), NS);
+  const int k = t & (NS - 1);
+  return LastTw{tw[TOFF + k], tw[TOFF + 3 * NS + k]};
 }
 
 // Copies the stage-ordered twiddle table of length-n transforms to shared

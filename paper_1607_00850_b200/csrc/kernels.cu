@@ -283,6 +283,18 @@ struct ZFCfg {
   static constexpr size_t SMEM = sizeof(double2) * (static_cast<size_t>(RPC) * 6 * HP + N);
 };
 
+// z-pass transform; SDNS_ZNOFFT builds a transform-free variant (wrong
+// results) for A/B measurements of the pass's memory/shared-memory floor.
+template <int N, int S, class Bar>
+__device__ __forceinline__ void zfft(double2 (&v)[fft_elems(N)], double2* sm, SwzIdx sw, int t,
+                                     const double2* tws, Bar bar, const LastTw& lt) {
+#ifdef SDNS_ZNOFFT
+  bar();
+#else
+  block_fft_lt<N, S>(v, sm, sw, t, tws, bar, lt);
+#endif
+}
+
 template <int N>
 __global__ void __launch_bounds__(ZFCfg<N>::THREADS, 2)
 k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __restrict__ tw) {
@@ -324,11 +336,12 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   cp_commit();
   cp_wait0();
   __syncthreads();  // twiddles + staging
+  const LastTw lt = last_twiddles<N>(tws, t);
   double2 p1[E], v[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) v[m] = pair_sample_kz<N, +1>(S, S + HP, t + m * TPC);
   bar();
-  block_fft<N, +1>(v, S, sw, t, tws, bar);
+  zfft<N, +1>(v, S, sw, t, tws, bar, lt);
   // pair 0 result parks in its own (now free) region at this thread's positions
 #pragma unroll
   for (int m = 0; m < E; ++m) {
@@ -336,14 +349,14 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
     v[m] = pair_sample_kz<N, -1>(S + 2 * HP, S + 3 * HP, t + m * TPC);
   }
   bar();
-  block_fft<N, +1>(v, S + 2 * HP, sw, t, tws, bar);
+  zfft<N, +1>(v, S + 2 * HP, sw, t, tws, bar, lt);
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     p1[m] = v[m];
     v[m] = pair_sample<N>(S + 4 * HP, S + 5 * HP, t + m * TPC);
   }
   bar();
-  block_fft<N, +1>(v, S + 4 * HP, sw, t, tws, bar);
+  zfft<N, +1>(v, S + 4 * HP, sw, t, tws, bar, lt);
   // (u0,w1) = p0, (u1,w0) = p1, (u2,w2) = v; 1/n^3 then u x omega
   double n2r[E];
 #pragma unroll
@@ -357,7 +370,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
     v[m] = make_double2(n0, n1);
   }
   bar();  // every thread has read its parked pair-0 values
-  block_fft<N, -1>(v, S, sw, t, tws, bar);
+  zfft<N, -1>(v, S, sw, t, tws, bar, lt);
 #pragma unroll
   for (int m = 0; m < E; ++m) S[sw(t + m * TPC)] = v[m];
   bar();
@@ -379,7 +392,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   }
 #pragma unroll
   for (int m = 0; m < E; ++m) v[m] = make_double2(n2r[m], 0.0);
-  block_fft<N, -1>(v, S + 2 * HP, sw, t, tws, bar);
+  zfft<N, -1>(v, S + 2 * HP, sw, t, tws, bar, lt);
   if (valid) {
     double2* o2 = f + 2 * cs;
 #pragma unroll

@@ -37,7 +37,7 @@ namespace {
 #define SDNS_VYI 0
 #endif
 #ifndef SDNS_VXI
-#define SDNS_VXI 0
+#define SDNS_VXI 8
 #endif
 #ifndef SDNS_NB0
 #define SDNS_NB0 3
@@ -55,9 +55,12 @@ struct PipeCfg {
   static constexpr int NBUF = (V == 2 || V == 3 || V == 4) ? 1
                              : (V == 0 && N == 512) ? SDNS_NB0 : 2;
   static constexpr int MINB = V == 1 ? 3 : (V == 2 ? 4 : (V == 3 ? 2 : 1));
+  // V = 8: one extra tile-sized exchange buffer (the x inverse pass runs its
+  // first transform there and re-reads the input tile for the second)
+  static constexpr int SCR = V == 8 ? 1 : 0;
   static constexpr int TILE = N * CS;  // complex elements per tile buffer
-  // tile buffers + the twiddle table
-  static constexpr size_t SMEM = sizeof(double2) * (NBUF * TILE + N);
+  // tile buffers + scratch + the twiddle table
+  static constexpr size_t SMEM = sizeof(double2) * ((NBUF + SCR) * TILE + N);
 };
 
 __device__ __forceinline__ double wavenum(int j, int n) {
@@ -81,6 +84,13 @@ struct TileIdx {
   }
 };
 
+// Shared-memory index of (position x, column col) of a tile buffer.
+template <int CS>
+struct CIdx {
+  int col;
+  __device__ __forceinline__ int operator()(int x) const { return TileIdx<CS>{}(x) + col; }
+};
+
 template <int CS>
 __device__ __forceinline__ Tile tile_of(int tile, int col, const ColGeom& g) {
   const int gc = tile * CS + col;
@@ -95,39 +105,38 @@ __device__ __forceinline__ Tile tile_of(int tile, int col, const ColGeom& g) {
   return t;
 }
 
-// Per-thread element offsets of positions t + m*TPC (fixed for the kernel).
+// Per-thread element offsets of positions t + m*TPC, evaluated on use (a
+// few integer ops) rather than held in E registers: the two-transform
+// inverse passes sit at the 128-register limit.
 template <int N>
 struct PosOff {
-  int o[fft_elems(N)];
-  __device__ __forceinline__ PosOff(const ColGeom& g, int t) {
-    constexpr int E = fft_elems(N), TPC = N / E;
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-      const int pos = t + m * TPC;
-      o[m] = static_cast<int>(static_cast<long long>(pos >> g.pb_shift) * g.ps1 +
-                              static_cast<long long>(pos & ((1 << g.pb_shift) - 1)) * g.ps0);
-    }
+  int t, ps0, ps1, shift;
+  __device__ __forceinline__ PosOff(const ColGeom& g, int t_)
+      : t(t_), ps0(static_cast<int>(g.ps0)), ps1(static_cast<int>(g.ps1)), shift(g.pb_shift) {}
+  __device__ __forceinline__ int o(int m) const {
+    const int pos = t + m * (N / fft_elems(N));
+    return (pos >> shift) * ps1 + (pos & ((1 << shift) - 1)) * ps0;
   }
 };
 
-template <int N, int CS>
+template <int N, class IDX>
 __device__ __forceinline__ void issue_tile(double2* buf, const double2* src, const Tile& tl,
-                                           const PosOff<N>& po, int col, int t) {
+                                           const PosOff<N>& po, IDX idx, int t) {
   constexpr int E = fft_elems(N), TPC = N / E;
   const double2* b = src + tl.base;
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const int pos = t + m * TPC;
-    cp_async16(buf + TileIdx<CS>{}(pos) + col, tl.valid ? b + po.o[m] : src, tl.valid);
+    cp_async16(buf + idx(pos), tl.valid ? b + po.o(m) : src, tl.valid);
   }
 }
 
-template <int N, int CS>
-__device__ __forceinline__ void read_own(double2 (&v)[fft_elems(N)], const double2* buf, int col,
+template <int N, class IDX>
+__device__ __forceinline__ void read_own(double2 (&v)[fft_elems(N)], const double2* buf, IDX idx,
                                          int t) {
   constexpr int E = fft_elems(N), TPC = N / E;
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = buf[TileIdx<CS>{}(t + m * TPC) + col];
+  for (int m = 0; m < E; ++m) v[m] = buf[idx(t + m * TPC)];
 }
 
 template <int N>
@@ -141,7 +150,7 @@ __device__ __forceinline__ void store_own(double2* dst, const double2 (&v)[fft_e
   for (int m = 0; m < E; ++m) {
     const int pos = t + m * TPC;
     if (g.keep_k >= 0 && pos > g.keep_k && pos < N - g.keep_k) continue;  // masked mode
-    b[po.o[m]] = v[m];
+    b[po.o(m)] = v[m];
   }
 }
 
@@ -169,42 +178,61 @@ struct OutSel<N, true> {
 
 // Column transform; SDNS_NOFFT builds a memory-only variant (wrong results)
 // for A/B measurements of the pipelines' memory ceiling.
-template <int N, int S, class IDX>
+template <int N, int S, class IDX, class BAR>
 __device__ __forceinline__ void col_fft(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
-                                        const double2* __restrict__ tw) {
+                                        const double2* __restrict__ tw, BAR bar) {
 #ifdef SDNS_NOFFT
-  __syncthreads();
+  bar();
 #else
-  block_fft<N, S>(v, sm, idx, t, tw);
+  block_fft<N, S>(v, sm, idx, t, tw, bar);
 #endif
 }
+
+// Lane roles: column-minor (col = tid % CS, t = tid / CS), so a warp's
+// global accesses are 32/CS positions x CS*16 B along kz. (Measured: warps
+// covering 8 positions x 64 B -- two independent half-CTAs of 4 columns each
+// -- are ~1.5x slower on both axes than 4 positions x 128 B.)
+template <int N, int V>
+struct Lanes {
+  using C = PipeCfg<N, V>;
+  int col, t;
+  CIdx<C::CS> idx;
+  CtaBar bar;
+  __device__ __forceinline__ Lanes() {
+    col = threadIdx.x % C::CS;
+    t = threadIdx.x / C::CS;
+    idx.col = col;
+  }
+};
 
 __device__ __forceinline__ double2 times_i(double2 a) { return make_double2(-a.y, a.x); }
 __device__ __forceinline__ double2 times_mi(double2 a) { return make_double2(a.y, -a.x); }
 
 // Generic persistent pipeline driver: `items` items per tile; src(f) gives
-// the input field of item f; body(f, buf, tile, pos_offsets, col, t,
+// the input field of item f; body(f, buf, tile, pos_offsets, lanes,
 // twiddles) transforms.
 template <int N, int V, class SrcF, class BodyF>
 __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g, SrcF src,
                                          const double2* __restrict__ tw_global, BodyF body) {
   extern __shared__ double2 smem[];
   constexpr int CS = PipeCfg<N, V>::CS, NBUF = PipeCfg<N, V>::NBUF;
-  const int col = threadIdx.x % CS, t = threadIdx.x / CS;
+  const Lanes<N, V> ln;
+  const int col = ln.col, t = ln.t;
   const PosOff<N> po(g, t);
-  double2* tws = smem + NBUF * N * CS;
-  load_twiddles(tws, tw_global, N);  // visible after the first __syncthreads below
+  double2* tws = smem + (NBUF + PipeCfg<N, V>::SCR) * N * CS;
+  load_twiddles(tws, tw_global, N);
+  __syncthreads();
   const int G = gridDim.x;
   int f = 0, tile = blockIdx.x;
   if (NBUF == 1) {
     for (; tile < ntiles;) {
       const Tile tl = tile_of<CS>(tile, col, g);
-      issue_tile<N, CS>(smem, src(f), tl, po, col, t);
+      issue_tile<N>(smem, src(f), tl, po, ln.idx, t);
       cp_commit();
       cp_wait0();
-      __syncthreads();
-      body(f, smem, tl, po, col, t, static_cast<const double2*>(tws));
-      __syncthreads();
+      ln.bar();
+      body(f, smem, tl, po, ln, static_cast<const double2*>(tws));
+      ln.bar();
       if (++f == items) {
         f = 0;
         tile += G;
@@ -229,36 +257,38 @@ __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g
     }
     return it;
   };
-  double2* ring[3] = {smem, smem + N * CS, smem + (NBUF > 2 ? 2 : 0) * N * CS};
+  // ring slot j at smem + j*N*CS (arithmetic, not a pointer array: that
+  // would live in local memory)
+  auto ring = [&](int j) { return smem + j * (N * CS); };
   Item cur{static_cast<int>(blockIdx.x), 0};
   Tile tc = tile_of<CS>(cur.t0, col, g);
-  if (cur.t0 < ntiles) issue_tile<N, CS>(ring[0], src(0), tc, po, col, t);
+  if (cur.t0 < ntiles) issue_tile<N>(ring(0), src(0), tc, po, ln.idx, t);
   cp_commit();
   Item n1 = adv(cur);
   Tile tn1 = tile_of<CS>(n1.t0, col, g);
   if (NBUF > 2) {
-    if (n1.t0 < ntiles) issue_tile<N, CS>(ring[1], src(n1.f), tn1, po, col, t);
+    if (n1.t0 < ntiles) issue_tile<N>(ring(1), src(n1.f), tn1, po, ln.idx, t);
     cp_commit();
   }
   for (int i = 0; cur.t0 < ntiles; ++i) {
     if (NBUF > 2) {
       const Item n2 = adv(n1);
       const Tile tn2 = tile_of<CS>(n2.t0, col, g);
-      if (n2.t0 < ntiles) issue_tile<N, CS>(ring[(i + 2) % 3], src(n2.f), tn2, po, col, t);
+      if (n2.t0 < ntiles) issue_tile<N>(ring((i + 2) % 3), src(n2.f), tn2, po, ln.idx, t);
       cp_commit();
       cp_wait2();
-      __syncthreads();
-      body(cur.f, ring[i % 3], tc, po, col, t, static_cast<const double2*>(tws));
+      ln.bar();
+      body(cur.f, ring(i % 3), tc, po, ln, static_cast<const double2*>(tws));
       cur = n1;
       tc = tn1;
       n1 = n2;
       tn1 = tn2;
     } else {
-      if (n1.t0 < ntiles) issue_tile<N, CS>(ring[(i + 1) & 1], src(n1.f), tn1, po, col, t);
+      if (n1.t0 < ntiles) issue_tile<N>(ring((i + 1) & 1), src(n1.f), tn1, po, ln.idx, t);
       cp_commit();
       cp_wait1();
-      __syncthreads();
-      body(cur.f, ring[i & 1], tc, po, col, t, static_cast<const double2*>(tws));
+      ln.bar();
+      body(cur.f, ring(i & 1), tc, po, ln, static_cast<const double2*>(tws));
       cur = n1;
       tc = tn1;
       n1 = adv(n1);
@@ -276,15 +306,15 @@ template <int N, int S, int V, bool SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs, int nfields,
              ColGeom g, ColGeom go, int ntiles, const double2* __restrict__ tw) {
-  constexpr int CS = PipeCfg<N, V>::CS;
-  const OutSel<N, SEP> os(go, threadIdx.x / CS);
+  const OutSel<N, SEP> os(go, Lanes<N, V>().t);
   pipeline<N, V>(ntiles, nfields, g, [&](int f) { return in + f * in_cs; }, tw,
-                 [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po, int col,
-                     int t, const double2* tws) {
+                 [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po,
+                     const Lanes<N, V>& ln, const double2* tws) {
+                   const int t = ln.t;
                    double2 v[fft_elems(N)];
-                   read_own<N, CS>(v, buf, col, t);
-                   __syncthreads();
-                   col_fft<N, S>(v, buf + col, TileIdx<CS>{}, t, tws);
+                   read_own<N>(v, buf, ln.idx, t);
+                   ln.bar();
+                   col_fft<N, S>(v, buf, ln.idx, t, tws, ln.bar);
                    store_own<N>(out + f * out_cs, v, go, os.tile(tl, go), os.po(po), t);
                  });
 }
@@ -297,20 +327,28 @@ template <int N, int V>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, ColGeom g,
             int ntiles, const double2* __restrict__ tw) {
-  constexpr int CS = PipeCfg<N, V>::CS, E = fft_elems(N), TPC = N / E;
+  constexpr int E = fft_elems(N), TPC = N / E;
+  constexpr bool SCR = PipeCfg<N, V>::SCR > 0;
+  extern __shared__ double2 smem[];
+  double2* const scr = smem + PipeCfg<N, V>::NBUF * N * PipeCfg<N, V>::CS;
   pipeline<N, V>(ntiles, 3, g, [&](int f) { return u + f * u_cs; }, tw,
-                 [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po, int col,
-                     int t, const double2* tws) {
-                   double2 vin[E], v[E];
-                   read_own<N, CS>(vin, buf, col, t);
-                   __syncthreads();
+                 [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po,
+                     const Lanes<N, V>& ln, const double2* tws) {
+                   const int t = ln.t;
+                   double2 v[E], vin[SCR ? 1 : E];
+                   read_own<N>(v, buf, ln.idx, t);
+                   if constexpr (!SCR) {
+#pragma unroll
+                     for (int m = 0; m < E; ++m) vin[m] = v[m];
+                   }
                    if (f > 0) {
+                     if constexpr (!SCR) ln.bar();  // the transform below reuses buf
 #pragma unroll
                      for (int m = 0; m < E; ++m) {
                        const double kx = wavenum(t + m * TPC, N);
-                       v[m] = make_double2(kx * vin[m].x, kx * vin[m].y);
+                       v[m] = make_double2(kx * v[m].x, kx * v[m].y);
                      }
-                     col_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                     col_fft<N, +1>(v, SCR ? scr : buf, ln.idx, t, tws, ln.bar);
                      if (f == 1) {
                        // w2' = i (K1 - ky U0): ky is constant along an x column and
                        // U0 of this tile was stored by item 0 (L2-resident)
@@ -319,16 +357,21 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                          const double2* u0 = out + tl.base;
 #pragma unroll
                          for (int m = 0; m < E; ++m) {
-                           const double2 a = u0[po.o[m]];
+                           const double2 a = u0[po.o(m)];
                            v[m] = times_i(make_double2(v[m].x - ky * a.x, v[m].y - ky * a.y));
                          }
                        }
                      }
                      store_own<N>(out + (2 + f) * out_cs, v, g, tl, po, t);
-                   }
+                     if constexpr (SCR) {
+                       read_own<N>(v, buf, ln.idx, t);
+                     } else {
 #pragma unroll
-                   for (int m = 0; m < E; ++m) v[m] = vin[m];
-                   col_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                       for (int m = 0; m < E; ++m) v[m] = vin[m];
+                     }
+                   }
+                   if (SCR || f == 0) ln.bar();  // buf is read; the transform reuses it
+                   col_fft<N, +1>(v, buf, ln.idx, t, tws, ln.bar);
                    store_own<N>(out + f * out_cs, v, g, tl, po, t);
                  });
 }
@@ -343,38 +386,40 @@ template <int N, int V, bool SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGeom g, ColGeom go,
             int ntiles, const double2* __restrict__ tw) {
-  constexpr int CS = PipeCfg<N, V>::CS, E = fft_elems(N), TPC = N / E;
-  const int order[5] = {0, 1, 3, 2, 4};
-  const OutSel<N, SEP> os(go, threadIdx.x / CS);
+  constexpr int E = fft_elems(N), TPC = N / E;
+  // field of item it: 0, 1, 3, 2, 4
+  auto order = [](int it) { return it ^ ((it >> 1) & ~(it >> 2) & 1); };
+  const OutSel<N, SEP> os(go, Lanes<N, V>().t);
   auto put = [&](int field, const double2(&r)[E], const Tile& tl, const PosOff<N>& po, int t) {
     store_own<N>(f + field * cs, r, go, os.tile(tl, go), os.po(po), t);
   };
-  pipeline<N, V>(ntiles, 5, g, [&](int it) { return fin + order[it] * cs_in; }, tw,
-                 [&](int it, double2* buf, const Tile& tl, const PosOff<N>& po, int col,
-                     int t, const double2* tws) {
+  pipeline<N, V>(ntiles, 5, g, [&](int it) { return fin + order(it) * cs_in; }, tw,
+                 [&](int it, double2* buf, const Tile& tl, const PosOff<N>& po,
+                     const Lanes<N, V>& ln, const double2* tws) {
+                   const int t = ln.t;
                    double2 vin[E], v[E];
-                   read_own<N, CS>(vin, buf, col, t);
-                   __syncthreads();
+                   read_own<N>(vin, buf, ln.idx, t);
+                   ln.bar();
                    if (it == 3) {  // U2 -> w0' = F(i ky U2) (and u2 below)
 #pragma unroll
                      for (int m = 0; m < E; ++m) {
                        const double ky = wavenum(t + m * TPC, N);
                        v[m] = times_i(make_double2(ky * vin[m].x, ky * vin[m].y));
                      }
-                     col_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                     col_fft<N, +1>(v, buf, ln.idx, t, tws, ln.bar);
                      put(3, v, tl, po, t);
                    }
                    if (it == 2) {  // w2' -> w2 = F(w2')
-                     col_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
+                     col_fft<N, +1>(vin, buf, ln.idx, t, tws, ln.bar);
                      put(5, vin, tl, po, t);
                    } else if (it == 4) {  // K2 -> w1' = F(-i K2)
 #pragma unroll
                      for (int m = 0; m < E; ++m) v[m] = times_mi(vin[m]);
-                     col_fft<N, +1>(v, buf + col, TileIdx<CS>{}, t, tws);
+                     col_fft<N, +1>(v, buf, ln.idx, t, tws, ln.bar);
                      put(4, v, tl, po, t);
                    } else {  // U0, U1, U2 -> u_c
-                     col_fft<N, +1>(vin, buf + col, TileIdx<CS>{}, t, tws);
-                     put(order[it], vin, tl, po, t);
+                     col_fft<N, +1>(vin, buf, ln.idx, t, tws, ln.bar);
+                     put(order(it), vin, tl, po, t);
                    }
                  });
 }
