@@ -28,10 +28,10 @@ namespace sdns_dev {
 namespace {
 
 #ifndef SDNS_VX
-#define SDNS_VX 3
+#define SDNS_VX 0
 #endif
 #ifndef SDNS_VY
-#define SDNS_VY 3
+#define SDNS_VY 1
 #endif
 #ifndef SDNS_VYI
 #define SDNS_VYI 0
