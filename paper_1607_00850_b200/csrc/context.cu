@@ -511,6 +511,9 @@ bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool wa
       a.accum = st->accum;
       a.w = kW[stage];
       a.bdt = kB[stage] * dt;
+      // stage 1: u_1 = u0 + b0 dt du_0 and accum = 1 * du_0 hold the same bits
+      // the stage-0 update wrote, so the update rebuilds u_1 instead of reading it
+      if (stage == 1) a.ubdt = kB[0] * dt;
       rhs_pipeline(c, a.u, stage == 0 ? sdns_dev::XF_RK0 : sdns_dev::XF_RK12, a);
     } else {
       a.u = st->nxt;

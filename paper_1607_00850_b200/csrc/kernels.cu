@@ -131,9 +131,13 @@ k_rk_update(XfArgs a, SpecGeom g) {
     double2 uq[3], bq[3], sq[3], cr[3];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      uq[q] = a.u[q * a.cs + e];
       if (MODE != XF_TAIL) bq[q] = a.base[q * a.cs + e];
       if (MODE == XF_RK12 || MODE == XF_RK3) sq[q] = a.accum[q * a.cs + e];
+      if (MODE == XF_RK12 && a.ubdt != 0.0)
+        uq[q] = make_double2(dadd(bq[q].x, dmul(a.ubdt, sq[q].x)),
+                             dadd(bq[q].y, dmul(a.ubdt, sq[q].y)));
+      else
+        uq[q] = a.u[q * a.cs + e];
       if (MODE == XF_RK3) cr[q] = a.carry[q * a.cs + e];
     }
     // wavenumbers(), mesh.cpp:56-60

@@ -88,6 +88,8 @@ struct XfArgs {
   double nu;
   double w;            // accum weight
   double bdt;          // stage offset * dt
+  double ubdt;         // XF_RK12: != 0 -> u = base + ubdt * accum (stage 1: u_1
+                       // rebuilt bitwise from accum = du_0, saving the read of u)
   double sixth;        // dt/6 (stage 3)
   int dealias;
   int project;         // stage 3: post-step projection
