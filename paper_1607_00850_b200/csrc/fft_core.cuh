@@ -20,6 +20,10 @@
 
 namespace sdns_dev {
 
+#ifndef SDNS_MIDREG
+#define SDNS_MIDREG 1
+#endif
+
 // LDGSTS: 16-byte global->shared copy (zero-filled when !valid).
 __device__ __forceinline__ void cp_async16(double2* dst, const double2* src, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -180,14 +184,32 @@ struct NamedBar {
 
 // One Stockham stage (and the rest, recursively). `sm` points at this
 // column's element 0 in shared memory; element x lives at sm[idx(x)].
-// Final-stage twiddles held in registers by kernels that run several
-// transforms per thread (the z pass): W^k and W^{4k} of a last radix-8 stage
-// (k = the thread's butterfly index, forward sign); the other powers follow
-// by complex products (at most three roundings), replacing seven
-// shared-memory reads per butterfly.
+// Stage twiddles held in registers by kernels that run several transforms
+// per thread (the z pass): W^k and W^{4k} of the radix-8 stages with NS =
+// N/64 (m*) and NS = N/8 (w*) (k = the thread's butterfly index, forward
+// sign); the other powers follow by complex products (at most three
+// roundings), replacing seven 128-bit shared-memory reads -- four wavefronts
+// each, whatever the address overlap -- per butterfly.
 struct LastTw {
-  double2 w1, w4;
+  double2 w1, w4;  // last stage
+  double2 m1, m4;  // middle stage
 };
+
+template <int S>
+__device__ __forceinline__ void apply_tw8(double2* a, double2 w1, double2 w4) {
+  if (S > 0) {
+    w1.y = -w1.y;
+    w4.y = -w4.y;
+  }
+  const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+  a[1] = cmul(a[1], w1);
+  a[2] = cmul(a[2], w2);
+  a[3] = cmul(a[3], w3);
+  a[4] = cmul(a[4], w4);
+  a[5] = cmul(a[5], cmul(w4, w1));
+  a[6] = cmul(a[6], cmul(w4, w2));
+  a[7] = cmul(a[7], cmul(w4, w3));
+}
 
 template <int N, int E, int S, int NS, class IDX, class BAR = CtaBar, bool LREG = false>
 __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx, int t,
@@ -206,16 +228,10 @@ __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx
 #pragma unroll
     for (int r = 0; r < R; ++r) a[r] = v[b + r * NB];
     if constexpr (LREG && LAST && NS > 1 && R == 8 && NB == 1) {
-      const double2 w1 = S < 0 ? lt.w1 : make_double2(lt.w1.x, -lt.w1.y);
-      const double2 w4 = S < 0 ? lt.w4 : make_double2(lt.w4.x, -lt.w4.y);
-      const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
-      a[1] = cmul(a[1], w1);
-      a[2] = cmul(a[2], w2);
-      a[3] = cmul(a[3], w3);
-      a[4] = cmul(a[4], w4);
-      a[5] = cmul(a[5], cmul(w4, w1));
-      a[6] = cmul(a[6], cmul(w4, w2));
-      a[7] = cmul(a[7], cmul(w4, w3));
+      apply_tw8<S>(a, lt.w1, lt.w4);
+    } else if constexpr (SDNS_MIDREG && LREG && !LAST && NS == N / 64 && NS > 1 && R == 8 &&
+                         NB == 1) {
+      apply_tw8<S>(a, lt.m1, lt.m4);
     } else if (NS > 1) {
       constexpr int TOFF = tw_stage_off(N, E, NS);
 #pragma unroll
@@ -260,10 +276,11 @@ __device__ __forceinline__ void block_fft_lt(double2 (&v)[fft_elems(N)], double2
 // with one butterfly per thread (tw = the stage-ordered table).
 template <int N>
 __device__ __forceinline__ LastTw last_twiddles(const double2* tw, int t) {
-  constexpr int NS = N / 8;
+  constexpr int NS = N / 8, MS = N >= 128 ? N / 64 : 1;
   constexpr int TOFF = tw_stage_off(N, fft_elems(N), NS);
-  const int k = t & (NS - 1);
-  return LastTw{tw[TOFF + k], tw[TOFF + 3 * NS + k]};
+  constexpr int MOFF = tw_stage_off(N, fft_elems(N), MS);
+  const int k = t & (NS - 1), km = t & (MS - 1);
+  return LastTw{tw[TOFF + k], tw[TOFF + 3 * NS + k], tw[MOFF + km], tw[MOFF + 3 * MS + km]};
 }
 
 // Copies the stage-ordered twiddle table of length-n transforms to shared

@@ -287,6 +287,10 @@ struct ZFCfg {
   static constexpr size_t SMEM = sizeof(double2) * (static_cast<size_t>(RPC) * 6 * HP + N);
 };
 
+#ifndef SDNS_ZPARK1
+#define SDNS_ZPARK1 0
+#endif
+
 // z-pass transform; SDNS_ZNOFFT builds a transform-free variant (wrong
 // results) for A/B measurements of the pass's memory/shared-memory floor.
 template <int N, int S, class Bar>
@@ -341,7 +345,10 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   cp_wait0();
   __syncthreads();  // twiddles + staging
   const LastTw lt = last_twiddles<N>(tws, t);
-  double2 p1[E], v[E];
+  double2 v[E];
+#if !SDNS_ZPARK1
+  double2 p1[E];
+#endif
 #pragma unroll
   for (int m = 0; m < E; ++m) v[m] = pair_sample_kz<N, +1>(S, S + HP, t + m * TPC);
   bar();
@@ -356,21 +363,32 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   zfft<N, +1>(v, S + 2 * HP, sw, t, tws, bar, lt);
 #pragma unroll
   for (int m = 0; m < E; ++m) {
+#if SDNS_ZPARK1
+    S[2 * HP + sw(t + m * TPC)] = v[m];
+#else
     p1[m] = v[m];
+#endif
     v[m] = pair_sample<N>(S + 4 * HP, S + 5 * HP, t + m * TPC);
   }
   bar();
   zfft<N, +1>(v, S + 4 * HP, sw, t, tws, bar, lt);
-  // (u0,w1) = p0, (u1,w0) = p1, (u2,w2) = v; 1/n^3 then u x omega
-  double n2r[E];
+  // (u0,w1) = p0, (u1,w0) = p1, (u2,w2) = v; 1/n^3 then u x omega. The third
+  // product parks in pair 2's (now free) region: each thread re-reads its own
+  // slots, so no barrier, and 8 fewer live registers through the next FFT.
+  double* n2r = reinterpret_cast<double*>(S + 4 * HP);
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const double2 q0 = S[sw(t + m * TPC)];
-    const double ua = dmul(q0.x, norm), ub = dmul(p1[m].x, norm), uc = dmul(v[m].x, norm);
-    const double wa = dmul(p1[m].y, norm), wb = dmul(q0.y, norm), wc = dmul(v[m].y, norm);
+#if SDNS_ZPARK1
+    const double2 q1 = S[2 * HP + sw(t + m * TPC)];
+#else
+    const double2 q1 = p1[m];
+#endif
+    const double ua = dmul(q0.x, norm), ub = dmul(q1.x, norm), uc = dmul(v[m].x, norm);
+    const double wa = dmul(q1.y, norm), wb = dmul(q0.y, norm), wc = dmul(v[m].y, norm);
     const double n0 = dsub(dmul(ub, wc), dmul(uc, wb));
     const double n1 = dsub(dmul(uc, wa), dmul(ua, wc));
-    n2r[m] = dsub(dmul(ua, wb), dmul(ub, wa));
+    n2r[t + m * TPC] = dsub(dmul(ua, wb), dmul(ub, wa));
     v[m] = make_double2(n0, n1);
   }
   bar();  // every thread has read its parked pair-0 values
@@ -395,7 +413,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
     }
   }
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = make_double2(n2r[m], 0.0);
+  for (int m = 0; m < E; ++m) v[m] = make_double2(n2r[t + m * TPC], 0.0);
   zfft<N, -1>(v, S + 2 * HP, sw, t, tws, bar, lt);
   if (valid) {
     double2* o2 = f + 2 * cs;

@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (tracked).
 
-  python tools/profile_summary.py <round-tag> <n> <launches.csv> <full.ncu-rep>
+  python tools/profile_summary.py <round-tag> <n> <launches.csv> <full.ncu-rep> [more.ncu-rep ...]
 
 Writes profiles/<tag>_launches_<n>.md (per-kernel share of the launch list),
 profiles/<tag>_ncu_full_<n>.md (per-kernel counters of the full capture) and
@@ -70,7 +70,7 @@ def to_bytes(v, unit):
 
 
 def main():
-    tag, n, lpath, fpath = sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4]
+    tag, n, lpath, fpaths = sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4:]
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     tot, cnt = launches(lpath)
     allns = sum(tot.values())
@@ -82,7 +82,7 @@ def main():
         lines.append(f"| `{k}` | {cnt[k]} | {v / 1e6:.3f} | {100 * v / allns:.1f}% |")
     open(os.path.join(ROOT, "profiles", f"{tag}_launches_{n}.md"), "w").write("\n".join(lines) + "\n")
 
-    res = full(fpath)
+    res = [d for fp in fpaths for d in full(fp)]
     lines = [f"# {tag}: ncu --set full, n = {n} (one launch per kernel, --clock-control none)", "",
              "| kernel | ms | DRAM read GB | DRAM write GB | DRAM % | warps active % | regs | smem KB |"
              " block | fp64 pipe % | issue % | smem bank conflicts |",
