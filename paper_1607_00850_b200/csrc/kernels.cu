@@ -287,6 +287,9 @@ struct ZFCfg {
   static constexpr size_t SMEM = sizeof(double2) * (static_cast<size_t>(RPC) * 6 * HP + N);
 };
 
+#ifndef SDNS_ZTMA
+#define SDNS_ZTMA 1
+#endif
 #ifndef SDNS_ZPARK1
 #define SDNS_ZPARK1 0
 #endif
@@ -322,11 +325,40 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   Bar bar;
   if constexpr (TPC >= 64) bar = Bar{1 + r, TPC};
   const SwzIdx sw;
+  // fields: 0..2 = u, 3 = w0', 4 = w1', 5 = w2, staged as the pairs
+  // (u0, w1') (u1, w0') (u2, w2) -- slot s holds field kZSlot[s] -- all of
+  // the row in flight at once. The z part of the curl (w0 = w0' - i kz u1,
+  // w1 = w1' + i kz u0) is applied when the pair is sampled.
+#if SDNS_ZTMA
+  // One thread per row hands the 6 contiguous half-rows (n2 * 16 B each; one
+  // piece per kz segment on pencil rows) to the bulk-copy engine; the row
+  // waits on its mbarrier.
+  __shared__ alignas(8) unsigned long long zbar[RPC];
+  if (t == 0) mbar_init(&zbar[r], 1);
+  __syncthreads();  // barrier init visible before anyone waits on it
+  if (valid && t == 0) {
+    const int fld[6] = {0, 4, 1, 3, 2, 5};
+    mbar_expect_tx(&zbar[r], 6u * static_cast<unsigned>(rm.n2) * 16u);
+#pragma unroll
+    for (int sl = 0; sl < 6; ++sl) {
+      const double2* src = f + fld[sl] * cs;
+      if (rm.nseg == 0) {
+        bulk_g2s(S + sl * HP, src + ro, static_cast<unsigned>(rm.n2) * 16u, &zbar[r]);
+      } else {
+        for (int q = 0; q < rm.nseg; ++q) {
+          const int k0 = rm.seg_k0[q], k1 = rm.seg_k0[q + 1];
+          if (k1 > k0)
+            bulk_g2s(S + sl * HP + k0,
+                     src + rm.seg_base[q] + static_cast<long long>(ri) * rm.seg_pitch[q],
+                     static_cast<unsigned>(k1 - k0) * 16u, &zbar[r]);
+        }
+      }
+    }
+  }
+  __syncthreads();  // twiddles
+  if (valid) mbar_wait(&zbar[r], 0);
+#else
   if (valid) {
-    // fields: 0..2 = u, 3 = w0', 4 = w1', 5 = w2, staged as the pairs
-    // (u0, w1') (u1, w0') (u2, w2): LDGSTS straight to shared memory, all of
-    // the row in flight at once. The z part of the curl (w0 = w0' - i kz u1,
-    // w1 = w1' + i kz u0) is applied when the pair is sampled.
 #pragma unroll
     for (int k0 = 0; k0 <= N / 2; k0 += TPC) {
       const int k = k0 + t;
@@ -344,6 +376,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   cp_commit();
   cp_wait0();
   __syncthreads();  // twiddles + staging
+#endif
   const LastTw lt = last_twiddles<N>(tws, t);
   double2 v[E];
 #if !SDNS_ZPARK1
