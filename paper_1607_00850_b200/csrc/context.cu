@@ -174,6 +174,8 @@ struct sdns_ctx {
     g.n2 = static_cast<int>(lo.spec_shape[2]);
     g.pitch = pitch;
     g.row_off = static_cast<int>(lo.spec_offset[1]);
+    g.mpitch = pitch;
+    g.mrows = prow;
     return g;
   }
   WaveGeom xwave() const {
@@ -194,6 +196,8 @@ struct sdns_ctx {
     g.nrows = np;
     g.n2 = static_cast<int>(lo.spec_shape[2]);
     g.pitch = pitch;
+    g.mpitch = pitch;
+    g.mrows = np;
     return g;
   }
   // Largest kept |k| of the 2/3 rule: |k| < n/3  <=>  |k| <= (n-1)/3

@@ -68,6 +68,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
   }
 }
 
+// Orders this thread's generic-proxy shared-memory accesses before later
+// async-proxy (bulk copy / TMA) accesses to the same addresses.
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void cp_wait2() { asm volatile("cp.async.wait_group 2;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 

@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(ZFCfg<N>::THREADS, 2)
 k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __restrict__ tw) {
   constexpr int E = ZFCfg<N>::E, TPC = ZFCfg<N>::TPC, HP = ZFCfg<N>::HP, RPC = ZFCfg<N>::RPC;
   using Bar = typename std::conditional<(TPC >= 64), NamedBar, WarpBar>::type;
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(128) double2 smem[];
   const int t = threadIdx.x % TPC, r = threadIdx.x / TPC;
   const int ri = blockIdx.x * RPC + r;
   const bool valid = ri < rm.nrows;
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(ZCfg<N>::THREADS)
 k_z_c2r(const double2* __restrict__ spec, double* __restrict__ real, RowMap rm, double norm,
         const double2* __restrict__ tw) {
   constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC, HP = ZCfg<N>::HP;
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(128) double2 smem[];
   const int t = threadIdx.x % TPC, r = threadIdx.x / TPC;
   const int pr = blockIdx.x * ZCfg<N>::RPC + r;
   const int ri = 2 * pr;
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(ZCfg<N>::THREADS)
 k_z_r2c(const double* __restrict__ real, double2* __restrict__ spec, RowMap rm,
         const double2* __restrict__ tw) {
   constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC;
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(128) double2 smem[];
   const int t = threadIdx.x % TPC, r = threadIdx.x / TPC;
   const int pr = blockIdx.x * ZCfg<N>::RPC + r;
   const int ri = 2 * pr;

@@ -30,6 +30,10 @@ struct ColGeom {
   int seg_a = 1 << 30, off0 = 0, off1 = 0;
   int keep_k = -1;
   int row_off = 0;  // global index of storage row 0 (x pass: the y offset)
+  // Tensor-map tile loads (launcher-set): memory row pitch (complex) and
+  // storage-row extent of the source; tma = 1/2: positions are the faster /
+  // slower tensor dimension; 0: LDGSTS path.
+  int mpitch = 0, mrows = 0, tma = 0;
 };
 
 // Wavenumbers of a column pass: which physical axis the transform runs

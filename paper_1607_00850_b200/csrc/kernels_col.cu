@@ -20,6 +20,11 @@
 // tiles throughout; the two-FFT-per-item inverse passes run one 512-thread
 // CTA per SM with two buffers, the plain forward passes one buffer and two
 // CTAs per SM.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
 #include "fft_core.cuh"
 #include "kernels.cuh"
 
@@ -38,6 +43,9 @@ namespace {
 #endif
 #ifndef SDNS_VXI
 #define SDNS_VXI 8
+#endif
+#ifndef SDNS_COLTMA
+#define SDNS_COLTMA 1
 #endif
 #ifndef SDNS_NB0
 #define SDNS_NB0 3
@@ -208,29 +216,80 @@ struct Lanes {
 __device__ __forceinline__ double2 times_i(double2 a) { return make_double2(-a.y, a.x); }
 __device__ __forceinline__ double2 times_mi(double2 a) { return make_double2(a.y, -a.x); }
 
+// Tile source by the tensor-memory accelerator: two (N <= 256: one) box
+// loads of 2*CS doubles x 256 positions from a 4-D tensor map (kz doubles,
+// the faster of rows/positions, the slower, fields), completing on the
+// slot's mbarrier. The box lands position-major, CS complex per position --
+// TileIdx<8>. Issued by thread 0 (its tile coordinates are column 0's).
+__device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                          int c3, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_addr(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar))
+      : "memory");
+}
+
+template <int N, int CS>
+__device__ __forceinline__ void tma_tile(double2* buf, const CUtensorMap* tm, const ColGeom& g,
+                                         const Tile& tl, int field, unsigned long long* bar) {
+  constexpr int BP = N < 256 ? N : 256;
+  mbar_expect_tx(bar, static_cast<unsigned>(N * CS * sizeof(double2)));
+#pragma unroll
+  for (int h = 0; h < N / BP; ++h) {
+    if (g.tma == 2)  // positions are the slower dimension (x pass)
+      tma_load4(buf + h * BP * CS, tm, 2 * tl.kz, tl.row, h * BP, field, bar);
+    else
+      tma_load4(buf + h * BP * CS, tm, 2 * tl.kz, h * BP, tl.row, field, bar);
+  }
+}
+
 // Generic persistent pipeline driver: `items` items per tile; src(f) gives
-// the input field of item f; body(f, buf, tile, pos_offsets, lanes,
-// twiddles) transforms.
-template <int N, int V, class SrcF, class BodyF>
+// the input field of item f (fld(f) its index in the tensor map tm when
+// g.tma != 0); body(f, buf, tile, pos_offsets, lanes, twiddles) transforms.
+template <int N, int V, class SrcF, class FldF, class BodyF>
 __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g, SrcF src,
+                                         FldF fld, const CUtensorMap* tm,
                                          const double2* __restrict__ tw_global, BodyF body) {
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(128) double2 smem[];
+  __shared__ alignas(8) unsigned long long tbar[3];
   constexpr int CS = PipeCfg<N, V>::CS, NBUF = PipeCfg<N, V>::NBUF;
   const Lanes<N, V> ln;
   const int col = ln.col, t = ln.t;
   const PosOff<N> po(g, t);
+  const bool tma = g.tma != 0;
   double2* tws = smem + (NBUF + PipeCfg<N, V>::SCR) * N * CS;
   load_twiddles(tws, tw_global, N);
+  if (tma && threadIdx.x == 0)
+    for (int j = 0; j < NBUF; ++j) mbar_init(&tbar[j], 1);
   __syncthreads();
+  // ring slot j at smem + j*N*CS (arithmetic, not a pointer array: that
+  // would live in local memory)
+  auto ring = [&](int j) { return smem + j * (N * CS); };
+  auto issue = [&](int slot, int f, const Tile& tl) {
+    if (tma) {
+      if (threadIdx.x == 0) tma_tile<N, CS>(ring(slot), tm, g, tl, fld(f), &tbar[slot]);
+    } else {
+      issue_tile<N>(ring(slot), src(f), tl, po, ln.idx, t);
+    }
+  };
+  // A slot is refilled only after the barrier that ends its last transform
+  // (block_fft's trailing barrier follows its last shared-memory access; the
+  // single-buffer path has an explicit one): the same release the mbarrier
+  // empty/full pipelines of TMA producers rely on.
   const int G = gridDim.x;
   int f = 0, tile = blockIdx.x;
   if (NBUF == 1) {
-    for (; tile < ntiles;) {
+    for (int i = 0; tile < ntiles; ++i) {
       const Tile tl = tile_of<CS>(tile, col, g);
-      issue_tile<N>(smem, src(f), tl, po, ln.idx, t);
-      cp_commit();
-      cp_wait0();
-      ln.bar();
+      issue(0, f, tl);
+      if (tma) {
+        mbar_wait(&tbar[0], i & 1);
+      } else {
+        cp_commit();
+        cp_wait0();
+        ln.bar();
+      }
       body(f, smem, tl, po, ln, static_cast<const double2*>(tws));
       ln.bar();
       if (++f == items) {
@@ -257,37 +316,42 @@ __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g
     }
     return it;
   };
-  // ring slot j at smem + j*N*CS (arithmetic, not a pointer array: that
-  // would live in local memory)
-  auto ring = [&](int j) { return smem + j * (N * CS); };
   Item cur{static_cast<int>(blockIdx.x), 0};
   Tile tc = tile_of<CS>(cur.t0, col, g);
-  if (cur.t0 < ntiles) issue_tile<N>(ring(0), src(0), tc, po, ln.idx, t);
+  if (cur.t0 < ntiles) issue(0, 0, tc);
   cp_commit();
   Item n1 = adv(cur);
   Tile tn1 = tile_of<CS>(n1.t0, col, g);
   if (NBUF > 2) {
-    if (n1.t0 < ntiles) issue_tile<N>(ring(1), src(n1.f), tn1, po, ln.idx, t);
+    if (n1.t0 < ntiles) issue(1, n1.f, tn1);
     cp_commit();
   }
   for (int i = 0; cur.t0 < ntiles; ++i) {
     if (NBUF > 2) {
       const Item n2 = adv(n1);
       const Tile tn2 = tile_of<CS>(n2.t0, col, g);
-      if (n2.t0 < ntiles) issue_tile<N>(ring((i + 2) % 3), src(n2.f), tn2, po, ln.idx, t);
-      cp_commit();
-      cp_wait2();
-      ln.bar();
+      if (n2.t0 < ntiles) issue((i + 2) % 3, n2.f, tn2);
+      if (tma) {
+        mbar_wait(&tbar[i % 3], (i / 3) & 1);
+      } else {
+        cp_commit();
+        cp_wait2();
+        ln.bar();
+      }
       body(cur.f, ring(i % 3), tc, po, ln, static_cast<const double2*>(tws));
       cur = n1;
       tc = tn1;
       n1 = n2;
       tn1 = tn2;
     } else {
-      if (n1.t0 < ntiles) issue_tile<N>(ring((i + 1) & 1), src(n1.f), tn1, po, ln.idx, t);
-      cp_commit();
-      cp_wait1();
-      ln.bar();
+      if (n1.t0 < ntiles) issue((i + 1) & 1, n1.f, tn1);
+      if (tma) {
+        mbar_wait(&tbar[i & 1], (i >> 1) & 1);
+      } else {
+        cp_commit();
+        cp_wait1();
+        ln.bar();
+      }
       body(cur.f, ring(i & 1), tc, po, ln, static_cast<const double2*>(tws));
       cur = n1;
       tc = tn1;
@@ -305,9 +369,11 @@ __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g
 template <int N, int S, int V, bool SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs, int nfields,
-             ColGeom g, ColGeom go, int ntiles, const double2* __restrict__ tw) {
+             ColGeom g, ColGeom go, int ntiles, const double2* __restrict__ tw,
+             const __grid_constant__ CUtensorMap tm) {
   const OutSel<N, SEP> os(go, Lanes<N, V>().t);
-  pipeline<N, V>(ntiles, nfields, g, [&](int f) { return in + f * in_cs; }, tw,
+  pipeline<N, V>(ntiles, nfields, g, [&](int f) { return in + f * in_cs; },
+                 [](int f) { return f; }, &tm, tw,
                  [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po,
                      const Lanes<N, V>& ln, const double2* tws) {
                    const int t = ln.t;
@@ -326,12 +392,13 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
 template <int N, int V>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, ColGeom g,
-            int ntiles, const double2* __restrict__ tw) {
+            int ntiles, const double2* __restrict__ tw, const __grid_constant__ CUtensorMap tm) {
   constexpr int E = fft_elems(N), TPC = N / E;
   constexpr bool SCR = PipeCfg<N, V>::SCR > 0;
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(128) double2 smem[];
   double2* const scr = smem + PipeCfg<N, V>::NBUF * N * PipeCfg<N, V>::CS;
-  pipeline<N, V>(ntiles, 3, g, [&](int f) { return u + f * u_cs; }, tw,
+  pipeline<N, V>(ntiles, 3, g, [&](int f) { return u + f * u_cs; }, [](int f) { return f; },
+                 &tm, tw,
                  [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po,
                      const Lanes<N, V>& ln, const double2* tws) {
                    const int t = ln.t;
@@ -385,7 +452,7 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
 template <int N, int V, bool SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGeom g, ColGeom go,
-            int ntiles, const double2* __restrict__ tw) {
+            int ntiles, const double2* __restrict__ tw, const __grid_constant__ CUtensorMap tm) {
   constexpr int E = fft_elems(N), TPC = N / E;
   // field of item it: 0, 1, 3, 2, 4
   auto order = [](int it) { return it ^ ((it >> 1) & ~(it >> 2) & 1); };
@@ -393,7 +460,7 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
   auto put = [&](int field, const double2(&r)[E], const Tile& tl, const PosOff<N>& po, int t) {
     store_own<N>(f + field * cs, r, go, os.tile(tl, go), os.po(po), t);
   };
-  pipeline<N, V>(ntiles, 5, g, [&](int it) { return fin + order(it) * cs_in; }, tw,
+  pipeline<N, V>(ntiles, 5, g, [&](int it) { return fin + order(it) * cs_in; }, order, &tm, tw,
                  [&](int it, double2* buf, const Tile& tl, const PosOff<N>& po,
                      const Lanes<N, V>& ln, const double2* tws) {
                    const int t = ln.t;
@@ -462,6 +529,60 @@ static long long ntiles_of(const ColGeom& g) {
   return (cols + PipeCfg<N, V>::CS - 1) / PipeCfg<N, V>::CS;
 }
 
+// Tensor map of a column pass's tile source, or false (LDGSTS path) when the
+// layout is not a plain (kz, rows, positions) block: split position strides
+// (slab receive layouts), no memory pitch recorded, or tiles narrower than
+// the TileIdx<8> rows a box lands in.
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <int N, int CS>
+static ColGeom with_tile_map(const ColGeom& g, const double2* base, long long fcs, int nfields,
+                             CUtensorMap* tm) {
+  ColGeom r = g;
+  r.tma = 0;
+  std::memset(tm, 0, sizeof(*tm));
+  if (!SDNS_COLTMA || CS != 8 || g.mpitch <= 0 || g.mrows <= 0 || ((N - 1) >> g.pb_shift) != 0)
+    return r;
+  const auto enc = tmap_encoder();
+  if (!enc) return r;
+  const bool pos_slow = g.ps0 > g.rs;
+  constexpr cuuint32_t BP = N < 256 ? N : 256;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(2 * g.mpitch), 0, 0,
+                        static_cast<cuuint64_t>(nfields)};
+  cuuint64_t strides[3] = {0, 0, static_cast<cuuint64_t>(fcs) * sizeof(double2)};
+  cuuint32_t box[4] = {2 * CS, 1, 1, 1}, es[4] = {1, 1, 1, 1};
+  const cuuint64_t rows = static_cast<cuuint64_t>(g.mrows), pos = N;
+  const cuuint64_t rsb = static_cast<cuuint64_t>(g.rs) * sizeof(double2);
+  const cuuint64_t psb = static_cast<cuuint64_t>(g.ps0) * sizeof(double2);
+  if (pos_slow) {
+    dims[1] = rows; strides[0] = rsb;
+    dims[2] = pos;  strides[1] = psb; box[2] = BP;
+  } else {
+    dims[1] = pos;  strides[0] = psb; box[1] = BP;
+    dims[2] = rows; strides[1] = rsb;
+  }
+  if (nfields == 1) strides[2] = strides[1] * dims[2];
+  const CUresult e = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double2*>(base), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (e == CUDA_SUCCESS) r.tma = pos_slow ? 2 : 1;
+  return r;
+}
+
 template <int N, int S, int V, bool SEP>
 static void plain_launch(const double2* in, double2* out, long long in_cs, long long out_cs,
                          int nfields, const ColGeom& g, const ColGeom& go, const double2* tw,
@@ -472,8 +593,10 @@ static void plain_launch(const double2* in, double2* out, long long in_cs, long 
   static int occ = 0;
   const unsigned grid =
       persistent_grid(k_pipe_plain<N, S, V, SEP>, C::THREADS, C::SMEM, nt, &occ);
+  CUtensorMap tm;
+  const ColGeom gt = with_tile_map<N, C::CS>(g, in, in_cs, nfields, &tm);
   k_pipe_plain<N, S, V, SEP><<<grid, C::THREADS, C::SMEM, s>>>(in, out, in_cs, out_cs, nfields,
-                                                               g, go, static_cast<int>(nt), tw);
+                                                               gt, go, static_cast<int>(nt), tw, tm);
 }
 
 template <int N>
@@ -523,8 +646,10 @@ static void x_inv_n(const double2* u, long long u_cs, double2* out, long long ou
   const long long nt = ntiles_of<N, VXI>(g);
   static int occ = 0;
   const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI>, C::THREADS, C::SMEM, nt, &occ);
-  k_pipe_xinv<N, VXI><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, g,
-                                                        static_cast<int>(nt), tw);
+  CUtensorMap tm;
+  const ColGeom gt = with_tile_map<N, C::CS>(g, u, u_cs, 3, &tm);
+  k_pipe_xinv<N, VXI><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, gt,
+                                                        static_cast<int>(nt), tw, tm);
 }
 
 void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
@@ -546,14 +671,18 @@ static void y_inv_n(const double2* fin, double2* f, long long cs_in, long long c
     static int occ = 0;
     const unsigned grid =
         persistent_grid(k_pipe_yinv<N, VYI, true>, C::THREADS, C::SMEM, nt, &occ);
-    k_pipe_yinv<N, VYI, true><<<grid, C::THREADS, C::SMEM, s>>>(fin, f, cs_in, cs, g, *go,
-                                                                static_cast<int>(nt), tw);
+    CUtensorMap tm;
+    const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
+    k_pipe_yinv<N, VYI, true><<<grid, C::THREADS, C::SMEM, s>>>(fin, f, cs_in, cs, gt, *go,
+                                                                static_cast<int>(nt), tw, tm);
   } else {
     static int occ = 0;
     const unsigned grid =
         persistent_grid(k_pipe_yinv<N, VYI, false>, C::THREADS, C::SMEM, nt, &occ);
-    k_pipe_yinv<N, VYI, false><<<grid, C::THREADS, C::SMEM, s>>>(fin, f, cs_in, cs, g, g,
-                                                                 static_cast<int>(nt), tw);
+    CUtensorMap tm;
+    const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
+    k_pipe_yinv<N, VYI, false><<<grid, C::THREADS, C::SMEM, s>>>(fin, f, cs_in, cs, gt, g,
+                                                                 static_cast<int>(nt), tw, tm);
   }
 }
 
