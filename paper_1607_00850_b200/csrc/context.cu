@@ -15,6 +15,7 @@
 //        read directly by the y pass (no unpack pass); aliases wa at p = 1.
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -103,6 +104,12 @@ struct sdns_ctx {
   double2* tw = nullptr;
   double2* wa = nullptr;
   double2* wb = nullptr;
+  // p = 1 slab: P1 output / P2 input in the chunk-major layout
+  // [kz chunk][y][x][8] (5 fields of cs_x): P1 writes every tile as one
+  // contiguous 64 KB block instead of 512 rows 2 MB apart, P2 reads it back
+  // with 64 KB strides.
+  double2* wx = nullptr;
+  long long cs_x = 0;
   long long spec_cs = 0;   // complex elements per spectral component (padded)
   int prow = 0;            // rows per x plane incl. one pad row (s1 + 1)
   long long real_cs = 0;   // doubles per real component
@@ -176,6 +183,32 @@ struct sdns_ctx {
     g.row_off = static_cast<int>(lo.spec_offset[1]);
     g.mpitch = pitch;
     g.mrows = prow;
+    return g;
+  }
+  ColGeom xl_out() const {  // x-pass view of wx: rows = y, positions = x
+    ColGeom g = xgeom();
+    const long long n = cfg.n;
+    g.rs = n * 8;
+    g.ps0 = 8;
+    g.ps1 = 0;
+    g.pb_shift = 30;
+    g.kcs = static_cast<long long>(lo.spec_shape[1]) * n * 8;
+    g.mrows = static_cast<int>(lo.spec_shape[1]);
+    return g;
+  }
+  ColGeom xl_in() const {  // y-pass view of wx: rows = x, positions = y
+    ColGeom g;
+    const long long n = cfg.n;
+    g.rs = 8;
+    g.ps0 = n * 8;
+    g.ps1 = 0;
+    g.pb_shift = 30;
+    g.kcs = static_cast<long long>(lo.spec_shape[1]) * n * 8;
+    g.nrows = static_cast<int>(n);
+    g.n2 = static_cast<int>(lo.spec_shape[2]);
+    g.pitch = pitch;
+    g.mpitch = pitch;
+    g.mrows = static_cast<int>(n);
     return g;
   }
   WaveGeom xwave() const {
@@ -397,16 +430,28 @@ void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args
   const int n = c->cfg.n;
   cudaStream_t s = c->stream;
   int tk = c->tick(SDNS_PASS_X_INV_CURL);
-  sdns_dev::x_inverse_split(n, u_in, c->spec_cs, c->wa, c->spec_cs, c->xgeom(), c->tw, s);
+  if (c->wx) {
+    const ColGeom go = c->xl_out();
+    sdns_dev::x_inverse_split(n, u_in, c->spec_cs, c->wx, c->cs_x, c->xgeom(), &go, c->tw, s);
+  } else {
+    sdns_dev::x_inverse_split(n, u_in, c->spec_cs, c->wa, c->spec_cs, c->xgeom(), nullptr, c->tw,
+                              s);
+  }
   c->tock(tk);
   // Forward direction: with the 2/3 rule on, modes the mask zeroes are never
   // computed or stored (kept modes are computed by identical transforms).
   RowMap zm = c->zmap(false);
   if (c->cfg.dealias) zm.kz_keep = c->keep_k() + 1;
   if (!c->pencil) {
-    c->exchange(true, 5);
-    tk = c->tick(SDNS_PASS_Y_INV);
-    sdns_dev::y_inverse_curl(n, c->wb, c->spec_cs, c->ygeom(), c->tw, s);
+    if (c->wx) {
+      tk = c->tick(SDNS_PASS_Y_INV);
+      sdns_dev::y_inverse_curl_to(n, c->wx, c->wb, c->cs_x, c->spec_cs, c->xl_in(), c->ygeom(),
+                                  c->tw, s);
+    } else {
+      c->exchange(true, 5);
+      tk = c->tick(SDNS_PASS_Y_INV);
+      sdns_dev::y_inverse_curl(n, c->wb, c->spec_cs, c->ygeom(), c->tw, s);
+    }
     c->tock(tk);
     tk = c->tick(SDNS_PASS_Z_FUSED);
     sdns_dev::z_fused(n, c->wb, c->spec_cs, zm, c->norm, c->tw, s);
@@ -716,6 +761,11 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
       c->wd = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * static_cast<size_t>(c->cs_d) * 6));
     } else {
       c->wb = cfg->p == 1 ? c->wa : static_cast<double2*>(dev_alloc(c.get(), wbytes));
+      const char* xl = std::getenv("SDNS_XLAYOUT");
+      if (cfg->p == 1 && !(xl && xl[0] == '0')) {
+        c->cs_x = static_cast<long long>(c->pitch) * c->lo.spec_shape[1] * n;
+        c->wx = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * c->cs_x * 5));
+      }
     }
     const int stride = c->shells + 3;
     const int nblk = std::max<int>(static_cast<int>(c->lo.spec_shape[0]), 592);
@@ -739,6 +789,7 @@ int sdns_ctx_destroy(sdns_ctx* c) {
     if (c->wb != c->wa) cudaFree(c->wb);
     if (c->wc) cudaFree(c->wc);
     if (c->wd) cudaFree(c->wd);
+    if (c->wx) cudaFree(c->wx);
     cudaFree(c->wa);
     cudaFree(c->d_partial);
     cudaFree(c->d_out);

@@ -23,6 +23,8 @@ namespace sdns_dev {
 // the stored output positions to |wavenumber| <= keep_k.
 struct ColGeom {
   long long rs = 0, ps0 = 0, ps1 = 0;
+  long long kcs = 8;  // stride of 8-column kz chunks: 8 = plain rows; larger
+                      // for chunk-major layouts ((kz>>3)*kcs + (kz&7))
   int pb_shift = 30;
   int nrows = 0;
   int n2 = 0;     // transformed kz entries per row
@@ -30,9 +32,9 @@ struct ColGeom {
   int seg_a = 1 << 30, off0 = 0, off1 = 0;
   int keep_k = -1;
   int row_off = 0;  // global index of storage row 0 (x pass: the y offset)
-  // Tensor-map tile loads (launcher-set): memory row pitch (complex) and
-  // storage-row extent of the source; tma = 1/2: positions are the faster /
-  // slower tensor dimension; 0: LDGSTS path.
+  // Tensor-map tile loads (launcher-set): memory row pitch (complex; 8 *
+  // the number of kz chunks) and storage-row extent of the source; tma = 1:
+  // tiles come from the tensor map, 0: LDGSTS path.
   int mpitch = 0, mrows = 0, tma = 0;
 };
 
@@ -107,9 +109,10 @@ void make_twiddles(int n, double2* d_tw, cudaStream_t s);
 void col_plain(int n, int dir, bool xaxis, const double2* in, double2* out, long long in_cs,
                long long out_cs, int nfields, const ColGeom& g, const double2* tw,
                cudaStream_t s);
-// P1: u_hat (3 comps) -> [U0, U1, U2, K1, K2] (5 comps of `out`)
+// P1: u_hat (3 comps) -> [U0, U1, U2, w2', K2] (5 comps of `out`), written
+// in geometry go (the input geometry g when go is NULL)
 void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
-                     const ColGeom& g, const double2* tw, cudaStream_t s);
+                     const ColGeom& g, const ColGeom* go, const double2* tw, cudaStream_t s);
 // P2: in place, fields [U0, U1, U2, K1, K2] -> [u0, u1, u2, w0', w1', w2]
 void y_inverse_curl(int n, double2* f, long long cs, const ColGeom& g, const double2* tw,
                     cudaStream_t s);

@@ -23,6 +23,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "fft_core.cuh"
@@ -109,7 +111,7 @@ __device__ __forceinline__ Tile tile_of(int tile, int col, const ColGeom& g) {
   t.valid = re < g.nrows && kz < g.n2;
   t.row = row;
   t.kz = kz;
-  t.base = static_cast<long long>(row) * g.rs + kz;
+  t.base = static_cast<long long>(row) * g.rs + static_cast<long long>(kz >> 3) * g.kcs + (kz & 7);
   return t;
 }
 
@@ -152,6 +154,19 @@ __device__ __forceinline__ void store_own(double2* dst, const double2 (&v)[fft_e
                                           const ColGeom& g, const Tile& tl, const PosOff<N>& po,
                                           int t) {
   constexpr int E = fft_elems(N), TPC = N / E;
+#ifdef SDNS_NOSTORE  // A/B measurement only (wrong results)
+  if (tl.valid || !tl.valid) return;
+#endif
+#ifdef SDNS_TMSTORE  // A/B measurement only (wrong results): tile-major writes
+  {
+    if (!tl.valid) return;
+    double2* b = dst + (static_cast<long long>(tl.row) * (g.pitch / 8) + (tl.kz >> 3)) * N * 8 +
+                 (tl.kz & 7);
+#pragma unroll
+    for (int m = 0; m < E; ++m) b[(t + m * TPC) * 8] = v[m];
+    return;
+  }
+#endif
   if (!tl.valid) return;
   double2* b = dst + tl.base;
 #pragma unroll
@@ -178,7 +193,8 @@ struct OutSel<N, true> {
   __device__ __forceinline__ OutSel(const ColGeom& go, int t) : p(go, t) {}
   __device__ __forceinline__ Tile tile(const Tile& t, const ColGeom& go) const {
     Tile o = t;
-    o.base = static_cast<long long>(t.row) * go.rs + t.kz;
+    o.base = static_cast<long long>(t.row) * go.rs + static_cast<long long>(t.kz >> 3) * go.kcs +
+             (t.kz & 7);
     return o;
   }
   __device__ __forceinline__ const PosOff<N>& po(const PosOff<N>&) const { return p; }
@@ -217,16 +233,16 @@ __device__ __forceinline__ double2 times_i(double2 a) { return make_double2(-a.y
 __device__ __forceinline__ double2 times_mi(double2 a) { return make_double2(a.y, -a.x); }
 
 // Tile source by the tensor-memory accelerator: two (N <= 256: one) box
-// loads of 2*CS doubles x 256 positions from a 4-D tensor map (kz doubles,
-// the faster of rows/positions, the slower, fields), completing on the
-// slot's mbarrier. The box lands position-major, CS complex per position --
+// loads of 2*CS doubles x 256 positions from a 5-D tensor map (doubles of a
+// kz chunk, kz chunks, rows, positions, fields), completing on the slot's
+// mbarrier. The box lands position-major, CS complex per position --
 // TileIdx<8>. Issued by thread 0 (its tile coordinates are column 0's).
-__device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
-                                          int c3, unsigned long long* bar) {
+__device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                          int c3, int c4, unsigned long long* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_addr(dst)),
-      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar))
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_addr(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_addr(bar))
       : "memory");
 }
 
@@ -236,12 +252,8 @@ __device__ __forceinline__ void tma_tile(double2* buf, const CUtensorMap* tm, co
   constexpr int BP = N < 256 ? N : 256;
   mbar_expect_tx(bar, static_cast<unsigned>(N * CS * sizeof(double2)));
 #pragma unroll
-  for (int h = 0; h < N / BP; ++h) {
-    if (g.tma == 2)  // positions are the slower dimension (x pass)
-      tma_load4(buf + h * BP * CS, tm, 2 * tl.kz, tl.row, h * BP, field, bar);
-    else
-      tma_load4(buf + h * BP * CS, tm, 2 * tl.kz, h * BP, tl.row, field, bar);
-  }
+  for (int h = 0; h < N / BP; ++h)
+    tma_load5(buf + h * BP * CS, tm, 2 * (tl.kz & 7), tl.kz >> 3, tl.row, h * BP, field, bar);
 }
 
 // Generic persistent pipeline driver: `items` items per tile; src(f) gives
@@ -389,13 +401,15 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
 // P1: x inverse of u_hat -> [U0, U1, U2, w2', K2] (fields 0..4 of `out`),
 // w2' = i (F(kx u1) - ky U0).
 
-template <int N, int V>
+template <int N, int V, bool SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, ColGeom g,
-            int ntiles, const double2* __restrict__ tw, const __grid_constant__ CUtensorMap tm) {
+            ColGeom go, int ntiles, const double2* __restrict__ tw,
+            const __grid_constant__ CUtensorMap tm) {
   constexpr int E = fft_elems(N), TPC = N / E;
   constexpr bool SCR = PipeCfg<N, V>::SCR > 0;
   extern __shared__ __align__(128) double2 smem[];
+  const OutSel<N, SEP> os(go, Lanes<N, V>().t);
   double2* const scr = smem + PipeCfg<N, V>::NBUF * N * PipeCfg<N, V>::CS;
   pipeline<N, V>(ntiles, 3, g, [&](int f) { return u + f * u_cs; }, [](int f) { return f; },
                  &tm, tw,
@@ -421,15 +435,17 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                        // U0 of this tile was stored by item 0 (L2-resident)
                        if (tl.valid) {
                          const double ky = wavenum(g.row_off + tl.row, N);
-                         const double2* u0 = out + tl.base;
+                         const Tile to = os.tile(tl, go);
+                         const PosOff<N>& pout = os.po(po);
+                         const double2* u0 = out + to.base;
 #pragma unroll
                          for (int m = 0; m < E; ++m) {
-                           const double2 a = u0[po.o(m)];
+                           const double2 a = u0[pout.o(m)];
                            v[m] = times_i(make_double2(v[m].x - ky * a.x, v[m].y - ky * a.y));
                          }
                        }
                      }
-                     store_own<N>(out + (2 + f) * out_cs, v, g, tl, po, t);
+                     store_own<N>(out + (2 + f) * out_cs, v, go, os.tile(tl, go), os.po(po), t);
                      if constexpr (SCR) {
                        read_own<N>(v, buf, ln.idx, t);
                      } else {
@@ -439,7 +455,7 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                    }
                    if (SCR || f == 0) ln.bar();  // buf is read; the transform reuses it
                    col_fft<N, +1>(v, buf, ln.idx, t, tws, ln.bar);
-                   store_own<N>(out + f * out_cs, v, g, tl, po, t);
+                   store_own<N>(out + f * out_cs, v, go, os.tile(tl, go), os.po(po), t);
                  });
 }
 
@@ -558,28 +574,26 @@ static ColGeom with_tile_map(const ColGeom& g, const double2* base, long long fc
     return r;
   const auto enc = tmap_encoder();
   if (!enc) return r;
-  const bool pos_slow = g.ps0 > g.rs;
   constexpr cuuint32_t BP = N < 256 ? N : 256;
-  cuuint64_t dims[4] = {static_cast<cuuint64_t>(2 * g.mpitch), 0, 0,
-                        static_cast<cuuint64_t>(nfields)};
-  cuuint64_t strides[3] = {0, 0, static_cast<cuuint64_t>(fcs) * sizeof(double2)};
-  cuuint32_t box[4] = {2 * CS, 1, 1, 1}, es[4] = {1, 1, 1, 1};
-  const cuuint64_t rows = static_cast<cuuint64_t>(g.mrows), pos = N;
-  const cuuint64_t rsb = static_cast<cuuint64_t>(g.rs) * sizeof(double2);
-  const cuuint64_t psb = static_cast<cuuint64_t>(g.ps0) * sizeof(double2);
-  if (pos_slow) {
-    dims[1] = rows; strides[0] = rsb;
-    dims[2] = pos;  strides[1] = psb; box[2] = BP;
-  } else {
-    dims[1] = pos;  strides[0] = psb; box[1] = BP;
-    dims[2] = rows; strides[1] = rsb;
-  }
-  if (nfields == 1) strides[2] = strides[1] * dims[2];
-  const CUresult e = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double2*>(base), dims,
+  const cuuint64_t B = sizeof(double2);
+  const cuuint64_t dims[5] = {16, static_cast<cuuint64_t>(g.mpitch / 8),
+                              static_cast<cuuint64_t>(g.mrows), N,
+                              static_cast<cuuint64_t>(nfields)};
+  const cuuint64_t strides[4] = {static_cast<cuuint64_t>(g.kcs) * B,
+                                 static_cast<cuuint64_t>(g.rs) * B,
+                                 static_cast<cuuint64_t>(g.ps0) * B,
+                                 static_cast<cuuint64_t>(fcs) * B};
+  const cuuint32_t box[5] = {2 * CS, 1, 1, BP, 1}, es[5] = {1, 1, 1, 1, 1};
+  const CUresult e = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2*>(base), dims,
                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (e == CUDA_SUCCESS) r.tma = pos_slow ? 2 : 1;
+  if (e == CUDA_SUCCESS) {
+    r.tma = 1;
+  } else if (std::getenv("SDNS_DEBUG_TMA")) {
+    std::fprintf(stderr, "sdns: tensor map encode failed (%d), LDGSTS tile loads\n",
+                 static_cast<int>(e));
+  }
   return r;
 }
 
@@ -641,22 +655,30 @@ void col_plain_to(int n, int dir, const double2* in, double2* out, long long in_
 
 template <int N>
 static void x_inv_n(const double2* u, long long u_cs, double2* out, long long out_cs,
-                    const ColGeom& g, const double2* tw, cudaStream_t s) {
+                    const ColGeom& g, const ColGeom* go, const double2* tw, cudaStream_t s) {
   using C = PipeCfg<N, VXI>;
   const long long nt = ntiles_of<N, VXI>(g);
-  static int occ = 0;
-  const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI>, C::THREADS, C::SMEM, nt, &occ);
   CUtensorMap tm;
   const ColGeom gt = with_tile_map<N, C::CS>(g, u, u_cs, 3, &tm);
-  k_pipe_xinv<N, VXI><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, gt,
-                                                        static_cast<int>(nt), tw, tm);
+  if (go) {
+    static int occ = 0;
+    const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, true>, C::THREADS, C::SMEM, nt, &occ);
+    k_pipe_xinv<N, VXI, true><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, gt, *go,
+                                                                static_cast<int>(nt), tw, tm);
+  } else {
+    static int occ = 0;
+    const unsigned grid =
+        persistent_grid(k_pipe_xinv<N, VXI, false>, C::THREADS, C::SMEM, nt, &occ);
+    k_pipe_xinv<N, VXI, false><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, gt, gt,
+                                                                 static_cast<int>(nt), tw, tm);
+  }
 }
 
 void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
-                     const ColGeom& g, const double2* tw, cudaStream_t s) {
+                     const ColGeom& g, const ColGeom* go, const double2* tw, cudaStream_t s) {
   switch (n) {
 #define X(NN) \
-  case NN: x_inv_n<NN>(u, u_cs, out, out_cs, g, tw, s); return;
+  case NN: x_inv_n<NN>(u, u_cs, out, out_cs, g, go, tw, s); return;
     SDNS_FOR_N(X)
 #undef X
   }
