@@ -59,7 +59,10 @@ struct PipeCfg {
   static constexpr int E = fft_elems(N);
   static constexpr int TPC = N / E;
   static constexpr int CSW = (V == 1 || V == 2) ? 4 : 8;  // columns at TPC >= 64
-  static constexpr int CS0 = TPC >= 64 ? CSW : (512 / TPC > 64 ? 64 : 512 / TPC);
+  // n < 512: threads per CTA (measured at n = 64/128/256: small CTAs win
+  // except for the two-transform inverse passes at 256)
+  static constexpr int ST = (N >= 256 && (V == 0 || V == 8)) ? 512 : 64;
+  static constexpr int CS0 = TPC >= 64 ? CSW : (ST / TPC > 64 ? 64 : (ST / TPC < 8 ? 8 : ST / TPC));
   static constexpr int CS = N >= 1024 ? 4 : CS0;
   static constexpr int THREADS = TPC * CS;
   static constexpr int NBUF = (V == 2 || V == 3 || V == 4) ? 1
