@@ -567,6 +567,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
+// L2 promotion of the tile loads: a tile row is exactly one 128 B line; a
+// 256 B promotion drags in the neighbouring line, which belongs to another
+// tile and is often evicted before that tile runs. SDNS_TMA_PROMO=0/64/128/256
+// overrides (A/B measurements).
+static CUtensorMapL2promotion tma_promotion() {
+  const char* e = std::getenv("SDNS_TMA_PROMO");
+  const int v = e ? std::atoi(e) : 128;
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                          : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                     : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+}
+
 template <int N, int CS>
 static ColGeom with_tile_map(const ColGeom& g, const double2* base, long long fcs, int nfields,
                              CUtensorMap* tm) {
@@ -589,7 +602,7 @@ static ColGeom with_tile_map(const ColGeom& g, const double2* base, long long fc
   const cuuint32_t box[5] = {2 * CS, 1, 1, BP, 1}, es[5] = {1, 1, 1, 1, 1};
   const CUresult e = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2*>(base), dims,
                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, tma_promotion(),
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (e == CUDA_SUCCESS) {
     r.tma = 1;
