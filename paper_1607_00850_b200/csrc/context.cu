@@ -130,6 +130,11 @@ struct sdns_ctx {
   std::vector<int> seg_pitch, seg_k0, seg_b;
   double* d_partial = nullptr;
   double* d_out = nullptr;
+  // sampled diagnostics fused into the last stage of a step (sdns_advance):
+  // valid for field fused_u while the sample hook runs
+  double* d_fpartial = nullptr;
+  double* d_fout = nullptr;
+  const sdns_field* fused_u = nullptr;
   double* h_out = nullptr;  // pinned
   int* d_flag = nullptr;
   int* h_flag = nullptr;    // pinned
@@ -545,7 +550,8 @@ void fft_inverse_impl(sdns_ctx* c, const sdns_field* spec, sdns_field* real) {
   post_launch("fft inverse");
 }
 
-bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool want_flag) {
+bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool want_flag,
+               bool want_stats = false) {
   static const double kW[3] = {1.0, 2.0, 2.0};
   static const double kB[3] = {0.5, 0.5, 1.0};
   double2* u = st->u.spec();
@@ -572,6 +578,11 @@ bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool wa
       a.sixth = dt / 6.0;
       a.project = post_project;
       a.finite = c->d_flag;
+      if (want_stats) {
+        a.stats_partial = c->d_fpartial;
+        a.stats_out = c->d_fout;
+        a.shells = c->shells;
+      }
       SDNS_CUDA(cudaMemsetAsync(c->d_flag, 0xff, sizeof(int), c->stream));
       rhs_pipeline(c, st->nxt, sdns_dev::XF_RK3, a);
     }
@@ -588,10 +599,14 @@ bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool wa
 
 void stats_impl(sdns_ctx* c, const sdns_field* u, double nu, double t, double* row) {
   const SpecGeom g = c->sgeom();
-  sdns_dev::stats_local(u->spec(), g, c->shells, c->d_partial, c->d_out, c->stream);
-  post_launch("collect_stats");
+  const double* src = c->d_fout;
+  if (u != c->fused_u) {
+    sdns_dev::stats_local(u->spec(), g, c->shells, c->d_partial, c->d_out, c->stream);
+    post_launch("collect_stats");
+    src = c->d_out;
+  }
   const int stride = c->shells + 3;
-  SDNS_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(double) * stride, cudaMemcpyDeviceToHost,
+  SDNS_CUDA(cudaMemcpyAsync(c->h_out, src, sizeof(double) * stride, cudaMemcpyDeviceToHost,
                             c->stream));
   SDNS_CUDA(cudaStreamSynchronize(c->stream));
   std::vector<double> sums(static_cast<size_t>(2 + c->shells));
@@ -770,6 +785,8 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
     const int stride = c->shells + 3;
     const int nblk = std::max<int>(static_cast<int>(c->lo.spec_shape[0]), 592);
     c->d_partial = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride * nblk));
+    c->d_fpartial = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride * nblk));
+    c->d_fout = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride));
     c->d_out = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride));
     c->d_flag = static_cast<int*>(dev_alloc(c.get(), sizeof(int)));
     SDNS_CUDA(cudaMallocHost(&c->h_out, sizeof(double) * stride));
@@ -792,6 +809,8 @@ int sdns_ctx_destroy(sdns_ctx* c) {
     if (c->wx) cudaFree(c->wx);
     cudaFree(c->wa);
     cudaFree(c->d_partial);
+    cudaFree(c->d_fpartial);
+    cudaFree(c->d_fout);
     cudaFree(c->d_out);
     cudaFree(c->d_flag);
     cudaFreeHost(c->h_out);
@@ -1036,14 +1055,24 @@ int sdns_advance(sdns_ctx* c, sdns_state* st, sdns_sample_fn sample, void* user,
       const bool last = k == n_steps;
       const double target = last ? cfg.t_end : static_cast<double>(k) * cfg.dt;
       const double dt = target - st->t;
-      const bool ok = step_impl(c, st, dt, 1, true);
+      const bool samp = sample && (k % cfg.out_every == 0 || last);
+      // a sampled step accumulates the diagnostics of its final state in the
+      // last update (collect_stats of st->u inside the hook reads them)
+      const bool ok = step_impl(c, st, dt, 1, true, samp);
       st->t = target;
       if (!ok) {
         if (fail_step) *fail_step = k;
         throw Error(SDNS_DIVERGENCE_ERROR,
                     "non-finite values in solution update at step " + std::to_string(k));
       }
-      if (sample && (k % cfg.out_every == 0 || last)) sample(k, st->t, user);
+      if (samp) {
+        c->fused_u = &st->u;
+        struct Clear {
+          sdns_ctx* c;
+          ~Clear() { c->fused_u = nullptr; }
+        } clear{c};
+        sample(k, st->t, user);
+      }
     }
   });
 }

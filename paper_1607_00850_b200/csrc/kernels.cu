@@ -23,6 +23,21 @@
 
 namespace sdns_dev {
 
+// Opt in to >48 KB dynamic shared memory once per kernel instantiation (the
+// call sites below are templates, so each static flag is per kernel).
+#define SDNS_SET_SMEM(kernel, bytes)                                              \
+  do {                                                                           \
+    static bool sdns_smem_done_ = false;                                          \
+    if (!sdns_smem_done_) {                                                       \
+      if ((bytes) > 48 * 1024)                                                    \
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             static_cast<int>(bytes));                            \
+      cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, \
+                           100);                                                  \
+      sdns_smem_done_ = true;                                                     \
+    }                                                                            \
+  } while (0)
+
 namespace {
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -104,11 +119,93 @@ __device__ __forceinline__ double two_sum_err(double a, double b, double s) {
 // k_pipe_plain): dealias mask, projection, viscous term and the RK4 stage
 // update (+ Neumaier carry, post-step projection, finite flag). Bitwise the
 // reference operation order.
+// One mode of P5b: the compute_rhs tail and the stage update at element e
+// = (i, j, k) of the local spectral block. un receives the new state
+// (XF_RK3). Explicit round-to-nearest operations: the result does not depend
+// on the kernel it is inlined into.
+template <int MODE>
+__device__ __forceinline__ void rk_elem(const XfArgs& a, const SpecGeom& g, long long e, int i,
+                                        int j, int k, bool& finite, double2 (&un)[3]) {
+  const double kmax = static_cast<double>(g.n) / 3.0;
+  const double kx = wavenum(g.o0 + i, g.n), ky = wavenum(g.o1 + j, g.n);
+  const double kzd = static_cast<double>(g.o2 + k);
+  // dealias mask (navier_stokes.cpp:123-125): masked modes of the nonlinear
+  // term are zero and were never computed by the pruned forward passes
+  const bool keep = !a.dealias || (fabs(kx) < kmax && fabs(ky) < kmax && fabs(kzd) < kmax);
+  double2 c0 = make_double2(0.0, 0.0), c1 = c0, c2 = c0;
+  if (keep) {
+    c0 = a.nl[e];
+    c1 = a.nl[a.nl_cs + e];
+    c2 = a.nl[2 * a.nl_cs + e];
+  }
+  double2 uq[3], bq[3], sq[3], cr[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    if (MODE != XF_TAIL) bq[q] = a.base[q * a.cs + e];
+    if (MODE == XF_RK12 || MODE == XF_RK3) sq[q] = a.accum[q * a.cs + e];
+    if (MODE == XF_RK12 && a.ubdt != 0.0)
+      uq[q] = make_double2(dadd(bq[q].x, dmul(a.ubdt, sq[q].x)),
+                           dadd(bq[q].y, dmul(a.ubdt, sq[q].y)));
+    else
+      uq[q] = a.u[q * a.cs + e];
+    if (MODE == XF_RK3) cr[q] = a.carry[q * a.cs + e];
+  }
+  // wavenumbers(), mesh.cpp:56-60
+  const double k2 = dadd(dadd(dmul(kx, kx), dmul(ky, ky)), dmul(kzd, kzd));
+  const double inv = k2 > 0.0 ? 1.0 / k2 : 0.0;
+  const double kxk = dmul(kx, inv), kyk = dmul(ky, inv), kzk = dmul(kzd, inv);
+  // kd = kx c0 + ky c1 + kz c2; c -= (k/k^2) kd  (navier_stokes.cpp:128-133)
+  const double kdr = dadd(dadd(dmul(kx, c0.x), dmul(ky, c1.x)), dmul(kzd, c2.x));
+  const double kdi = dadd(dadd(dmul(kx, c0.y), dmul(ky, c1.y)), dmul(kzd, c2.y));
+  c0 = make_double2(dsub(c0.x, dmul(kxk, kdr)), dsub(c0.y, dmul(kxk, kdi)));
+  c1 = make_double2(dsub(c1.x, dmul(kyk, kdr)), dsub(c1.y, dmul(kyk, kdi)));
+  c2 = make_double2(dsub(c2.x, dmul(kzk, kdr)), dsub(c2.y, dmul(kzk, kdi)));
+  const double visc = dmul(a.nu, k2);
+  double2 du[3];
+  const double2 cc[3] = {c0, c1, c2};
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+    du[q] = make_double2(dsub(cc[q].x, dmul(visc, uq[q].x)), dsub(cc[q].y, dmul(visc, uq[q].y)));
+  if (MODE == XF_TAIL) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) a.out[q * a.cs + e] = du[q];
+  } else if (MODE == XF_RK0 || MODE == XF_RK12) {
+    // rk4.cpp:47-50
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      double2 s = make_double2(dmul(a.w, du[q].x), dmul(a.w, du[q].y));
+      if (MODE == XF_RK12) s = make_double2(dadd(sq[q].x, s.x), dadd(sq[q].y, s.y));
+      a.accum[q * a.cs + e] = s;
+      a.out[q * a.cs + e] = make_double2(dadd(bq[q].x, dmul(a.bdt, du[q].x)),
+                                         dadd(bq[q].y, dmul(a.bdt, du[q].y)));
+    }
+  } else {  // XF_RK3, rk4.cpp:55-64
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double dr = dadd(dmul(a.sixth, dadd(sq[q].x, du[q].x)), cr[q].x);
+      const double di = dadd(dmul(a.sixth, dadd(sq[q].y, du[q].y)), cr[q].y);
+      const double nr = dadd(bq[q].x, dr), ni = dadd(bq[q].y, di);
+      a.carry[q * a.cs + e] = make_double2(two_sum_err(bq[q].x, dr, nr), two_sum_err(bq[q].y, di, ni));
+      un[q] = make_double2(nr, ni);
+      finite = finite && isfinite(nr) && isfinite(ni);
+    }
+    if (a.project) {
+      // project(), navier_stokes.cpp:85-102
+      const double pr = dadd(dadd(dmul(kx, un[0].x), dmul(ky, un[1].x)), dmul(kzd, un[2].x));
+      const double pi = dadd(dadd(dmul(kx, un[0].y), dmul(ky, un[1].y)), dmul(kzd, un[2].y));
+      un[0] = make_double2(dsub(un[0].x, dmul(kxk, pr)), dsub(un[0].y, dmul(kxk, pi)));
+      un[1] = make_double2(dsub(un[1].x, dmul(kyk, pr)), dsub(un[1].y, dmul(kyk, pi)));
+      un[2] = make_double2(dsub(un[2].x, dmul(kzk, pr)), dsub(un[2].y, dmul(kzk, pi)));
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) a.base_out[q * a.cs + e] = un[q];
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256)
 k_rk_update(XfArgs a, SpecGeom g) {
   const long long total = static_cast<long long>(g.s0) * g.prow * g.pitch;
-  const double kmax = static_cast<double>(g.n) / 3.0;
   bool finite = true;
   for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -117,80 +214,8 @@ k_rk_update(XfArgs a, SpecGeom g) {
     const int j = static_cast<int>(row % g.prow);
     const int i = static_cast<int>(row / g.prow);
     if (k >= g.s2 || j >= g.s1) continue;
-    const double kx = wavenum(g.o0 + i, g.n), ky = wavenum(g.o1 + j, g.n);
-    const double kzd = static_cast<double>(g.o2 + k);
-    // dealias mask (navier_stokes.cpp:123-125): masked modes of the nonlinear
-    // term are zero and were never computed by the pruned forward passes
-    const bool keep = !a.dealias || (fabs(kx) < kmax && fabs(ky) < kmax && fabs(kzd) < kmax);
-    double2 c0 = make_double2(0.0, 0.0), c1 = c0, c2 = c0;
-    if (keep) {
-      c0 = a.nl[e];
-      c1 = a.nl[a.nl_cs + e];
-      c2 = a.nl[2 * a.nl_cs + e];
-    }
-    double2 uq[3], bq[3], sq[3], cr[3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      if (MODE != XF_TAIL) bq[q] = a.base[q * a.cs + e];
-      if (MODE == XF_RK12 || MODE == XF_RK3) sq[q] = a.accum[q * a.cs + e];
-      if (MODE == XF_RK12 && a.ubdt != 0.0)
-        uq[q] = make_double2(dadd(bq[q].x, dmul(a.ubdt, sq[q].x)),
-                             dadd(bq[q].y, dmul(a.ubdt, sq[q].y)));
-      else
-        uq[q] = a.u[q * a.cs + e];
-      if (MODE == XF_RK3) cr[q] = a.carry[q * a.cs + e];
-    }
-    // wavenumbers(), mesh.cpp:56-60
-    const double k2 = dadd(dadd(dmul(kx, kx), dmul(ky, ky)), dmul(kzd, kzd));
-    const double inv = k2 > 0.0 ? 1.0 / k2 : 0.0;
-    const double kxk = dmul(kx, inv), kyk = dmul(ky, inv), kzk = dmul(kzd, inv);
-    // kd = kx c0 + ky c1 + kz c2; c -= (k/k^2) kd  (navier_stokes.cpp:128-133)
-    const double kdr = dadd(dadd(dmul(kx, c0.x), dmul(ky, c1.x)), dmul(kzd, c2.x));
-    const double kdi = dadd(dadd(dmul(kx, c0.y), dmul(ky, c1.y)), dmul(kzd, c2.y));
-    c0 = make_double2(dsub(c0.x, dmul(kxk, kdr)), dsub(c0.y, dmul(kxk, kdi)));
-    c1 = make_double2(dsub(c1.x, dmul(kyk, kdr)), dsub(c1.y, dmul(kyk, kdi)));
-    c2 = make_double2(dsub(c2.x, dmul(kzk, kdr)), dsub(c2.y, dmul(kzk, kdi)));
-    const double visc = dmul(a.nu, k2);
-    double2 du[3];
-    const double2 cc[3] = {c0, c1, c2};
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-      du[q] = make_double2(dsub(cc[q].x, dmul(visc, uq[q].x)), dsub(cc[q].y, dmul(visc, uq[q].y)));
-    if (MODE == XF_TAIL) {
-#pragma unroll
-      for (int q = 0; q < 3; ++q) a.out[q * a.cs + e] = du[q];
-    } else if (MODE == XF_RK0 || MODE == XF_RK12) {
-      // rk4.cpp:47-50
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        double2 s = make_double2(dmul(a.w, du[q].x), dmul(a.w, du[q].y));
-        if (MODE == XF_RK12) s = make_double2(dadd(sq[q].x, s.x), dadd(sq[q].y, s.y));
-        a.accum[q * a.cs + e] = s;
-        a.out[q * a.cs + e] = make_double2(dadd(bq[q].x, dmul(a.bdt, du[q].x)),
-                                           dadd(bq[q].y, dmul(a.bdt, du[q].y)));
-      }
-    } else {  // XF_RK3, rk4.cpp:55-64
-      double2 un[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const double dr = dadd(dmul(a.sixth, dadd(sq[q].x, du[q].x)), cr[q].x);
-        const double di = dadd(dmul(a.sixth, dadd(sq[q].y, du[q].y)), cr[q].y);
-        const double nr = dadd(bq[q].x, dr), ni = dadd(bq[q].y, di);
-        a.carry[q * a.cs + e] = make_double2(two_sum_err(bq[q].x, dr, nr), two_sum_err(bq[q].y, di, ni));
-        un[q] = make_double2(nr, ni);
-        finite = finite && isfinite(nr) && isfinite(ni);
-      }
-      if (a.project) {
-        // project(), navier_stokes.cpp:85-102
-        const double pr = dadd(dadd(dmul(kx, un[0].x), dmul(ky, un[1].x)), dmul(kzd, un[2].x));
-        const double pi = dadd(dadd(dmul(kx, un[0].y), dmul(ky, un[1].y)), dmul(kzd, un[2].y));
-        un[0] = make_double2(dsub(un[0].x, dmul(kxk, pr)), dsub(un[0].y, dmul(kxk, pi)));
-        un[1] = make_double2(dsub(un[1].x, dmul(kyk, pr)), dsub(un[1].y, dmul(kyk, pi)));
-        un[2] = make_double2(dsub(un[2].x, dmul(kzk, pr)), dsub(un[2].y, dmul(kzk, pi)));
-      }
-#pragma unroll
-      for (int q = 0; q < 3; ++q) a.base_out[q * a.cs + e] = un[q];
-    }
+    double2 un[3];
+    rk_elem<MODE>(a, g, e, i, j, k, finite, un);
   }
   if (MODE == XF_RK3 && !finite) atomicAnd(a.finite, 0);
 }
@@ -685,6 +710,90 @@ void pw_fill_pad(double2* f, int ncomp, const SpecGeom& g, cudaStream_t s) {
 
 constexpr int kStatsWarps = 8;
 
+// Per-mode terms of accumulate_local (diagnostics.cpp:34-57) in the
+// reference's operation order with explicit round-to-nearest operations (so
+// the standalone and the fused kernel agree bit for bit).
+struct StatsTerm {
+  double e, z, we, ratio;
+  int shell;
+};
+__device__ __forceinline__ StatsTerm stats_term(double kx, double ky, double kz, double w,
+                                                double2 u0, double2 u1, double2 u2) {
+  const double eps = 2.220446049250313e-16;
+  auto nrm = [](double2 c) { return dadd(dmul(c.x, c.x), dmul(c.y, c.y)); };
+  StatsTerm r;
+  r.e = dadd(dadd(nrm(u0), nrm(u1)), nrm(u2));
+  const double2 c0 = make_double2(dsub(dmul(ky, u2.x), dmul(kz, u1.x)),
+                                  dsub(dmul(ky, u2.y), dmul(kz, u1.y)));
+  const double2 c1 = make_double2(dsub(dmul(kz, u0.x), dmul(kx, u2.x)),
+                                  dsub(dmul(kz, u0.y), dmul(kx, u2.y)));
+  const double2 c2 = make_double2(dsub(dmul(kx, u1.x), dmul(ky, u0.x)),
+                                  dsub(dmul(kx, u1.y), dmul(ky, u0.y)));
+  r.z = dadd(dadd(nrm(c0), nrm(c1)), nrm(c2));
+  const double k2 = dadd(dadd(dmul(kx, kx), dmul(ky, ky)), dmul(kz, kz));
+  const double kn = sqrt(k2);
+  r.shell = static_cast<int>(llround(kn));
+  r.we = dmul(dmul(0.5, w), r.e);
+  const double kdr = dadd(dadd(dmul(kx, u0.x), dmul(ky, u1.x)), dmul(kz, u2.x));
+  const double kdi = dadd(dadd(dmul(kx, u0.y), dmul(ky, u1.y)), dmul(kz, u2.y));
+  r.ratio = hypot(kdr, kdi) / dadd(dmul(kn, sqrt(r.e)), eps);
+  return r;
+}
+
+// Warp-synchronous: adds the lanes' shell energies to the warp histogram in
+// a fixed order (segmented inclusive scan over lanes with equal shell; the
+// shell index is nondecreasing in kz along a row).
+__device__ __forceinline__ void hist_add(double* hist, int shells, int lane, bool ok, double we,
+                                         int shell) {
+  double acc = we;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double o = __shfl_up_sync(0xffffffffu, acc, d);
+    const int os = __shfl_up_sync(0xffffffffu, shell, d);
+    if (lane >= d && os == shell) acc += o;
+  }
+  const int nxt = __shfl_down_sync(0xffffffffu, shell, 1);
+  const bool tail = ok && (lane == 31 || nxt != shell);
+  if (tail && shell < shells) hist[shell] += acc;
+  __syncwarp();
+}
+
+// Fixed-order CTA reduction of (se, sz, dmax) and the warp histograms into
+// this plane's partial row [se, sz, dmax, shells...].
+__device__ __forceinline__ void stats_flush(double* sh, int shells, double se, double sz,
+                                            double dmax, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    se += __shfl_xor_sync(0xffffffffu, se, d);
+    sz += __shfl_xor_sync(0xffffffffu, sz, d);
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, d));
+  }
+  double* red = sh + kStatsWarps * shells;
+  if (lane == 0) {
+    red[warp * 3 + 0] = se;
+    red[warp * 3 + 1] = sz;
+    red[warp * 3 + 2] = dmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int w = 0; w < kStatsWarps; ++w) {
+      a += red[w * 3 + 0];
+      b += red[w * 3 + 1];
+      c = fmax(c, red[w * 3 + 2]);
+    }
+    out[0] = a;
+    out[1] = b;
+    out[2] = c;
+  }
+  for (int s = threadIdx.x; s < shells; s += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < kStatsWarps; ++w) v += sh[w * shells + s];
+    out[3 + s] = v;
+  }
+}
+
 __global__ void __launch_bounds__(kStatsWarps * 32)
 k_stats_partial(const double2* __restrict__ u, SpecGeom g, int shells, double* partial) {
   extern __shared__ double sh[];  // [kStatsWarps][shells] + reductions
@@ -694,7 +803,6 @@ k_stats_partial(const double2* __restrict__ u, SpecGeom g, int shells, double* p
   __syncwarp();
   const int i = blockIdx.x;
   const double kx = wavenum(g.o0 + i, g.n);
-  const double eps = 2.220446049250313e-16;
   const double half = static_cast<double>(g.n / 2);
   double se = 0.0, sz = 0.0, dmax = 0.0;
   for (int j = warp; j < g.s1; j += kStatsWarps) {
@@ -709,71 +817,63 @@ k_stats_partial(const double2* __restrict__ u, SpecGeom g, int shells, double* p
         const double kz = static_cast<double>(g.o2 + k);
         const double w = (kz == 0.0 || kz == half) ? 1.0 : 2.0;
         const long long e = rowoff + k;
-        const double2 u0 = u[e], u1 = u[g.cs + e], u2 = u[2 * g.cs + e];
-        const double ee = (u0.x * u0.x + u0.y * u0.y) + (u1.x * u1.x + u1.y * u1.y) +
-                          (u2.x * u2.x + u2.y * u2.y);
-        const double2 c0 = make_double2(ky * u2.x - kz * u1.x, ky * u2.y - kz * u1.y);
-        const double2 c1 = make_double2(kz * u0.x - kx * u2.x, kz * u0.y - kx * u2.y);
-        const double2 c2 = make_double2(kx * u1.x - ky * u0.x, kx * u1.y - ky * u0.y);
-        const double zz = (c0.x * c0.x + c0.y * c0.y) + (c1.x * c1.x + c1.y * c1.y) +
-                          (c2.x * c2.x + c2.y * c2.y);
-        se += w * ee;
-        sz += w * zz;
-        const double k2 = (kx * kx + ky * ky) + kz * kz;
-        const double kn = sqrt(k2);
-        shell = static_cast<int>(llround(kn));
-        we = 0.5 * w * ee;
-        const double kdr = (kx * u0.x + ky * u1.x) + kz * u2.x;
-        const double kdi = (kx * u0.y + ky * u1.y) + kz * u2.y;
-        const double ratio = hypot(kdr, kdi) / (kn * sqrt(ee) + eps);
-        dmax = fmax(dmax, ratio);
+        const StatsTerm st = stats_term(kx, ky, kz, w, u[e], u[g.cs + e], u[2 * g.cs + e]);
+        se = dadd(se, dmul(w, st.e));
+        sz = dadd(sz, dmul(w, st.z));
+        we = st.we;
+        shell = st.shell;
+        dmax = fmax(dmax, st.ratio);
       }
-      // segmented inclusive scan over lanes with equal shell (fixed order)
-      double acc = we;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const double o = __shfl_up_sync(0xffffffffu, acc, d);
-        const int os = __shfl_up_sync(0xffffffffu, shell, d);
-        if (lane >= d && os == shell) acc += o;
-      }
-      const int nxt = __shfl_down_sync(0xffffffffu, shell, 1);
-      const bool tail = ok && (lane == 31 || nxt != shell);
-      if (tail && shell < shells) hist[shell] += acc;
-      __syncwarp();
+      hist_add(hist, shells, lane, ok, we, shell);
     }
-  }
-  // fixed-order warp reductions
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    se += __shfl_xor_sync(0xffffffffu, se, d);
-    sz += __shfl_xor_sync(0xffffffffu, sz, d);
-    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, d));
-  }
-  double* red = sh + kStatsWarps * shells;
-  if (lane == 0) {
-    red[warp * 3 + 0] = se;
-    red[warp * 3 + 1] = sz;
-    red[warp * 3 + 2] = dmax;
   }
   __syncthreads();
-  const int stride = shells + 3;
-  double* out = partial + static_cast<long long>(blockIdx.x) * stride;
-  if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0, c = 0.0;
-    for (int w = 0; w < kStatsWarps; ++w) {
-      a += red[w * 3 + 0];
-      b += red[w * 3 + 1];
-      c = fmax(c, red[w * 3 + 2]);
+  stats_flush(sh, shells, se, sz, dmax, partial + static_cast<long long>(blockIdx.x) * (shells + 3));
+}
+
+// P5b stage 3 fused with the sampled diagnostics of the new state (SURVEY
+// 8(f) rank 1): the update of k_rk_update<XF_RK3> walked in the stats
+// kernel's order, accumulating the statistics of the projected new state as
+// it is written -- the sample costs no extra pass over u_hat and equals
+// collect_stats of that state bit for bit.
+__global__ void __launch_bounds__(kStatsWarps * 32)
+k_rk3_stats(XfArgs a, SpecGeom g, int shells, double* partial) {
+  extern __shared__ double sh[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* hist = sh + warp * shells;
+  for (int s = lane; s < shells; s += 32) hist[s] = 0.0;
+  __syncwarp();
+  const int i = blockIdx.x;
+  const double kx = wavenum(g.o0 + i, g.n);
+  const double half = static_cast<double>(g.n / 2);
+  double se = 0.0, sz = 0.0, dmax = 0.0;
+  bool finite = true;
+  for (int j = warp; j < g.s1; j += kStatsWarps) {
+    const double ky = wavenum(g.o1 + j, g.n);
+    const long long rowoff = (static_cast<long long>(i) * g.prow + j) * g.pitch;
+    for (int k0 = 0; k0 < g.s2; k0 += 32) {
+      const int k = k0 + lane;
+      const bool ok = k < g.s2;
+      double we = 0.0;
+      int shell = -1;
+      if (ok) {
+        double2 un[3];
+        rk_elem<XF_RK3>(a, g, rowoff + k, i, j, k, finite, un);
+        const double kz = static_cast<double>(g.o2 + k);
+        const double w = (kz == 0.0 || kz == half) ? 1.0 : 2.0;
+        const StatsTerm st = stats_term(kx, ky, kz, w, un[0], un[1], un[2]);
+        se = dadd(se, dmul(w, st.e));
+        sz = dadd(sz, dmul(w, st.z));
+        we = st.we;
+        shell = st.shell;
+        dmax = fmax(dmax, st.ratio);
+      }
+      hist_add(hist, shells, lane, ok, we, shell);
     }
-    out[0] = a;
-    out[1] = b;
-    out[2] = c;
   }
-  for (int s = threadIdx.x; s < shells; s += blockDim.x) {
-    double acc = 0.0;
-    for (int w = 0; w < kStatsWarps; ++w) acc += sh[w * shells + s];
-    out[3 + s] = acc;
-  }
+  if (!finite) atomicAnd(a.finite, 0);
+  __syncthreads();
+  stats_flush(sh, shells, se, sz, dmax, partial + static_cast<long long>(blockIdx.x) * (shells + 3));
 }
 
 __global__ void k_fold_partials(const double* partial, int nblocks, int stride, double* out) {
@@ -793,6 +893,9 @@ int stats_blocks(const SpecGeom& g) { return g.s0; }
 void stats_local(const double2* u, const SpecGeom& g, int shells, double* d_partial,
                  double* d_out, cudaStream_t s) {
   const size_t shm = sizeof(double) * (kStatsWarps * shells + kStatsWarps * 3);
+  if (shm > 48 * 1024)  // depends on n: set per launch
+    cudaFuncSetAttribute(k_stats_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(shm));
   k_stats_partial<<<g.s0, kStatsWarps * 32, shm, s>>>(u, g, shells, d_partial);
   const int stride = shells + 3;
   k_fold_partials<<<(stride + 127) / 128, 128, 0, s>>>(d_partial, g.s0, stride, d_out);
@@ -829,21 +932,6 @@ void l2_local(const double* a, const double* b, long long count, double* d_parti
 
 #define SDNS_FOR_N(X) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
 
-// Opt in to >48 KB dynamic shared memory once per kernel instantiation (the
-// call sites below are templates, so each static flag is per kernel).
-#define SDNS_SET_SMEM(kernel, bytes)                                              \
-  do {                                                                           \
-    static bool sdns_smem_done_ = false;                                          \
-    if (!sdns_smem_done_) {                                                       \
-      if ((bytes) > 48 * 1024)                                                    \
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             static_cast<int>(bytes));                            \
-      cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, \
-                           100);                                                  \
-      sdns_smem_done_ = true;                                                     \
-    }                                                                            \
-  } while (0)
-
 template <int MODE>
 static void rk_update_mode(const XfArgs& a, const SpecGeom& g, cudaStream_t s) {
   static int grid = 0;
@@ -864,7 +952,20 @@ void rk_update(int mode, const XfArgs& a, const SpecGeom& g, cudaStream_t s) {
     case XF_TAIL: rk_update_mode<XF_TAIL>(a, g, s); return;
     case XF_RK0: rk_update_mode<XF_RK0>(a, g, s); return;
     case XF_RK12: rk_update_mode<XF_RK12>(a, g, s); return;
-    default: rk_update_mode<XF_RK3>(a, g, s); return;
+    default:
+      if (a.stats_partial) {
+        const size_t shm = sizeof(double) * (kStatsWarps * a.shells + kStatsWarps * 3);
+        if (shm > 48 * 1024)
+          cudaFuncSetAttribute(k_rk3_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(shm));
+        k_rk3_stats<<<g.s0, kStatsWarps * 32, shm, s>>>(a, g, a.shells, a.stats_partial);
+        const int stride = a.shells + 3;
+        k_fold_partials<<<(stride + 127) / 128, 128, 0, s>>>(a.stats_partial, g.s0, stride,
+                                                             a.stats_out);
+      } else {
+        rk_update_mode<XF_RK3>(a, g, s);
+      }
+      return;
   }
 }
 

@@ -100,6 +100,11 @@ struct XfArgs {
   int dealias;
   int project;         // stage 3: post-step projection
   int* finite;         // stage 3: cleared to 0 on a non-finite value
+  // stage 3: when set, the sampled diagnostics of the new state are
+  // accumulated in the same pass (per-plane partials, folded into stats_out)
+  double* stats_partial = nullptr;
+  double* stats_out = nullptr;
+  int shells = 0;
 };
 
 // twiddle table exp(-2 pi i q / n), q in [0, n)

@@ -287,6 +287,44 @@ def test_stats_deterministic_bitwise():
     assert np.array_equal(a.spectrum, b.spectrum)
 
 
+@pytest.mark.parametrize("n", [16, 64])
+def test_sampled_stats_fused_into_last_stage(n):
+    """advance() accumulates the diagnostics of each sampled step's final state
+    inside the last stage update. Inside the hook they must
+    equal, bit for bit, collect_stats of a copy of that state, and sampling must
+    not change the trajectory."""
+    lo = S.build_layout(S.SolverConfig(n=n), 0)
+    uh0 = S.iso_init(n, lo, seed=3)
+    nu, dt, steps = 2e-3, 2e-3, 4
+
+    def run(every, check):
+        cfg = S.SolverConfig(n=n, nu=nu, dt=dt, t_end=steps * dt, out_every=every)
+        with S.Context(cfg) as c:
+            st = S.Rk4State(c)
+            st.set(c.spectral_field().upload(uh0))
+            seen = []
+
+            def hook(k, t):
+                fused = S.collect_stats(c, st.u_hat, nu, t)
+                copy = c.spectral_field().upload(st.u_hat.download())
+                plain = S.collect_stats(c, copy, nu, t)
+                seen.append((k, fused, plain))
+
+            st.advance(hook if check else None)
+            final = st.u_hat.download()
+            st.close()
+        return final, seen
+
+    final_s, seen = run(1, True)
+    final_n, _ = run(steps, False)
+    assert np.array_equal(final_s, final_n)
+    assert [k for k, _, _ in seen] == list(range(steps + 1))
+    for _, f, p in seen:
+        assert f.energy == p.energy and f.enstrophy == p.enstrophy
+        assert f.divergence_max == p.divergence_max
+        assert np.array_equal(f.spectrum, p.spectrum)
+
+
 # --- advance semantics and errors ------------------------------------------------
 
 def test_advance_schedule_and_shortened_last_step():
