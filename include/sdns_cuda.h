@@ -196,6 +196,21 @@ int sdns_collect_stats(sdns_ctx* ctx, const sdns_field* u_hat, double nu, double
                        double* row);
 int sdns_l2_diff(sdns_ctx* ctx, const sdns_field* a, const sdns_field* b, double* out);
 
+/* ---- checkpoints (checkpoint.hpp:11-33, checkpoint.cpp:64-187) ---------- */
+/* Collective. u_real: this rank's block of the real velocity (3 comps). The
+ * file is the reference's format: 32-byte header (magic "SDNS", u32 version
+ * 1, u32 n, u32 components 3, f64 t, u64 step) + three n^3 little-endian f64
+ * payloads in global x-major order, so any decomposition reads any other's
+ * file bit-exactly (and the reference reads ours). Rank 0 gathers and
+ * writes; SDNS_IO_ERROR on every rank when the path cannot be written. */
+int sdns_checkpoint_write(sdns_ctx* ctx, const sdns_field* u_real, const char* path, double t,
+                          int64_t step);
+/* Collective inverse: rank 0 reads and validates (magic, version, n,
+ * components, size -> SDNS_IO_ERROR on every rank), scatters the blocks;
+ * every rank receives t and step. */
+int sdns_checkpoint_read(sdns_ctx* ctx, const char* path, sdns_field* u_real, double* t,
+                         int64_t* step);
+
 /* ---- per-pass timing (CUDA events on the context stream) --------------- */
 /* Pass tags of one RHS evaluation. */
 enum {

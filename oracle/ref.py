@@ -47,6 +47,10 @@ def lib():
         L.sdns_ref_rk4_steps.argtypes = [I, I, I, I, I, D, D, I, I, P]
         L.sdns_ref_bench.argtypes = [I, I, I, I, I, I, ctypes.POINTER(D)]
         L.sdns_ref_time_units.argtypes = [I, I, I, I, I, D, D, I, I, I, P, ctypes.POINTER(D)]
+        L.sdns_ref_checkpoint_write.argtypes = [I, I, I, I, I, P, ctypes.c_char_p, D,
+                                                ctypes.c_int64]
+        L.sdns_ref_checkpoint_read.argtypes = [I, I, I, I, I, ctypes.c_char_p, P,
+                                               ctypes.POINTER(D), ctypes.POINTER(ctypes.c_int64)]
         _lib = L
     return _lib
 
@@ -151,3 +155,20 @@ def bench(n, p=1, steps=2, decomp="slab", p1=0, p2=0):
     s = ctypes.c_double()
     _check(lib().sdns_ref_bench(n, DECOMP[decomp], p, p1, p2, steps, ctypes.byref(s)))
     return s.value
+
+
+def checkpoint_write(path, u, n, t, step, decomp="slab", p=1, p1=1, p2=1):
+    """write_checkpoint of the global real field u (3, n, n, n)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    _check(lib().sdns_ref_checkpoint_write(n, DECOMP[decomp], p, p1, p2, _p(u),
+                                           os.fsencode(path), float(t), int(step)))
+
+
+def checkpoint_read(path, n, decomp="slab", p=1, p1=1, p2=1):
+    """read_checkpoint -> (u (3, n, n, n), t, step)."""
+    u = np.zeros((3, n, n, n))
+    t = ctypes.c_double()
+    step = ctypes.c_int64()
+    _check(lib().sdns_ref_checkpoint_read(n, DECOMP[decomp], p, p1, p2, os.fsencode(path), _p(u),
+                                          ctypes.byref(t), ctypes.byref(step)))
+    return u, t.value, step.value

@@ -21,6 +21,7 @@
 #include <string>
 #include <vector>
 
+#include "sdns/checkpoint.hpp"
 #include "sdns/diagnostics.hpp"
 #include "sdns/fft.hpp"
 #include "sdns/layout.hpp"
@@ -419,6 +420,38 @@ int sdns_ref_bench(int n, int decomp, int p, int p1, int p2, int steps,
     if (rows.empty() || rows[0].status != "ok")
       throw ConfigError(rows.empty() ? "bench produced no rows" : rows[0].status);
     *sec_per_step = rows[0].sec_per_step;
+  });
+}
+
+// write_checkpoint / read_checkpoint (checkpoint.hpp:24-33) of the global
+// real field u (3, n, n, n), decomposed like the given config.
+int sdns_ref_checkpoint_write(int n, int decomp, int p, int p1, int p2, const double* u,
+                              const char* path, double t, std::int64_t step) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, decomp, p, p1, p2, 0.0, 1.0, 1.0, 1, 1);
+    group(p, [&](int rank, std::shared_ptr<Communicator> comm) {
+      const RankLayout lo = build_layout(cfg, rank);
+      RealField3 f(lo.real.shape);
+      scatter_real(u, n, lo.real, f);
+      write_checkpoint(path, cfg, lo, *comm, f, t, step);
+    });
+  });
+}
+
+int sdns_ref_checkpoint_read(int n, int decomp, int p, int p1, int p2, const char* path,
+                             double* u, double* t, std::int64_t* step) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, decomp, p, p1, p2, 0.0, 1.0, 1.0, 1, 1);
+    group(p, [&](int rank, std::shared_ptr<Communicator> comm) {
+      const RankLayout lo = build_layout(cfg, rank);
+      RealField3 f(lo.real.shape);
+      const CheckpointInfo info = read_checkpoint(path, cfg, lo, *comm, f);
+      gather_real(f, n, lo.real, u);  // disjoint blocks
+      if (rank == 0) {
+        *t = info.t;
+        *step = info.step;
+      }
+    });
   });
 }
 

@@ -25,7 +25,7 @@ __all__ = [
     "build_layout", "device_layout", "exchange_plan", "block_size", "block_start", "step_count", "spectrum_shells",
     "iso_init", "Comm", "Context", "Field", "DistributedFFT", "curl_hat", "cross",
     "project", "pressure_hat", "compute_rhs", "Rk4State", "FlowStats", "collect_stats",
-    "l2_diff", "run_group",
+    "l2_diff", "write_checkpoint", "read_checkpoint", "run_group",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -167,6 +167,9 @@ def load_library(path: str = LIB_PATH):
             "sdns_rk4_step_host": (I, [P, P, P, D, I]),
             "sdns_collect_stats": (I, [P, P, D, D, P]),
             "sdns_l2_diff": (I, [P, P, P, ctypes.POINTER(D)]),
+            "sdns_checkpoint_write": (I, [P, P, ctypes.c_char_p, D, ctypes.c_int64]),
+            "sdns_checkpoint_read": (I, [P, ctypes.c_char_p, P, ctypes.POINTER(D),
+                                         ctypes.POINTER(ctypes.c_int64)]),
             "sdns_ctx_timing": (I, [P, I]),
             "sdns_ctx_timing_read": (I, [P, P, P]),
             "sdns_device_layout": (I, [ctypes.POINTER(_Config), I, ctypes.POINTER(_DevLayout)]),
@@ -655,6 +658,22 @@ def collect_stats(ctx: Context, u_hat: Field, nu: float, t: float = 0.0) -> Flow
     row = np.zeros(5 + shells)
     _check(ctx._lib.sdns_collect_stats(ctx._h, u_hat._h, nu, t, _ptr(row)))
     return FlowStats(row[0], row[1], row[2], row[3], row[4], row[5:].copy())
+
+
+def write_checkpoint(ctx: Context, path: str, u: Field, t: float, step: int):
+    """write_checkpoint, checkpoint.cpp:64-121 (collective; u = this rank's
+    real velocity block). The reference's file format and error behaviour."""
+    _check(ctx._lib.sdns_checkpoint_write(ctx._h, u._h, os.fsencode(path), float(t), int(step)))
+
+
+def read_checkpoint(ctx: Context, path: str, u: Field):
+    """read_checkpoint, checkpoint.cpp:123-187: fills u (this rank's block),
+    returns (t, step)."""
+    t = ctypes.c_double()
+    step = ctypes.c_int64()
+    _check(ctx._lib.sdns_checkpoint_read(ctx._h, os.fsencode(path), u._h, ctypes.byref(t),
+                                         ctypes.byref(step)))
+    return t.value, step.value
 
 
 def l2_diff(ctx: Context, a: Field, b: Field) -> float:

@@ -15,8 +15,10 @@
 //        read directly by the y pass (no unpack pass); aliases wa at p = 1.
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <filesystem>
 #include <mutex>
 
 #include "host.h"
@@ -626,6 +628,203 @@ void stats_impl(sdns_ctx* c, const sdns_field* u, double nu, double t, double* r
   for (int i = 0; i < c->shells; ++i) row[5 + i] = sums[2 + i] / n6;
 }
 
+// ---- checkpoints (checkpoint.cpp:64-187) --------------------------------
+
+constexpr char kCkMagic[4] = {'S', 'D', 'N', 'S'};
+constexpr uint32_t kCkVersion = 1;
+struct CkHeader {
+  char magic[4];
+  uint32_t version;
+  uint32_t n;
+  uint32_t components;
+  double t;
+  uint64_t step;
+};
+static_assert(sizeof(CkHeader) == 32, "reference checkpoint header is 32 bytes");
+
+// Root's verdict to every rank (the reference broadcasts the message, so a
+// bad path fails all ranks instead of hanging them): an allreduce-sum of
+// the message bytes, zeros from the other ranks.
+void share_io_error(sdns_ctx* c, const std::string& root_err) {
+  constexpr int kMax = 480;
+  std::vector<double> buf(kMax + 1, 0.0);
+  if (c->world->rank() == 0 && !root_err.empty()) {
+    const int len = static_cast<int>(std::min<size_t>(root_err.size(), kMax));
+    buf[0] = len;
+    for (int i = 0; i < len; ++i) buf[1 + i] = static_cast<unsigned char>(root_err[i]);
+  }
+  c->world->allreduce(buf.data(), static_cast<int>(buf.size()), 0);
+  const int len = static_cast<int>(buf[0]);
+  if (len <= 0) return;
+  std::string m(static_cast<size_t>(len), ' ');
+  for (int i = 0; i < len; ++i) m[static_cast<size_t>(i)] = static_cast<char>(buf[1 + i]);
+  throw Error(SDNS_IO_ERROR, m);
+}
+
+// Copies one rank's row-major real block into / out of the global x-major
+// array (blit_block, checkpoint.cpp:45-60).
+void blit_block(const sdns_layout& rl, int64_t n, double* global, double* block, bool to_global) {
+  const int64_t s0 = rl.real_shape[0], s1 = rl.real_shape[1], s2 = rl.real_shape[2];
+  for (int64_t i = 0; i < s0; ++i)
+    for (int64_t j = 0; j < s1; ++j) {
+      double* g = global + ((rl.real_offset[0] + i) * n + (rl.real_offset[1] + j)) * n +
+                  rl.real_offset[2];
+      double* b = block + (i * s1 + j) * s2;
+      if (to_global) std::memcpy(g, b, sizeof(double) * static_cast<size_t>(s2));
+      else std::memcpy(b, g, sizeof(double) * static_cast<size_t>(s2));
+    }
+}
+
+// Gather (to_root) or scatter of one real component between every rank's
+// block and rank 0's device staging buffer `stage` (blocks in rank order).
+void ck_exchange(sdns_ctx* c, const std::vector<int64_t>& cnt, double* mine, double* stage,
+                 bool to_root) {
+  const int p = c->cfg.p;
+  const bool root = c->world->rank() == 0;
+  const size_t my = sizeof(double) * static_cast<size_t>(c->real_cs);
+  std::vector<Xfer> xs;
+  int64_t off = 0;
+  for (int q = 0; q < p; ++q) {
+    const size_t qb = sizeof(double) * static_cast<size_t>(cnt[static_cast<size_t>(q)]);
+    double* slot = root ? stage + off : nullptr;
+    if (to_root)
+      xs.push_back({q, q == 0 ? mine : nullptr, slot, q == 0 ? my : 0, root ? qb : 0});
+    else
+      xs.push_back({q, slot, q == 0 ? mine : nullptr, root ? qb : 0, q == 0 ? my : 0});
+    off += cnt[static_cast<size_t>(q)];
+  }
+  c->world->alltoall(xs, c->stream);
+  SDNS_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void checkpoint_write_impl(sdns_ctx* c, const sdns_field* u, const std::string& path, double t,
+                           int64_t step) {
+  const int64_t n = c->cfg.n, n3 = n * n * n;
+  const bool root = c->world->rank() == 0;
+  std::vector<int64_t> cnt;
+  std::vector<sdns_layout> lays;
+  for (int r = 0; r < c->cfg.p; ++r) {
+    lays.push_back(build_layout(c->cfg, r));
+    cnt.push_back(lays.back().real_shape[0] * lays.back().real_shape[1] * lays.back().real_shape[2]);
+  }
+  FILE* fp = nullptr;
+  std::string err;
+  if (root) {
+    try {
+      const auto dir = std::filesystem::path(path).parent_path();
+      if (!dir.empty()) std::filesystem::create_directories(dir);
+    } catch (const std::exception&) {
+    }
+    fp = std::fopen(path.c_str(), "wb");
+    if (!fp) {
+      err = "cannot open checkpoint '" + path + "' for writing";
+    } else {
+      CkHeader h{};
+      std::memcpy(h.magic, kCkMagic, 4);
+      h.version = kCkVersion;
+      h.n = static_cast<uint32_t>(n);
+      h.components = 3;
+      h.t = t;
+      h.step = static_cast<uint64_t>(step);
+      if (std::fwrite(&h, sizeof(h), 1, fp) != 1) err = "short write to checkpoint '" + path + "'";
+    }
+  }
+  try {
+    share_io_error(c, err);
+  } catch (...) {
+    if (fp) std::fclose(fp);
+    throw;
+  }
+  double* stage = nullptr;
+  std::vector<double> blocks, global;
+  if (root) {
+    SDNS_CUDA(cudaMalloc(&stage, sizeof(double) * static_cast<size_t>(n3)));
+    blocks.resize(static_cast<size_t>(n3));
+    global.resize(static_cast<size_t>(n3));
+  }
+  bool ok = true;
+  for (int comp = 0; comp < 3; ++comp) {
+    ck_exchange(c, cnt, u->real() + comp * c->real_cs, stage, true);
+    if (!root) continue;
+    SDNS_CUDA(cudaMemcpy(blocks.data(), stage, sizeof(double) * static_cast<size_t>(n3),
+                         cudaMemcpyDeviceToHost));
+    int64_t off = 0;
+    for (int r = 0; r < c->cfg.p; ++r) {
+      blit_block(lays[static_cast<size_t>(r)], n, global.data(), blocks.data() + off, true);
+      off += cnt[static_cast<size_t>(r)];
+    }
+    ok = ok && std::fwrite(global.data(), sizeof(double), global.size(), fp) == global.size();
+  }
+  if (root) {
+    cudaFree(stage);
+    ok = (std::fclose(fp) == 0) && ok;
+    if (!ok) throw Error(SDNS_IO_ERROR, "short write to checkpoint '" + path + "'");
+  }
+}
+
+void checkpoint_read_impl(sdns_ctx* c, const std::string& path, sdns_field* u, double* t,
+                          int64_t* step) {
+  const int64_t n = c->cfg.n, n3 = n * n * n;
+  const bool root = c->world->rank() == 0;
+  std::vector<int64_t> cnt;
+  std::vector<sdns_layout> lays;
+  for (int r = 0; r < c->cfg.p; ++r) {
+    lays.push_back(build_layout(c->cfg, r));
+    cnt.push_back(lays.back().real_shape[0] * lays.back().real_shape[1] * lays.back().real_shape[2]);
+  }
+  std::vector<double> global;
+  CkHeader h{};
+  std::string err;
+  if (root) {
+    FILE* fp = std::fopen(path.c_str(), "rb");
+    if (!fp) {
+      err = "cannot open checkpoint '" + path + "'";
+    } else {
+      if (std::fread(&h, sizeof(h), 1, fp) != 1 || std::memcmp(h.magic, kCkMagic, 4) != 0)
+        err = "checkpoint '" + path + "': bad magic";
+      else if (h.version != kCkVersion)
+        err = "checkpoint '" + path + "': unsupported version " + std::to_string(h.version);
+      else if (h.n != static_cast<uint32_t>(n))
+        err = "checkpoint '" + path + "': grid size " + std::to_string(h.n) +
+              " does not match configured n=" + std::to_string(n);
+      else if (h.components != 3)
+        err = "checkpoint '" + path + "': expected 3 components";
+      if (err.empty()) {
+        global.resize(static_cast<size_t>(3 * n3));
+        if (std::fread(global.data(), sizeof(double), global.size(), fp) != global.size())
+          err = "checkpoint '" + path + "': truncated payload";
+      }
+      std::fclose(fp);
+    }
+  }
+  share_io_error(c, err);
+  double* stage = nullptr;
+  std::vector<double> blocks;
+  if (root) {
+    SDNS_CUDA(cudaMalloc(&stage, sizeof(double) * static_cast<size_t>(n3)));
+    blocks.resize(static_cast<size_t>(n3));
+  }
+  for (int comp = 0; comp < 3; ++comp) {
+    if (root) {
+      int64_t off = 0;
+      for (int r = 0; r < c->cfg.p; ++r) {
+        blit_block(lays[static_cast<size_t>(r)], n, global.data() + comp * n3, blocks.data() + off,
+                   false);
+        off += cnt[static_cast<size_t>(r)];
+      }
+      SDNS_CUDA(cudaMemcpy(stage, blocks.data(), sizeof(double) * static_cast<size_t>(n3),
+                           cudaMemcpyHostToDevice));
+    }
+    ck_exchange(c, cnt, u->real() + comp * c->real_cs, stage, false);
+  }
+  if (root) cudaFree(stage);
+  // every rank learns t and step from the root's header
+  double meta[2] = {root ? h.t : 0.0, root ? static_cast<double>(h.step) : 0.0};
+  c->world->allreduce(meta, 2, 0);
+  if (t) *t = meta[0];
+  if (step) *step = static_cast<int64_t>(meta[1]);
+}
+
 void* dev_alloc(sdns_ctx* c, size_t bytes) {
   void* p = nullptr;
   SDNS_CUDA(cudaMalloc(&p, bytes));
@@ -1112,6 +1311,25 @@ int sdns_l2_diff(sdns_ctx* c, const sdns_field* a, const sdns_field* b, double* 
     c->world->allreduce(&v, 1, 0);
     const double n3 = static_cast<double>(c->cfg.n) * c->cfg.n * c->cfg.n;
     *out = std::sqrt(v / n3);
+  });
+}
+
+int sdns_checkpoint_write(sdns_ctx* c, const sdns_field* u, const char* path, double t,
+                          int64_t step) {
+  return guarded([&] {
+    require_real(u, 3, "write_checkpoint");
+    set_device(c);
+    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    checkpoint_write_impl(c, u, path ? path : "", t, step);
+  });
+}
+
+int sdns_checkpoint_read(sdns_ctx* c, const char* path, sdns_field* u, double* t, int64_t* step) {
+  return guarded([&] {
+    require_real(u, 3, "read_checkpoint");
+    set_device(c);
+    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    checkpoint_read_impl(c, path ? path : "", u, t, step);
   });
 }
 

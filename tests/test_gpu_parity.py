@@ -527,3 +527,74 @@ def test_pencil_compute_rhs_vs_reference_pencil(ref):
     for lo, du in S.run_group(4, body):
         e = _scatter_spec(expect, lo)
         assert np.linalg.norm(du - e) <= 1e-12 * np.linalg.norm(expect)
+
+
+# --- checkpoints (checkpoint.cpp:64-187) ----------------------
+
+def test_checkpoint_round_trip_with_reference(ref, tmp_path):
+    """Our file is the reference's format: the reference reads what we write
+    and we read what it writes, bit for bit, header included."""
+    n = 16
+    u = np.random.default_rng(5).uniform(-1, 1, (3, n, n, n))
+    ours = str(tmp_path / "ours.ck")
+    theirs = str(tmp_path / "sub" / "theirs.ck")
+    with ctx_for(n) as c:
+        S.write_checkpoint(c, ours, c.real_field().upload(u), 0.25, 12)
+        v, t, step = ref.checkpoint_read(ours, n)
+        assert np.array_equal(v, u) and t == 0.25 and step == 12
+        ref.checkpoint_write(theirs, u[::-1].copy(), n, 1.5, 3)
+        back = c.real_field()
+        t2, s2 = S.read_checkpoint(c, theirs, back)
+        assert np.array_equal(back.download(), u[::-1]) and (t2, s2) == (1.5, 3)
+
+
+@pytest.mark.parametrize("decomp,p,p1,p2", [("slab", 2, 1, 1), ("pencil", 4, 2, 2)])
+def test_checkpoint_decomposition_independent(ref, tmp_path, decomp, p, p1, p2):
+    """A file written by p ranks is read by any other decomposition (here the
+    reference at p = 1 and our own ranks again) bit-exactly."""
+    n = 16
+    u = np.random.default_rng(6).uniform(-1, 1, (3, n, n, n))
+    path = str(tmp_path / "multi.ck")
+    cfg = S.SolverConfig(n=n, decomp=decomp, p=p, p1=p1, p2=p2)
+
+    def write(rank, comm):
+        with S.Context(cfg, rank=rank, comm=comm) as c:
+            S.write_checkpoint(c, path, c.real_field().upload(_scatter_real(u, c.layout)), 2.0, 9)
+
+    S.run_group(p, write)
+    v, t, step = ref.checkpoint_read(path, n)
+    assert np.array_equal(v, u) and (t, step) == (2.0, 9)
+
+    def read(rank, comm):
+        with S.Context(cfg, rank=rank, comm=comm) as c:
+            f = c.real_field()
+            meta = S.read_checkpoint(c, path, f)
+            return c.layout, f.download(), meta
+
+    for lo, blk, meta in S.run_group(p, read):
+        assert np.array_equal(blk, _scatter_real(u, lo)) and meta == (2.0, 9)
+
+
+def test_checkpoint_errors(tmp_path):
+    """IoError on every failure the reference checks (checkpoint.cpp:139-160)."""
+    n = 8
+    with ctx_for(n) as c:
+        f = c.real_field()
+        with pytest.raises(S.IoError, match="cannot open"):
+            S.read_checkpoint(c, str(tmp_path / "missing.ck"), f)
+        bad = tmp_path / "bad.ck"
+        bad.write_bytes(b"NOPE" + bytes(60))
+        with pytest.raises(S.IoError, match="bad magic"):
+            S.read_checkpoint(c, str(bad), f)
+        good = str(tmp_path / "good.ck")
+        S.write_checkpoint(c, good, c.real_field(), 0.0, 0)
+        raw = open(good, "rb").read()
+        open(str(tmp_path / "short.ck"), "wb").write(raw[:-8])
+        with pytest.raises(S.IoError, match="truncated"):
+            S.read_checkpoint(c, str(tmp_path / "short.ck"), f)
+        with S.Context(S.SolverConfig(n=16)) as c16:
+            with pytest.raises(S.IoError, match="does not match configured n=16"):
+                S.read_checkpoint(c16, good, c16.real_field())
+        (tmp_path / "dir.ck").mkdir()
+        with pytest.raises(S.IoError, match="for writing"):
+            S.write_checkpoint(c, str(tmp_path / "dir.ck"), f, 0.0, 0)

@@ -140,3 +140,20 @@ def test_np_vs_reference_pencil_and_slab_run(ref):
     st = O.Rk4State(O.project(uh0, wm))
     O.advance(st, wm, 0.01, 0.01, 0.04)
     assert rel(st.u_hat, f1) < 1e-11
+
+
+def test_reference_checkpoint_decomposition_independent(ref, tmp_path):
+    """Pins the checkpoint format the product writes: the compiled reference
+    reads across decompositions bit-exactly (checkpoint.hpp:11-15)."""
+    n = 8
+    u = np.random.default_rng(11).uniform(-1, 1, (3, n, n, n))
+    path = str(tmp_path / "c.ck")
+    ref.checkpoint_write(path, u, n, 0.75, 4, decomp="pencil", p=4, p1=2, p2=2)
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"SDNS" and len(raw) == 32 + 3 * n ** 3 * 8
+    assert np.frombuffer(raw[:16], dtype="<u4")[1:].tolist() == [1, n, 3]
+    assert np.frombuffer(raw[16:24], dtype="<f8")[0] == 0.75
+    assert np.frombuffer(raw[24:32], dtype="<u8")[0] == 4
+    assert np.array_equal(np.frombuffer(raw[32:], dtype="<f8").reshape(3, n, n, n), u)
+    v, t, step = ref.checkpoint_read(path, n, decomp="slab", p=2)
+    assert np.array_equal(v, u) and (t, step) == (0.75, 4)
