@@ -588,6 +588,8 @@ static ColGeom with_tile_map(const ColGeom& g, const double2* base, long long fc
   std::memset(tm, 0, sizeof(*tm));
   if (!SDNS_COLTMA || CS != 8 || g.mpitch <= 0 || g.mrows <= 0 || ((N - 1) >> g.pb_shift) != 0)
     return r;
+  const char* off = std::getenv("SDNS_NO_TMA");  // LDGSTS tile loads (parity checks)
+  if (off && off[0] == '1') return r;
   const auto enc = tmap_encoder();
   if (!enc) return r;
   constexpr cuuint32_t BP = N < 256 ? N : 256;
