@@ -1,11 +1,12 @@
-import time, sys
+import time, sys, os
+DT = float(os.environ.get("DT", "0.01"))
 sys.path.insert(0, '.')
 import numpy as np
 import paper_1607_00850_b200 as S
 from oracle import sdns_np as O
 for n, steps, every in [(64, 100, 1), (64, 100, 0), (128, 50, 1), (256, 20, 1)]:
     lo = S.build_layout(S.SolverConfig(n=n), 0)
-    cfg = S.SolverConfig(n=n, nu=0.01, dt=0.01, t_end=steps * 0.01, out_every=max(every, 1))
+    cfg = S.SolverConfig(n=n, nu=0.01, dt=DT, t_end=steps * DT, out_every=max(every, 1))
     with S.Context(cfg) as c:
         u = c.spectral_field().upload(S.iso_init(n, lo, seed=1))
         st = S.Rk4State(c); st.set(u)

@@ -137,6 +137,7 @@ struct sdns_ctx {
   double* d_fpartial = nullptr;
   double* d_fout = nullptr;
   const sdns_field* fused_u = nullptr;
+  double* d_dts = nullptr;  // dt-dependent scalars of captured steps
   double* h_out = nullptr;  // pinned
   int* d_flag = nullptr;
   int* h_flag = nullptr;    // pinned
@@ -145,6 +146,13 @@ struct sdns_ctx {
   // Optional per-pass CUDA-event timing (bench.py's live roofline). Events
   // are created when timing is enabled, never inside a step.
   bool timing = false;
+  // captured steps (see step_impl): [0] plain, [1] with fused diagnostics
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    const sdns_state* st = nullptr;
+    int post_project = -1;
+  };
+  StepGraph graphs[2];
   std::vector<cudaEvent_t> ev;
   std::vector<int> ev_tag;
   size_t ev_used = 0;
@@ -552,8 +560,9 @@ void fft_inverse_impl(sdns_ctx* c, const sdns_field* spec, sdns_field* real) {
   post_launch("fft inverse");
 }
 
-bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool want_flag,
-               bool want_stats = false) {
+// The four stages of one step (device work only; see step_impl).
+void step_stages(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool want_stats,
+                 const double* dts = nullptr) {
   static const double kW[3] = {1.0, 2.0, 2.0};
   static const double kB[3] = {0.5, 0.5, 1.0};
   double2* u = st->u.spec();
@@ -562,6 +571,8 @@ bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool wa
     a.nu = c->cfg.nu;
     a.base = u;
     a.cs = c->spec_cs;
+    a.dts = dts;
+    a.dts_stage = stage;
     if (stage < 3) {
       a.u = stage == 0 ? u : st->nxt;
       a.out = st->nxt;
@@ -588,6 +599,43 @@ bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool wa
       SDNS_CUDA(cudaMemsetAsync(c->d_flag, 0xff, sizeof(int), c->stream));
       rhs_pipeline(c, st->nxt, sdns_dev::XF_RK3, a);
     }
+  }
+}
+
+// One RK4 step. On a single rank (no collectives inside the step) the
+// stages replay as a CUDA graph captured once per (state, dt, flags): the
+// ~25 launches of a step cost one graph launch, which matters where the
+// kernels are short (64^3: config 1). Per-pass timing runs eagerly.
+bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool want_flag,
+               bool want_stats = false) {
+  const char* gv = std::getenv("SDNS_GRAPH");
+  const bool graph = c->cfg.p == 1 && !c->timing && !(gv && gv[0] == '0');
+  if (!graph) {
+    step_stages(c, st, dt, post_project, want_stats);
+  } else {
+    sdns_ctx::StepGraph& g = c->graphs[want_stats ? 1 : 0];
+    // dt is a device-side scalar of the captured step (advance's dt_k varies
+    // in its last bits from step to step)
+    sdns_dev::set_step_scalars(c->d_dts, dt, c->stream);
+    if (!g.exec || g.st != st || g.post_project != post_project) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+      cudaGraph_t graph_def = nullptr;
+      SDNS_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        step_stages(c, st, dt, post_project, want_stats, c->d_dts);
+      } catch (...) {
+        cudaStreamEndCapture(c->stream, &graph_def);
+        if (graph_def) cudaGraphDestroy(graph_def);
+        throw;
+      }
+      SDNS_CUDA(cudaStreamEndCapture(c->stream, &graph_def));
+      SDNS_CUDA(cudaGraphInstantiate(&g.exec, graph_def, 0));
+      cudaGraphDestroy(graph_def);
+      g.st = st;
+      g.post_project = post_project;
+    }
+    SDNS_CUDA(cudaGraphLaunch(g.exec, c->stream));
   }
   st->t += dt;
   st->step += 1;
@@ -986,6 +1034,7 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
     c->d_partial = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride * nblk));
     c->d_fpartial = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride * nblk));
     c->d_fout = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride));
+    c->d_dts = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * 4));
     c->d_out = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride));
     c->d_flag = static_cast<int*>(dev_alloc(c.get(), sizeof(int)));
     SDNS_CUDA(cudaMallocHost(&c->h_out, sizeof(double) * stride));
@@ -1001,6 +1050,8 @@ int sdns_ctx_destroy(sdns_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    for (auto& g : c->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     cudaFree(c->tw);
     if (c->wb != c->wa) cudaFree(c->wb);
     if (c->wc) cudaFree(c->wc);
@@ -1009,6 +1060,7 @@ int sdns_ctx_destroy(sdns_ctx* c) {
     cudaFree(c->wa);
     cudaFree(c->d_partial);
     cudaFree(c->d_fpartial);
+    cudaFree(c->d_dts);
     cudaFree(c->d_fout);
     cudaFree(c->d_out);
     cudaFree(c->d_flag);
@@ -1199,6 +1251,11 @@ int sdns_state_destroy(sdns_state* st) {
     if (!st) return;
     cudaSetDevice(st->ctx->device);
     cudaStreamSynchronize(st->ctx->stream);
+    for (auto& g : st->ctx->graphs)  // captured steps bake this state's buffers in
+      if (g.st == st && g.exec) {
+        cudaGraphExecDestroy(g.exec);
+        g = sdns_ctx::StepGraph{};
+      }
     cudaFree(st->u.data);
     cudaFree(st->nxt);
     cudaFree(st->accum);

@@ -127,6 +127,9 @@ template <int MODE>
 __device__ __forceinline__ void rk_elem(const XfArgs& a, const SpecGeom& g, long long e, int i,
                                         int j, int k, bool& finite, double2 (&un)[3]) {
   const double kmax = static_cast<double>(g.n) / 3.0;
+  const double bdt = a.dts ? a.dts[a.dts_stage] : a.bdt;
+  const double ubdt = a.dts ? a.dts[0] : a.ubdt;
+  const double sixth = a.dts ? a.dts[3] : a.sixth;
   const double kx = wavenum(g.o0 + i, g.n), ky = wavenum(g.o1 + j, g.n);
   const double kzd = static_cast<double>(g.o2 + k);
   // dealias mask (navier_stokes.cpp:123-125): masked modes of the nonlinear
@@ -144,8 +147,7 @@ __device__ __forceinline__ void rk_elem(const XfArgs& a, const SpecGeom& g, long
     if (MODE != XF_TAIL) bq[q] = a.base[q * a.cs + e];
     if (MODE == XF_RK12 || MODE == XF_RK3) sq[q] = a.accum[q * a.cs + e];
     if (MODE == XF_RK12 && a.ubdt != 0.0)
-      uq[q] = make_double2(dadd(bq[q].x, dmul(a.ubdt, sq[q].x)),
-                           dadd(bq[q].y, dmul(a.ubdt, sq[q].y)));
+      uq[q] = make_double2(dadd(bq[q].x, dmul(ubdt, sq[q].x)), dadd(bq[q].y, dmul(ubdt, sq[q].y)));
     else
       uq[q] = a.u[q * a.cs + e];
     if (MODE == XF_RK3) cr[q] = a.carry[q * a.cs + e];
@@ -176,14 +178,14 @@ __device__ __forceinline__ void rk_elem(const XfArgs& a, const SpecGeom& g, long
       double2 s = make_double2(dmul(a.w, du[q].x), dmul(a.w, du[q].y));
       if (MODE == XF_RK12) s = make_double2(dadd(sq[q].x, s.x), dadd(sq[q].y, s.y));
       a.accum[q * a.cs + e] = s;
-      a.out[q * a.cs + e] = make_double2(dadd(bq[q].x, dmul(a.bdt, du[q].x)),
-                                         dadd(bq[q].y, dmul(a.bdt, du[q].y)));
+      a.out[q * a.cs + e] = make_double2(dadd(bq[q].x, dmul(bdt, du[q].x)),
+                                         dadd(bq[q].y, dmul(bdt, du[q].y)));
     }
   } else {  // XF_RK3, rk4.cpp:55-64
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const double dr = dadd(dmul(a.sixth, dadd(sq[q].x, du[q].x)), cr[q].x);
-      const double di = dadd(dmul(a.sixth, dadd(sq[q].y, du[q].y)), cr[q].y);
+      const double dr = dadd(dmul(sixth, dadd(sq[q].x, du[q].x)), cr[q].x);
+      const double di = dadd(dmul(sixth, dadd(sq[q].y, du[q].y)), cr[q].y);
       const double nr = dadd(bq[q].x, dr), ni = dadd(bq[q].y, di);
       a.carry[q * a.cs + e] = make_double2(two_sum_err(bq[q].x, dr, nr), two_sum_err(bq[q].y, di, ni));
       un[q] = make_double2(nr, ni);
@@ -945,6 +947,17 @@ static void rk_update_mode(const XfArgs& a, const SpecGeom& g, cudaStream_t s) {
   const long long total = static_cast<long long>(g.s0) * g.prow * g.pitch;
   const long long need = (total + 255) / 256;
   k_rk_update<MODE><<<static_cast<unsigned>(need < grid ? need : grid), 256, 0, s>>>(a, g);
+}
+
+__global__ void k_set_step_scalars(double* dts, double b0, double b1, double b2, double sixth) {
+  dts[0] = b0;
+  dts[1] = b1;
+  dts[2] = b2;
+  dts[3] = sixth;
+}
+void set_step_scalars(double* dts, double dt, cudaStream_t s) {
+  // the same host products the eager path passes by value (bitwise equal)
+  k_set_step_scalars<<<1, 1, 0, s>>>(dts, 0.5 * dt, 0.5 * dt, 1.0 * dt, dt / 6.0);
 }
 
 void rk_update(int mode, const XfArgs& a, const SpecGeom& g, cudaStream_t s) {

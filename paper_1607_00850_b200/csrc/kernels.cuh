@@ -96,6 +96,11 @@ struct XfArgs {
   double bdt;          // stage offset * dt
   double ubdt;         // XF_RK12: != 0 -> u = base + ubdt * accum (stage 1: u_1
                        // rebuilt bitwise from accum = du_0, saving the read of u)
+  // When set, the dt-dependent scalars come from device memory instead
+  // (captured steps replay with any dt): dts = [b0 dt, b1 dt, b2 dt, dt/6],
+  // bdt = dts[dts_stage], ubdt = dts[0] (if ubdt != 0), sixth = dts[3].
+  const double* dts = nullptr;
+  int dts_stage = 0;
   double sixth;        // dt/6 (stage 3)
   int dealias;
   int project;         // stage 3: post-step projection
@@ -133,6 +138,8 @@ struct SpecGeom;
 // P5b: mask + projection + viscous + RK4 stage update, streaming over the
 // x layout (a.nl holds the x-forward-transformed nonlinear term).
 void rk_update(int mode, const XfArgs& a, const SpecGeom& g, cudaStream_t s);
+// dts[0..3] = b dt (b = 1/2, 1/2, 1), dt/6 for the next captured step
+void set_step_scalars(double* dts, double dt, cudaStream_t s);
 
 void z_fused(int n, double2* rows, long long cs, const RowMap& rm, double norm,
              const double2* tw, cudaStream_t s);
