@@ -1,4 +1,6 @@
-# A/B over environment settings: each arg is "NAME=VALUE" (or "default")
+#!/bin/bash
+# A/B timing over runtime switches (run from the repo root on the GPU box):
+#   bash tools/ab_env.sh SDNS_XLAYOUT=0 SDNS_NO_TMA=1 ...
 show() { python3 -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$1', d['ms_per_step'], {k: round(v['avg_ms'],3) for k,v in d['passes'].items()})"; }
 for v in default "$@"; do
   for rep in 1 2; do

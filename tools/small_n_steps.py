@@ -1,3 +1,5 @@
+"""Steps/s of advance() at small n (config 1 is TG 64^3 sampled every step):
+   python tools/small_n_steps.py      (GPU box; DT=... overrides dt)"""
 import time, sys, os
 DT = float(os.environ.get("DT", "0.01"))
 sys.path.insert(0, '.')
