@@ -13,7 +13,9 @@
 //        transpose / receive buffer of the forward one
 //   wb  "y layout"  [peer][x_l][y_l][pitch] x 6 comps -- the receive layout,
 //        read directly by the y pass (no unpack pass); aliases wa at p = 1.
+#include <algorithm>
 #include <array>
+#include <initializer_list>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -138,6 +140,10 @@ struct sdns_ctx {
   double* d_fout = nullptr;
   const sdns_field* fused_u = nullptr;
   double* d_dts = nullptr;  // dt-dependent scalars of captured steps
+  // slab p > 1: transposes on their own stream, overlapped with the FFT
+  // passes of the other field groups (events order the two streams)
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t xev[12] = {};
   double* h_out = nullptr;  // pinned
   int* d_flag = nullptr;
   int* h_flag = nullptr;    // pinned
@@ -368,6 +374,22 @@ struct sdns_ctx {
     SDNS_CUDA(cudaMemcpy3DAsync(&p, stream));
   }
   // transpose between wa (x layout) and wb (receive layout)
+  // Transpose of the fields `fl` on stream `st` (the overlapped pipeline).
+  void exchange_fields(bool inverse_dir, std::initializer_list<int> fl, cudaStream_t st) {
+    const int nf = *std::max_element(fl.begin(), fl.end()) + 1;
+    const auto plan = exchange_plan(cfg, lo, inverse_dir, nf);
+    std::vector<Xfer> xs;
+    double2* src = inverse_dir ? wa : wb;
+    double2* dst = inverse_dir ? wb : wa;
+    const long long per = static_cast<long long>(plan.size()) / nf;  // entries per field
+    for (int f : fl)
+      for (long long q = 0; q < per; ++q) {
+        const auto& e = plan[static_cast<size_t>(f * per + q)];
+        const size_t bytes = sizeof(double2) * static_cast<size_t>(e[3]);
+        xs.push_back({static_cast<int>(e[0]), src + e[1], dst + e[2], bytes, bytes});
+      }
+    world->alltoall(xs, st);
+  }
   void exchange(bool inverse_dir, int nfields) {
     if (cfg.p == 1) return;
     const int tk = tick(inverse_dir ? SDNS_PASS_A2A_INV : SDNS_PASS_A2A_FWD);
@@ -440,8 +462,74 @@ void pencil_yfwd_geoms(const sdns_ctx* c, bool prune, ColGeom& gi, ColGeom& go) 
   go.keep_k = K;
 }
 
+// Slab p > 1 with the transposes overlapped: P1 runs per input component
+// (component c writes fields {c} or {c, 2 + c}); each group's transpose goes
+// out on the comm stream while the next component transforms, and P2 runs
+// per group as its data arrives. On the forward side P4 and P5a run per
+// field around the per-field transposes. Kernels and arithmetic are those of
+// the serial path, so results are bitwise identical.
+void rhs_slab_overlap(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args_in) {
+  const int n = c->cfg.n;
+  cudaStream_t s = c->stream, cs = c->cstream;
+  cudaEvent_t* ev = c->xev;
+  const long long sc = c->spec_cs;
+  int tk = c->tick(SDNS_PASS_X_INV_CURL);
+  for (int g = 0; g < 3; ++g) {
+    sdns_dev::x_inverse_split(n, u_in, sc, c->wa, sc, c->xgeom(), nullptr, c->tw, s, g, 1);
+    SDNS_CUDA(cudaEventRecord(ev[g], s));
+    SDNS_CUDA(cudaStreamWaitEvent(cs, ev[g], 0));
+    if (g == 0) c->exchange_fields(true, {0}, cs);
+    else if (g == 1) c->exchange_fields(true, {1, 3}, cs);
+    else c->exchange_fields(true, {2, 4}, cs);
+    SDNS_CUDA(cudaEventRecord(ev[3 + g], cs));
+  }
+  c->tock(tk);
+  tk = c->tick(SDNS_PASS_Y_INV);
+  const int item_lo[3] = {0, 1, 3}, item_cnt[3] = {1, 2, 2};
+  for (int g = 0; g < 3; ++g) {
+    SDNS_CUDA(cudaStreamWaitEvent(s, ev[3 + g], 0));
+    sdns_dev::y_inverse_curl(n, c->wb, sc, c->ygeom(), c->tw, s, item_lo[g], item_cnt[g]);
+  }
+  c->tock(tk);
+  RowMap zm = c->zmap(false);
+  if (c->cfg.dealias) zm.kz_keep = c->keep_k() + 1;
+  tk = c->tick(SDNS_PASS_Z_FUSED);
+  sdns_dev::z_fused(n, c->wb, sc, zm, c->norm, c->tw, s);
+  c->tock(tk);
+  tk = c->tick(SDNS_PASS_Y_FWD);
+  for (int f = 0; f < 3; ++f) {
+    sdns_dev::col_plain(n, -1, false, c->wb + f * sc, c->wb + f * sc, sc, sc, 1, c->ygeom_fwd(),
+                        c->tw, s);
+    SDNS_CUDA(cudaEventRecord(ev[6 + f], s));
+    SDNS_CUDA(cudaStreamWaitEvent(cs, ev[6 + f], 0));
+    c->exchange_fields(false, {f}, cs);
+    SDNS_CUDA(cudaEventRecord(ev[9 + f], cs));
+  }
+  c->tock(tk);
+  XfArgs a = args_in;
+  a.nl = c->wa;
+  a.nl_cs = sc;
+  a.cs = sc;
+  a.dealias = c->cfg.dealias;
+  tk = c->tick(SDNS_PASS_X_FWD_FFT);
+  for (int f = 0; f < 3; ++f) {
+    SDNS_CUDA(cudaStreamWaitEvent(s, ev[9 + f], 0));
+    sdns_dev::col_plain(n, -1, true, c->wa + f * sc, c->wa + f * sc, sc, sc, 1, c->xgeom_fwd(),
+                        c->tw, s);
+  }
+  c->tock(tk);
+  tk = c->tick(SDNS_PASS_X_FWD_TAIL + mode);
+  sdns_dev::rk_update(mode, a, c->sgeom(), s);
+  c->tock(tk);
+  post_launch("rhs pipeline (overlapped transposes)");
+}
+
 // One fused RHS evaluation: P1 .. P5 (kernels*.cu) with the transposes.
 void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args_in) {
+  if (c->cstream) {
+    rhs_slab_overlap(c, u_in, mode, args_in);
+    return;
+  }
   const int n = c->cfg.n;
   cudaStream_t s = c->stream;
   int tk = c->tick(SDNS_PASS_X_INV_CURL);
@@ -1023,6 +1111,11 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
       c->wd = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * static_cast<size_t>(c->cs_d) * 6));
     } else {
       c->wb = cfg->p == 1 ? c->wa : static_cast<double2*>(dev_alloc(c.get(), wbytes));
+      const char* ov = std::getenv("SDNS_OVERLAP");
+      if (cfg->p > 1 && !(ov && ov[0] == '0')) {
+        SDNS_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+        for (auto& e : c->xev) SDNS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
       const char* xl = std::getenv("SDNS_XLAYOUT");
       if (cfg->p == 1 && !(xl && xl[0] == '0')) {
         c->cs_x = static_cast<long long>(c->pitch) * c->lo.spec_shape[1] * n;
@@ -1052,6 +1145,11 @@ int sdns_ctx_destroy(sdns_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (auto& g : c->graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (c->cstream) {
+      cudaStreamSynchronize(c->cstream);
+      for (auto& e : c->xev) cudaEventDestroy(e);
+      cudaStreamDestroy(c->cstream);
+    }
     cudaFree(c->tw);
     if (c->wb != c->wa) cudaFree(c->wb);
     if (c->wc) cudaFree(c->wc);

@@ -121,11 +121,16 @@ void col_plain(int n, int dir, bool xaxis, const double2* in, double2* out, long
                cudaStream_t s);
 // P1: u_hat (3 comps) -> [U0, U1, U2, w2', K2] (5 comps of `out`), written
 // in geometry go (the input geometry g when go is NULL)
+// comp_lo/comp_cnt: input components (items) to run; component c writes
+// fields c and (c > 0) 2 + c.
 void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
-                     const ColGeom& g, const ColGeom* go, const double2* tw, cudaStream_t s);
+                     const ColGeom& g, const ColGeom* go, const double2* tw, cudaStream_t s,
+                     int comp_lo = 0, int comp_cnt = 3);
 // P2: in place, fields [U0, U1, U2, K1, K2] -> [u0, u1, u2, w0', w1', w2]
+// items item_lo .. item_lo+item_cnt-1 of the order U0, U1, w2', U2, K2
+// (fields 0, 1, 3, 2, 4)
 void y_inverse_curl(int n, double2* f, long long cs, const ColGeom& g, const double2* tw,
-                    cudaStream_t s);
+                    cudaStream_t s, int item_lo = 0, int item_cnt = 5);
 // Same, reading geometry g of `fin` and writing geometry go of `fout`
 // (pencil: col-receive layout in, row-send layout out).
 void y_inverse_curl_to(int n, const double2* fin, double2* fout, long long cs_in, long long cs_out,

@@ -263,7 +263,7 @@ __device__ __forceinline__ void tma_tile(double2* buf, const CUtensorMap* tm, co
 // the input field of item f (fld(f) its index in the tensor map tm when
 // g.tma != 0); body(f, buf, tile, pos_offsets, lanes, twiddles) transforms.
 template <int N, int V, class SrcF, class FldF, class BodyF>
-__device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g, SrcF src,
+__device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const ColGeom& g, SrcF src,
                                          FldF fld, const CUtensorMap* tm,
                                          const double2* __restrict__ tw_global, BodyF body) {
   extern __shared__ __align__(128) double2 smem[];
@@ -293,7 +293,9 @@ __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g
   // single-buffer path has an explicit one): the same release the mbarrier
   // empty/full pipelines of TMA producers rely on.
   const int G = gridDim.x;
-  int f = 0, tile = blockIdx.x;
+  // items f_lo .. f_lo + items - 1 of every tile
+  const int f_hi = f_lo + items;
+  int f = f_lo, tile = blockIdx.x;
   if (NBUF == 1) {
     for (int i = 0; tile < ntiles; ++i) {
       const Tile tl = tile_of<CS>(tile, col, g);
@@ -307,8 +309,8 @@ __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g
       }
       body(f, smem, tl, po, ln, static_cast<const double2*>(tws));
       ln.bar();
-      if (++f == items) {
-        f = 0;
+      if (++f == f_hi) {
+        f = f_lo;
         tile += G;
       }
     }
@@ -325,15 +327,15 @@ __device__ __forceinline__ void pipeline(int ntiles, int items, const ColGeom& g
     int t0, f;
   };
   auto adv = [&](Item it) {
-    if (++it.f == items) {
-      it.f = 0;
+    if (++it.f == f_hi) {
+      it.f = f_lo;
       it.t0 += G;
     }
     return it;
   };
-  Item cur{static_cast<int>(blockIdx.x), 0};
+  Item cur{static_cast<int>(blockIdx.x), f_lo};
   Tile tc = tile_of<CS>(cur.t0, col, g);
-  if (cur.t0 < ntiles) issue(0, 0, tc);
+  if (cur.t0 < ntiles) issue(0, f_lo, tc);
   cp_commit();
   Item n1 = adv(cur);
   Tile tn1 = tile_of<CS>(n1.t0, col, g);
@@ -387,7 +389,7 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
              ColGeom g, ColGeom go, int ntiles, const double2* __restrict__ tw,
              const __grid_constant__ CUtensorMap tm) {
   const OutSel<N, SEP> os(go, Lanes<N, V>().t);
-  pipeline<N, V>(ntiles, nfields, g, [&](int f) { return in + f * in_cs; },
+  pipeline<N, V>(ntiles, 0, nfields, g, [&](int f) { return in + f * in_cs; },
                  [](int f) { return f; }, &tm, tw,
                  [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po,
                      const Lanes<N, V>& ln, const double2* tws) {
@@ -407,14 +409,15 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
 template <int N, int V, bool SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, ColGeom g,
-            ColGeom go, int ntiles, const double2* __restrict__ tw,
+            ColGeom go, int ntiles, int f_lo, int f_cnt, const double2* __restrict__ tw,
             const __grid_constant__ CUtensorMap tm) {
   constexpr int E = fft_elems(N), TPC = N / E;
   constexpr bool SCR = PipeCfg<N, V>::SCR > 0;
   extern __shared__ __align__(128) double2 smem[];
   const OutSel<N, SEP> os(go, Lanes<N, V>().t);
   double2* const scr = smem + PipeCfg<N, V>::NBUF * N * PipeCfg<N, V>::CS;
-  pipeline<N, V>(ntiles, 3, g, [&](int f) { return u + f * u_cs; }, [](int f) { return f; },
+  pipeline<N, V>(ntiles, f_lo, f_cnt, g, [&](int f) { return u + f * u_cs; },
+                 [](int f) { return f; },
                  &tm, tw,
                  [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po,
                      const Lanes<N, V>& ln, const double2* tws) {
@@ -471,7 +474,8 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
 template <int N, int V, bool SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGeom g, ColGeom go,
-            int ntiles, const double2* __restrict__ tw, const __grid_constant__ CUtensorMap tm) {
+            int ntiles, int f_lo, int f_cnt, const double2* __restrict__ tw,
+            const __grid_constant__ CUtensorMap tm) {
   constexpr int E = fft_elems(N), TPC = N / E;
   // field of item it: 0, 1, 3, 2, 4
   auto order = [](int it) { return it ^ ((it >> 1) & ~(it >> 2) & 1); };
@@ -479,7 +483,8 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
   auto put = [&](int field, const double2(&r)[E], const Tile& tl, const PosOff<N>& po, int t) {
     store_own<N>(f + field * cs, r, go, os.tile(tl, go), os.po(po), t);
   };
-  pipeline<N, V>(ntiles, 5, g, [&](int it) { return fin + order(it) * cs_in; }, order, &tm, tw,
+  pipeline<N, V>(ntiles, f_lo, f_cnt, g, [&](int it) { return fin + order(it) * cs_in; }, order,
+                 &tm, tw,
                  [&](int it, double2* buf, const Tile& tl, const PosOff<N>& po,
                      const Lanes<N, V>& ln, const double2* tws) {
                    const int t = ln.t;
@@ -673,7 +678,8 @@ void col_plain_to(int n, int dir, const double2* in, double2* out, long long in_
 
 template <int N>
 static void x_inv_n(const double2* u, long long u_cs, double2* out, long long out_cs,
-                    const ColGeom& g, const ColGeom* go, const double2* tw, cudaStream_t s) {
+                    const ColGeom& g, const ColGeom* go, int f_lo, int f_cnt, const double2* tw,
+                    cudaStream_t s) {
   using C = PipeCfg<N, VXI>;
   const long long nt = ntiles_of<N, VXI>(g);
   CUtensorMap tm;
@@ -681,22 +687,23 @@ static void x_inv_n(const double2* u, long long u_cs, double2* out, long long ou
   if (go) {
     static int occ = 0;
     const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, true>, C::THREADS, C::SMEM, nt, &occ);
-    k_pipe_xinv<N, VXI, true><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, gt, *go,
-                                                                static_cast<int>(nt), tw, tm);
+    k_pipe_xinv<N, VXI, true><<<grid, C::THREADS, C::SMEM, s>>>(
+        u, u_cs, out, out_cs, gt, *go, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   } else {
     static int occ = 0;
     const unsigned grid =
         persistent_grid(k_pipe_xinv<N, VXI, false>, C::THREADS, C::SMEM, nt, &occ);
-    k_pipe_xinv<N, VXI, false><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, gt, gt,
-                                                                 static_cast<int>(nt), tw, tm);
+    k_pipe_xinv<N, VXI, false><<<grid, C::THREADS, C::SMEM, s>>>(
+        u, u_cs, out, out_cs, gt, gt, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   }
 }
 
 void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
-                     const ColGeom& g, const ColGeom* go, const double2* tw, cudaStream_t s) {
+                     const ColGeom& g, const ColGeom* go, const double2* tw, cudaStream_t s,
+                     int comp_lo, int comp_cnt) {
   switch (n) {
 #define X(NN) \
-  case NN: x_inv_n<NN>(u, u_cs, out, out_cs, g, go, tw, s); return;
+  case NN: x_inv_n<NN>(u, u_cs, out, out_cs, g, go, comp_lo, comp_cnt, tw, s); return;
     SDNS_FOR_N(X)
 #undef X
   }
@@ -704,7 +711,8 @@ void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long
 
 template <int N>
 static void y_inv_n(const double2* fin, double2* f, long long cs_in, long long cs,
-                    const ColGeom& g, const ColGeom* go, const double2* tw, cudaStream_t s) {
+                    const ColGeom& g, const ColGeom* go, int f_lo, int f_cnt, const double2* tw,
+                    cudaStream_t s) {
   using C = PipeCfg<N, VYI>;
   const long long nt = ntiles_of<N, VYI>(g);
   if (go) {
@@ -713,24 +721,24 @@ static void y_inv_n(const double2* fin, double2* f, long long cs_in, long long c
         persistent_grid(k_pipe_yinv<N, VYI, true>, C::THREADS, C::SMEM, nt, &occ);
     CUtensorMap tm;
     const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
-    k_pipe_yinv<N, VYI, true><<<grid, C::THREADS, C::SMEM, s>>>(fin, f, cs_in, cs, gt, *go,
-                                                                static_cast<int>(nt), tw, tm);
+    k_pipe_yinv<N, VYI, true><<<grid, C::THREADS, C::SMEM, s>>>(
+        fin, f, cs_in, cs, gt, *go, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   } else {
     static int occ = 0;
     const unsigned grid =
         persistent_grid(k_pipe_yinv<N, VYI, false>, C::THREADS, C::SMEM, nt, &occ);
     CUtensorMap tm;
     const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
-    k_pipe_yinv<N, VYI, false><<<grid, C::THREADS, C::SMEM, s>>>(fin, f, cs_in, cs, gt, g,
-                                                                 static_cast<int>(nt), tw, tm);
+    k_pipe_yinv<N, VYI, false><<<grid, C::THREADS, C::SMEM, s>>>(
+        fin, f, cs_in, cs, gt, g, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   }
 }
 
 void y_inverse_curl(int n, double2* f, long long cs, const ColGeom& g, const double2* tw,
-                    cudaStream_t s) {
+                    cudaStream_t s, int item_lo, int item_cnt) {
   switch (n) {
 #define X(NN) \
-  case NN: y_inv_n<NN>(f, f, cs, cs, g, nullptr, tw, s); return;
+  case NN: y_inv_n<NN>(f, f, cs, cs, g, nullptr, item_lo, item_cnt, tw, s); return;
     SDNS_FOR_N(X)
 #undef X
   }
@@ -740,7 +748,7 @@ void y_inverse_curl_to(int n, const double2* fin, double2* fout, long long cs_in
                        const ColGeom& g, const ColGeom& go, const double2* tw, cudaStream_t s) {
   switch (n) {
 #define X(NN) \
-  case NN: y_inv_n<NN>(fin, fout, cs_in, cs_out, g, &go, tw, s); return;
+  case NN: y_inv_n<NN>(fin, fout, cs_in, cs_out, g, &go, 0, 5, tw, s); return;
     SDNS_FOR_N(X)
 #undef X
   }

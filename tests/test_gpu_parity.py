@@ -435,6 +435,35 @@ def test_inprocess_slab_rk4_matches_single_rank(p):
             assert a.energy == b.energy and a.enstrophy == b.enstrophy
 
 
+@pytest.mark.parametrize("p", [2, 4])
+def test_inprocess_slab_overlapped_transposes_bitwise(p):
+    """Slab p > 1 overlaps each field group's transpose with the transforms of
+    the next (comm stream + events); the kernels and arithmetic are those of
+    the serial pipeline (SDNS_OVERLAP=0), so one RHS must agree bit for bit."""
+    n = 32
+    lo1 = S.build_layout(S.SolverConfig(n=n), 0)
+    uh0 = S.iso_init(n, lo1, seed=9)
+    cfg = S.SolverConfig(n=n, p=p, nu=1e-3, dt=1e-3, t_end=1e-3)
+
+    def run():
+        def body(rank, comm):
+            with S.Context(cfg, rank=rank, comm=comm) as c:
+                u = c.spectral_field().upload(_scatter_spec(uh0, c.layout))
+                du = c.spectral_field()
+                S.compute_rhs(c, u, 1e-3, du)
+                return du.download()
+        return S.run_group(p, body)
+
+    over = run()
+    os.environ["SDNS_OVERLAP"] = "0"
+    try:
+        serial = run()
+    finally:
+        os.environ.pop("SDNS_OVERLAP", None)
+    for a, b in zip(over, serial):
+        assert np.array_equal(a, b)
+
+
 # --- pencil decomposition (fft.cpp:130-227) on one GPU ---------------------------
 
 PENCILS = [(2, 1), (1, 2), (2, 2), (2, 4), (4, 2)]
