@@ -169,6 +169,74 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def other_configs(S, ctx, peak):
+    """The other BASELINE configs, measured quickly beside the headline line
+    (informational; each on seeded synthetic fields of the config's shape):
+    config 5 round trip at 512^3 (3 comps) against its HBM roofline
+    3*(2R + 10C) bytes, config 1 (TG 64^3, 100 steps, E and Z
+    every step) and config 2 (iso 256^3, 50 steps)."""
+    import numpy as np
+    import torch
+
+    out = {}
+    n = ctx.cfg.n
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    fft = S.DistributedFFT(ctx)
+    ur, ub, fu = ctx.real_field(), ctx.real_field(), ctx.spectral_field()
+    ur.upload(np.random.default_rng(42 + n).uniform(-1.0, 1.0, (3, n, n, n)))
+    fft.forward(ur, fu)
+    fft.inverse(fu, ub)
+    ctx.sync()
+    reps = 3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fft.forward(ur, fu)
+        fft.inverse(fu, ub)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    R, C = 8.0 * n**3, spectral_bytes(n, 1)
+    rt_bytes = 3 * (2 * R + 10 * C)
+    out["config5_round_trip_512"] = {
+        "ms": ms, "roofline_ms": rt_bytes / peak / 1e6, "frac": rt_bytes / (ms * 1e-3) / 1e9 / peak,
+        "rel_l2": S.l2_diff(ctx, ub, ur) / S.l2_diff(ctx, ur, ctx.real_field())}
+    for f in (ur, ub, fu):
+        f.free()
+    for key, (m, steps, every, nu, dt, tg) in {
+            "config1_tg64_sampled": (64, 100, 1, 0.01, 0.01, True),
+            "config2_iso256": (256, 50, 50, 1e-3, 1e-3, False)}.items():
+        cfg = S.SolverConfig(n=m, nu=nu, dt=dt, t_end=steps * dt, out_every=every)
+        with S.Context(cfg) as c:
+            lo = c.layout
+            if tg:
+                x = 2 * np.pi * np.arange(m) / m
+                X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
+                u = np.stack([np.sin(X) * np.cos(Y) * np.cos(Z),
+                              -np.cos(X) * np.sin(Y) * np.cos(Z), np.zeros_like(X)])
+                uh = c.spectral_field()
+                S.DistributedFFT(c).forward(c.real_field().upload(u), uh)
+                S.project(c, uh)
+            else:
+                uh = c.spectral_field().upload(S.iso_init(m, lo, seed=1607))
+            st = S.Rk4State(c)
+            rows = []
+            hook = lambda k, t: rows.append(S.collect_stats(c, st.u_hat, nu, t))  # noqa: E731
+            st.set(uh)
+            st.advance(hook)  # warm (captures the step graph)
+            st.set(uh)
+            rows.clear()
+            c.sync()
+            t0 = time.perf_counter()
+            st.advance(hook)
+            c.sync()
+            sec = time.perf_counter() - t0
+            out[key] = {"steps_per_s": steps / sec, "ms_per_step": sec / steps * 1e3,
+                        "samples": len(rows), "energy_last": rows[-1].energy}
+            st.close()
+    return out
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -308,6 +376,9 @@ def run_ours(args):
                   "div_max": stats.divergence_max},
         "init_s": init_s,
     }
+    if world == 1 and n == 512 and not args.no_other_configs:
+        state.close()
+        line["other_configs"] = other_configs(S, ctx, peak)
     state.close()
     ctx.close()
     if world == 1 and not args.no_cpu_baseline:
@@ -338,6 +409,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
