@@ -235,7 +235,7 @@ template <int N>
 struct ZCfg {
   static constexpr int E = fft_elems(N);
   static constexpr int TPC = N / E;
-  static constexpr int RPC = TPC >= 128 ? 1 : (128 / TPC > 32 ? 32 : 128 / TPC);
+  static constexpr int RPC = TPC >= 64 ? 4 : (128 / TPC > 32 ? 32 : 128 / TPC);
   static constexpr int THREADS = TPC * RPC;
   static constexpr int HP = N / 2 + 8;  // padded half-row (n/2+1 modes)
 };
@@ -486,36 +486,63 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
 }
 
 // Standalone c2r along z (DistributedFFT::inverse tail, fft.cpp:124-125):
-// rows 2i and 2i+1 of one field share one complex inverse FFT.
+// rows 2i and 2i+1 of one field share one complex inverse FFT. Each pair of
+// rows is one TPC-thread group with its own named barrier (n >= 512); its
+// two half-rows arrive by bulk copy on the group's mbarrier; at n = 512 the
+// twiddles of both twiddled stages come from registers (no table in shared
+// memory).
 template <int N>
 __global__ void __launch_bounds__(ZCfg<N>::THREADS)
 k_z_c2r(const double2* __restrict__ spec, double* __restrict__ real, RowMap rm, double norm,
         const double2* __restrict__ tw) {
-  constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC, HP = ZCfg<N>::HP;
+  constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC, HP = ZCfg<N>::HP, RPC = ZCfg<N>::RPC;
+  constexpr bool REG = N == 512;
+  using Bar = typename std::conditional<(TPC >= 64), NamedBar, CtaBar>::type;
   extern __shared__ __align__(128) double2 smem[];
+  __shared__ alignas(8) unsigned long long zbar[RPC];
   const int t = threadIdx.x % TPC, r = threadIdx.x / TPC;
-  const int pr = blockIdx.x * ZCfg<N>::RPC + r;
+  const int pr = blockIdx.x * RPC + r;
   const int ri = 2 * pr;
   const bool valid = ri < rm.nrows;
-  // stage both half-rows (a pencil z line is spread over kz blocks)
+  Bar bar;
+  if constexpr (TPC >= 64) bar = Bar{1 + r, TPC};
   double2* S = smem + r * 2 * HP;
-  double2* tws = smem + ZCfg<N>::RPC * 2 * HP;
-  load_twiddles(tws, tw, N);
-  if (valid) {
-    const long long ra = rm.nseg ? 0 : zrow_off(rm, ri);
-    const long long rb = rm.nseg ? 0 : zrow_off(rm, ri + 1);
-    for (int k = t; k <= N / 2; k += TPC) {
-      S[k] = spec[zel(rm, ra, ri, k)];
-      S[HP + k] = spec[zel(rm, rb, ri + 1, k)];
+  const double2* tws = tw;
+  if constexpr (!REG) {
+    double2* t2 = smem + RPC * 2 * HP;
+    load_twiddles(t2, tw, N);
+    tws = t2;
+  }
+  if (t == 0) mbar_init(&zbar[r], 1);
+  __syncthreads();
+  if (valid && t == 0) {
+    // both half-rows (a pencil z line is spread over kz blocks)
+    mbar_expect_tx(&zbar[r], 2u * static_cast<unsigned>(rm.n2) * 16u);
+    for (int h = 0; h < 2; ++h) {
+      if (rm.nseg == 0) {
+        bulk_g2s(S + h * HP, spec + zrow_off(rm, ri + h), static_cast<unsigned>(rm.n2) * 16u,
+                 &zbar[r]);
+      } else {
+        for (int q = 0; q < rm.nseg; ++q) {
+          const int k0 = rm.seg_k0[q], k1 = rm.seg_k0[q + 1];
+          if (k1 > k0)
+            bulk_g2s(S + h * HP + k0,
+                     spec + rm.seg_base[q] + static_cast<long long>(ri + h) * rm.seg_pitch[q],
+                     static_cast<unsigned>(k1 - k0) * 16u, &zbar[r]);
+        }
+      }
     }
   }
-  __syncthreads();
+  LastTw lt{};
+  if constexpr (REG) lt = last_twiddles<N>(tw, t);
+  if (valid) mbar_wait(&zbar[r], 0);
   double2 v[E];
 #pragma unroll
   for (int m = 0; m < E; ++m)
     v[m] = valid ? pair_sample<N>(S, S + HP, t + m * TPC) : make_double2(0.0, 0.0);
-  __syncthreads();
-  block_fft<N, +1>(v, S, SwzIdx{}, t, tws);
+  bar();
+  if constexpr (REG) block_fft_lt<N, +1>(v, S, SwzIdx{}, t, tws, bar, lt);
+  else block_fft<N, +1>(v, S, SwzIdx{}, t, tws, bar);
   if (valid) {
     double* a = real + static_cast<long long>(ri) * N;
     double* b = a + N;
@@ -527,17 +554,22 @@ k_z_c2r(const double2* __restrict__ spec, double* __restrict__ real, RowMap rm, 
   }
 }
 
-// Standalone r2c along z (DistributedFFT::forward head, fft.cpp:87).
+// Standalone r2c along z (DistributedFFT::forward head, fft.cpp:87): two real
+// rows in one complex FFT, split by the mirror relation.
 template <int N>
 __global__ void __launch_bounds__(ZCfg<N>::THREADS)
 k_z_r2c(const double* __restrict__ real, double2* __restrict__ spec, RowMap rm,
         const double2* __restrict__ tw) {
-  constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC;
+  constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC, RPC = ZCfg<N>::RPC;
+  constexpr bool REG = N == 512;
+  using Bar = typename std::conditional<(TPC >= 64), NamedBar, CtaBar>::type;
   extern __shared__ __align__(128) double2 smem[];
   const int t = threadIdx.x % TPC, r = threadIdx.x / TPC;
-  const int pr = blockIdx.x * ZCfg<N>::RPC + r;
+  const int pr = blockIdx.x * RPC + r;
   const int ri = 2 * pr;
   const bool valid = ri < rm.nrows;
+  Bar bar;
+  if constexpr (TPC >= 64) bar = Bar{1 + r, TPC};
   double2* reg = smem + r * N;
   const SwzIdx sw;
   double2 v[E];
@@ -550,13 +582,22 @@ k_z_r2c(const double* __restrict__ real, double2* __restrict__ spec, RowMap rm,
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = make_double2(0.0, 0.0);
   }
-  double2* tws = smem + ZCfg<N>::RPC * N;
-  load_twiddles(tws, tw, N);
-  __syncthreads();
-  block_fft<N, -1>(v, reg, sw, t, tws);
+  const double2* tws = tw;
+  if constexpr (!REG) {
+    double2* t2 = smem + RPC * N;
+    load_twiddles(t2, tw, N);
+    tws = t2;
+    __syncthreads();
+  }
+  if constexpr (REG) {
+    const LastTw lt = last_twiddles<N>(tw, t);
+    block_fft_lt<N, -1>(v, reg, sw, t, tws, bar, lt);
+  } else {
+    block_fft<N, -1>(v, reg, sw, t, tws, bar);
+  }
 #pragma unroll
   for (int m = 0; m < E; ++m) reg[sw(t + m * TPC)] = v[m];
-  __syncthreads();
+  bar();
   if (valid) {
     const long long ra = rm.nseg ? 0 : zrow_off(rm, ri);
     const long long rb = rm.nseg ? 0 : zrow_off(rm, ri + 1);

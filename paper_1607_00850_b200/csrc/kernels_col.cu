@@ -38,7 +38,7 @@ namespace {
 #define SDNS_VX 0
 #endif
 #ifndef SDNS_VY
-#define SDNS_VY 1
+#define SDNS_VY 0
 #endif
 #ifndef SDNS_VYI
 #define SDNS_VYI 0
