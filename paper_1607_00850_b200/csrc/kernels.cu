@@ -317,9 +317,6 @@ struct ZFCfg {
 #ifndef SDNS_ZTMA
 #define SDNS_ZTMA 1
 #endif
-#ifndef SDNS_ZPARK1
-#define SDNS_ZPARK1 0
-#endif
 
 // z-pass transform; SDNS_ZNOFFT builds a transform-free variant (wrong
 // results) for A/B measurements of the pass's memory/shared-memory floor.
@@ -405,10 +402,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   __syncthreads();  // twiddles + staging
 #endif
   const LastTw lt = last_twiddles<N>(tws, t);
-  double2 v[E];
-#if !SDNS_ZPARK1
-  double2 p1[E];
-#endif
+  double2 v[E], p1[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) v[m] = pair_sample_kz<N, +1>(S, S + HP, t + m * TPC);
   bar();
@@ -423,11 +417,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   zfft<N, +1>(v, S + 2 * HP, sw, t, tws, bar, lt);
 #pragma unroll
   for (int m = 0; m < E; ++m) {
-#if SDNS_ZPARK1
-    S[2 * HP + sw(t + m * TPC)] = v[m];
-#else
     p1[m] = v[m];
-#endif
     v[m] = pair_sample<N>(S + 4 * HP, S + 5 * HP, t + m * TPC);
   }
   bar();
@@ -439,11 +429,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const double2 q0 = S[sw(t + m * TPC)];
-#if SDNS_ZPARK1
-    const double2 q1 = S[2 * HP + sw(t + m * TPC)];
-#else
     const double2 q1 = p1[m];
-#endif
     const double ua = dmul(q0.x, norm), ub = dmul(q1.x, norm), uc = dmul(v[m].x, norm);
     const double wa = dmul(q1.y, norm), wb = dmul(q0.y, norm), wc = dmul(v[m].y, norm);
     const double n0 = dsub(dmul(ub, wc), dmul(uc, wb));

@@ -160,16 +160,6 @@ __device__ __forceinline__ void store_own(double2* dst, const double2 (&v)[fft_e
 #ifdef SDNS_NOSTORE  // A/B measurement only (wrong results)
   if (tl.valid || !tl.valid) return;
 #endif
-#ifdef SDNS_TMSTORE  // A/B measurement only (wrong results): tile-major writes
-  {
-    if (!tl.valid) return;
-    double2* b = dst + (static_cast<long long>(tl.row) * (g.pitch / 8) + (tl.kz >> 3)) * N * 8 +
-                 (tl.kz & 7);
-#pragma unroll
-    for (int m = 0; m < E; ++m) b[(t + m * TPC) * 8] = v[m];
-    return;
-  }
-#endif
   if (!tl.valid) return;
   double2* b = dst + tl.base;
 #pragma unroll
