@@ -556,11 +556,27 @@ k_z_r2c(const double* __restrict__ real, double2* __restrict__ spec, RowMap rm,
   const bool valid = ri < rm.nrows;
   Bar bar;
   if constexpr (TPC >= 64) bar = Bar{1 + r, TPC};
+  __shared__ alignas(8) unsigned long long zbar[RPC];
   double2* reg = smem + r * N;
   const SwzIdx sw;
   double2 v[E];
+  // the pair's two real rows (2 x 8n B, contiguous) arrive by bulk copy into
+  // its region, which then serves as the transform's exchange buffer
+  if (t == 0) mbar_init(&zbar[r], 1);
+  const double2* tws = tw;
+  if constexpr (!REG) {
+    double2* t2 = smem + RPC * N;
+    load_twiddles(t2, tw, N);
+    tws = t2;
+  }
+  __syncthreads();
+  if (valid && t == 0) {
+    mbar_expect_tx(&zbar[r], 2u * N * 8u);
+    bulk_g2s(reg, real + static_cast<long long>(ri) * N, 2u * N * 8u, &zbar[r]);
+  }
   if (valid) {
-    const double* a = real + static_cast<long long>(ri) * N;
+    mbar_wait(&zbar[r], 0);
+    const double* a = reinterpret_cast<const double*>(reg);
     const double* b = a + N;
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = make_double2(a[t + m * TPC], b[t + m * TPC]);
@@ -568,13 +584,7 @@ k_z_r2c(const double* __restrict__ real, double2* __restrict__ spec, RowMap rm,
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = make_double2(0.0, 0.0);
   }
-  const double2* tws = tw;
-  if constexpr (!REG) {
-    double2* t2 = smem + RPC * N;
-    load_twiddles(t2, tw, N);
-    tws = t2;
-    __syncthreads();
-  }
+  bar();  // the region is read; the transform reuses it
   if constexpr (REG) {
     const LastTw lt = last_twiddles<N>(tw, t);
     block_fft_lt<N, -1>(v, reg, sw, t, tws, bar, lt);
