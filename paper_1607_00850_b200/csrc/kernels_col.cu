@@ -288,18 +288,45 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
   // items f_lo .. f_lo + items - 1 of every tile
   const int f_hi = f_lo + items;
   int f = f_lo, tile = blockIdx.x;
+  auto no_release = [] {};
+  if (NBUF == 1 && tma) {
+    // single buffer fed by TMA: the body calls release() once its transform
+    // has finished with the buffer (the trailing barrier of block_fft), and
+    // the next tile loads while this one is stored from registers
+    Tile tl = tile_of<CS>(tile, col, g);
+    if (tile < ntiles) issue(0, f, tl);
+    for (int i = 0; tile < ntiles; ++i) {
+      int fn = f + 1, tn = tile;
+      if (fn == f_hi) {
+        fn = f_lo;
+        tn += G;
+      }
+      const Tile tln = tile_of<CS>(tn, col, g);
+      mbar_wait(&tbar[0], i & 1);
+      bool issued = false;
+      auto release = [&] {
+        if (tn < ntiles) issue(0, fn, tln);
+        issued = true;
+      };
+      body(f, smem, tl, po, ln, static_cast<const double2*>(tws), release);
+      if (!issued) {
+        ln.bar();
+        release();
+      }
+      f = fn;
+      tile = tn;
+      tl = tln;
+    }
+    return;
+  }
   if (NBUF == 1) {
     for (int i = 0; tile < ntiles; ++i) {
       const Tile tl = tile_of<CS>(tile, col, g);
       issue(0, f, tl);
-      if (tma) {
-        mbar_wait(&tbar[0], i & 1);
-      } else {
-        cp_commit();
-        cp_wait0();
-        ln.bar();
-      }
-      body(f, smem, tl, po, ln, static_cast<const double2*>(tws));
+      cp_commit();
+      cp_wait0();
+      ln.bar();
+      body(f, smem, tl, po, ln, static_cast<const double2*>(tws), no_release);
       ln.bar();
       if (++f == f_hi) {
         f = f_lo;
@@ -347,7 +374,7 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
         cp_wait2();
         ln.bar();
       }
-      body(cur.f, ring(i % 3), tc, po, ln, static_cast<const double2*>(tws));
+      body(cur.f, ring(i % 3), tc, po, ln, static_cast<const double2*>(tws), no_release);
       cur = n1;
       tc = tn1;
       n1 = n2;
@@ -361,7 +388,7 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
         cp_wait1();
         ln.bar();
       }
-      body(cur.f, ring(i & 1), tc, po, ln, static_cast<const double2*>(tws));
+      body(cur.f, ring(i & 1), tc, po, ln, static_cast<const double2*>(tws), no_release);
       cur = n1;
       tc = tn1;
       n1 = adv(n1);
@@ -384,12 +411,13 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
   pipeline<N, V>(ntiles, 0, nfields, g, [&](int f) { return in + f * in_cs; },
                  [](int f) { return f; }, &tm, tw,
                  [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po,
-                     const Lanes<N, V>& ln, const double2* tws) {
+                     const Lanes<N, V>& ln, const double2* tws, auto&& release) {
                    const int t = ln.t;
                    double2 v[fft_elems(N)];
                    read_own<N>(v, buf, ln.idx, t);
                    ln.bar();
                    col_fft<N, S>(v, buf, ln.idx, t, tws, ln.bar);
+                   release();  // buffer no longer read: the next tile may load
                    store_own<N>(out + f * out_cs, v, go, os.tile(tl, go), os.po(po), t);
                  });
 }
@@ -412,9 +440,10 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                  [](int f) { return f; },
                  &tm, tw,
                  [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po,
-                     const Lanes<N, V>& ln, const double2* tws) {
+                     const Lanes<N, V>& ln, const double2* tws, auto&&) {
                    const int t = ln.t;
                    double2 v[E], vin[SCR ? 1 : E];
+                   (void)vin;
                    read_own<N>(v, buf, ln.idx, t);
                    if constexpr (!SCR) {
 #pragma unroll
@@ -478,7 +507,7 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
   pipeline<N, V>(ntiles, f_lo, f_cnt, g, [&](int it) { return fin + order(it) * cs_in; }, order,
                  &tm, tw,
                  [&](int it, double2* buf, const Tile& tl, const PosOff<N>& po,
-                     const Lanes<N, V>& ln, const double2* tws) {
+                     const Lanes<N, V>& ln, const double2* tws, auto&&) {
                    const int t = ln.t;
                    double2 vin[E], v[E];
                    read_own<N>(vin, buf, ln.idx, t);
