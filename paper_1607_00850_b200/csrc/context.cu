@@ -359,19 +359,22 @@ struct sdns_ctx {
     row->alltoall(xs, stream);
     tock(tk);
   }
-  // Host block (s0, s1, s2) <-> device planes (s0, prow, pitch) copy.
-  void copy_spec(void* dst, const void* src, bool to_device) const {
-    cudaMemcpy3DParms p{};
-    const size_t s2b = sizeof(double2) * static_cast<size_t>(lo.spec_shape[2]);
-    const size_t s1 = static_cast<size_t>(lo.spec_shape[1]);
-    cudaPitchedPtr host = make_cudaPitchedPtr(const_cast<void*>(to_device ? src : dst), s2b, s2b, s1);
-    cudaPitchedPtr dev = make_cudaPitchedPtr(const_cast<void*>(to_device ? dst : src),
-                                             sizeof(double2) * pitch, s2b, prow);
-    p.srcPtr = to_device ? host : dev;
-    p.dstPtr = to_device ? dev : host;
-    p.extent = make_cudaExtent(s2b, s1, static_cast<size_t>(lo.spec_shape[0]));
-    p.kind = to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
-    SDNS_CUDA(cudaMemcpy3DAsync(&p, stream));
+  // ncomp host components (RankLayout block order, contiguous) <-> the
+  // padded device layout: one contiguous DMA through the free work buffer
+  // plus an HBM-speed repack kernel (the copy engines move contiguous blocks
+  // markedly faster than the 2-D pitched copy). Only between pipeline runs.
+  void copy_spec_all(double2* dev, double* host, int ncomp, bool to_device) const {
+    const size_t bytes = sizeof(double2) * static_cast<size_t>(lo.spec_shape[0]) *
+                         static_cast<size_t>(lo.spec_shape[1]) *
+                         static_cast<size_t>(lo.spec_shape[2]) * static_cast<size_t>(ncomp);
+    double2* stage = wa;  // >= 6 padded components
+    if (to_device) {
+      SDNS_CUDA(cudaMemcpyAsync(stage, host, bytes, cudaMemcpyHostToDevice, stream));
+      sdns_dev::pw_repack(stage, dev, ncomp, sgeom(), false, stream);
+    } else {
+      sdns_dev::pw_repack(dev, stage, ncomp, sgeom(), true, stream);
+      SDNS_CUDA(cudaMemcpyAsync(host, stage, bytes, cudaMemcpyDeviceToHost, stream));
+    }
   }
   // transpose between wa (x layout) and wb (receive layout)
   // Transpose of the fields `fl` on stream `st` (the overlapped pipeline).
@@ -1217,10 +1220,7 @@ int sdns_field_upload(sdns_ctx* c, sdns_field* f, const double* host) {
       SDNS_CUDA(cudaMemcpyAsync(f->data, host, sizeof(double) * c->real_cs * f->ncomp,
                                 cudaMemcpyHostToDevice, c->stream));
     } else {
-      const size_t s2 = static_cast<size_t>(c->lo.spec_shape[2]);
-      const size_t rows = static_cast<size_t>(c->lo.spec_shape[0] * c->lo.spec_shape[1]);
-      for (int q = 0; q < f->ncomp; ++q)
-        c->copy_spec(f->spec() + q * c->spec_cs, host + 2 * q * s2 * rows, true);
+      c->copy_spec_all(f->spec(), const_cast<double*>(host), f->ncomp, true);
     }
     SDNS_CUDA(cudaStreamSynchronize(c->stream));
   });
@@ -1233,10 +1233,7 @@ int sdns_field_download(sdns_ctx* c, const sdns_field* f, double* host) {
       SDNS_CUDA(cudaMemcpyAsync(host, f->data, sizeof(double) * c->real_cs * f->ncomp,
                                 cudaMemcpyDeviceToHost, c->stream));
     } else {
-      const size_t s2 = static_cast<size_t>(c->lo.spec_shape[2]);
-      const size_t rows = static_cast<size_t>(c->lo.spec_shape[0] * c->lo.spec_shape[1]);
-      for (int q = 0; q < f->ncomp; ++q)
-        c->copy_spec(host + 2 * q * s2 * rows, f->spec() + q * c->spec_cs, false);
+      c->copy_spec_all(f->spec(), host, f->ncomp, false);
     }
     SDNS_CUDA(cudaStreamSynchronize(c->stream));
   });
@@ -1434,13 +1431,9 @@ int sdns_advance(sdns_ctx* c, sdns_state* st, sdns_sample_fn sample, void* user,
 int sdns_rk4_step_host(sdns_ctx* c, sdns_state* st, double* host, double dt, int steps) {
   return guarded([&] {
     set_device(c);
-    const size_t s2 = static_cast<size_t>(c->lo.spec_shape[2]);
-    const size_t rows = static_cast<size_t>(c->lo.spec_shape[0] * c->lo.spec_shape[1]);
-    for (int q = 0; q < 3; ++q)
-      c->copy_spec(st->u.spec() + q * c->spec_cs, host + 2 * q * s2 * rows, true);
+    c->copy_spec_all(st->u.spec(), host, 3, true);
     for (int k = 0; k < steps; ++k) step_impl(c, st, dt, 1, false);
-    for (int q = 0; q < 3; ++q)
-      c->copy_spec(host + 2 * q * s2 * rows, st->u.spec() + q * c->spec_cs, false);
+    c->copy_spec_all(st->u.spec(), host, 3, false);
     SDNS_CUDA(cudaStreamSynchronize(c->stream));
   });
 }

@@ -735,6 +735,27 @@ __global__ void k_fill_pad(double2* f, SpecGeom g, int ncomp) {
   if (m.i >= g.s0 || m.k < g.s2) return;
   for (int c = 0; c < ncomp; ++c) f[c * g.cs + e] = make_double2(0.0, 0.0);
 }
+__global__ void k_repack(const double2* __restrict__ src, double2* __restrict__ dst, int ncomp,
+                         SpecGeom g, long long packed_cs, int to_packed) {
+  const long long per = static_cast<long long>(g.s0) * g.s1 * g.s2;
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+       e < per * ncomp; e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long c = e / per, r = e - c * per;
+    const long long row = r / g.s2;
+    const int k = static_cast<int>(r - row * g.s2);
+    const long long i = row / g.s1, j = row - i * g.s1;
+    const long long pad = c * g.cs + (i * g.prow + j) * g.pitch + k;
+    const long long pk = c * packed_cs + r;
+    if (to_packed) dst[pk] = src[pad];
+    else dst[pad] = src[pk];
+  }
+}
+void pw_repack(const double2* src, double2* dst, int ncomp, const SpecGeom& g, bool to_packed,
+               cudaStream_t s) {
+  const long long per = static_cast<long long>(g.s0) * g.s1 * g.s2;
+  k_repack<<<grid_for(per * ncomp, 256), 256, 0, s>>>(src, dst, ncomp, g, per, to_packed ? 1 : 0);
+}
+
 void pw_fill_pad(double2* f, int ncomp, const SpecGeom& g, cudaStream_t s) {
   const long long tot = static_cast<long long>(g.s0) * g.prow * g.pitch;
   k_fill_pad<<<grid_for(tot, 256), 256, 0, s>>>(f, g, ncomp);

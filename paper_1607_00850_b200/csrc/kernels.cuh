@@ -169,6 +169,10 @@ void pw_pressure(const double2* nl, double2* p, const SpecGeom& g, cudaStream_t 
 void pw_cross(const double* a, const double* b, double* o, long long count, long long cs,
               cudaStream_t s);
 void pw_fill_pad(double2* f, int ncomp, const SpecGeom& g, cudaStream_t s);
+// ncomp spectral components between the padded device layout and the packed
+// RankLayout block order (to_packed: padded -> packed)
+void pw_repack(const double2* src, double2* dst, int ncomp, const SpecGeom& g, bool to_packed,
+               cudaStream_t s);
 void pw_finite(const double2* u, const SpecGeom& g, int* flag, cudaStream_t s);
 
 // Deterministic diagnostics partials: per x-plane block sums, then a fixed
