@@ -41,7 +41,7 @@ namespace {
 #define SDNS_VY 0
 #endif
 #ifndef SDNS_VYI
-#define SDNS_VYI 0
+#define SDNS_VYI 10
 #endif
 #ifndef SDNS_VXI
 #define SDNS_VXI 8
@@ -72,7 +72,9 @@ struct PipeCfg {
   static constexpr int MINB = V == 1 ? 3 : (V == 2 ? 4 : (V == 3 ? 2 : 1));
   // V = 8: one extra tile-sized exchange buffer (the x inverse pass runs its
   // first transform there and re-reads the input tile for the second)
-  static constexpr int SCR = V == 8 ? 1 : 0;
+  // V = 10: one extra tile buffer staging the y inverse pass's outputs for
+  // TMA tensor stores (input ring of two)
+  static constexpr int SCR = (V == 8 || V == 10) ? 1 : 0;
   static constexpr int TILE = N * CS;  // complex elements per tile buffer
   // tile buffers + scratch + the twiddle table
   static constexpr size_t SMEM = sizeof(double2) * ((NBUF + SCR) * TILE + N);
@@ -249,6 +251,47 @@ __device__ __forceinline__ void tma_tile(double2* buf, const CUtensorMap* tm, co
 #pragma unroll
   for (int h = 0; h < N / BP; ++h)
     tma_load5(buf + h * BP * CS, tm, 2 * (tl.kz & 7), tl.kz >> 3, tl.row, h * BP, field, bar);
+}
+
+// Tile stores by the tensor-memory accelerator from a dedicated staging
+// buffer (V = 10): the transformed tile is written there in the tile layout
+// and thread 0 issues two box stores that drain while the CTA transforms the
+// next item; the buffer is rewritten only after the previous stores have
+// read it (one transform later, normally without waiting).
+__device__ __forceinline__ void tma_store5(const CUtensorMap* tm, const void* src, int c0, int c1,
+                                           int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n" ::"l"(
+          tm),
+      "r"(smem_addr(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+template <int N, int CS, class IDX>
+__device__ __forceinline__ void tma_put(const CUtensorMap* tm, const double2 (&v)[fft_elems(N)],
+                                        double2* out, IDX idx, int t, const Tile& tl, int field) {
+  constexpr int E = fft_elems(N), TPC = N / E, BP = N < 256 ? N : 256;
+  if (threadIdx.x == 0) bulk_wait_read0();
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < E; ++m) out[idx(t + m * TPC)] = v[m];
+  fence_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int h = 0; h < N / BP; ++h)
+      tma_store5(tm, out + h * BP * CS, 2 * (tl.kz & 7), tl.kz >> 3, tl.row, h * BP, field);
+    bulk_commit();
+  }
 }
 
 // Generic persistent pipeline driver: `items` items per tile; src(f) gives
@@ -496,13 +539,20 @@ template <int N, int V, bool SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGeom g, ColGeom go,
             int ntiles, int f_lo, int f_cnt, const double2* __restrict__ tw,
-            const __grid_constant__ CUtensorMap tm) {
+            const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo) {
   constexpr int E = fft_elems(N), TPC = N / E;
   // field of item it: 0, 1, 3, 2, 4
   auto order = [](int it) { return it ^ ((it >> 1) & ~(it >> 2) & 1); };
   const OutSel<N, SEP> os(go, Lanes<N, V>().t);
+  extern __shared__ __align__(128) double2 smem[];
+  double2* const stage = smem + PipeCfg<N, V>::NBUF * N * PipeCfg<N, V>::CS;
+  const bool tst = PipeCfg<N, V>::SCR > 0 && go.tma != 0;
   auto put = [&](int field, const double2(&r)[E], const Tile& tl, const PosOff<N>& po, int t) {
-    store_own<N>(f + field * cs, r, go, os.tile(tl, go), os.po(po), t);
+    if (tst)
+      tma_put<N, PipeCfg<N, V>::CS>(&tmo, r, stage, CIdx<PipeCfg<N, V>::CS>{Lanes<N, V>().col}, t,
+                                    tl, field);
+    else
+      store_own<N>(f + field * cs, r, go, os.tile(tl, go), os.po(po), t);
   };
   pipeline<N, V>(ntiles, f_lo, f_cnt, g, [&](int it) { return fin + order(it) * cs_in; }, order,
                  &tm, tw,
@@ -534,6 +584,7 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
                      put(order(it), vin, tl, po, t);
                    }
                  });
+  if (tst && threadIdx.x == 0) bulk_wait0();
 }
 
 // ---------------------------------------------------------------------------
@@ -743,16 +794,22 @@ static void y_inv_n(const double2* fin, double2* f, long long cs_in, long long c
         persistent_grid(k_pipe_yinv<N, VYI, true>, C::THREADS, C::SMEM, nt, &occ);
     CUtensorMap tm;
     const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
+    CUtensorMap tmo;
+    const ColGeom got = with_tile_map<N, C::CS>(*go, f, cs, 6, &tmo);
     k_pipe_yinv<N, VYI, true><<<grid, C::THREADS, C::SMEM, s>>>(
-        fin, f, cs_in, cs, gt, *go, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
+        fin, f, cs_in, cs, gt, got, static_cast<int>(nt), f_lo, f_cnt, tw, tm, tmo);
   } else {
     static int occ = 0;
     const unsigned grid =
         persistent_grid(k_pipe_yinv<N, VYI, false>, C::THREADS, C::SMEM, nt, &occ);
     CUtensorMap tm;
     const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
+    CUtensorMap tmo;
+    std::memset(&tmo, 0, sizeof(tmo));
+    ColGeom go = gt;
+    go.tma = 0;  // in place: LSU stores
     k_pipe_yinv<N, VYI, false><<<grid, C::THREADS, C::SMEM, s>>>(
-        fin, f, cs_in, cs, gt, g, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
+        fin, f, cs_in, cs, gt, go, static_cast<int>(nt), f_lo, f_cnt, tw, tm, tmo);
   }
 }
 
