@@ -61,7 +61,7 @@ struct PipeCfg {
   static constexpr int CSW = (V == 1 || V == 2) ? 4 : 8;  // columns at TPC >= 64
   // n < 512: threads per CTA (measured at n = 64/128/256: small CTAs win
   // except for the two-transform inverse passes at 256)
-  static constexpr int ST = (N >= 256 && (V == 0 || V == 8)) ? 512 : 64;
+  static constexpr int ST = (N >= 256 && (V == 8 || V == 10)) ? 512 : 64;
   static constexpr int CS0 = TPC >= 64 ? CSW : (ST / TPC > 64 ? 64 : (ST / TPC < 8 ? 8 : ST / TPC));
   // n = 1024: 4-column tiles fit two buffers; V = 9 (plain passes) keeps
   // 128 B rows with a single 128 KB buffer (measured 2x faster on the x axis)
