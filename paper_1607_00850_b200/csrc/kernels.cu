@@ -8,9 +8,11 @@
 //   P3 k_z_fused      z-axis c2r of the 6 fields (+ the kz part of the curl),
 //                     1/n^3, u x omega, z r2c of 3
 //   P4 k_pipe_plain   y-axis forward c2c of the 3 fields (in place)
-// (P1, P2, P4 live in kernels_col.cu.)
-//   P5 k_x_fwd_fused  x-axis forward c2c + dealias + projection + viscous term
-//                     + RK4 stage update (+ Neumaier carry, projection, finite)
+//   P5a k_pipe_plain  x-axis forward c2c of the 3 fields (in place)
+// (P1, P2, P4, P5a live in kernels_col.cu.)
+//   P5b k_rk_update   dealias mask + projection + viscous term + RK4 stage
+//                     update (+ Neumaier carry, projection, finite flag);
+//                     k_rk3_stats also accumulates the sampled diagnostics
 // Pointwise parts follow the reference operation order with explicit
 // round-to-nearest intrinsics (no FMA contraction), so the standalone
 // pointwise kernels are bitwise equal to the reference CPU functions.

@@ -1,25 +1,27 @@
-// Column passes (FFTs along x or y) as persistent, cp.async-fed tile
-// pipelines for sm_100a.
+// Column passes (FFTs along x or y) as persistent tile pipelines for sm_100a.
 //
 // A tile is CS consecutive kz columns of one row (CS*16 B contiguous per
 // position) over all N positions of the transformed axis. Each CTA walks a
-// strided list of work items; tiles are copied global->shared with cp.async
-// (LDGSTS, zero-filled outside the valid kz range) -- with two buffers the
-// copy of item i+1 overlaps the transform of item i -- then transformed in
-// place and written back with coalesced 16-byte stores. Every item reads
-// exactly one input tile, which is what the linearity restructuring of the
-// curl allows:
-//   P1 x inverse:  U_c = F_x^-1(u_c),  K_c = F_x^-1(kx u_c)   (c = 1, 2)
+// strided list of (tile, item) work; tiles arrive in shared memory through a
+// ring of buffers -- by TMA tensor-map box loads completing on per-slot
+// mbarriers where the source is a plain (kz, rows, positions) block, by
+// cp.async (LDGSTS, zero-filled outside the valid kz range) otherwise -- so
+// items i+1.. load while item i is transformed in place. Results leave with
+// coalesced 16-byte stores (P2: TMA tensor stores from a staging tile).
+// Every item reads exactly one input tile, which is what the linearity
+// restructuring of the curl allows:
+//   P1 x inverse:  U_c = F_x^-1(u_c),  K2 = F_x^-1(kx u2),
+//                  w2' = i (F_x^-1(kx u1) - ky U0)
 //   P2 y inverse:  u_c = F_y^-1(U_c),  w0' = F_y^-1(i ky U2),
-//                  w1' = F_y^-1(-i K2), w2 = i(F_y^-1(K1) - F_y^-1(ky U0))
+//                  w1' = F_y^-1(-i K2), w2 = F_y^-1(w2')
 //   P3 (z pass) then completes w0 = w0' - i kz u1 and w1 = w1' + i kz u0,
 // which is omega_hat = i k x u_hat (curl_hat, navier_stokes.cpp:52-72)
 // distributed over the three axes.
 //
-// Tile shapes (measured on B200 at n = 512): 8-column / 128 B
-// tiles throughout; the two-FFT-per-item inverse passes run one 512-thread
-// CTA per SM with two buffers, the plain forward passes one buffer and two
-// CTAs per SM.
+// Tile shapes and ring depths are per pass variant (PipeCfg, measured on
+// B200): 8-column / 128 B tiles at n = 512, a three-deep ring
+// for the plain and y-inverse-input passes, two plus a scratch tile for P1,
+// two plus a store-staging tile for P2, single 128 KB buffers at n = 1024.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
