@@ -1120,7 +1120,8 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
         for (auto& e : c->xev) SDNS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       }
       const char* xl = std::getenv("SDNS_XLAYOUT");
-      if (cfg->p == 1 && !(xl && xl[0] == '0')) {
+      // (not at 1024^3: a p = 1 RK4 state + work then needs ~157 GB without it)
+      if (cfg->p == 1 && n <= 512 && !(xl && xl[0] == '0')) {
         c->cs_x = static_cast<long long>(c->pitch) * c->lo.spec_shape[1] * n;
         c->wx = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * c->cs_x * 5));
       }

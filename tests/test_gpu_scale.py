@@ -185,3 +185,28 @@ def test_512_pipeline_variants_bitwise():
     assert np.array_equal(a, rhs(SDNS_NO_TMA="1"))
     assert np.array_equal(a, rhs(SDNS_XLAYOUT="0"))
     assert np.isfinite(a).all() and np.abs(a).max() > 0
+
+
+def test_1024_single_gpu_rk4_step():
+    """Maximum size on one B200: a 1024^3 fp64 RK4 step (state + work ~157 GB)
+    stays finite, divergence-free and dissipative, and repeating it from the
+    same host state agrees bit for bit (no race at the largest grid)."""
+    n, nu, dt = 1024, 2.5e-4, 2.5e-4
+    lo = S.build_layout(S.SolverConfig(n=n), 0)
+    uh = S.iso_init(n, lo, seed=1607)
+    cfg = S.SolverConfig(n=n, nu=nu, dt=dt, t_end=dt)
+    with S.Context(cfg) as c:
+        st = S.Rk4State(c)
+        a = uh.copy()
+        st.step_host(a, dt, 1)  # host in, one step, host out (no extra device field)
+        s1 = S.collect_stats(c, st.u_hat, nu)
+        st.close()  # a fresh state (zero Neumaier carry) for the repeat
+        st = S.Rk4State(c)
+        b = uh.copy()
+        st.step_host(b, dt, 1)
+        st.close()
+    assert np.array_equal(a, b)
+    assert np.isfinite(a).all()
+    e0 = 0.5  # iso_init normalisation
+    assert s1.energy < e0
+    assert s1.divergence_max <= 1e-10
