@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional
 
@@ -443,6 +444,8 @@ class Context:
                                          ctypes.c_void_p(stream) if stream else None,
                                          ctypes.byref(h)))
         self._h = h
+        # fields and states allocated under this context: freed before it
+        self._children = weakref.WeakSet()
         lo = _Layout()
         self._lib.sdns_ctx_layout(h, ctypes.byref(lo))
         self.layout = Layout._from_c(lo)
@@ -477,6 +480,15 @@ class Context:
 
     def close(self):
         if self._h:
+            # device fields and states reference the context: release them
+            # first (sdns_field_free / sdns_state_destroy use its device)
+            kids = list(self._children)
+            for k in kids:
+                if isinstance(k, Field):
+                    k.free()
+            for k in kids:
+                if isinstance(k, Rk4State):
+                    k.close()
             self._lib.sdns_ctx_destroy(self._h)
             self._h = None
         if self._own_comm:
@@ -502,6 +514,14 @@ class Field:
             _check(ctx._lib.sdns_field_alloc(ctx._h, kind, ncomp, ctypes.byref(h)))
             handle = h
         self._h = handle
+        ctx._children.add(self)
+
+    def __del__(self):
+        try:
+            if self._h and self._owned and self.ctx._h:
+                self.free()
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
 
     @property
     def shape(self) -> tuple:
@@ -581,6 +601,14 @@ class Rk4State:
         self._h = h
         self.u_hat = Field(ctx, 1, 3, handle=ctypes.c_void_p(ctx._lib.sdns_state_u_hat(h)),
                            owned=False)
+        ctx._children.add(self)
+
+    def __del__(self):
+        try:
+            if self._h and self.ctx._h:
+                self.close()
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
 
     def set(self, u_hat: Field, t: float = 0.0, step: int = 0):
         _check(self.ctx._lib.sdns_state_set(self.ctx._h, self._h, u_hat._h, t, step))

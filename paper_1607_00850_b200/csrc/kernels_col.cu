@@ -48,6 +48,9 @@ namespace {
 #ifndef SDNS_VXI
 #define SDNS_VXI 8
 #endif
+#ifndef SDNS_CS4TMA  // 4-column tiles (n = 1024 inverse passes) also load by TMA
+#define SDNS_CS4TMA 1
+#endif
 #ifndef SDNS_COLTMA
 #define SDNS_COLTMA 1
 #endif
@@ -99,7 +102,7 @@ struct Tile {
 template <int CS>
 struct TileIdx {
   __device__ __forceinline__ int operator()(int x) const {
-    return (CS == 4 ? (x ^ ((x >> 3) & 1)) : x) * CS;
+    return (CS == 4 && !SDNS_CS4TMA ? (x ^ ((x >> 3) & 1)) : x) * CS;
   }
 };
 
@@ -665,7 +668,7 @@ static ColGeom with_tile_map(const ColGeom& g, const double2* base, long long fc
   ColGeom r = g;
   r.tma = 0;
   std::memset(tm, 0, sizeof(*tm));
-  if (!SDNS_COLTMA || CS != 8 || g.mpitch <= 0 || g.mrows <= 0 || ((N - 1) >> g.pb_shift) != 0)
+  if (!SDNS_COLTMA || (CS != 8 && !(CS == 4 && SDNS_CS4TMA)) || g.mpitch <= 0 || g.mrows <= 0 || ((N - 1) >> g.pb_shift) != 0)
     return r;
   const char* off = std::getenv("SDNS_NO_TMA");  // LDGSTS tile loads (parity checks)
   if (off && off[0] == '1') return r;
