@@ -314,6 +314,9 @@ struct ZFCfg {
   static constexpr int THREADS = TPC * RPC;
   static constexpr int HP = N / 2 + 8;  // padded half-row (n/2+1 modes)
   static constexpr size_t SMEM = sizeof(double2) * (static_cast<size_t>(RPC) * 6 * HP + N);
+  // CTAs per SM the shared memory allows (n = 1024: one -- then give the
+  // 16-element transforms the registers, 128 would spill)
+  static constexpr int MINB = SMEM * 2 <= 227 * 1024 ? 2 : 1;
 };
 
 #ifndef SDNS_ZTMA
@@ -333,7 +336,7 @@ __device__ __forceinline__ void zfft(double2 (&v)[fft_elems(N)], double2* sm, Sw
 }
 
 template <int N>
-__global__ void __launch_bounds__(ZFCfg<N>::THREADS, 2)
+__global__ void __launch_bounds__(ZFCfg<N>::THREADS, ZFCfg<N>::MINB)
 k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __restrict__ tw) {
   constexpr int E = ZFCfg<N>::E, TPC = ZFCfg<N>::TPC, HP = ZFCfg<N>::HP, RPC = ZFCfg<N>::RPC;
   using Bar = typename std::conditional<(TPC >= 64), NamedBar, WarpBar>::type;
