@@ -131,6 +131,15 @@ int sdns_comm_barrier(sdns_comm* c);                                 /* transpor
 /* In-place reduction in ascending rank order (op 0 sum, 1 max, 2 min). */
 int sdns_comm_allreduce(sdns_comm* c, double* values, int count, int op); /* :61 */
 int sdns_comm_destroy(sdns_comm* c);
+/* split(color, key): members ordered by (key, rank) (transport.hpp:66-67). */
+int sdns_comm_split(sdns_comm* c, int color, int key, sdns_comm** out);
+/* all_to_all_bytes (transport.hpp:55-58, BlockTable :18-35) on DEVICE
+ * buffers: block q of `send` (send_bytes[q], displacements the prefix sums)
+ * goes to peer q, which receives it as its block for this rank. Enqueued on
+ * `stream` (a cudaStream_t; NULL = legacy stream, and the call returns after
+ * the exchange completed). Collective. */
+int sdns_comm_all_to_all_bytes(sdns_comm* c, const void* send, const int64_t* send_bytes,
+                               void* recv, const int64_t* recv_bytes, void* stream);
 
 /* ---- context (DistributedFFT ctor + wavenumbers + workspaces) ----------- */
 /* fft.cpp:15-57, mesh.cpp:23-72, navier_stokes.hpp:32-41. `stream` is a
@@ -210,6 +219,127 @@ int sdns_checkpoint_write(sdns_ctx* ctx, const sdns_field* u_real, const char* p
  * every rank receives t and step. */
 int sdns_checkpoint_read(sdns_ctx* ctx, const char* path, sdns_field* u_real, double* t,
                          int64_t* step);
+
+/* ---- advance with the full hook set (AdvanceHooks, rk4.hpp:45-55) ------- */
+/* timing(step, seconds): wall time of one step, from before the update to
+ * after its collective finite flag (rk4.cpp:93-105); the step synchronises
+ * its stream to read that flag, so the interval covers the device work. */
+typedef void (*sdns_timing_fn)(int64_t step, double seconds, void* user);
+typedef struct sdns_advance_hooks {
+  sdns_sample_fn sample; /* AdvanceHooks::sample, or NULL */
+  sdns_timing_fn timing; /* AdvanceHooks::timing, or NULL */
+  void* user;
+} sdns_advance_hooks;
+int sdns_advance_hooks_run(sdns_ctx* ctx, sdns_state* st, const sdns_advance_hooks* hooks,
+                           int64_t* fail_step);
+
+/* ---- runner, bench harness, config files (runner.hpp, config_file.hpp) -- */
+/* SolverConfig defaults (config.hpp:14-30): n 32, slab, p = p1 = p2 = 1,
+ * nu 1/1600, dt 1e-3, t_end 0.1, dealias on, out_every 10. */
+void sdns_config_defaults(sdns_config* cfg);
+/* parse_config_text / parse_config_file (config_file.hpp:24-29,
+ * config_file.cpp:57-147): `key = value` lines, '#' comments; keys n,
+ * decomp, p, p1, p2, nu, re, dt, t_end, dealias, case, out_every; then the
+ * ordered overrides (keys[i] = values[i]); then validate. initial_case
+ * receives `case`; notices receives the '\n'-terminated notices. */
+typedef struct sdns_parsed_config {
+  sdns_config cfg;
+  char initial_case[64];
+  char notices[512];
+} sdns_parsed_config;
+int sdns_parse_config_text(const char* text, const char* const* keys, const char* const* values,
+                           int n_overrides, sdns_parsed_config* out);
+int sdns_parse_config_file(const char* path, const char* const* keys, const char* const* values,
+                           int n_overrides, sdns_parsed_config* out);
+/* default_pencil_grid (config_file.cpp:43-55). */
+int sdns_default_pencil_grid(int n, int p, int* p1, int* p2);
+
+/* RunOptions (runner.hpp:11-15) plus the device and the isotropic seed. */
+typedef struct sdns_run_options {
+  const char* out_dir;          /* default "out" */
+  const char* backend;          /* "auto" | "loopback" | "inprocess" */
+  double collective_timeout_s;  /* default 30 */
+  int device;                   /* CUDA device of every rank of sdns_run */
+  uint64_t seed;                /* case "isotropic" only */
+} sdns_run_options;
+/* RunResult (runner.hpp:28-36). samples: optional caller buffers of
+ * sample_cap rows (step, and 5 + shells doubles: t, E, Z, eps, div_max,
+ * spectrum), filled on rank 0; n_samples is the count produced. */
+typedef struct sdns_run_result {
+  char backend[16];
+  char status[256];
+  int64_t steps;
+  double step_min_s, step_mean_s, step_max_s;
+  int64_t timed_steps;
+  int shells;
+  int64_t n_samples, sample_cap;
+  int64_t* sample_steps;
+  double* sample_rows;
+  char csv_path[512], checkpoint_path[512], manifest_path[512];
+} sdns_run_result;
+/* run() (runner.hpp:44, runner.cpp:197-213): one host thread per rank on
+ * `device` (threads-as-ranks for p > 1), initial condition (`taylor_green`
+ * = the reference's cos x sin y sin z case, navier_stokes.cpp:7-32;
+ * `taylor_green_baseline` = BASELINE configs[0]'s sin x cos y cos z;
+ * `isotropic` = BASELINE configs[1-3]'s seeded field set in spectral space)
+ * -> forward + project -> advance with sampling, per-step timing and the
+ * post-step projection -> final (or last-good) checkpoint ->
+ * diagnostics.csv and manifest.txt in out_dir (rank 0). On divergence the
+ * last sampled state is checkpointed, the manifest records the failure and
+ * SDNS_DIVERGENCE_ERROR is returned (the result is still filled). */
+int sdns_run(const sdns_config* cfg, const char* initial_case, const sdns_run_options* opts,
+             sdns_run_result* out);
+/* run_worker (runner.cpp:67-146) for one rank of a caller-made communicator
+ * (e.g. one process per GPU over NCCL); collective over `comm`. */
+int sdns_run_rank(const sdns_config* cfg, const char* initial_case, const sdns_run_options* opts,
+                  int rank, sdns_comm* comm, sdns_run_result* out);
+
+/* BenchEntry / BenchRow (runner.hpp:40-58). */
+typedef struct sdns_bench_entry {
+  int n, decomp, p, p1, p2; /* p1 = p2 = 0: near-square pencil grid */
+} sdns_bench_entry;
+typedef struct sdns_bench_row {
+  sdns_bench_entry entry;
+  int64_t nodes_per_rank;
+  double sec_per_step;
+  char status[256]; /* "ok" or the failure message */
+} sdns_bench_row;
+/* parse_bench_matrix_text/file (runner.cpp:249-297): `n, decomp, p[, p1,
+ * p2]` lines, '#' comments, commas or blanks. *count = entries (at most cap
+ * written; out may be NULL to count). */
+int sdns_parse_bench_matrix_text(const char* text, sdns_bench_entry* out, int cap, int* count);
+int sdns_parse_bench_matrix_file(const char* path, sdns_bench_entry* out, int cap, int* count);
+/* bench() (runner.cpp:375-397): per entry, the reference's Taylor-Green case
+ * (nu 1/1600, dt 1e-3, dealias), 5 warm-up steps, then `steps` timed fused
+ * RK4 steps with the post-step projection between barriers; rank 0's mean
+ * wall seconds per step. Per-entry failures go to status. */
+int sdns_bench(const sdns_bench_entry* entries, int count, int steps,
+               const sdns_run_options* opts, sdns_bench_row* rows);
+/* write_bench_csv / write_diagnostics_csv / write_manifest
+ * (runner.cpp:215-247, :399-414): byte-identical formats ("%.17g"). */
+int sdns_write_bench_csv(const char* path, const sdns_bench_row* rows, int count);
+int sdns_write_diagnostics_csv(const char* path, const int64_t* steps, const double* rows,
+                               int64_t nrows, int shells);
+int sdns_write_manifest(const char* path, const sdns_config* cfg, const char* initial_case,
+                        const sdns_run_result* result);
+
+/* run_acceptance_suite (verification.hpp:17-24, verification.cpp:548-614):
+ * the reference's nine acceptance criteria, evaluated on the device
+ * pipeline (FFT vs the serial transform for every decomposition, Parseval,
+ * divergence-free evolution, energy identities, RK4 order, parallel
+ * invariance, checkpoint portability, transport conformance, bench
+ * harness). Ranks are threads on `device`. If `print`, one
+ * "[PASS]/[FAIL] <index> <name> (<detail>, <s> s)" line per criterion goes
+ * to stdout. results (may be NULL) receives 9 entries. */
+typedef struct sdns_criterion_result {
+  int index;
+  char name[64];
+  int passed;
+  char detail[512];
+  double seconds;
+} sdns_criterion_result;
+int sdns_acceptance_suite(int device, int print, sdns_criterion_result* results,
+                          int* all_passed);
 
 /* ---- per-pass timing (CUDA events on the context stream) --------------- */
 /* Pass tags of one RHS evaluation. */

@@ -32,6 +32,10 @@ def lib():
     if _lib is None:
         if not available():
             raise FileNotFoundError(f"{LIB} missing: build with `make -C oracle`")
+        # The oracle's g++ links libstdc++ statically; its formatted stream
+        # output (the reference's CSV/manifest writers) needs the locale of
+        # an initialised libstdc++, so load the system one globally first.
+        ctypes.CDLL("libstdc++.so.6", mode=ctypes.RTLD_GLOBAL)
         L = ctypes.CDLL(LIB)
         I, D, P = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
         L.sdns_ref_last_error.restype = ctypes.c_char_p
@@ -51,6 +55,14 @@ def lib():
                                                 ctypes.c_int64]
         L.sdns_ref_checkpoint_read.argtypes = [I, I, I, I, I, ctypes.c_char_p, P,
                                                ctypes.POINTER(D), ctypes.POINTER(ctypes.c_int64)]
+        CP = ctypes.c_char_p
+        I64 = ctypes.c_int64
+        L.sdns_ref_parse_config.argtypes = [CP, P, P, I, P, P, P, I, P, I]
+        L.sdns_ref_parse_bench_matrix.argtypes = [CP, P, I, ctypes.POINTER(I)]
+        L.sdns_ref_write_diagnostics_csv.argtypes = [CP, P, P, I64, I]
+        L.sdns_ref_write_bench_csv.argtypes = [CP, P, P, P, P, I]
+        L.sdns_ref_write_manifest.argtypes = [CP, P, P, CP, CP, CP, I64, I64, CP, CP]
+        L.sdns_ref_run_files.argtypes = [CP, CP, P, I]
         _lib = L
     return _lib
 
@@ -172,3 +184,72 @@ def checkpoint_read(path, n, decomp="slab", p=1, p1=1, p2=1):
     _check(lib().sdns_ref_checkpoint_read(n, DECOMP[decomp], p, p1, p2, os.fsencode(path), _p(u),
                                           ctypes.byref(t), ctypes.byref(step)))
     return u, t.value, step.value
+
+
+# --- runner layer (config_file.hpp, runner.hpp) --------------------------------
+
+class RefError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+def _check_coded(rc):
+    if rc != 0:
+        raise RefError(rc, lib().sdns_ref_last_error().decode(errors="replace"))
+
+
+def parse_config(text, overrides=()):
+    """parse_config_text -> (dict of SolverConfig fields, notices list)."""
+    items = list(overrides)
+    keys = (ctypes.c_char_p * max(1, len(items)))(*[k.encode() for k, _ in items])
+    vals = (ctypes.c_char_p * max(1, len(items)))(*[str(v).encode() for _, v in items])
+    iv = np.zeros(7, dtype=np.int32)
+    dv = np.zeros(3)
+    case = ctypes.create_string_buffer(256)
+    notes = ctypes.create_string_buffer(4096)
+    _check_coded(lib().sdns_ref_parse_config(text.encode(), keys, vals, len(items), _p(iv),
+                                             _p(dv), case, 256, notes, 4096))
+    cfg = dict(n=int(iv[0]), decomp=["slab", "pencil"][iv[1]], p=int(iv[2]), p1=int(iv[3]),
+               p2=int(iv[4]), dealias=bool(iv[5]), out_every=int(iv[6]), nu=float(dv[0]),
+               dt=float(dv[1]), t_end=float(dv[2]), initial_case=case.value.decode())
+    return cfg, [x for x in notes.value.decode().split("\n") if x]
+
+
+def parse_bench_matrix(text):
+    cnt = ctypes.c_int()
+    out = np.zeros(5 * 256, dtype=np.int32)
+    _check_coded(lib().sdns_ref_parse_bench_matrix(text.encode(), _p(out), 256,
+                                                   ctypes.byref(cnt)))
+    return [tuple(int(v) for v in out[5 * i:5 * i + 5]) for i in range(cnt.value)]
+
+
+def write_diagnostics_csv(path, steps, rows, shells):
+    steps = np.ascontiguousarray(steps, dtype=np.int64)
+    rows = np.ascontiguousarray(rows, dtype=np.float64)
+    _check_coded(lib().sdns_ref_write_diagnostics_csv(os.fsencode(path), _p(steps), _p(rows),
+                                                      len(steps), shells))
+
+
+def write_bench_csv(path, entries, nodes, secs, statuses):
+    ent = np.ascontiguousarray(np.array(entries, dtype=np.int32).reshape(-1))
+    nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+    secs = np.ascontiguousarray(secs, dtype=np.float64)
+    st = (ctypes.c_char_p * max(1, len(statuses)))(*[x.encode() for x in statuses])
+    _check_coded(lib().sdns_ref_write_bench_csv(os.fsencode(path), _p(ent), _p(nodes), _p(secs),
+                                                st, len(statuses)))
+
+
+def write_manifest(path, ints, doubles, icase, backend, status, steps, timed_steps, csv, ckpt):
+    iv = np.ascontiguousarray(ints, dtype=np.int32)
+    dv = np.ascontiguousarray(doubles, dtype=np.float64)
+    _check_coded(lib().sdns_ref_write_manifest(os.fsencode(path), _p(iv), _p(dv), icase.encode(),
+                                               backend.encode(), status.encode(), steps,
+                                               timed_steps, csv.encode(), ckpt.encode()))
+
+
+def run_files(config_text, out_dir):
+    """The reference's run() (runner.cpp:197-213) into out_dir; returns status."""
+    st = ctypes.create_string_buffer(256)
+    _check_coded(lib().sdns_ref_run_files(config_text.encode(), os.fsencode(out_dir), st, 256))
+    return st.value.decode()

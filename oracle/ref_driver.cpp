@@ -10,9 +10,12 @@
 //   collect_stats           proj/core/include/sdns/diagnostics.hpp:36-38
 //   run_group               proj/core/include/sdns/transport.hpp:103-106
 //   bench                   proj/core/include/sdns/runner.hpp:73-74
+//   run / write_*_csv / write_manifest   runner.hpp:44-82
+//   parse_config_text       proj/core/include/sdns/config_file.hpp:24-26
 // Global arrays passed across this ABI are row-major: spectral (n, n, n/2+1)
 // complex as interleaved doubles, real (n, n, n); vector fields are three
 // such arrays back to back (component-major).
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -22,6 +25,7 @@
 #include <vector>
 
 #include "sdns/checkpoint.hpp"
+#include "sdns/config_file.hpp"
 #include "sdns/diagnostics.hpp"
 #include "sdns/fft.hpp"
 #include "sdns/layout.hpp"
@@ -452,6 +456,141 @@ int sdns_ref_checkpoint_read(int n, int decomp, int p, int p1, int p2, const cha
         *step = info.step;
       }
     });
+  });
+}
+
+
+// --- runner layer (host-only pieces and the full run) ------------------------
+
+void put_cstr(char* dst, int cap, const std::string& s) {
+  if (cap <= 0) return;
+  const std::size_t n = std::min<std::size_t>(static_cast<std::size_t>(cap - 1), s.size());
+  std::memcpy(dst, s.data(), n);
+  dst[n] = '\0';
+}
+
+/// parse_config_text (config_file.cpp:57-136). iout = [n, decomp, p, p1, p2,
+/// dealias, out_every], dout = [nu, dt, t_end]; notices '\n'-terminated.
+int sdns_ref_parse_config(const char* text, const char* const* keys, const char* const* values,
+                          int n_over, int* iout, double* dout, char* icase, int case_cap,
+                          char* notes, int notes_cap) {
+  return guarded([&] {
+    ConfigOverrides ov;
+    for (int i = 0; i < n_over; ++i) ov.emplace_back(keys[i], values[i]);
+    const ParsedConfig pc = parse_config_text(text, ov);
+    const SolverConfig& c = pc.cfg;
+    const int iv[7] = {c.n, c.decomp == Decomp::Slab ? 0 : 1, c.p, c.p1, c.p2,
+                       c.dealias ? 1 : 0, c.out_every};
+    std::memcpy(iout, iv, sizeof(iv));
+    dout[0] = c.nu;
+    dout[1] = c.dt;
+    dout[2] = c.t_end;
+    put_cstr(icase, case_cap, c.initial_case);
+    std::string all;
+    for (const auto& s : pc.notices) all += s + "\n";
+    put_cstr(notes, notes_cap, all);
+  });
+}
+
+/// parse_bench_matrix_text (runner.cpp:249-289): 5 ints per entry.
+int sdns_ref_parse_bench_matrix(const char* text, int* out, int cap, int* count) {
+  return guarded([&] {
+    const auto es = parse_bench_matrix_text(text);
+    for (std::size_t i = 0; i < es.size() && static_cast<int>(i) < cap; ++i) {
+      out[5 * i + 0] = es[i].n;
+      out[5 * i + 1] = es[i].decomp == Decomp::Slab ? 0 : 1;
+      out[5 * i + 2] = es[i].p;
+      out[5 * i + 3] = es[i].p1;
+      out[5 * i + 4] = es[i].p2;
+    }
+    *count = static_cast<int>(es.size());
+  });
+}
+
+/// write_diagnostics_csv (runner.cpp:215-231); rows of 5 + shells doubles.
+int sdns_ref_write_diagnostics_csv(const char* path, const std::int64_t* steps,
+                                   const double* rows, std::int64_t nrows, int shells) {
+  return guarded([&] {
+    std::vector<SampleRow> samples;
+    for (std::int64_t r = 0; r < nrows; ++r) {
+      const double* x = rows + r * (5 + shells);
+      SampleRow row;
+      row.step = steps[r];
+      row.stats.t = x[0];
+      row.stats.energy = x[1];
+      row.stats.enstrophy = x[2];
+      row.stats.dissipation = x[3];
+      row.stats.divergence_max = x[4];
+      row.stats.spectrum.assign(x + 5, x + 5 + shells);
+      samples.push_back(row);
+    }
+    write_diagnostics_csv(path, samples, shells);
+  });
+}
+
+/// write_bench_csv (runner.cpp:399-414); entries 5 ints each.
+int sdns_ref_write_bench_csv(const char* path, const int* ent, const std::int64_t* nodes,
+                             const double* secs, const char* const* statuses, int count) {
+  return guarded([&] {
+    std::vector<BenchRow> rows;
+    for (int i = 0; i < count; ++i) {
+      BenchRow r;
+      r.entry.n = ent[5 * i];
+      r.entry.decomp = ent[5 * i + 1] == 0 ? Decomp::Slab : Decomp::Pencil;
+      r.entry.p = ent[5 * i + 2];
+      r.entry.p1 = ent[5 * i + 3];
+      r.entry.p2 = ent[5 * i + 4];
+      r.nodes_per_rank = nodes[i];
+      r.sec_per_step = secs[i];
+      r.status = statuses[i];
+      rows.push_back(r);
+    }
+    write_bench_csv(path, rows);
+  });
+}
+
+/// write_manifest (runner.cpp:233-247). iin = [n, decomp, p, p1, p2,
+/// dealias, out_every]; din = [nu, dt, t_end, min_s, mean_s, max_s].
+int sdns_ref_write_manifest(const char* path, const int* iin, const double* din,
+                            const char* icase, const char* backend, const char* status,
+                            std::int64_t steps, std::int64_t timed_steps, const char* csv,
+                            const char* ckpt) {
+  return guarded([&] {
+    RunResult r;
+    r.cfg.n = iin[0];
+    r.cfg.decomp = iin[1] == 0 ? Decomp::Slab : Decomp::Pencil;
+    r.cfg.p = iin[2];
+    r.cfg.p1 = iin[3];
+    r.cfg.p2 = iin[4];
+    r.cfg.dealias = iin[5] != 0;
+    r.cfg.out_every = iin[6];
+    r.cfg.nu = din[0];
+    r.cfg.dt = din[1];
+    r.cfg.t_end = din[2];
+    r.cfg.initial_case = icase;
+    r.backend = backend;
+    r.status = status;
+    r.steps = steps;
+    r.timing.min_s = din[3];
+    r.timing.mean_s = din[4];
+    r.timing.max_s = din[5];
+    r.timing.timed_steps = timed_steps;
+    r.csv_path = csv;
+    r.checkpoint_path = ckpt;
+    write_manifest(path, r);
+  });
+}
+
+/// run() (runner.cpp:197-213) of a config text into out_dir: writes the
+/// reference's diagnostics.csv, checkpoint.sdns and manifest.txt.
+int sdns_ref_run_files(const char* config_text, const char* out_dir, char* status, int cap) {
+  return guarded([&] {
+    const ParsedConfig pc = parse_config_text(config_text);
+    RunOptions opts;
+    opts.out_dir = out_dir;
+    opts.collective_timeout = std::chrono::milliseconds(600 * 1000);
+    const RunResult r = run(pc.cfg, opts);
+    put_cstr(status, cap, r.status);
   });
 }
 

@@ -27,6 +27,10 @@ __all__ = [
     "iso_init", "Comm", "Context", "Field", "DistributedFFT", "curl_hat", "cross",
     "project", "pressure_hat", "compute_rhs", "Rk4State", "FlowStats", "collect_stats",
     "l2_diff", "write_checkpoint", "read_checkpoint", "run_group",
+    "ParsedConfig", "parse_config_text", "parse_config_file", "default_pencil_grid",
+    "RunOptions", "RunResult", "run", "BenchEntry", "BenchRow", "parse_bench_matrix_text",
+    "parse_bench_matrix_file", "bench", "write_bench_csv", "write_diagnostics_csv",
+    "write_manifest", "CriterionResult", "run_acceptance_suite",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -103,6 +107,44 @@ PASS_NAMES = ["x_inv_curl", "y_inv", "z_fused", "y_fwd", "x_fwd_tail", "x_fwd_rk
               "x_fwd_rk12", "x_fwd_rk3", "a2a_inv", "a2a_fwd", "x_fwd_fft"]
 NPASS = len(PASS_NAMES)
 
+class _ParsedConfig(ctypes.Structure):
+    _fields_ = [("cfg", _Config), ("initial_case", ctypes.c_char * 64),
+                ("notices", ctypes.c_char * 512)]
+
+
+class _RunOptions(ctypes.Structure):
+    _fields_ = [("out_dir", ctypes.c_char_p), ("backend", ctypes.c_char_p),
+                ("collective_timeout_s", ctypes.c_double), ("device", ctypes.c_int),
+                ("seed", ctypes.c_uint64)]
+
+
+class _RunResult(ctypes.Structure):
+    _fields_ = [("backend", ctypes.c_char * 16), ("status", ctypes.c_char * 256),
+                ("steps", ctypes.c_int64), ("step_min_s", ctypes.c_double),
+                ("step_mean_s", ctypes.c_double), ("step_max_s", ctypes.c_double),
+                ("timed_steps", ctypes.c_int64), ("shells", ctypes.c_int),
+                ("n_samples", ctypes.c_int64), ("sample_cap", ctypes.c_int64),
+                ("sample_steps", ctypes.POINTER(ctypes.c_int64)),
+                ("sample_rows", ctypes.POINTER(ctypes.c_double)),
+                ("csv_path", ctypes.c_char * 512), ("checkpoint_path", ctypes.c_char * 512),
+                ("manifest_path", ctypes.c_char * 512)]
+
+
+class _BenchEntry(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("decomp", ctypes.c_int), ("p", ctypes.c_int),
+                ("p1", ctypes.c_int), ("p2", ctypes.c_int)]
+
+
+class _BenchRow(ctypes.Structure):
+    _fields_ = [("entry", _BenchEntry), ("nodes_per_rank", ctypes.c_int64),
+                ("sec_per_step", ctypes.c_double), ("status", ctypes.c_char * 256)]
+
+
+class _CriterionResult(ctypes.Structure):
+    _fields_ = [("index", ctypes.c_int), ("name", ctypes.c_char * 64), ("passed", ctypes.c_int),
+                ("detail", ctypes.c_char * 512), ("seconds", ctypes.c_double)]
+
+
 SAMPLE_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p)
 
 _lib = None
@@ -175,6 +217,28 @@ def load_library(path: str = LIB_PATH):
             "sdns_ctx_timing_read": (I, [P, P, P]),
             "sdns_device_layout": (I, [ctypes.POINTER(_Config), I, ctypes.POINTER(_DevLayout)]),
             "sdns_exchange_plan": (I, [ctypes.POINTER(_Config), I, I, I, P, ctypes.POINTER(I)]),
+            "sdns_comm_split": (I, [P, I, I, PP]),
+            "sdns_comm_all_to_all_bytes": (I, [P, P, P, P, P, P]),
+            "sdns_config_defaults": (V, [ctypes.POINTER(_Config)]),
+            "sdns_parse_config_text": (I, [ctypes.c_char_p, P, P, I,
+                                           ctypes.POINTER(_ParsedConfig)]),
+            "sdns_parse_config_file": (I, [ctypes.c_char_p, P, P, I,
+                                           ctypes.POINTER(_ParsedConfig)]),
+            "sdns_default_pencil_grid": (I, [I, I, ctypes.POINTER(I), ctypes.POINTER(I)]),
+            "sdns_run": (I, [ctypes.POINTER(_Config), ctypes.c_char_p,
+                             ctypes.POINTER(_RunOptions), ctypes.POINTER(_RunResult)]),
+            "sdns_run_rank": (I, [ctypes.POINTER(_Config), ctypes.c_char_p,
+                                  ctypes.POINTER(_RunOptions), I, P,
+                                  ctypes.POINTER(_RunResult)]),
+            "sdns_parse_bench_matrix_text": (I, [ctypes.c_char_p, P, I, ctypes.POINTER(I)]),
+            "sdns_parse_bench_matrix_file": (I, [ctypes.c_char_p, P, I, ctypes.POINTER(I)]),
+            "sdns_bench": (I, [P, I, I, ctypes.POINTER(_RunOptions), P]),
+            "sdns_write_bench_csv": (I, [ctypes.c_char_p, P, I]),
+            "sdns_write_diagnostics_csv": (I, [ctypes.c_char_p, P, P, I64, I]),
+            "sdns_write_manifest": (I, [ctypes.c_char_p, ctypes.POINTER(_Config),
+                                        ctypes.c_char_p, ctypes.POINTER(_RunResult)]),
+            "sdns_acceptance_suite": (I, [I, I, P, ctypes.POINTER(I)]),
+            "sdns_advance_hooks_run": (I, [P, P, P, ctypes.POINTER(I64)]),
             "sdns_host_alloc": (P, [ctypes.c_size_t]),
             "sdns_host_free": (V, [P]),
         }
@@ -709,3 +773,261 @@ def l2_diff(ctx: Context, a: Field, b: Field) -> float:
     out = ctypes.c_double()
     _check(ctx._lib.sdns_l2_diff(ctx._h, a._h, b._h, ctypes.byref(out)))
     return out.value
+
+
+# --- config files, runner and bench harness (config_file.hpp, runner.hpp) ------
+
+_DECOMP = {"slab": 0, "pencil": 1}
+_DECOMP_NAME = {0: "slab", 1: "pencil"}
+
+
+@dataclass
+class ParsedConfig:
+    """ParsedConfig, proj/core/include/sdns/config_file.hpp:14-17."""
+    cfg: SolverConfig
+    notices: List[str]
+
+
+def _from_c_config(c: _Config, initial_case: str = "taylor_green") -> SolverConfig:
+    return SolverConfig(n=c.n, decomp=_DECOMP_NAME[c.decomp], p=c.p, p1=c.p1, p2=c.p2, nu=c.nu,
+                        dt=c.dt, t_end=c.t_end, dealias=bool(c.dealias),
+                        initial_case=initial_case, out_every=c.out_every)
+
+
+def _overrides(overrides):
+    items = list(overrides.items()) if isinstance(overrides, dict) else list(overrides or [])
+    keys = (ctypes.c_char_p * max(1, len(items)))(*[k.encode() for k, _ in items])
+    vals = (ctypes.c_char_p * max(1, len(items)))(*[str(v).encode() for _, v in items])
+    return keys, vals, len(items)
+
+
+def _parsed(out: _ParsedConfig) -> ParsedConfig:
+    notes = [x for x in out.notices.decode().split("\n") if x]
+    return ParsedConfig(_from_c_config(out.cfg, out.initial_case.decode()), notes)
+
+
+def parse_config_text(text: str, overrides=()) -> ParsedConfig:
+    """parse_config_text, config_file.cpp:57-136 (ordered overrides applied last)."""
+    L = load_library()
+    keys, vals, n = _overrides(overrides)
+    out = _ParsedConfig()
+    _check(L.sdns_parse_config_text(text.encode(), keys, vals, n, ctypes.byref(out)))
+    return _parsed(out)
+
+
+def parse_config_file(path: str, overrides=()) -> ParsedConfig:
+    """parse_config_file, config_file.cpp:138-145 (IoError on a missing file)."""
+    L = load_library()
+    keys, vals, n = _overrides(overrides)
+    out = _ParsedConfig()
+    _check(L.sdns_parse_config_file(os.fsencode(path), keys, vals, n, ctypes.byref(out)))
+    return _parsed(out)
+
+
+def default_pencil_grid(n: int, p: int):
+    """default_pencil_grid, config_file.cpp:43-55."""
+    a, b = ctypes.c_int(), ctypes.c_int()
+    _check(load_library().sdns_default_pencil_grid(n, p, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+@dataclass
+class RunOptions:
+    """RunOptions, proj/core/include/sdns/runner.hpp:11-15 (+ device, iso seed)."""
+    out_dir: str = "out"
+    backend: str = "auto"
+    collective_timeout_s: float = 30.0
+    device: int = 0
+    seed: int = 1607
+
+    def to_c(self) -> _RunOptions:
+        return _RunOptions(os.fsencode(self.out_dir), self.backend.encode(),
+                           self.collective_timeout_s, self.device, self.seed)
+
+
+@dataclass
+class RunResult:
+    """RunResult, proj/core/include/sdns/runner.hpp:28-36."""
+    cfg: SolverConfig
+    backend: str
+    status: str
+    steps: int
+    timing: dict
+    samples: list          # [(step, FlowStats)]
+    csv_path: str
+    checkpoint_path: str
+    manifest_path: str
+
+
+def _run_result(cfg, r: _RunResult, steps, rows) -> RunResult:
+    w = 5 + r.shells
+    samples = []
+    for i in range(min(r.n_samples, len(steps))):
+        row = rows[i * w:(i + 1) * w]
+        samples.append((int(steps[i]), FlowStats(row[0], row[1], row[2], row[3], row[4],
+                                                 row[5:].copy())))
+    return RunResult(cfg, r.backend.decode(), r.status.decode(), r.steps,
+                     {"min_s": r.step_min_s, "mean_s": r.step_mean_s, "max_s": r.step_max_s,
+                      "timed_steps": r.timed_steps},
+                     samples, r.csv_path.decode(), r.checkpoint_path.decode(),
+                     r.manifest_path.decode())
+
+
+def _result_buffers(cfg: SolverConfig):
+    cap = step_count(cfg.t_end, cfg.dt) // cfg.out_every + 2
+    steps = np.zeros(cap, dtype=np.int64)
+    rows = np.zeros(cap * (5 + spectrum_shells(cfg.n)))
+    r = _RunResult()
+    r.sample_cap = cap
+    r.sample_steps = steps.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    r.sample_rows = rows.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    return r, steps, rows
+
+
+def run(cfg: SolverConfig, opts: Optional[RunOptions] = None,
+        comm: Optional["Comm"] = None, rank: int = 0) -> RunResult:
+    """run(), runner.cpp:197-213: ranks as threads on one device (comm None),
+    or, with `comm`, one rank of a caller-made group (run_worker,
+    runner.cpp:67-146; e.g. one process per GPU over NCCL). Writes
+    diagnostics.csv, checkpoint.sdns and manifest.txt into opts.out_dir.
+    DivergenceError after the last-good checkpoint, like the reference."""
+    L = load_library()
+    opts = opts or RunOptions()
+    r, steps, rows = _result_buffers(cfg)
+    c = cfg.to_c()
+    o = opts.to_c()
+    if comm is None:
+        rc = L.sdns_run(ctypes.byref(c), cfg.initial_case.encode(), ctypes.byref(o),
+                        ctypes.byref(r))
+    else:
+        rc = L.sdns_run_rank(ctypes.byref(c), cfg.initial_case.encode(), ctypes.byref(o), rank,
+                             comm._h, ctypes.byref(r))
+    if rc == DivergenceError.code:
+        msg = L.sdns_last_error().decode(errors="replace")
+        st = r.status.decode()
+        step = int(st.rsplit(" ", 1)[-1]) if st.startswith("diverged at step") else 0
+        raise DivergenceError(msg, step)
+    _check(rc)
+    return _run_result(cfg, r, steps, rows)
+
+
+@dataclass
+class BenchEntry:
+    """BenchEntry, runner.hpp:40-45 (p1 = p2 = 0: near-square pencil grid)."""
+    n: int = 32
+    decomp: str = "slab"
+    p: int = 1
+    p1: int = 0
+    p2: int = 0
+
+
+@dataclass
+class BenchRow:
+    """BenchRow, runner.hpp:47-52."""
+    entry: BenchEntry
+    nodes_per_rank: int
+    sec_per_step: float
+    status: str
+
+
+def _entries(arr, count) -> List[BenchEntry]:
+    return [BenchEntry(e.n, _DECOMP_NAME[e.decomp], e.p, e.p1, e.p2) for e in arr[:count]]
+
+
+def parse_bench_matrix_text(text: str) -> List[BenchEntry]:
+    """parse_bench_matrix_text, runner.cpp:249-289."""
+    L = load_library()
+    n = ctypes.c_int()
+    _check(L.sdns_parse_bench_matrix_text(text.encode(), None, 0, ctypes.byref(n)))
+    arr = (_BenchEntry * max(1, n.value))()
+    _check(L.sdns_parse_bench_matrix_text(text.encode(), arr, n.value, ctypes.byref(n)))
+    return _entries(arr, n.value)
+
+
+def parse_bench_matrix_file(path: str) -> List[BenchEntry]:
+    """parse_bench_matrix_file, runner.cpp:291-297."""
+    L = load_library()
+    n = ctypes.c_int()
+    _check(L.sdns_parse_bench_matrix_file(os.fsencode(path), None, 0, ctypes.byref(n)))
+    arr = (_BenchEntry * max(1, n.value))()
+    _check(L.sdns_parse_bench_matrix_file(os.fsencode(path), arr, n.value, ctypes.byref(n)))
+    return _entries(arr, n.value)
+
+
+def _c_entries(entries):
+    arr = (_BenchEntry * max(1, len(entries)))()
+    for i, e in enumerate(entries):
+        if e.decomp not in _DECOMP:
+            raise ConfigError(f"unknown decomposition '{e.decomp}' (expected slab|pencil)")
+        arr[i] = _BenchEntry(e.n, _DECOMP[e.decomp], e.p, e.p1, e.p2)
+    return arr
+
+
+def bench(entries: List[BenchEntry], steps: int,
+          opts: Optional[RunOptions] = None) -> List[BenchRow]:
+    """bench(), runner.cpp:375-397: per entry the Taylor-Green case, 5 warm-up
+    steps, then `steps` timed steps (fused RK4 + projection) between barriers."""
+    L = load_library()
+    o = (opts or RunOptions()).to_c()
+    arr = _c_entries(entries)
+    rows = (_BenchRow * max(1, len(entries)))()
+    _check(L.sdns_bench(arr, len(entries), steps, ctypes.byref(o), rows))
+    return [BenchRow(BenchEntry(r.entry.n, _DECOMP_NAME[r.entry.decomp], r.entry.p, r.entry.p1,
+                                r.entry.p2), r.nodes_per_rank, r.sec_per_step,
+                     r.status.decode()) for r in rows[:len(entries)]]
+
+
+def write_bench_csv(path: str, rows: List[BenchRow]):
+    """write_bench_csv, runner.cpp:399-414."""
+    arr = (_BenchRow * max(1, len(rows)))()
+    for i, r in enumerate(rows):
+        e = r.entry
+        arr[i] = _BenchRow(_BenchEntry(e.n, _DECOMP[e.decomp], e.p, e.p1, e.p2),
+                           r.nodes_per_rank, r.sec_per_step, r.status.encode())
+    _check(load_library().sdns_write_bench_csv(os.fsencode(path), arr, len(rows)))
+
+
+def write_diagnostics_csv(path: str, samples, shells: int):
+    """write_diagnostics_csv, runner.cpp:215-231; samples = [(step, FlowStats)]."""
+    steps = np.array([s for s, _ in samples], dtype=np.int64)
+    rows = np.array([[f.t, f.energy, f.enstrophy, f.dissipation, f.divergence_max,
+                      *list(f.spectrum)] for _, f in samples], dtype=np.float64).reshape(-1)
+    _check(load_library().sdns_write_diagnostics_csv(os.fsencode(path), _ptr(steps), _ptr(rows),
+                                                     len(samples), shells))
+
+
+def write_manifest(path: str, result: RunResult):
+    """write_manifest, runner.cpp:233-247."""
+    r = _RunResult()
+    r.backend = result.backend.encode()
+    r.status = result.status.encode()
+    r.steps = result.steps
+    r.step_min_s = result.timing["min_s"]
+    r.step_mean_s = result.timing["mean_s"]
+    r.step_max_s = result.timing["max_s"]
+    r.timed_steps = result.timing["timed_steps"]
+    r.csv_path = result.csv_path.encode()
+    r.checkpoint_path = result.checkpoint_path.encode()
+    c = result.cfg.to_c()
+    _check(load_library().sdns_write_manifest(os.fsencode(path), ctypes.byref(c),
+                                              result.cfg.initial_case.encode(), ctypes.byref(r)))
+
+
+@dataclass
+class CriterionResult:
+    """CriterionResult, proj/core/include/sdns/verification.hpp:9-15."""
+    index: int
+    name: str
+    passed: bool
+    detail: str
+    seconds: float
+
+
+def run_acceptance_suite(device: int = 0, verbose: bool = True) -> List[CriterionResult]:
+    """run_acceptance_suite, verification.cpp:548-614, on the device pipeline."""
+    arr = (_CriterionResult * 9)()
+    ok = ctypes.c_int()
+    _check(load_library().sdns_acceptance_suite(device, 1 if verbose else 0, arr,
+                                                ctypes.byref(ok)))
+    return [CriterionResult(r.index, r.name.decode(), bool(r.passed), r.detail.decode(),
+                            r.seconds) for r in arr]

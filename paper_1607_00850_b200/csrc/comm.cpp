@@ -99,6 +99,21 @@ struct Board {
     for (auto e : done) cudaEventDestroy(e);
   }
 
+  // Poisons this board and every sub-communicator split from it.
+  void poison_all(const std::string& why) {
+    std::vector<std::shared_ptr<Board>> kids;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (!poisoned) {
+        poisoned = true;
+        reason = why;
+      }
+      for (auto& kv : children) kids.push_back(kv.second);
+      cv.notify_all();
+    }
+    for (auto& k : kids) k->poison_all(why);
+  }
+
   // Generation-counted barrier; throws on poison or timeout.
   void wait_all(std::unique_lock<std::mutex>& lk) {
     if (poisoned) protocol_error("group poisoned: " + reason);
@@ -128,6 +143,8 @@ class InProcessComm final : public Comm {
   InProcessComm(std::shared_ptr<Board> b, int rank) : Comm(rank, b->size), b_(std::move(b)) {}
 
   int device() const override { return b_->device; }
+
+  void poison(const std::string& why) override { b_->poison_all(why); }
 
   void alltoall(const std::vector<Xfer>& xs, cudaStream_t s) override {
     Board& b = *b_;

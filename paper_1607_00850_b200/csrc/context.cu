@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <array>
 #include <initializer_list>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -974,6 +975,10 @@ void* dev_alloc(sdns_ctx* c, size_t bytes) {
 
 }  // namespace
 
+namespace sdns_host {
+int run_guarded(const std::function<void()>& f) { return guarded(f); }
+}  // namespace sdns_host
+
 extern "C" {
 
 const char* sdns_last_error(void) { return g_last_error.c_str(); }
@@ -1048,6 +1053,28 @@ int sdns_comm_allreduce(sdns_comm* c, double* v, int n, int op) {
 }
 int sdns_comm_destroy(sdns_comm* c) {
   return guarded([&] { delete c; });
+}
+int sdns_comm_split(sdns_comm* c, int color, int key, sdns_comm** out) {
+  return guarded([&] { *out = new sdns_comm{c->c->split(color, key)}; });
+}
+int sdns_comm_all_to_all_bytes(sdns_comm* c, const void* send, const int64_t* send_bytes,
+                               void* recv, const int64_t* recv_bytes, void* stream) {
+  return guarded([&] {
+    const int p = c->c->size();
+    std::vector<Xfer> xs;
+    int64_t so = 0, ro = 0;
+    for (int q = 0; q < p; ++q) {
+      if (send_bytes[q] < 0 || recv_bytes[q] < 0) protocol_error("all_to_all: negative count");
+      xs.push_back({q, static_cast<const char*>(send) + so, static_cast<char*>(recv) + ro,
+                    static_cast<size_t>(send_bytes[q]), static_cast<size_t>(recv_bytes[q])});
+      so += send_bytes[q];
+      ro += recv_bytes[q];
+    }
+    SDNS_CUDA(cudaSetDevice(c->c->device()));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    c->c->alltoall(xs, s);
+    if (!stream) SDNS_CUDA(cudaStreamSynchronize(s));
+  });
 }
 
 int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* comm, void* stream,
@@ -1397,9 +1424,13 @@ int sdns_rk4_step(sdns_ctx* c, sdns_state* st, double dt, int post_project, int*
   });
 }
 
-int sdns_advance(sdns_ctx* c, sdns_state* st, sdns_sample_fn sample, void* user, int64_t* fail_step) {
+int sdns_advance_hooks_run(sdns_ctx* c, sdns_state* st, const sdns_advance_hooks* hooks,
+                           int64_t* fail_step) {
   return guarded([&] {
     set_device(c);
+    const sdns_sample_fn sample = hooks ? hooks->sample : nullptr;
+    const sdns_timing_fn timing = hooks ? hooks->timing : nullptr;
+    void* user = hooks ? hooks->user : nullptr;
     const sdns_config& cfg = c->cfg;
     const int64_t n_steps = step_count(cfg.t_end, cfg.dt);
     if (sample) sample(0, st->t, user);
@@ -1408,15 +1439,19 @@ int sdns_advance(sdns_ctx* c, sdns_state* st, sdns_sample_fn sample, void* user,
       const double target = last ? cfg.t_end : static_cast<double>(k) * cfg.dt;
       const double dt = target - st->t;
       const bool samp = sample && (k % cfg.out_every == 0 || last);
+      const auto t0 = std::chrono::steady_clock::now();
       // a sampled step accumulates the diagnostics of its final state in the
-      // last update (collect_stats of st->u inside the hook reads them)
+      // last update (collect_stats of st->u inside the hook reads them); the
+      // finite flag is collective and synchronises the stream
       const bool ok = step_impl(c, st, dt, 1, true, samp);
+      const auto t1 = std::chrono::steady_clock::now();
       st->t = target;
       if (!ok) {
         if (fail_step) *fail_step = k;
         throw Error(SDNS_DIVERGENCE_ERROR,
                     "non-finite values in solution update at step " + std::to_string(k));
       }
+      if (timing) timing(k, std::chrono::duration<double>(t1 - t0).count(), user);
       if (samp) {
         c->fused_u = &st->u;
         struct Clear {
@@ -1427,6 +1462,11 @@ int sdns_advance(sdns_ctx* c, sdns_state* st, sdns_sample_fn sample, void* user,
       }
     }
   });
+}
+
+int sdns_advance(sdns_ctx* c, sdns_state* st, sdns_sample_fn sample, void* user, int64_t* fail_step) {
+  const sdns_advance_hooks h{sample, nullptr, user};
+  return sdns_advance_hooks_run(c, st, &h, fail_step);
 }
 
 int sdns_rk4_step_host(sdns_ctx* c, sdns_state* st, double* host, double dt, int steps) {

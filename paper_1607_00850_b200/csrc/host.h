@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -24,6 +25,10 @@ struct Error : std::runtime_error {
 [[noreturn]] inline void timeout_error(const std::string& m) { throw Error(SDNS_TIMEOUT_ERROR, m); }
 
 void cuda_check(cudaError_t e, const char* what);
+
+// Runs f, mapping an escaping exception onto its status code and the
+// calling thread's sdns_last_error() message (the C ABI's error channel).
+int run_guarded(const std::function<void()>& f);
 #define SDNS_CUDA(call) ::sdns_host::cuda_check((call), #call)
 
 // layout.cpp
@@ -60,6 +65,10 @@ class Comm {
   // Split by color, ordered by (key, rank) (transport.hpp:66-67).
   virtual std::shared_ptr<Comm> split(int color, int key) = 0;
   virtual int device() const = 0;
+  // Fails every pending and future collective of the group with
+  // ProtocolError (InProcessBackend::poison, transport.hpp:125-128); a
+  // no-op where the transport has no shared state (loopback, NCCL).
+  virtual void poison(const std::string& reason) { (void)reason; }
 
  protected:
   Comm(int r, int s) : rank_(r), size_(s) {}
@@ -70,6 +79,13 @@ std::shared_ptr<Comm> make_loopback_comm();
 std::vector<std::shared_ptr<Comm>> make_inprocess_group(int size, int device, double timeout_s);
 void nccl_unique_id(unsigned char id[128]);
 std::shared_ptr<Comm> make_nccl_comm(const unsigned char id[128], int size, int rank, int device);
+
+// runner.cpp: a failed C ABI call becomes the exception it reported; the
+// Taylor-Green real block of a rank; a case's initial spectral state.
+void ck(int rc);
+std::vector<double> tg_real_block(const sdns_layout& lo, bool reference_variant);
+void initial_state(sdns_ctx* ctx, const sdns_config& cfg, const std::string& icase,
+                   uint64_t seed, sdns_field* u_hat);
 
 // iso_init.cpp
 void iso_init(int64_t n, uint64_t seed, double k0, double energy, const sdns_layout& lo,
