@@ -53,6 +53,7 @@ class LoopbackComm final : public Comm {
   }
   void allreduce(double*, int, int) override {}
   void barrier() override {}
+  std::vector<void*> map_peers(void* mine) override { return {mine}; }
   std::shared_ptr<Comm> split(int, int) override { return std::make_shared<LoopbackComm>(); }
   int device() const override {
     int d = 0;
@@ -75,6 +76,7 @@ struct Board {
   std::string reason;
   std::vector<std::vector<Xfer>> posted;
   std::vector<std::vector<double>> values;
+  std::vector<void*> ptrs;
   std::vector<cudaEvent_t> ready, done;
   std::vector<std::pair<int, int>> split_req;
   std::map<std::pair<long long, int>, std::shared_ptr<Board>> children;
@@ -82,6 +84,7 @@ struct Board {
   Board(int n, int dev, double to) : size(n), device(dev), timeout_s(to) {
     posted.resize(n);
     values.resize(n);
+    ptrs.resize(n);
     split_req.resize(n);
     int prev = 0;
     cudaGetDevice(&prev);
@@ -214,6 +217,30 @@ class InProcessComm final : public Comm {
     b_->wait_all(lk);
   }
 
+  // Ranks share the device: a peer's buffer is addressed directly.
+  std::vector<void*> map_peers(void* mine) override {
+    Board& b = *b_;
+    std::unique_lock<std::mutex> lk(b.mu);
+    b.ptrs[rank_] = mine;
+    b.wait_all(lk);
+    std::vector<void*> all = b.ptrs;
+    b.wait_all(lk);
+    return all;
+  }
+
+  // Every rank's stream waits for every rank's `ready` event; the second
+  // rendezvous keeps a fast rank from re-recording its event before the
+  // others captured it.
+  void stream_barrier(cudaStream_t s) override {
+    Board& b = *b_;
+    SDNS_CUDA(cudaEventRecord(b.ready[rank_], s));
+    std::unique_lock<std::mutex> lk(b.mu);
+    b.wait_all(lk);
+    for (int q = 0; q < size_; ++q)
+      if (q != rank_) SDNS_CUDA(cudaStreamWaitEvent(s, b.ready[q], 0));
+    b.wait_all(lk);
+  }
+
   std::shared_ptr<Comm> split(int color, int key) override {
     Board& b = *b_;
     std::unique_lock<std::mutex> lk(b.mu);
@@ -262,6 +289,7 @@ struct NcclApi {
   ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
   static NcclApi& get() {
@@ -284,6 +312,7 @@ struct NcclApi {
       api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
       api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
       api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+      api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
       api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
     });
     if (!api.h || !api.GetUniqueId || !api.Send || !api.CommSplit)
@@ -307,9 +336,12 @@ class NcclComm final : public Comm {
     SDNS_CUDA(cudaSetDevice(device_));
     SDNS_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
     SDNS_CUDA(cudaMalloc(&dbuf_, sizeof(double) * kMaxVals * (size + 1)));
+    SDNS_CUDA(cudaMalloc(&tok_, sizeof(double)));
+    SDNS_CUDA(cudaMemset(tok_, 0, sizeof(double)));
   }
   ~NcclComm() override {
     if (dbuf_) cudaFree(dbuf_);
+    if (tok_) cudaFree(tok_);
     if (side_) cudaStreamDestroy(side_);
     if (comm_) NcclApi::get().CommDestroy(comm_);
   }
@@ -356,6 +388,60 @@ class NcclComm final : public Comm {
     allreduce(&x, 1, 0);
   }
 
+  // CUDA IPC handles of every rank's buffer, exchanged over the
+  // communicator and opened with peer access (NVLink / NVSwitch). The
+  // outcome is agreed collectively: if any rank fails to export or map,
+  // every rank releases its mappings and returns empty.
+  std::vector<void*> map_peers(void* mine) override {
+    auto& api = NcclApi::get();
+    constexpr size_t H = sizeof(cudaIpcMemHandle_t);
+    static_assert(H % sizeof(double) == 0, "IPC handle size");
+    constexpr int HD = static_cast<int>(H / sizeof(double));
+    cudaIpcMemHandle_t h{};
+    double ok = cudaIpcGetMemHandle(&h, mine) == cudaSuccess ? 1.0 : 0.0;
+    cudaGetLastError();
+    double* d_mine = dbuf_ + static_cast<size_t>(kMaxVals) * size_;
+    SDNS_CUDA(cudaMemcpyAsync(d_mine, &h, H, cudaMemcpyHostToDevice, side_));
+    nccl_check(api.AllGather(d_mine, dbuf_, static_cast<size_t>(HD), ncclFloat64, comm_, side_),
+               "ncclAllGather");
+    std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(size_));
+    SDNS_CUDA(cudaMemcpyAsync(all.data(), dbuf_, H * size_, cudaMemcpyDeviceToHost, side_));
+    SDNS_CUDA(cudaStreamSynchronize(side_));
+    std::vector<void*> out(static_cast<size_t>(size_), nullptr);
+    out[rank_] = mine;
+    for (int q = 0; q < size_ && ok > 0.5; ++q) {
+      if (q == rank_) continue;
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0.0;
+        break;
+      }
+      out[q] = p;
+    }
+    allreduce(&ok, 1, 2);
+    if (ok < 0.5) {
+      unmap_peers(out);
+      return {};
+    }
+    return out;
+  }
+
+  void unmap_peers(const std::vector<void*>& ptrs) override {
+    for (int q = 0; q < static_cast<int>(ptrs.size()); ++q)
+      if (q != rank_ && ptrs[q]) cudaIpcCloseMemHandle(ptrs[q]);
+  }
+
+  // A one-element all-reduce on the compute stream: NCCL's kernel completes
+  // on a rank only after every rank's stream reached it, and the producing
+  // kernels end with a system-scope fence on their peer stores.
+  void stream_barrier(cudaStream_t s) override {
+    auto& api = NcclApi::get();
+    if (!api.AllReduce) throw Error(SDNS_CUDA_ERROR, "ncclAllReduce not found");
+    nccl_check(api.AllReduce(tok_, tok_, 1, ncclFloat64, 0 /* ncclSum */, comm_, s),
+               "ncclAllReduce");
+  }
+
   std::shared_ptr<Comm> split(int color, int key) override {
     auto& api = NcclApi::get();
     ncclComm_t nc = nullptr;
@@ -388,6 +474,7 @@ class NcclComm final : public Comm {
   int device_ = 0;
   cudaStream_t side_ = nullptr;
   double* dbuf_ = nullptr;
+  double* tok_ = nullptr;  // stream_barrier's all-reduce operand
 };
 
 }  // namespace

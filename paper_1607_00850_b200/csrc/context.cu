@@ -145,6 +145,12 @@ struct sdns_ctx {
   // passes of the other field groups (events order the two streams)
   cudaStream_t cstream = nullptr;
   cudaEvent_t xev[12] = {};
+  // slab p > 1, peer-direct transposes: P1 stores into every
+  // rank's wb and P4 into every rank's wa; d_seg = [inverse (wb) | forward
+  // (wa)] element offsets of each destination block from the own buffer.
+  bool peer = false;
+  std::vector<void*> peer_wa, peer_wb;
+  long long* d_seg = nullptr;
   double* h_out = nullptr;  // pinned
   int* d_flag = nullptr;
   int* h_flag = nullptr;    // pinned
@@ -528,8 +534,67 @@ void rhs_slab_overlap(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& 
   post_launch("rhs pipeline (overlapped transposes)");
 }
 
+// Slab p > 1 with peer-direct transposes: the transposes are fused into the
+// passes that produce their data. P1 stores each output x plane straight into
+// the receive layout of the rank that owns it (same device, or NVLink through
+// a CUDA IPC mapping), and P4 stores each y output into the owner's x
+// layout, so no all-to-all pass, staging buffer or copy engine is involved;
+// a stream barrier across the ranks follows each (its wait also orders the
+// next write into a buffer after the owner's last read of it: wb is last read
+// by P4 before the forward barrier, wa by P5 before the next inverse one).
+// The transforms are the serial path's, so results are bitwise identical.
+void rhs_slab_peer(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args_in) {
+  const int n = c->cfg.n, p = c->cfg.p;
+  cudaStream_t s = c->stream;
+  const long long sc = c->spec_cs;
+  int tk = c->tick(SDNS_PASS_X_INV_CURL);
+  ColGeom go1 = c->xgeom();
+  go1.pb_shift = ilog2(c->np);
+  go1.ps1 = 0;
+  go1.seg = c->d_seg;
+  sdns_dev::x_inverse_split(n, u_in, sc, c->wb, sc, c->xgeom(), &go1, c->tw, s);
+  c->tock(tk);
+  tk = c->tick(SDNS_PASS_A2A_INV);
+  c->world->stream_barrier(s);
+  c->tock(tk);
+  tk = c->tick(SDNS_PASS_Y_INV);
+  sdns_dev::y_inverse_curl(n, c->wb, sc, c->ygeom(), c->tw, s);
+  c->tock(tk);
+  RowMap zm = c->zmap(false);
+  if (c->cfg.dealias) zm.kz_keep = c->keep_k() + 1;
+  tk = c->tick(SDNS_PASS_Z_FUSED);
+  sdns_dev::z_fused(n, c->wb, sc, zm, c->norm, c->tw, s);
+  c->tock(tk);
+  tk = c->tick(SDNS_PASS_Y_FWD);
+  const ColGeom gi4 = c->ygeom_fwd();
+  ColGeom go4 = gi4;
+  go4.ps1 = 0;
+  go4.seg = c->d_seg + p;
+  sdns_dev::col_plain_to(n, -1, c->wb, c->wa, sc, sc, 3, gi4, go4, c->tw, s);
+  c->tock(tk);
+  tk = c->tick(SDNS_PASS_A2A_FWD);
+  c->world->stream_barrier(s);
+  c->tock(tk);
+  XfArgs a = args_in;
+  a.nl = c->wa;
+  a.nl_cs = sc;
+  a.cs = sc;
+  a.dealias = c->cfg.dealias;
+  tk = c->tick(SDNS_PASS_X_FWD_FFT);
+  sdns_dev::col_plain(n, -1, true, c->wa, c->wa, sc, sc, 3, c->xgeom_fwd(), c->tw, s);
+  c->tock(tk);
+  tk = c->tick(SDNS_PASS_X_FWD_TAIL + mode);
+  sdns_dev::rk_update(mode, a, c->sgeom(), s);
+  c->tock(tk);
+  post_launch("rhs pipeline (peer-direct transposes)");
+}
+
 // One fused RHS evaluation: P1 .. P5 (kernels*.cu) with the transposes.
 void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args_in) {
+  if (c->peer) {
+    rhs_slab_peer(c, u_in, mode, args_in);
+    return;
+  }
   if (c->cstream) {
     rhs_slab_overlap(c, u_in, mode, args_in);
     return;
@@ -1141,8 +1206,37 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
       c->wd = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * static_cast<size_t>(c->cs_d) * 6));
     } else {
       c->wb = cfg->p == 1 ? c->wa : static_cast<double2*>(dev_alloc(c.get(), wbytes));
+      const char* pe = std::getenv("SDNS_PEER");
+      if (cfg->p > 1 && !(pe && pe[0] == '0')) {
+        // collective on every rank: all map both buffers or none does
+        c->peer_wb = c->world->map_peers(c->wb);
+        c->peer_wa = c->world->map_peers(c->wa);
+        if (!c->peer_wb.empty() && !c->peer_wa.empty()) {
+          const int p = cfg->p, r = rank;
+          const long long blk = static_cast<long long>(c->np) * c->plane();
+          std::vector<long long> seg(2 * static_cast<size_t>(p));
+          auto delta = [](void* a, void* b) {
+            return static_cast<long long>((reinterpret_cast<intptr_t>(a) -
+                                           reinterpret_cast<intptr_t>(b)) /
+                                          static_cast<intptr_t>(sizeof(double2)));
+          };
+          for (int q = 0; q < p; ++q) {
+            seg[q] = delta(c->peer_wb[q], c->wb) + r * blk;
+            seg[p + q] = delta(c->peer_wa[q], c->wa) + r * blk;
+          }
+          c->d_seg = static_cast<long long*>(dev_alloc(c.get(), sizeof(long long) * seg.size()));
+          SDNS_CUDA(cudaMemcpyAsync(c->d_seg, seg.data(), sizeof(long long) * seg.size(),
+                                    cudaMemcpyHostToDevice, c->stream));
+          c->peer = true;
+        } else {
+          c->world->unmap_peers(c->peer_wb);
+          c->world->unmap_peers(c->peer_wa);
+          c->peer_wb.clear();
+          c->peer_wa.clear();
+        }
+      }
       const char* ov = std::getenv("SDNS_OVERLAP");
-      if (cfg->p > 1 && !(ov && ov[0] == '0')) {
+      if (cfg->p > 1 && !c->peer && !(ov && ov[0] == '0')) {
         SDNS_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
         for (auto& e : c->xev) SDNS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       }
@@ -1180,6 +1274,11 @@ int sdns_ctx_destroy(sdns_ctx* c) {
       cudaStreamSynchronize(c->cstream);
       for (auto& e : c->xev) cudaEventDestroy(e);
       cudaStreamDestroy(c->cstream);
+    }
+    if (c->peer) {
+      c->world->unmap_peers(c->peer_wb);
+      c->world->unmap_peers(c->peer_wa);
+      cudaFree(c->d_seg);
     }
     cudaFree(c->tw);
     if (c->wb != c->wa) cudaFree(c->wb);

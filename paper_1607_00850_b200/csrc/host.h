@@ -69,6 +69,19 @@ class Comm {
   // ProtocolError (InProcessBackend::poison, transport.hpp:125-128); a
   // no-op where the transport has no shared state (loopback, NCCL).
   virtual void poison(const std::string& reason) { (void)reason; }
+  // Peer-direct transposes: every rank's device address of `mine` (a buffer
+  // of this rank), usable by this rank's kernels -- the pointer itself on a
+  // shared device, a CUDA IPC mapping (NVLink peer access) across GPUs.
+  // Collective; empty when the transport cannot map peers (every rank then
+  // keeps the all-to-all). unmap_peers releases the mappings.
+  virtual std::vector<void*> map_peers(void* mine) {
+    (void)mine;
+    return {};
+  }
+  virtual void unmap_peers(const std::vector<void*>& ptrs) { (void)ptrs; }
+  // Work enqueued on `s` after this call starts only after the work every
+  // rank enqueued on its stream before the call has completed. Collective.
+  virtual void stream_barrier(cudaStream_t s) { (void)s; }
 
  protected:
   Comm(int r, int s) : rank_(r), size_(s) {}

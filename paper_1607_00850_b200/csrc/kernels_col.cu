@@ -161,7 +161,7 @@ __device__ __forceinline__ void read_own(double2 (&v)[fft_elems(N)], const doubl
   for (int m = 0; m < E; ++m) v[m] = buf[idx(t + m * TPC)];
 }
 
-template <int N>
+template <int N, bool PEER = false>
 __device__ __forceinline__ void store_own(double2* dst, const double2 (&v)[fft_elems(N)],
                                           const ColGeom& g, const Tile& tl, const PosOff<N>& po,
                                           int t) {
@@ -175,22 +175,27 @@ __device__ __forceinline__ void store_own(double2* dst, const double2 (&v)[fft_e
   for (int m = 0; m < E; ++m) {
     const int pos = t + m * TPC;
     if (g.keep_k >= 0 && pos > g.keep_k && pos < N - g.keep_k) continue;  // masked mode
-    b[po.o(m)] = v[m];
+    if constexpr (PEER)
+      b[po.o(m) + __ldg(g.seg + (pos >> g.pb_shift))] = v[m];
+    else
+      b[po.o(m)] = v[m];
   }
 }
 
-// Output placement: the input geometry (in-place passes) or a separate one
-// (pencil y passes write the next transpose's send layout directly).
-template <int N, bool SEP>
+// Output placement: the input geometry (in-place passes, SEP 0), a separate
+// one (SEP 1: pencil y passes write the next transpose's send layout
+// directly) or a separate one whose position segments are other ranks'
+// buffers (SEP 2: peer-direct slab transposes, ColGeom::seg).
+template <int N, int SEP>
 struct OutSel;
 template <int N>
-struct OutSel<N, false> {
+struct OutSel<N, 0> {
   __device__ __forceinline__ OutSel(const ColGeom&, int) {}
   __device__ __forceinline__ Tile tile(const Tile& t, const ColGeom&) const { return t; }
   __device__ __forceinline__ const PosOff<N>& po(const PosOff<N>& in) const { return in; }
 };
 template <int N>
-struct OutSel<N, true> {
+struct OutSel<N, 1> {
   PosOff<N> p;
   __device__ __forceinline__ OutSel(const ColGeom& go, int t) : p(go, t) {}
   __device__ __forceinline__ Tile tile(const Tile& t, const ColGeom& go) const {
@@ -201,6 +206,17 @@ struct OutSel<N, true> {
   }
   __device__ __forceinline__ const PosOff<N>& po(const PosOff<N>&) const { return p; }
 };
+template <int N>
+struct OutSel<N, 2> : OutSel<N, 1> {
+  using OutSel<N, 1>::OutSel;
+};
+
+// Stores of a peer-direct pass must be visible to the peers' next pass,
+// which starts after a stream barrier across the ranks.
+template <int SEP>
+__device__ __forceinline__ void peer_fence() {
+  if constexpr (SEP == 2) __threadfence_system();
+}
 
 // Column transform; SDNS_NOFFT builds a memory-only variant (wrong results)
 // for A/B measurements of the pipelines' memory ceiling.
@@ -450,7 +466,7 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
 // ---------------------------------------------------------------------------
 // Plain multi-field column transform (y passes, x-forward, API passes).
 
-template <int N, int S, int V, bool SEP>
+template <int N, int S, int V, int SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs, int nfields,
              ColGeom g, ColGeom go, int ntiles, const double2* __restrict__ tw,
@@ -466,15 +482,16 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
                    ln.bar();
                    col_fft<N, S>(v, buf, ln.idx, t, tws, ln.bar);
                    release();  // buffer no longer read: the next tile may load
-                   store_own<N>(out + f * out_cs, v, go, os.tile(tl, go), os.po(po), t);
+                   store_own<N, SEP == 2>(out + f * out_cs, v, go, os.tile(tl, go), os.po(po), t);
                  });
+  peer_fence<SEP>();
 }
 
 // ---------------------------------------------------------------------------
 // P1: x inverse of u_hat -> [U0, U1, U2, w2', K2] (fields 0..4 of `out`),
 // w2' = i (F(kx u1) - ky U0).
 
-template <int N, int V, bool SEP>
+template <int N, int V, int SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, ColGeom g,
             ColGeom go, int ntiles, int f_lo, int f_cnt, const double2* __restrict__ tw,
@@ -515,12 +532,14 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                          const double2* u0 = out + to.base;
 #pragma unroll
                          for (int m = 0; m < E; ++m) {
-                           const double2 a = u0[pout.o(m)];
+                           long long at = pout.o(m);
+                           if constexpr (SEP == 2) at += __ldg(go.seg + ((t + m * TPC) >> go.pb_shift));
+                           const double2 a = u0[at];
                            v[m] = times_i(make_double2(v[m].x - ky * a.x, v[m].y - ky * a.y));
                          }
                        }
                      }
-                     store_own<N>(out + (2 + f) * out_cs, v, go, os.tile(tl, go), os.po(po), t);
+                     store_own<N, SEP == 2>(out + (2 + f) * out_cs, v, go, os.tile(tl, go), os.po(po), t);
                      if constexpr (SCR) {
                        read_own<N>(v, buf, ln.idx, t);
                      } else {
@@ -530,8 +549,9 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                    }
                    if (SCR || f == 0) ln.bar();  // buf is read; the transform reuses it
                    col_fft<N, +1>(v, buf, ln.idx, t, tws, ln.bar);
-                   store_own<N>(out + f * out_cs, v, go, os.tile(tl, go), os.po(po), t);
+                   store_own<N, SEP == 2>(out + f * out_cs, v, go, os.tile(tl, go), os.po(po), t);
                  });
+  peer_fence<SEP>();
 }
 
 // ---------------------------------------------------------------------------
@@ -540,7 +560,7 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
 // layouts). Items per tile in the order U0, U1, w2', U2, K2: field 3 (w2') is
 // consumed before the U2 item writes w0' over it.
 
-template <int N, int V, bool SEP>
+template <int N, int V, int SEP>
 __global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
 k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGeom g, ColGeom go,
             int ntiles, int f_lo, int f_cnt, const double2* __restrict__ tw,
@@ -697,7 +717,7 @@ static ColGeom with_tile_map(const ColGeom& g, const double2* base, long long fc
   return r;
 }
 
-template <int N, int S, int V, bool SEP>
+template <int N, int S, int V, int SEP>
 static void plain_launch(const double2* in, double2* out, long long in_cs, long long out_cs,
                          int nfields, const ColGeom& g, const ColGeom& go, const double2* tw,
                          cudaStream_t s) {
@@ -718,17 +738,22 @@ static void col_plain_n(int dir, bool xaxis, const double2* in, double2* out, lo
                         long long out_cs, int nfields, const ColGeom& g, const ColGeom* go,
                         const double2* tw, cudaStream_t s) {
   constexpr int VX = N >= 1024 ? 9 : sdns_dev::VX, VY = sdns_dev::VY;
+  if (go && go->seg) {  // peer-direct output (slab y forward into the peers' x layouts)
+    if (dir < 0) plain_launch<N, -1, VY, 2>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+    else plain_launch<N, +1, VY, 2>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+    return;
+  }
   if (go) {  // separate output layout (pencil y passes; y-shaped tiles)
-    if (dir < 0) plain_launch<N, -1, VY, true>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
-    else plain_launch<N, +1, VY, true>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+    if (dir < 0) plain_launch<N, -1, VY, 1>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+    else plain_launch<N, +1, VY, 1>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
     return;
   }
   if (dir < 0) {
-    if (xaxis) plain_launch<N, -1, VX, false>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
-    else plain_launch<N, -1, VY, false>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
+    if (xaxis) plain_launch<N, -1, VX, 0>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
+    else plain_launch<N, -1, VY, 0>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
   } else {
-    if (xaxis) plain_launch<N, +1, VX, false>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
-    else plain_launch<N, +1, VY, false>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
+    if (xaxis) plain_launch<N, +1, VX, 0>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
+    else plain_launch<N, +1, VY, 0>(in, out, in_cs, out_cs, nfields, g, g, tw, s);
   }
 }
 
@@ -762,16 +787,21 @@ static void x_inv_n(const double2* u, long long u_cs, double2* out, long long ou
   const long long nt = ntiles_of<N, VXI>(g);
   CUtensorMap tm;
   const ColGeom gt = with_tile_map<N, C::CS>(g, u, u_cs, 3, &tm);
-  if (go) {
+  if (go && go->seg) {  // peer-direct output (slab x inverse into the peers' receive layouts)
     static int occ = 0;
-    const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, true>, C::THREADS, C::SMEM, nt, &occ);
-    k_pipe_xinv<N, VXI, true><<<grid, C::THREADS, C::SMEM, s>>>(
+    const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, 2>, C::THREADS, C::SMEM, nt, &occ);
+    k_pipe_xinv<N, VXI, 2><<<grid, C::THREADS, C::SMEM, s>>>(
+        u, u_cs, out, out_cs, gt, *go, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
+  } else if (go) {
+    static int occ = 0;
+    const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, 1>, C::THREADS, C::SMEM, nt, &occ);
+    k_pipe_xinv<N, VXI, 1><<<grid, C::THREADS, C::SMEM, s>>>(
         u, u_cs, out, out_cs, gt, *go, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   } else {
     static int occ = 0;
     const unsigned grid =
-        persistent_grid(k_pipe_xinv<N, VXI, false>, C::THREADS, C::SMEM, nt, &occ);
-    k_pipe_xinv<N, VXI, false><<<grid, C::THREADS, C::SMEM, s>>>(
+        persistent_grid(k_pipe_xinv<N, VXI, 0>, C::THREADS, C::SMEM, nt, &occ);
+    k_pipe_xinv<N, VXI, 0><<<grid, C::THREADS, C::SMEM, s>>>(
         u, u_cs, out, out_cs, gt, gt, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   }
 }
@@ -796,24 +826,24 @@ static void y_inv_n(const double2* fin, double2* f, long long cs_in, long long c
   if (go) {
     static int occ = 0;
     const unsigned grid =
-        persistent_grid(k_pipe_yinv<N, VYI, true>, C::THREADS, C::SMEM, nt, &occ);
+        persistent_grid(k_pipe_yinv<N, VYI, 1>, C::THREADS, C::SMEM, nt, &occ);
     CUtensorMap tm;
     const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
     CUtensorMap tmo;
     const ColGeom got = with_tile_map<N, C::CS>(*go, f, cs, 6, &tmo);
-    k_pipe_yinv<N, VYI, true><<<grid, C::THREADS, C::SMEM, s>>>(
+    k_pipe_yinv<N, VYI, 1><<<grid, C::THREADS, C::SMEM, s>>>(
         fin, f, cs_in, cs, gt, got, static_cast<int>(nt), f_lo, f_cnt, tw, tm, tmo);
   } else {
     static int occ = 0;
     const unsigned grid =
-        persistent_grid(k_pipe_yinv<N, VYI, false>, C::THREADS, C::SMEM, nt, &occ);
+        persistent_grid(k_pipe_yinv<N, VYI, 0>, C::THREADS, C::SMEM, nt, &occ);
     CUtensorMap tm;
     const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
     CUtensorMap tmo;
     std::memset(&tmo, 0, sizeof(tmo));
     ColGeom go = gt;
     go.tma = 0;  // in place: LSU stores
-    k_pipe_yinv<N, VYI, false><<<grid, C::THREADS, C::SMEM, s>>>(
+    k_pipe_yinv<N, VYI, 0><<<grid, C::THREADS, C::SMEM, s>>>(
         fin, f, cs_in, cs, gt, go, static_cast<int>(nt), f_lo, f_cnt, tw, tm, tmo);
   }
 }

@@ -435,11 +435,14 @@ def test_inprocess_slab_rk4_matches_single_rank(p):
             assert a.energy == b.energy and a.enstrophy == b.enstrophy
 
 
-@pytest.mark.parametrize("p", [2, 4])
-def test_inprocess_slab_overlapped_transposes_bitwise(p):
-    """Slab p > 1 overlaps each field group's transpose with the transforms of
-    the next (comm stream + events); the kernels and arithmetic are those of
-    the serial pipeline (SDNS_OVERLAP=0), so one RHS must agree bit for bit."""
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_inprocess_slab_transpose_modes_bitwise(p):
+    """Slab p > 1 runs its transposes fused into the producing passes by
+    default (P1 / P4 store straight into the owning rank's buffer, a stream
+    barrier after each: peer-direct), else as all-to-alls overlapped with the
+    next group's transforms (SDNS_PEER=0), else serially (SDNS_OVERLAP=0 as
+    well). The transforms and arithmetic are the same, so one RHS and two
+    RK4 steps must agree bit for bit across the three."""
     n = 32
     lo1 = S.build_layout(S.SolverConfig(n=n), 0)
     uh0 = S.iso_init(n, lo1, seed=9)
@@ -451,17 +454,28 @@ def test_inprocess_slab_overlapped_transposes_bitwise(p):
                 u = c.spectral_field().upload(_scatter_spec(uh0, c.layout))
                 du = c.spectral_field()
                 S.compute_rhs(c, u, 1e-3, du)
-                return du.download()
+                st = S.Rk4State(c)
+                st.set(u)
+                st.rk4_step(1e-3)
+                st.rk4_step(1e-3)
+                out = c.spectral_field()
+                st.get(out)
+                return du.download(), out.download()
         return S.run_group(p, body)
 
-    over = run()
-    os.environ["SDNS_OVERLAP"] = "0"
-    try:
-        serial = run()
-    finally:
-        os.environ.pop("SDNS_OVERLAP", None)
-    for a, b in zip(over, serial):
-        assert np.array_equal(a, b)
+    modes = {}
+    for name, env in (("peer", {}), ("overlap", {"SDNS_PEER": "0"}),
+                      ("serial", {"SDNS_PEER": "0", "SDNS_OVERLAP": "0"})):
+        os.environ.update(env)
+        try:
+            modes[name] = run()
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+    for name in ("overlap", "serial"):
+        for (a1, a2), (b1, b2) in zip(modes["peer"], modes[name]):
+            assert np.array_equal(a1, b1), name
+            assert np.array_equal(a2, b2), name
 
 
 # --- pencil decomposition (fft.cpp:130-227) on one GPU ---------------------------

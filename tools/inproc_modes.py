@@ -1,0 +1,21 @@
+"""Slab transpose modes at p > 1, ranks as threads on one GPU (sdns_bench:
+5 warm-up + K timed RK4 steps, wall time): peer-direct (default), all-to-all
+overlapped (SDNS_PEER=0), serial (SDNS_PEER=0 SDNS_OVERLAP=0).
+   python tools/inproc_modes.py [K]      (GPU box)"""
+import os
+import sys
+
+sys.path.insert(0, ".")
+import paper_1607_00850_b200 as S
+
+K = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+entries = [S.BenchEntry(n, "slab", p) for n in (256, 512) for p in (1, 2, 4, 8)]
+for name, env in (("peer", {}), ("overlap", {"SDNS_PEER": "0"}),
+                  ("serial", {"SDNS_PEER": "0", "SDNS_OVERLAP": "0"})):
+    os.environ.update(env)
+    rows = S.bench(entries, K, S.RunOptions(collective_timeout_s=600))
+    for k in env:
+        os.environ.pop(k, None)
+    for r in rows:
+        print(f"{name:8s} n={r.entry.n} p={r.entry.p}: {r.sec_per_step * 1e3:8.2f} ms/step "
+              f"{r.status}", flush=True)
