@@ -151,6 +151,8 @@ struct sdns_ctx {
   bool peer = false;
   std::vector<void*> peer_wa, peer_wb;
   long long* d_seg = nullptr;
+  Comm* peer_grp = nullptr;  // the group the peer-direct transposes run over
+  int peer_n = 0;            // its size
   double* h_out = nullptr;  // pinned
   int* d_flag = nullptr;
   int* h_flag = nullptr;    // pinned
@@ -329,6 +331,43 @@ struct sdns_ctx {
     g.n2 = static_cast<int>(lo.spec_shape[2]);
     g.pitch = pitch;
     return g;
+  }
+  // Peer-direct transposes over `grp` (slab: the world; pencil: the column
+  // group, whose transposes move x blocks <-> y blocks exactly like the
+  // slab's): map every member's wb and wa and build the store offsets
+  // d_seg = [inverse (wb) | forward (wa)], member q's block for this rank
+  // at its offset grp->rank() * blk. Collective over grp; SDNS_PEER=0 or a
+  // transport that cannot map keeps the all-to-all.
+  void map_peer_blocks(Comm* grp, int gp) {
+    const char* pe = std::getenv("SDNS_PEER");
+    if (gp <= 1 || (pe && pe[0] == '0')) return;
+    peer_wb = grp->map_peers(wb);
+    peer_wa = grp->map_peers(wa);
+    if (peer_wb.empty() || peer_wa.empty()) {
+      grp->unmap_peers(peer_wb);
+      grp->unmap_peers(peer_wa);
+      peer_wb.clear();
+      peer_wa.clear();
+      return;
+    }
+    const long long blk = static_cast<long long>(np) * plane();
+    const long long me = grp->rank();
+    std::vector<long long> seg(2 * static_cast<size_t>(gp));
+    auto delta = [](void* a, void* b) {
+      return static_cast<long long>((reinterpret_cast<intptr_t>(a) -
+                                     reinterpret_cast<intptr_t>(b)) /
+                                    static_cast<intptr_t>(sizeof(double2)));
+    };
+    for (int q = 0; q < gp; ++q) {
+      seg[q] = delta(peer_wb[q], wb) + me * blk;
+      seg[gp + q] = delta(peer_wa[q], wa) + me * blk;
+    }
+    SDNS_CUDA(cudaMalloc(&d_seg, sizeof(long long) * seg.size()));
+    SDNS_CUDA(cudaMemcpyAsync(d_seg, seg.data(), sizeof(long long) * seg.size(),
+                              cudaMemcpyHostToDevice, stream));
+    peer_grp = grp;
+    peer_n = gp;
+    peer = true;
   }
   // Pencil column-group transpose, wa <-> wb (x blocks <-> y2 blocks),
   // fft.cpp:166-173 / :191-199 without the pack/unpack passes.
@@ -544,7 +583,7 @@ void rhs_slab_overlap(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& 
 // by P4 before the forward barrier, wa by P5 before the next inverse one).
 // The transforms are the serial path's, so results are bitwise identical.
 void rhs_slab_peer(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args_in) {
-  const int n = c->cfg.n, p = c->cfg.p;
+  const int n = c->cfg.n, p = c->peer_n;
   cudaStream_t s = c->stream;
   const long long sc = c->spec_cs;
   int tk = c->tick(SDNS_PASS_X_INV_CURL);
@@ -555,7 +594,7 @@ void rhs_slab_peer(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& arg
   sdns_dev::x_inverse_split(n, u_in, sc, c->wb, sc, c->xgeom(), &go1, c->tw, s);
   c->tock(tk);
   tk = c->tick(SDNS_PASS_A2A_INV);
-  c->world->stream_barrier(s);
+  c->peer_grp->stream_barrier(s);
   c->tock(tk);
   tk = c->tick(SDNS_PASS_Y_INV);
   sdns_dev::y_inverse_curl(n, c->wb, sc, c->ygeom(), c->tw, s);
@@ -573,7 +612,7 @@ void rhs_slab_peer(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& arg
   sdns_dev::col_plain_to(n, -1, c->wb, c->wa, sc, sc, 3, gi4, go4, c->tw, s);
   c->tock(tk);
   tk = c->tick(SDNS_PASS_A2A_FWD);
-  c->world->stream_barrier(s);
+  c->peer_grp->stream_barrier(s);
   c->tock(tk);
   XfArgs a = args_in;
   a.nl = c->wa;
@@ -591,7 +630,7 @@ void rhs_slab_peer(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& arg
 
 // One fused RHS evaluation: P1 .. P5 (kernels*.cu) with the transposes.
 void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args_in) {
-  if (c->peer) {
+  if (c->peer && !c->pencil) {
     rhs_slab_peer(c, u_in, mode, args_in);
     return;
   }
@@ -605,6 +644,12 @@ void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args
   if (c->wx) {
     const ColGeom go = c->xl_out();
     sdns_dev::x_inverse_split(n, u_in, c->spec_cs, c->wx, c->cs_x, c->xgeom(), &go, c->tw, s);
+  } else if (c->peer) {  // pencil: P1 stores into the column peers' wb (see rhs_slab_peer)
+    ColGeom go1 = c->xgeom();
+    go1.pb_shift = ilog2(c->np);
+    go1.ps1 = 0;
+    go1.seg = c->d_seg;
+    sdns_dev::x_inverse_split(n, u_in, c->spec_cs, c->wb, c->spec_cs, c->xgeom(), &go1, c->tw, s);
   } else {
     sdns_dev::x_inverse_split(n, u_in, c->spec_cs, c->wa, c->spec_cs, c->xgeom(), nullptr, c->tw,
                               s);
@@ -634,7 +679,13 @@ void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args
     c->tock(tk);
     c->exchange(false, 3);
   } else {
-    c->exchange_col(true, 5);
+    if (c->peer) {
+      const int tb = c->tick(SDNS_PASS_A2A_INV);
+      c->peer_grp->stream_barrier(s);
+      c->tock(tb);
+    } else {
+      c->exchange_col(true, 5);
+    }
     tk = c->tick(SDNS_PASS_Y_INV);
     sdns_dev::y_inverse_curl_to(n, c->wb, c->wc, c->spec_cs, c->cs_c, c->ygeom(), c->ygeom_row(),
                                 c->tw, s);
@@ -647,9 +698,19 @@ void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args
     ColGeom gi, go;
     pencil_yfwd_geoms(c, true, gi, go);
     tk = c->tick(SDNS_PASS_Y_FWD);
-    sdns_dev::col_plain_to(n, -1, c->wc, c->wb, c->cs_c, c->spec_cs, 3, gi, go, c->tw, s);
-    c->tock(tk);
-    c->exchange_col(false, 3);
+    if (c->peer) {  // P4 stores into the column peers' x layouts (wa)
+      go.ps1 = 0;
+      go.seg = c->d_seg + c->peer_n;
+      sdns_dev::col_plain_to(n, -1, c->wc, c->wa, c->cs_c, c->spec_cs, 3, gi, go, c->tw, s);
+      c->tock(tk);
+      const int tb = c->tick(SDNS_PASS_A2A_FWD);
+      c->peer_grp->stream_barrier(s);
+      c->tock(tb);
+    } else {
+      sdns_dev::col_plain_to(n, -1, c->wc, c->wb, c->cs_c, c->spec_cs, 3, gi, go, c->tw, s);
+      c->tock(tk);
+      c->exchange_col(false, 3);
+    }
   }
   XfArgs a = args_in;
   a.nl = c->wa;
@@ -1202,39 +1263,12 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
       }
       c->cs_d = base;
       c->wb = static_cast<double2*>(dev_alloc(c.get(), wbytes));
+      c->map_peer_blocks(c->col.get(), cfg->p1);
       c->wc = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * static_cast<size_t>(c->cs_c) * 6));
       c->wd = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * static_cast<size_t>(c->cs_d) * 6));
     } else {
       c->wb = cfg->p == 1 ? c->wa : static_cast<double2*>(dev_alloc(c.get(), wbytes));
-      const char* pe = std::getenv("SDNS_PEER");
-      if (cfg->p > 1 && !(pe && pe[0] == '0')) {
-        // collective on every rank: all map both buffers or none does
-        c->peer_wb = c->world->map_peers(c->wb);
-        c->peer_wa = c->world->map_peers(c->wa);
-        if (!c->peer_wb.empty() && !c->peer_wa.empty()) {
-          const int p = cfg->p, r = rank;
-          const long long blk = static_cast<long long>(c->np) * c->plane();
-          std::vector<long long> seg(2 * static_cast<size_t>(p));
-          auto delta = [](void* a, void* b) {
-            return static_cast<long long>((reinterpret_cast<intptr_t>(a) -
-                                           reinterpret_cast<intptr_t>(b)) /
-                                          static_cast<intptr_t>(sizeof(double2)));
-          };
-          for (int q = 0; q < p; ++q) {
-            seg[q] = delta(c->peer_wb[q], c->wb) + r * blk;
-            seg[p + q] = delta(c->peer_wa[q], c->wa) + r * blk;
-          }
-          c->d_seg = static_cast<long long*>(dev_alloc(c.get(), sizeof(long long) * seg.size()));
-          SDNS_CUDA(cudaMemcpyAsync(c->d_seg, seg.data(), sizeof(long long) * seg.size(),
-                                    cudaMemcpyHostToDevice, c->stream));
-          c->peer = true;
-        } else {
-          c->world->unmap_peers(c->peer_wb);
-          c->world->unmap_peers(c->peer_wa);
-          c->peer_wb.clear();
-          c->peer_wa.clear();
-        }
-      }
+      c->map_peer_blocks(c->world.get(), cfg->p);
       const char* ov = std::getenv("SDNS_OVERLAP");
       if (cfg->p > 1 && !c->peer && !(ov && ov[0] == '0')) {
         SDNS_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
@@ -1276,8 +1310,8 @@ int sdns_ctx_destroy(sdns_ctx* c) {
       cudaStreamDestroy(c->cstream);
     }
     if (c->peer) {
-      c->world->unmap_peers(c->peer_wb);
-      c->world->unmap_peers(c->peer_wa);
+      c->peer_grp->unmap_peers(c->peer_wb);
+      c->peer_grp->unmap_peers(c->peer_wa);
       cudaFree(c->d_seg);
     }
     cudaFree(c->tw);

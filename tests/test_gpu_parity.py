@@ -435,18 +435,23 @@ def test_inprocess_slab_rk4_matches_single_rank(p):
             assert a.energy == b.energy and a.enstrophy == b.enstrophy
 
 
-@pytest.mark.parametrize("p", [2, 4, 8])
-def test_inprocess_slab_transpose_modes_bitwise(p):
-    """Slab p > 1 runs its transposes fused into the producing passes by
-    default (P1 / P4 store straight into the owning rank's buffer, a stream
-    barrier after each: peer-direct), else as all-to-alls overlapped with the
-    next group's transforms (SDNS_PEER=0), else serially (SDNS_OVERLAP=0 as
-    well). The transforms and arithmetic are the same, so one RHS and two
-    RK4 steps must agree bit for bit across the three."""
+@pytest.mark.parametrize("geom", [dict(p=2), dict(p=4), dict(p=8),
+                                  dict(decomp="pencil", p=2, p1=2, p2=1),
+                                  dict(decomp="pencil", p=4, p1=2, p2=2),
+                                  dict(decomp="pencil", p=8, p1=4, p2=2)])
+def test_inprocess_transpose_modes_bitwise(geom):
+    """Slab p > 1 (and the pencil column-group transposes, p1 > 1) run fused
+    into the producing passes by default (P1 / P4 store straight into the
+    owning rank's buffer, a stream barrier after each: peer-direct), else as
+    all-to-alls -- overlapped with the next group's transforms for slab
+    (SDNS_PEER=0), else serial (SDNS_OVERLAP=0 as well). The transforms and
+    arithmetic are the same, so one RHS and two RK4 steps must agree bit for
+    bit across the modes."""
     n = 32
+    p = geom["p"]
     lo1 = S.build_layout(S.SolverConfig(n=n), 0)
     uh0 = S.iso_init(n, lo1, seed=9)
-    cfg = S.SolverConfig(n=n, p=p, nu=1e-3, dt=1e-3, t_end=1e-3)
+    cfg = S.SolverConfig(n=n, nu=1e-3, dt=1e-3, t_end=1e-3, **geom)
 
     def run():
         def body(rank, comm):

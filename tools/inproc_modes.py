@@ -10,6 +10,8 @@ import paper_1607_00850_b200 as S
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 entries = [S.BenchEntry(n, "slab", p) for n in (256, 512) for p in (1, 2, 4, 8)]
+entries += [S.BenchEntry(n, "pencil", p, p1, p2) for n in (256, 512)
+            for p, p1, p2 in ((4, 2, 2), (8, 2, 4), (8, 4, 2))]
 for name, env in (("peer", {}), ("overlap", {"SDNS_PEER": "0"}),
                   ("serial", {"SDNS_PEER": "0", "SDNS_OVERLAP": "0"})):
     os.environ.update(env)
@@ -17,5 +19,6 @@ for name, env in (("peer", {}), ("overlap", {"SDNS_PEER": "0"}),
     for k in env:
         os.environ.pop(k, None)
     for r in rows:
-        print(f"{name:8s} n={r.entry.n} p={r.entry.p}: {r.sec_per_step * 1e3:8.2f} ms/step "
+        print(f"{name:8s} n={r.entry.n} {r.entry.decomp} p={r.entry.p} ({r.entry.p1}x{r.entry.p2}): "
+              f"{r.sec_per_step * 1e3:8.2f} ms/step "
               f"{r.status}", flush=True)
