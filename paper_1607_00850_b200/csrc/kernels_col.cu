@@ -48,6 +48,9 @@ namespace {
 #ifndef SDNS_VXI
 #define SDNS_VXI 8
 #endif
+#ifndef SDNS_PAIR  // n = 1024 4-column tiles: both 64 B halves of a 128 B row back to back
+#define SDNS_PAIR 1
+#endif
 #ifndef SDNS_CS4TMA  // 4-column tiles (n = 1024 inverse passes) also load by TMA
 #define SDNS_CS4TMA 1
 #endif
@@ -406,22 +409,37 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
   // kz chunk of consecutive fields, and at any time the grid covers one
   // contiguous range of tiles (measured better on the x axis than walking
   // groups of adjacent tiles per CTA).
+  // n = 1024 (4-column, 64 B tile rows): a CTA walks tile PAIRS and
+  // interleaves their items -- (2j, f) then (2j+1, f) -- so both 64 B halves
+  // of every 128 B row are requested one item apart and the second is served
+  // by L2 (measured: walking single tiles, persistent CTAs drift apart and
+  // DRAM delivers every 128 B line twice). Items of one tile keep their order.
+  constexpr bool PAIR = CS == 4 && N >= 1024 && SDNS_PAIR;
+  constexpr int TS = PAIR ? 2 : 1;
   struct Item {
-    int t0, f;
+    int t0, f, h;  // pair base (PAIR) or tile, item, half
   };
   auto adv = [&](Item it) {
+    if constexpr (PAIR) {
+      if (it.h == 0) {
+        it.h = 1;
+        return it;
+      }
+      it.h = 0;
+    }
     if (++it.f == f_hi) {
       it.f = f_lo;
-      it.t0 += G;
+      it.t0 += G * TS;
     }
     return it;
   };
-  Item cur{static_cast<int>(blockIdx.x), f_lo};
-  Tile tc = tile_of<CS>(cur.t0, col, g);
+  auto tile_at = [&](const Item& it) { return tile_of<CS>(it.t0 + it.h, col, g); };
+  Item cur{static_cast<int>(blockIdx.x) * TS, f_lo, 0};
+  Tile tc = tile_at(cur);
   if (cur.t0 < ntiles) issue(0, f_lo, tc);
   cp_commit();
   Item n1 = adv(cur);
-  Tile tn1 = tile_of<CS>(n1.t0, col, g);
+  Tile tn1 = tile_at(n1);
   if (NBUF > 2) {
     if (n1.t0 < ntiles) issue(1, n1.f, tn1);
     cp_commit();
@@ -429,7 +447,7 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
   for (int i = 0; cur.t0 < ntiles; ++i) {
     if (NBUF > 2) {
       const Item n2 = adv(n1);
-      const Tile tn2 = tile_of<CS>(n2.t0, col, g);
+      const Tile tn2 = tile_at(n2);
       if (n2.t0 < ntiles) issue((i + 2) % 3, n2.f, tn2);
       if (tma) {
         mbar_wait(&tbar[i % 3], (i / 3) & 1);
@@ -456,7 +474,7 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
       cur = n1;
       tc = tn1;
       n1 = adv(n1);
-      tn1 = tile_of<CS>(n1.t0, col, g);
+      tn1 = tile_at(n1);
     }
   }
 }
@@ -644,6 +662,13 @@ static unsigned persistent_grid(K kernel, int threads, size_t smem, long long nt
   return static_cast<unsigned>(ntiles < g ? ntiles : g);
 }
 
+// Work units of a column pass: tiles, or tile pairs where the pipeline
+// walks pairs (n = 1024, 4-column tiles).
+template <int N, int V>
+static long long work_units(long long ntiles) {
+  return (PipeCfg<N, V>::CS == 4 && N >= 1024 && SDNS_PAIR) ? (ntiles + 1) / 2 : ntiles;
+}
+
 template <int N, int V>
 static long long ntiles_of(const ColGeom& g) {
   const long long cols = static_cast<long long>(g.nrows) * g.pitch;
@@ -726,7 +751,7 @@ static void plain_launch(const double2* in, double2* out, long long in_cs, long 
   if (nt <= 0) return;
   static int occ = 0;
   const unsigned grid =
-      persistent_grid(k_pipe_plain<N, S, V, SEP>, C::THREADS, C::SMEM, nt, &occ);
+      persistent_grid(k_pipe_plain<N, S, V, SEP>, C::THREADS, C::SMEM, work_units<N, V>(nt), &occ);
   CUtensorMap tm;
   const ColGeom gt = with_tile_map<N, C::CS>(g, in, in_cs, nfields, &tm);
   k_pipe_plain<N, S, V, SEP><<<grid, C::THREADS, C::SMEM, s>>>(in, out, in_cs, out_cs, nfields,
@@ -789,18 +814,18 @@ static void x_inv_n(const double2* u, long long u_cs, double2* out, long long ou
   const ColGeom gt = with_tile_map<N, C::CS>(g, u, u_cs, 3, &tm);
   if (go && go->seg) {  // peer-direct output (slab x inverse into the peers' receive layouts)
     static int occ = 0;
-    const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, 2>, C::THREADS, C::SMEM, nt, &occ);
+    const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, 2>, C::THREADS, C::SMEM, work_units<N, VXI>(nt), &occ);
     k_pipe_xinv<N, VXI, 2><<<grid, C::THREADS, C::SMEM, s>>>(
         u, u_cs, out, out_cs, gt, *go, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   } else if (go) {
     static int occ = 0;
-    const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, 1>, C::THREADS, C::SMEM, nt, &occ);
+    const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, 1>, C::THREADS, C::SMEM, work_units<N, VXI>(nt), &occ);
     k_pipe_xinv<N, VXI, 1><<<grid, C::THREADS, C::SMEM, s>>>(
         u, u_cs, out, out_cs, gt, *go, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   } else {
     static int occ = 0;
     const unsigned grid =
-        persistent_grid(k_pipe_xinv<N, VXI, 0>, C::THREADS, C::SMEM, nt, &occ);
+        persistent_grid(k_pipe_xinv<N, VXI, 0>, C::THREADS, C::SMEM, work_units<N, VXI>(nt), &occ);
     k_pipe_xinv<N, VXI, 0><<<grid, C::THREADS, C::SMEM, s>>>(
         u, u_cs, out, out_cs, gt, gt, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   }
@@ -826,7 +851,7 @@ static void y_inv_n(const double2* fin, double2* f, long long cs_in, long long c
   if (go) {
     static int occ = 0;
     const unsigned grid =
-        persistent_grid(k_pipe_yinv<N, VYI, 1>, C::THREADS, C::SMEM, nt, &occ);
+        persistent_grid(k_pipe_yinv<N, VYI, 1>, C::THREADS, C::SMEM, work_units<N, VYI>(nt), &occ);
     CUtensorMap tm;
     const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
     CUtensorMap tmo;
@@ -836,7 +861,7 @@ static void y_inv_n(const double2* fin, double2* f, long long cs_in, long long c
   } else {
     static int occ = 0;
     const unsigned grid =
-        persistent_grid(k_pipe_yinv<N, VYI, 0>, C::THREADS, C::SMEM, nt, &occ);
+        persistent_grid(k_pipe_yinv<N, VYI, 0>, C::THREADS, C::SMEM, work_units<N, VYI>(nt), &occ);
     CUtensorMap tm;
     const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
     CUtensorMap tmo;
