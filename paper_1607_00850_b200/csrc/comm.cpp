@@ -54,6 +54,7 @@ class LoopbackComm final : public Comm {
   void allreduce(double*, int, int) override {}
   void barrier() override {}
   std::vector<void*> map_peers(void* mine) override { return {mine}; }
+  const char* kind() const override { return "loopback"; }
   std::shared_ptr<Comm> split(int, int) override { return std::make_shared<LoopbackComm>(); }
   int device() const override {
     int d = 0;
@@ -148,6 +149,7 @@ class InProcessComm final : public Comm {
   int device() const override { return b_->device; }
 
   void poison(const std::string& why) override { b_->poison_all(why); }
+  const char* kind() const override { return "inprocess"; }
 
   void alltoall(const std::vector<Xfer>& xs, cudaStream_t s) override {
     Board& b = *b_;
@@ -346,6 +348,7 @@ class NcclComm final : public Comm {
     if (comm_) NcclApi::get().CommDestroy(comm_);
   }
   int device() const override { return device_; }
+  const char* kind() const override { return "nccl"; }
 
   void alltoall(const std::vector<Xfer>& xs, cudaStream_t s) override {
     auto& api = NcclApi::get();

@@ -65,6 +65,8 @@ class Comm {
   // Split by color, ordered by (key, rank) (transport.hpp:66-67).
   virtual std::shared_ptr<Comm> split(int color, int key) = 0;
   virtual int device() const = 0;
+  // Transport name as the runner's manifest reports it (runner.cpp:29-40).
+  virtual const char* kind() const = 0;
   // Fails every pending and future collective of the group with
   // ProtocolError (InProcessBackend::poison, transport.hpp:125-128); a
   // no-op where the transport has no shared state (loopback, NCCL).

@@ -691,7 +691,7 @@ int sdns_run_rank(const sdns_config* cfg, const char* initial_case, const sdns_r
     validate_case(icase);
     if (rank == 0) std::filesystem::create_directories(o.out_dir);
     ck(sdns_comm_barrier(comm));
-    copy_str(out->backend, sizeof(out->backend), cfg->p > 1 ? "nccl" : "loopback");
+    copy_str(out->backend, sizeof(out->backend), comm->c->kind());
     copy_str(out->status, sizeof(out->status), "ok");
     run_worker(*cfg, icase, o, rank, comm, o.device, *out);
   });

@@ -173,3 +173,18 @@ def test_acceptance_suite_python():
     res = S.run_acceptance_suite(verbose=False)
     assert [r.index for r in res] == list(range(1, 10))
     assert all(r.passed for r in res), [(r.name, r.detail) for r in res if not r.passed]
+
+
+def test_run_rank_matches_run(tmp_path):
+    """run_worker for one rank of a caller-made group (sdns_run_rank: one
+    process per GPU over NCCL in production) equals run() of the same config."""
+    cfg = S.SolverConfig(n=32, p=2, t_end=0.02, out_every=5)
+    S.run(cfg, S.RunOptions(out_dir=str(tmp_path / "run")))
+    results = S.run_group(2, lambda rank, comm: S.run(
+        cfg, S.RunOptions(out_dir=str(tmp_path / "rank")), comm=comm, rank=rank))
+    assert results[0].backend == "inprocess" and results[0].status == "ok"
+    a = open(tmp_path / "run" / "diagnostics.csv").read()
+    b = open(tmp_path / "rank" / "diagnostics.csv").read()
+    assert a == b
+    assert (tmp_path / "run" / "checkpoint.sdns").read_bytes() == \
+        (tmp_path / "rank" / "checkpoint.sdns").read_bytes()
