@@ -153,6 +153,13 @@ struct sdns_ctx {
   long long* d_seg = nullptr;
   Comm* peer_grp = nullptr;  // the group the peer-direct transposes run over
   int peer_n = 0;            // its size
+  // pencil row group (p2 > 1), peer-direct kz-block transposes: P2 stores its
+  // y-block q rows into member q's wd (d_seg_row), the z pass stores kz
+  // segment q into member q's wc (zmo_row, an output RowMap).
+  bool peer_row = false;
+  std::vector<void*> peer_wd, peer_wc;
+  long long* d_seg_row = nullptr;
+  RowMap zmo_row;
   double* h_out = nullptr;  // pinned
   int* d_flag = nullptr;
   int* h_flag = nullptr;    // pinned
@@ -368,6 +375,43 @@ struct sdns_ctx {
     peer_grp = grp;
     peer_n = gp;
     peer = true;
+  }
+  // Pencil row group (same coord1, ordered by coord2 = its kz block): map
+  // the members' wd and wc; collective over the row group.
+  void map_row_peers() {
+    const char* pe = std::getenv("SDNS_PEER");
+    const int p2 = cfg.p2;
+    if (!pencil || p2 <= 1 || (pe && pe[0] == '0')) return;
+    peer_wd = row->map_peers(wd);
+    peer_wc = row->map_peers(wc);
+    if (peer_wd.empty() || peer_wc.empty()) {
+      row->unmap_peers(peer_wd);
+      row->unmap_peers(peer_wc);
+      peer_wd.clear();
+      peer_wc.clear();
+      return;
+    }
+    auto delta = [](void* a, void* b) {
+      return static_cast<long long>((reinterpret_cast<intptr_t>(a) -
+                                     reinterpret_cast<intptr_t>(b)) /
+                                    static_cast<intptr_t>(sizeof(double2)));
+    };
+    const int me = row->rank();
+    const long long rows = static_cast<long long>(np) * yl;
+    std::vector<long long> seg(static_cast<size_t>(p2));
+    RowMap r = zmap(false);
+    for (int q = 0; q < p2; ++q) {
+      const size_t uq = static_cast<size_t>(q);
+      seg[uq] = delta(peer_wd[uq], wd) + seg_base[static_cast<size_t>(me)];
+      r.seg_base[q] = delta(peer_wc[uq], wc) + me * rows * seg_pitch[uq];
+      r.seg_pitch[q] = seg_pitch[uq];
+      r.seg_cs[q] = rows * p2 * seg_pitch[uq];
+    }
+    zmo_row = r;
+    SDNS_CUDA(cudaMalloc(&d_seg_row, sizeof(long long) * seg.size()));
+    SDNS_CUDA(cudaMemcpyAsync(d_seg_row, seg.data(), sizeof(long long) * seg.size(),
+                              cudaMemcpyHostToDevice, stream));
+    peer_row = true;
   }
   // Pencil column-group transpose, wa <-> wb (x blocks <-> y2 blocks),
   // fft.cpp:166-173 / :191-199 without the pack/unpack passes.
@@ -686,15 +730,36 @@ void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args
     } else {
       c->exchange_col(true, 5);
     }
-    tk = c->tick(SDNS_PASS_Y_INV);
-    sdns_dev::y_inverse_curl_to(n, c->wb, c->wc, c->spec_cs, c->cs_c, c->ygeom(), c->ygeom_row(),
-                                c->tw, s);
-    c->tock(tk);
-    c->exchange_row(true, 6);
-    tk = c->tick(SDNS_PASS_Z_FUSED);
-    sdns_dev::z_fused(n, c->wd, c->cs_d, zm, c->norm, c->tw, s);
-    c->tock(tk);
-    c->exchange_row(false, 3);
+    if (c->peer_row) {  // the row transposes fused into P2 and the z pass
+      ColGeom go2 = c->ygeom_row();
+      go2.ps1 = 0;
+      go2.seg = c->d_seg_row;
+      tk = c->tick(SDNS_PASS_Y_INV);
+      sdns_dev::y_inverse_curl_to(n, c->wb, c->wd, c->spec_cs, c->cs_d, c->ygeom(), go2, c->tw,
+                                  s);
+      c->tock(tk);
+      int tb = c->tick(SDNS_PASS_A2A_INV);
+      c->row->stream_barrier(s);
+      c->tock(tb);
+      tk = c->tick(SDNS_PASS_Z_FUSED);
+      RowMap zo = c->zmo_row;
+      zo.kz_keep = zm.kz_keep;
+      sdns_dev::z_fused_to(n, c->wd, c->cs_d, zm, c->wc, zo, c->norm, c->tw, s);
+      c->tock(tk);
+      tb = c->tick(SDNS_PASS_A2A_FWD);
+      c->row->stream_barrier(s);
+      c->tock(tb);
+    } else {
+      tk = c->tick(SDNS_PASS_Y_INV);
+      sdns_dev::y_inverse_curl_to(n, c->wb, c->wc, c->spec_cs, c->cs_c, c->ygeom(),
+                                  c->ygeom_row(), c->tw, s);
+      c->tock(tk);
+      c->exchange_row(true, 6);
+      tk = c->tick(SDNS_PASS_Z_FUSED);
+      sdns_dev::z_fused(n, c->wd, c->cs_d, zm, c->norm, c->tw, s);
+      c->tock(tk);
+      c->exchange_row(false, 3);
+    }
     ColGeom gi, go;
     pencil_yfwd_geoms(c, true, gi, go);
     tk = c->tick(SDNS_PASS_Y_FWD);
@@ -1266,6 +1331,7 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
       c->map_peer_blocks(c->col.get(), cfg->p1);
       c->wc = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * static_cast<size_t>(c->cs_c) * 6));
       c->wd = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * static_cast<size_t>(c->cs_d) * 6));
+      c->map_row_peers();
     } else {
       c->wb = cfg->p == 1 ? c->wa : static_cast<double2*>(dev_alloc(c.get(), wbytes));
       c->map_peer_blocks(c->world.get(), cfg->p);
@@ -1313,6 +1379,11 @@ int sdns_ctx_destroy(sdns_ctx* c) {
       c->peer_grp->unmap_peers(c->peer_wb);
       c->peer_grp->unmap_peers(c->peer_wa);
       cudaFree(c->d_seg);
+    }
+    if (c->peer_row) {
+      c->row->unmap_peers(c->peer_wd);
+      c->row->unmap_peers(c->peer_wc);
+      cudaFree(c->d_seg_row);
     }
     cudaFree(c->tw);
     if (c->wb != c->wa) cudaFree(c->wb);

@@ -335,9 +335,23 @@ __device__ __forceinline__ void zfft(double2 (&v)[fft_elems(N)], double2* sm, Sw
 #endif
 }
 
-template <int N>
+// Output element (ri, kz k) of a peer-direct z pass and its destination's
+// component stride (see z_fused_to).
+struct ZDst {
+  long long el, cs;
+};
+__device__ __forceinline__ ZDst zdst(const RowMap& rmo, int ri, int k) {
+  int sg = 0;
+  while (sg + 1 < rmo.nseg && k >= rmo.seg_k0[sg + 1]) ++sg;
+  return ZDst{rmo.seg_base[sg] + static_cast<long long>(ri) * rmo.seg_pitch[sg] +
+                  (k - rmo.seg_k0[sg]),
+              rmo.seg_cs[sg]};
+}
+
+template <int N, bool PO = false>
 __global__ void __launch_bounds__(ZFCfg<N>::THREADS, ZFCfg<N>::MINB)
-k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __restrict__ tw) {
+k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __restrict__ tw,
+          double2* fo = nullptr, RowMap rmo = RowMap{}) {
   constexpr int E = ZFCfg<N>::E, TPC = ZFCfg<N>::TPC, HP = ZFCfg<N>::HP, RPC = ZFCfg<N>::RPC;
   using Bar = typename std::conditional<(TPC >= 64), NamedBar, WarpBar>::type;
   extern __shared__ __align__(128) double2 smem[];
@@ -456,10 +470,16 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
       if (k <= N / 2 && k < rm.kz_keep) {  // kz >= n/3 is dealiased away
         const double2 d = S[sw(k)];
         const double2 e = cconj(S[sw((N - k) & (N - 1))]);
-        const long long el = zel(rm, ro, ri, k);
-        o0[el] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
         const double2 dd = csub(d, e);
-        o1[el] = make_double2(0.5 * dd.y, -0.5 * dd.x);
+        if constexpr (PO) {
+          const ZDst z = zdst(rmo, ri, k);
+          fo[z.el] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
+          fo[z.el + z.cs] = make_double2(0.5 * dd.y, -0.5 * dd.x);
+        } else {
+          const long long el = zel(rm, ro, ri, k);
+          o0[el] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
+          o1[el] = make_double2(0.5 * dd.y, -0.5 * dd.x);
+        }
       }
     }
   }
@@ -471,9 +491,17 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
 #pragma unroll
     for (int m = 0; m < E; ++m) {
       const int k = t + m * TPC;
-      if (k <= N / 2 && k < rm.kz_keep) o2[zel(rm, ro, ri, k)] = v[m];
+      if (k <= N / 2 && k < rm.kz_keep) {
+        if constexpr (PO) {
+          const ZDst z = zdst(rmo, ri, k);
+          fo[z.el + 2 * z.cs] = v[m];
+        } else {
+          o2[zel(rm, ro, ri, k)] = v[m];
+        }
+      }
     }
   }
+  if constexpr (PO) __threadfence_system();  // peers read after a stream barrier
 }
 
 // Standalone c2r along z (DistributedFFT::inverse tail, fft.cpp:124-125):
@@ -1060,6 +1088,26 @@ void z_fused(int n, double2* rows, long long cs, const RowMap& rm, double norm,
   switch (n) {
 #define X(NN) \
   case NN: z_fused_n<NN>(rows, cs, rm, norm, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
+}
+
+template <int N>
+static void z_fused_to_n(double2* rows, long long cs, const RowMap& rm, double2* out,
+                         const RowMap& rmo, double norm, const double2* tw, cudaStream_t s) {
+  using C = ZFCfg<N>;
+  const unsigned grid = static_cast<unsigned>((rm.nrows + C::RPC - 1) / C::RPC);
+  const size_t shm = C::SMEM;
+  SDNS_SET_SMEM((k_z_fused<N, true>), shm);
+  k_z_fused<N, true><<<grid, C::THREADS, shm, s>>>(rows, cs, rm, norm, tw, out, rmo);
+}
+
+void z_fused_to(int n, double2* rows, long long cs, const RowMap& rm, double2* out,
+                const RowMap& rmo, double norm, const double2* tw, cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: z_fused_to_n<NN>(rows, cs, rm, out, rmo, norm, tw, s); return;
     SDNS_FOR_N(X)
 #undef X
   }

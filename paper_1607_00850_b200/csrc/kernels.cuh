@@ -76,6 +76,9 @@ struct RowMap {
   long long seg_base[kMaxSeg] = {};
   int seg_pitch[kMaxSeg] = {};
   int seg_k0[kMaxSeg + 1] = {};
+  // Output maps of a peer-direct z pass (z_fused_to): component stride of
+  // each segment's destination (segments then live in different buffers).
+  long long seg_cs[kMaxSeg] = {};
 };
 
 // Fused x-pass forward epilogue variants.
@@ -153,6 +156,12 @@ void set_step_scalars(double* dts, double dt, cudaStream_t s);
 
 void z_fused(int n, double2* rows, long long cs, const RowMap& rm, double norm,
              const double2* tw, cudaStream_t s);
+// Same, storing the 3 outputs through the segmented output map `rmo`
+// (element (ri, kz) of component c at out + seg_base + c*seg_cs +
+// ri*seg_pitch + kz - seg_k0 of kz's segment): the pencil forward row
+// transpose fused into the z pass (peer-direct).
+void z_fused_to(int n, double2* rows, long long cs, const RowMap& rm, double2* out,
+                const RowMap& rmo, double norm, const double2* tw, cudaStream_t s);
 void z_c2r(int n, const double2* spec, double* real, const RowMap& rm, double norm,
            const double2* tw, cudaStream_t s);
 void z_r2c(int n, const double* real, double2* spec, const RowMap& rm, const double2* tw,

@@ -589,13 +589,15 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
   const OutSel<N, SEP> os(go, Lanes<N, V>().t);
   extern __shared__ __align__(128) double2 smem[];
   double2* const stage = smem + PipeCfg<N, V>::NBUF * N * PipeCfg<N, V>::CS;
-  const bool tst = PipeCfg<N, V>::SCR > 0 && go.tma != 0;
+  // peer-direct output (SEP 2) has one destination per position segment:
+  // LSU stores; otherwise TMA tensor stores where an output map exists
+  const bool tst = SEP != 2 && PipeCfg<N, V>::SCR > 0 && go.tma != 0;
   auto put = [&](int field, const double2(&r)[E], const Tile& tl, const PosOff<N>& po, int t) {
     if (tst)
       tma_put<N, PipeCfg<N, V>::CS>(&tmo, r, stage, CIdx<PipeCfg<N, V>::CS>{Lanes<N, V>().col}, t,
                                     tl, field);
     else
-      store_own<N>(f + field * cs, r, go, os.tile(tl, go), os.po(po), t);
+      store_own<N, SEP == 2>(f + field * cs, r, go, os.tile(tl, go), os.po(po), t);
   };
   pipeline<N, V>(ntiles, f_lo, f_cnt, g, [&](int it) { return fin + order(it) * cs_in; }, order,
                  &tm, tw,
@@ -628,6 +630,7 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
                    }
                  });
   if (tst && threadIdx.x == 0) bulk_wait0();
+  peer_fence<SEP>();
 }
 
 // ---------------------------------------------------------------------------
@@ -848,7 +851,19 @@ static void y_inv_n(const double2* fin, double2* f, long long cs_in, long long c
                     cudaStream_t s) {
   using C = PipeCfg<N, VYI>;
   const long long nt = ntiles_of<N, VYI>(g);
-  if (go) {
+  if (go && go->seg) {  // peer-direct output (pencil y inverse into the row peers' z lines)
+    static int occ = 0;
+    const unsigned grid =
+        persistent_grid(k_pipe_yinv<N, VYI, 2>, C::THREADS, C::SMEM, work_units<N, VYI>(nt), &occ);
+    CUtensorMap tm;
+    const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
+    CUtensorMap tmo;
+    std::memset(&tmo, 0, sizeof(tmo));
+    ColGeom got = *go;
+    got.tma = 0;
+    k_pipe_yinv<N, VYI, 2><<<grid, C::THREADS, C::SMEM, s>>>(
+        fin, f, cs_in, cs, gt, got, static_cast<int>(nt), f_lo, f_cnt, tw, tm, tmo);
+  } else if (go) {
     static int occ = 0;
     const unsigned grid =
         persistent_grid(k_pipe_yinv<N, VYI, 1>, C::THREADS, C::SMEM, work_units<N, VYI>(nt), &occ);

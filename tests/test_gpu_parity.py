@@ -437,12 +437,15 @@ def test_inprocess_slab_rk4_matches_single_rank(p):
 
 @pytest.mark.parametrize("geom", [dict(p=2), dict(p=4), dict(p=8),
                                   dict(decomp="pencil", p=2, p1=2, p2=1),
+                                  dict(decomp="pencil", p=2, p1=1, p2=2),
                                   dict(decomp="pencil", p=4, p1=2, p2=2),
+                                  dict(decomp="pencil", p=8, p1=2, p2=4),
                                   dict(decomp="pencil", p=8, p1=4, p2=2)])
 def test_inprocess_transpose_modes_bitwise(geom):
-    """Slab p > 1 (and the pencil column-group transposes, p1 > 1) run fused
-    into the producing passes by default (P1 / P4 store straight into the
-    owning rank's buffer, a stream barrier after each: peer-direct), else as
+    """Slab p > 1 and the pencil transposes (column group p1 > 1: P1 / P4;
+    row group p2 > 1: P2 / the z pass) run fused into the producing passes by
+    default (stores straight into the owning rank's buffer, a stream barrier
+    after each: peer-direct), else as
     all-to-alls -- overlapped with the next group's transforms for slab
     (SDNS_PEER=0), else serial (SDNS_OVERLAP=0 as well). The transforms and
     arithmetic are the same, so one RHS and two RK4 steps must agree bit for
