@@ -125,6 +125,15 @@ int sdns_comm_inprocess_group(int size, int device, double timeout_s, sdns_comm*
 int sdns_comm_nccl_unique_id(unsigned char id[128]);
 int sdns_comm_nccl_init(const unsigned char id[128], int size, int rank, int device,
                         sdns_comm** out);
+/* One process per rank over the caller's host all-gather (e.g.
+ * torch.distributed on gloo): `allgather(send, bytes, recv, user)` must put
+ * every rank's `bytes` into recv in rank order and return 0. Buffers and
+ * stream barriers go through CUDA IPC (memory and events), so several ranks
+ * may share one GPU and no kernel waits on another. Carries the peer-direct
+ * transposes only: all_to_all and split raise SDNS_PROTOCOL_ERROR. Collective. */
+typedef int (*sdns_allgather_fn)(const void* send, size_t bytes, void* recv, void* user);
+int sdns_comm_host_init(int size, int rank, int device, sdns_allgather_fn allgather, void* user,
+                        sdns_comm** out);
 int sdns_comm_rank(const sdns_comm* c);
 int sdns_comm_size(const sdns_comm* c);
 int sdns_comm_barrier(sdns_comm* c);                                 /* transport.hpp:64 */
@@ -150,6 +159,9 @@ int sdns_ctx_destroy(sdns_ctx* ctx);
 int sdns_ctx_layout(const sdns_ctx* ctx, sdns_layout* out);
 void* sdns_ctx_stream(const sdns_ctx* ctx);
 int sdns_ctx_sync(sdns_ctx* ctx);
+/* Which transposes of the RHS pipeline run peer-direct: bit 0
+ * the slab / pencil-column ones, bit 1 the pencil-row ones; 0 = all-to-all. */
+int sdns_ctx_transposes(const sdns_ctx* ctx);
 /* Device bytes held by the context (workspaces) and per field. */
 int64_t sdns_ctx_device_bytes(const sdns_ctx* ctx);
 

@@ -146,6 +146,8 @@ class _CriterionResult(ctypes.Structure):
 
 
 SAMPLE_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                ctypes.c_void_p)
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -218,6 +220,8 @@ def load_library(path: str = LIB_PATH):
             "sdns_device_layout": (I, [ctypes.POINTER(_Config), I, ctypes.POINTER(_DevLayout)]),
             "sdns_exchange_plan": (I, [ctypes.POINTER(_Config), I, I, I, P, ctypes.POINTER(I)]),
             "sdns_comm_split": (I, [P, I, I, PP]),
+            "sdns_comm_host_init": (I, [I, I, I, ALLGATHER_FN, P, PP]),
+            "sdns_ctx_transposes": (I, [P]),
             "sdns_comm_all_to_all_bytes": (I, [P, P, P, P, P, P]),
             "sdns_config_defaults": (V, [ctypes.POINTER(_Config)]),
             "sdns_parse_config_text": (I, [ctypes.c_char_p, P, P, I,
@@ -436,6 +440,29 @@ class Comm:
         _check(load_library().sdns_comm_nccl_init(uid, size, rank, device, ctypes.byref(h)))
         return Comm(h)
 
+    @staticmethod
+    def host(size: int, rank: int, device: int, allgather: Callable[[bytes], list]) -> "Comm":
+        """One process per rank over a host all-gather: `allgather(data)`
+        returns every rank's `data` (bytes) in rank order, e.g. through
+        torch.distributed on gloo. Peer-direct transposes only (CUDA IPC
+        memory and events; several ranks may share a GPU)."""
+        def cb(send, nbytes, recv, _user):
+            try:
+                parts = allgather(ctypes.string_at(send, nbytes))
+                buf = b"".join(parts)
+                if len(buf) != nbytes * size:
+                    return 1
+                ctypes.memmove(recv, buf, len(buf))
+                return 0
+            except BaseException:  # noqa: BLE001
+                return 1
+        fn = ALLGATHER_FN(cb)
+        h = ctypes.c_void_p()
+        _check(load_library().sdns_comm_host_init(size, rank, device, fn, None, ctypes.byref(h)))
+        c = Comm(h)
+        c._keep = fn  # the callback must outlive the communicator
+        return c
+
     @property
     def rank(self) -> int:
         return self._lib.sdns_comm_rank(self._h)
@@ -521,6 +548,18 @@ class Context:
     @property
     def device_bytes(self) -> int:
         return self._lib.sdns_ctx_device_bytes(self._h)
+
+    @property
+    def transposes(self) -> str:
+        """How the RHS pipeline's transposes run: "peer-direct" (all),
+        "peer-direct (column)" / "peer-direct (row)" (pencil, one group) or
+        "all-to-all"."""
+        f = self._lib.sdns_ctx_transposes(self._h)
+        if self.cfg.decomp == "pencil" and self.cfg.p > 1:
+            need = (1 if self.cfg.p1 > 1 else 0) | (2 if self.cfg.p2 > 1 else 0)
+            if f and f != need:
+                return "peer-direct (column)" if f == 1 else "peer-direct (row)"
+        return "peer-direct" if f else "all-to-all"
 
     def sync(self):
         _check(self._lib.sdns_ctx_sync(self._h))

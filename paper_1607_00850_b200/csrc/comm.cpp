@@ -18,6 +18,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 
@@ -274,6 +275,120 @@ class InProcessComm final : public Comm {
 };
 
 // --------------------------------------------------------------------------
+// CUDA IPC mapping of every rank's buffer for the peer-direct transposes
+// (one process per GPU): the 64-byte handles travel through `gather` (every
+// rank's bytes, rank order); `agree_min` reduces the success flag so every
+// rank keeps or drops the mappings together.
+std::vector<void*> ipc_map_peers(void* mine, int rank, int size,
+                                 const std::function<void(const void*, size_t, void*)>& gather,
+                                 const std::function<double(double)>& agree_min) {
+  cudaIpcMemHandle_t h{};
+  double ok = cudaIpcGetMemHandle(&h, mine) == cudaSuccess ? 1.0 : 0.0;
+  cudaGetLastError();
+  std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(size));
+  gather(&h, sizeof(h), all.data());
+  std::vector<void*> out(static_cast<size_t>(size), nullptr);
+  out[static_cast<size_t>(rank)] = mine;
+  for (int q = 0; q < size && ok > 0.5; ++q) {
+    if (q == rank) continue;
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, all[static_cast<size_t>(q)], cudaIpcMemLazyEnablePeerAccess) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      ok = 0.0;
+      break;
+    }
+    out[static_cast<size_t>(q)] = p;
+  }
+  if (agree_min(ok) < 0.5) {
+    for (int q = 0; q < size; ++q)
+      if (q != rank && out[static_cast<size_t>(q)]) cudaIpcCloseMemHandle(out[static_cast<size_t>(q)]);
+    return {};
+  }
+  return out;
+}
+
+void ipc_unmap_peers(const std::vector<void*>& ptrs, int rank) {
+  for (int q = 0; q < static_cast<int>(ptrs.size()); ++q)
+    if (q != rank && ptrs[static_cast<size_t>(q)]) cudaIpcCloseMemHandle(ptrs[static_cast<size_t>(q)]);
+}
+
+// --------------------------------------------------------------------------
+// Host-callback transport: one process per rank (several may share a GPU)
+// with the caller's host all-gather (e.g. torch.distributed over gloo) as the
+// only primitive. Reductions fold gathered values in rank order; buffers are
+// exchanged by CUDA IPC and stream barriers wait on the ranks' IPC events, so
+// no kernel ever waits on another. It carries the peer-direct transposes
+// only: the all-to-all and split are not provided (ProtocolError).
+class HostComm final : public Comm {
+ public:
+  HostComm(int rank, int size, int device, sdns_allgather_fn fn, void* user)
+      : Comm(rank, size), device_(device), fn_(fn), user_(user) {
+    SDNS_CUDA(cudaSetDevice(device_));
+    SDNS_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming | cudaEventInterprocess));
+    cudaIpcEventHandle_t h{};
+    SDNS_CUDA(cudaIpcGetEventHandle(&h, ev_));
+    std::vector<cudaIpcEventHandle_t> all(static_cast<size_t>(size));
+    gather(&h, sizeof(h), all.data());
+    peer_ev_.assign(static_cast<size_t>(size), nullptr);
+    for (int q = 0; q < size; ++q)
+      if (q != rank) SDNS_CUDA(cudaIpcOpenEventHandle(&peer_ev_[static_cast<size_t>(q)], all[static_cast<size_t>(q)]));
+  }
+  ~HostComm() override {
+    for (auto e : peer_ev_)
+      if (e) cudaEventDestroy(e);
+    if (ev_) cudaEventDestroy(ev_);
+  }
+  int device() const override { return device_; }
+  const char* kind() const override { return "host"; }
+
+  void alltoall(const std::vector<Xfer>&, cudaStream_t) override {
+    protocol_error("host-callback transport: all_to_all is not provided (peer-direct transposes only)");
+  }
+  void allreduce(double* v, int n, int op) override {
+    std::vector<double> all(static_cast<size_t>(n) * size_);
+    gather(v, sizeof(double) * static_cast<size_t>(n), all.data());
+    std::vector<double> acc(all.begin(), all.begin() + n);
+    for (int q = 1; q < size_; ++q) fold(acc.data(), all.data() + static_cast<size_t>(q) * n, n, op);
+    std::memcpy(v, acc.data(), sizeof(double) * static_cast<size_t>(n));
+  }
+  void barrier() override {
+    char b = 0;
+    std::vector<char> all(static_cast<size_t>(size_));
+    gather(&b, 1, all.data());
+  }
+  std::shared_ptr<Comm> split(int, int) override {
+    protocol_error("host-callback transport: split is not provided");
+  }
+  std::vector<void*> map_peers(void* mine) override {
+    return ipc_map_peers(
+        mine, rank_, size_, [this](const void* a, size_t b, void* c) { gather(a, b, c); },
+        [this](double x) {
+          allreduce(&x, 1, 2);
+          return x;
+        });
+  }
+  void unmap_peers(const std::vector<void*>& ptrs) override { ipc_unmap_peers(ptrs, rank_); }
+  void stream_barrier(cudaStream_t s) override {
+    SDNS_CUDA(cudaEventRecord(ev_, s));
+    barrier();
+    for (int q = 0; q < size_; ++q)
+      if (q != rank_) SDNS_CUDA(cudaStreamWaitEvent(s, peer_ev_[static_cast<size_t>(q)], 0));
+    barrier();  // nobody re-records before every rank captured the events
+  }
+
+ private:
+  void gather(const void* send, size_t bytes, void* recv) {
+    if (fn_(send, bytes, recv, user_) != 0) protocol_error("host all-gather callback failed");
+  }
+  int device_;
+  sdns_allgather_fn fn_;
+  void* user_;
+  cudaEvent_t ev_ = nullptr;
+  std::vector<cudaEvent_t> peer_ev_;
+};
+
+// --------------------------------------------------------------------------
 // NCCL through dlopen (the subset we call; ABI per /usr/include/nccl.h).
 typedef struct ncclComm* ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
@@ -396,44 +511,15 @@ class NcclComm final : public Comm {
   // outcome is agreed collectively: if any rank fails to export or map,
   // every rank releases its mappings and returns empty.
   std::vector<void*> map_peers(void* mine) override {
-    auto& api = NcclApi::get();
-    constexpr size_t H = sizeof(cudaIpcMemHandle_t);
-    static_assert(H % sizeof(double) == 0, "IPC handle size");
-    constexpr int HD = static_cast<int>(H / sizeof(double));
-    cudaIpcMemHandle_t h{};
-    double ok = cudaIpcGetMemHandle(&h, mine) == cudaSuccess ? 1.0 : 0.0;
-    cudaGetLastError();
-    double* d_mine = dbuf_ + static_cast<size_t>(kMaxVals) * size_;
-    SDNS_CUDA(cudaMemcpyAsync(d_mine, &h, H, cudaMemcpyHostToDevice, side_));
-    nccl_check(api.AllGather(d_mine, dbuf_, static_cast<size_t>(HD), ncclFloat64, comm_, side_),
-               "ncclAllGather");
-    std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(size_));
-    SDNS_CUDA(cudaMemcpyAsync(all.data(), dbuf_, H * size_, cudaMemcpyDeviceToHost, side_));
-    SDNS_CUDA(cudaStreamSynchronize(side_));
-    std::vector<void*> out(static_cast<size_t>(size_), nullptr);
-    out[rank_] = mine;
-    for (int q = 0; q < size_ && ok > 0.5; ++q) {
-      if (q == rank_) continue;
-      void* p = nullptr;
-      if (cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-        cudaGetLastError();
-        ok = 0.0;
-        break;
-      }
-      out[q] = p;
-    }
-    allreduce(&ok, 1, 2);
-    if (ok < 0.5) {
-      unmap_peers(out);
-      return {};
-    }
-    return out;
+    return ipc_map_peers(
+        mine, rank_, size_, [this](const void* a, size_t b, void* c) { gather_bytes(a, b, c); },
+        [this](double x) {
+          allreduce(&x, 1, 2);
+          return x;
+        });
   }
 
-  void unmap_peers(const std::vector<void*>& ptrs) override {
-    for (int q = 0; q < static_cast<int>(ptrs.size()); ++q)
-      if (q != rank_ && ptrs[q]) cudaIpcCloseMemHandle(ptrs[q]);
-  }
+  void unmap_peers(const std::vector<void*>& ptrs) override { ipc_unmap_peers(ptrs, rank_); }
 
   // A one-element all-reduce on the compute stream: NCCL's kernel completes
   // on a rank only after every rank's stream reached it, and the producing
@@ -465,6 +551,24 @@ class NcclComm final : public Comm {
 
  private:
   static constexpr int kMaxVals = 4096;
+  // Every rank's `bytes` (<= 8 * kMaxVals) in rank order, through the device
+  // all-gather.
+  void gather_bytes(const void* mine, size_t bytes, void* all) {
+    auto& api = NcclApi::get();
+    const size_t nd = (bytes + sizeof(double) - 1) / sizeof(double);
+    if (nd > static_cast<size_t>(kMaxVals)) protocol_error("gather_bytes: too large");
+    std::vector<double> pad(nd, 0.0);
+    std::memcpy(pad.data(), mine, bytes);
+    double* d_mine = dbuf_ + static_cast<size_t>(kMaxVals) * size_;
+    SDNS_CUDA(cudaMemcpyAsync(d_mine, pad.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, side_));
+    nccl_check(api.AllGather(d_mine, dbuf_, nd, ncclFloat64, comm_, side_), "ncclAllGather");
+    std::vector<double> got(nd * size_);
+    SDNS_CUDA(cudaMemcpyAsync(got.data(), dbuf_, sizeof(double) * nd * size_, cudaMemcpyDeviceToHost,
+                              side_));
+    SDNS_CUDA(cudaStreamSynchronize(side_));
+    for (int q = 0; q < size_; ++q)
+      std::memcpy(static_cast<char*>(all) + bytes * q, got.data() + nd * q, bytes);
+  }
   void gather2(const double* mine, double* all) {
     auto& api = NcclApi::get();
     double* d_mine = dbuf_ + static_cast<size_t>(kMaxVals) * size_;
@@ -483,6 +587,13 @@ class NcclComm final : public Comm {
 }  // namespace
 
 std::shared_ptr<Comm> make_loopback_comm() { return std::make_shared<LoopbackComm>(); }
+
+std::shared_ptr<Comm> make_host_comm(int size, int rank, int device, sdns_allgather_fn fn,
+                                     void* user) {
+  if (size < 1 || rank < 0 || rank >= size) config_error("host comm: bad rank/size");
+  if (!fn) config_error("host comm: all-gather callback is NULL");
+  return std::make_shared<HostComm>(rank, size, device, fn, user);
+}
 
 std::vector<std::shared_ptr<Comm>> make_inprocess_group(int size, int device, double timeout_s) {
   if (size < 1) config_error("in-process group size must be >= 1");

@@ -1231,6 +1231,11 @@ int sdns_comm_nccl_init(const unsigned char id[128], int size, int rank, int dev
   return guarded([&] { *out = new sdns_comm{make_nccl_comm(id, size, rank, device)}; });
 }
 
+int sdns_comm_host_init(int size, int rank, int device, sdns_allgather_fn fn, void* user,
+                        sdns_comm** out) {
+  return guarded([&] { *out = new sdns_comm{make_host_comm(size, rank, device, fn, user)}; });
+}
+
 int sdns_comm_rank(const sdns_comm* c) { return c->c->rank(); }
 int sdns_comm_size(const sdns_comm* c) { return c->c->size(); }
 int sdns_comm_barrier(sdns_comm* c) {
@@ -1409,6 +1414,8 @@ int sdns_ctx_layout(const sdns_ctx* c, sdns_layout* out) {
   return SDNS_OK;
 }
 void* sdns_ctx_stream(const sdns_ctx* c) { return c->stream; }
+int sdns_ctx_transposes(const sdns_ctx* c) { return (c->peer ? 1 : 0) | (c->peer_row ? 2 : 0); }
+
 int sdns_ctx_sync(sdns_ctx* c) {
   return guarded([&] {
     set_device(c);
