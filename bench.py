@@ -260,6 +260,7 @@ def run_ours(args):
     n, nu, dt = args.n, 5e-4, 5e-4
     cfg = S.SolverConfig(n=n, p=world, nu=nu, dt=dt, t_end=args.steps * dt)
     ctx = S.Context(cfg, rank=rank, device=local, comm=comm)
+    transposes = ctx.transposes if world > 1 else "none (p = 1)"
     lo = ctx.layout
     t0 = time.time()
     uh0 = S.iso_init(n, lo, seed=1607)
@@ -358,6 +359,7 @@ def run_ours(args):
         "data": "synthetic (seeded isotropic field, BASELINE configs[2] construction)",
         "config": {"workload": f"configs[2]: isotropic {n}^3 fp64, nu=5e-4, dt=5e-4, slab x {world}",
                    "n": n, "decomp": "slab", "p": world, "global_points": n**3,
+                   "transposes": transposes,
                    "l2": "inputs larger than L2 (u_hat alone is %.1f GB per rank)" % (3 * C / 1e9)},
         "ns_per_gridpoint_step": ms * 1e6 / n**3,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
