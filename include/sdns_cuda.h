@@ -127,13 +127,18 @@ int sdns_comm_nccl_init(const unsigned char id[128], int size, int rank, int dev
                         sdns_comm** out);
 /* One process per rank over the caller's host all-gather (e.g.
  * torch.distributed on gloo): `allgather(send, bytes, recv, user)` must put
- * every rank's `bytes` into recv in rank order and return 0. Buffers and
- * stream barriers go through CUDA IPC (memory and events), so several ranks
- * may share one GPU and no kernel waits on another. Carries the peer-direct
- * transposes only: all_to_all and split raise SDNS_PROTOCOL_ERROR. Collective. */
+ * every rank's `bytes` of the group `user` into recv in rank order and
+ * return 0. split() calls `group(ranks, n, user, &child_user)` once per new
+ * group, in the same order and with the same member list (indices in the
+ * group `user`) on every rank, and the child uses child_user (NULL group
+ * callback: no split). Buffers and stream barriers go through CUDA IPC
+ * (memory and events), so several ranks may share one GPU and no kernel
+ * waits on another. Carries the peer-direct transposes only: all_to_all
+ * raises SDNS_PROTOCOL_ERROR. Collective. */
 typedef int (*sdns_allgather_fn)(const void* send, size_t bytes, void* recv, void* user);
-int sdns_comm_host_init(int size, int rank, int device, sdns_allgather_fn allgather, void* user,
-                        sdns_comm** out);
+typedef int (*sdns_group_fn)(const int* ranks, int n, void* user, void** child_user);
+int sdns_comm_host_init(int size, int rank, int device, sdns_allgather_fn allgather,
+                        sdns_group_fn group, void* user, sdns_comm** out);
 int sdns_comm_rank(const sdns_comm* c);
 int sdns_comm_size(const sdns_comm* c);
 int sdns_comm_barrier(sdns_comm* c);                                 /* transport.hpp:64 */

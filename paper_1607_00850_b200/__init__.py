@@ -148,6 +148,8 @@ class _CriterionResult(ctypes.Structure):
 SAMPLE_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p)
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
                                 ctypes.c_void_p)
+GROUP_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+                            ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p))
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -220,7 +222,7 @@ def load_library(path: str = LIB_PATH):
             "sdns_device_layout": (I, [ctypes.POINTER(_Config), I, ctypes.POINTER(_DevLayout)]),
             "sdns_exchange_plan": (I, [ctypes.POINTER(_Config), I, I, I, P, ctypes.POINTER(I)]),
             "sdns_comm_split": (I, [P, I, I, PP]),
-            "sdns_comm_host_init": (I, [I, I, I, ALLGATHER_FN, P, PP]),
+            "sdns_comm_host_init": (I, [I, I, I, ALLGATHER_FN, GROUP_FN, P, PP]),
             "sdns_ctx_transposes": (I, [P]),
             "sdns_comm_all_to_all_bytes": (I, [P, P, P, P, P, P]),
             "sdns_config_defaults": (V, [ctypes.POINTER(_Config)]),
@@ -441,26 +443,47 @@ class Comm:
         return Comm(h)
 
     @staticmethod
-    def host(size: int, rank: int, device: int, allgather: Callable[[bytes], list]) -> "Comm":
-        """One process per rank over a host all-gather: `allgather(data)`
-        returns every rank's `data` (bytes) in rank order, e.g. through
-        torch.distributed on gloo. Peer-direct transposes only (CUDA IPC
-        memory and events; several ranks may share a GPU)."""
-        def cb(send, nbytes, recv, _user):
+    def host(size: int, rank: int, device: int, allgather: Callable,
+             new_group: Optional[Callable] = None) -> "Comm":
+        """One process per rank over a host all-gather: `allgather(data,
+        group)` returns every member's `data` (bytes) in rank order for the
+        group handle `group` (None = the world); `new_group(ranks)` (world
+        ranks, called on every rank for every group, as
+        torch.distributed.new_group requires) returns a handle and enables
+        split() for the pencil row/column groups. CUDA IPC memory and events
+        carry the peer-direct transposes; several ranks may share a GPU."""
+        groups = {0: (None, list(range(size)))}
+
+        def cb(send, nbytes, recv, user):
             try:
-                parts = allgather(ctypes.string_at(send, nbytes))
+                g, members = groups[user or 0]
+                parts = allgather(ctypes.string_at(send, nbytes), g)
                 buf = b"".join(parts)
-                if len(buf) != nbytes * size:
+                if len(buf) != nbytes * len(members):
                     return 1
                 ctypes.memmove(recv, buf, len(buf))
                 return 0
             except BaseException:  # noqa: BLE001
                 return 1
+
+        def gcb(ranks, n, user, child):
+            try:
+                _, members = groups[user or 0]
+                world = [members[ranks[i]] for i in range(n)]
+                key = len(groups)
+                groups[key] = (new_group(world), world)
+                child[0] = key
+                return 0
+            except BaseException:  # noqa: BLE001
+                return 1
+
         fn = ALLGATHER_FN(cb)
+        gfn = GROUP_FN(gcb) if new_group else GROUP_FN()
         h = ctypes.c_void_p()
-        _check(load_library().sdns_comm_host_init(size, rank, device, fn, None, ctypes.byref(h)))
+        _check(load_library().sdns_comm_host_init(size, rank, device, fn, gfn, None,
+                                                  ctypes.byref(h)))
         c = Comm(h)
-        c._keep = fn  # the callback must outlive the communicator
+        c._keep = (fn, gfn, groups)  # the callbacks must outlive the communicator
         return c
 
     @property

@@ -316,14 +316,15 @@ void ipc_unmap_peers(const std::vector<void*>& ptrs, int rank) {
 // --------------------------------------------------------------------------
 // Host-callback transport: one process per rank (several may share a GPU)
 // with the caller's host all-gather (e.g. torch.distributed over gloo) as the
-// only primitive. Reductions fold gathered values in rank order; buffers are
-// exchanged by CUDA IPC and stream barriers wait on the ranks' IPC events, so
-// no kernel ever waits on another. It carries the peer-direct transposes
-// only: the all-to-all and split are not provided (ProtocolError).
+// only primitive (plus a group callback for split). Reductions fold gathered
+// values in rank order; buffers are exchanged by CUDA IPC and stream barriers
+// wait on the ranks' IPC events, so no kernel ever waits on another. It
+// carries the peer-direct transposes only: the all-to-all is not provided
+// (ProtocolError).
 class HostComm final : public Comm {
  public:
-  HostComm(int rank, int size, int device, sdns_allgather_fn fn, void* user)
-      : Comm(rank, size), device_(device), fn_(fn), user_(user) {
+  HostComm(int rank, int size, int device, sdns_allgather_fn fn, sdns_group_fn gfn, void* user)
+      : Comm(rank, size), device_(device), fn_(fn), gfn_(gfn), user_(user) {
     SDNS_CUDA(cudaSetDevice(device_));
     SDNS_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming | cudaEventInterprocess));
     cudaIpcEventHandle_t h{};
@@ -342,8 +343,16 @@ class HostComm final : public Comm {
   int device() const override { return device_; }
   const char* kind() const override { return "host"; }
 
-  void alltoall(const std::vector<Xfer>&, cudaStream_t) override {
-    protocol_error("host-callback transport: all_to_all is not provided (peer-direct transposes only)");
+  // Only the blocks a rank sends itself (a one-member group's transposes).
+  void alltoall(const std::vector<Xfer>& xs, cudaStream_t s) override {
+    for (const Xfer& x : xs) {
+      if (x.peer != rank_)
+        protocol_error("host-callback transport: all_to_all between ranks is not provided "
+                       "(peer-direct transposes only)");
+      if (x.send_bytes != x.recv_bytes) protocol_error("all_to_all: self block size mismatch");
+      if (x.send_bytes && x.send != x.recv)
+        SDNS_CUDA(cudaMemcpyAsync(x.recv, x.send, x.send_bytes, cudaMemcpyDeviceToDevice, s));
+    }
   }
   void allreduce(double* v, int n, int op) override {
     std::vector<double> all(static_cast<size_t>(n) * size_);
@@ -357,8 +366,38 @@ class HostComm final : public Comm {
     std::vector<char> all(static_cast<size_t>(size_));
     gather(&b, 1, all.data());
   }
-  std::shared_ptr<Comm> split(int, int) override {
-    protocol_error("host-callback transport: split is not provided");
+  // Every rank gathers all (color, key) pairs, then the groups are created
+  // through the caller's group callback in ascending color order with
+  // identical arguments on every rank (members ordered by (key, rank),
+  // transport.hpp:66-67); each rank joins its own.
+  std::shared_ptr<Comm> split(int color, int key) override {
+    if (!gfn_) protocol_error("host-callback transport: no group callback, split not provided");
+    const int mine[2] = {color, key};
+    std::vector<int> all(2 * static_cast<size_t>(size_));
+    gather(mine, sizeof(mine), all.data());
+    std::vector<int> colors;
+    for (int q = 0; q < size_; ++q) colors.push_back(all[2 * static_cast<size_t>(q)]);
+    std::sort(colors.begin(), colors.end());
+    colors.erase(std::unique(colors.begin(), colors.end()), colors.end());
+    void* my_user = nullptr;
+    int my_rank = 0, my_size = 0;
+    for (int c : colors) {
+      std::vector<std::pair<int, int>> mem;  // (key, rank)
+      for (int q = 0; q < size_; ++q)
+        if (all[2 * static_cast<size_t>(q)] == c) mem.push_back({all[2 * static_cast<size_t>(q) + 1], q});
+      std::sort(mem.begin(), mem.end());
+      std::vector<int> ranks;
+      for (const auto& m : mem) ranks.push_back(m.second);
+      void* gu = nullptr;
+      if (gfn_(ranks.data(), static_cast<int>(ranks.size()), user_, &gu) != 0)
+        protocol_error("host group callback failed");
+      if (c == color) {
+        my_user = gu;
+        my_size = static_cast<int>(ranks.size());
+        my_rank = static_cast<int>(std::find(ranks.begin(), ranks.end(), rank_) - ranks.begin());
+      }
+    }
+    return std::make_shared<HostComm>(my_rank, my_size, device_, fn_, gfn_, my_user);
   }
   std::vector<void*> map_peers(void* mine) override {
     return ipc_map_peers(
@@ -383,6 +422,7 @@ class HostComm final : public Comm {
   }
   int device_;
   sdns_allgather_fn fn_;
+  sdns_group_fn gfn_;
   void* user_;
   cudaEvent_t ev_ = nullptr;
   std::vector<cudaEvent_t> peer_ev_;
@@ -589,10 +629,10 @@ class NcclComm final : public Comm {
 std::shared_ptr<Comm> make_loopback_comm() { return std::make_shared<LoopbackComm>(); }
 
 std::shared_ptr<Comm> make_host_comm(int size, int rank, int device, sdns_allgather_fn fn,
-                                     void* user) {
+                                     sdns_group_fn gfn, void* user) {
   if (size < 1 || rank < 0 || rank >= size) config_error("host comm: bad rank/size");
   if (!fn) config_error("host comm: all-gather callback is NULL");
-  return std::make_shared<HostComm>(rank, size, device, fn, user);
+  return std::make_shared<HostComm>(rank, size, device, fn, gfn, user);
 }
 
 std::vector<std::shared_ptr<Comm>> make_inprocess_group(int size, int device, double timeout_s) {

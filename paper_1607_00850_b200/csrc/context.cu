@@ -1231,9 +1231,9 @@ int sdns_comm_nccl_init(const unsigned char id[128], int size, int rank, int dev
   return guarded([&] { *out = new sdns_comm{make_nccl_comm(id, size, rank, device)}; });
 }
 
-int sdns_comm_host_init(int size, int rank, int device, sdns_allgather_fn fn, void* user,
-                        sdns_comm** out) {
-  return guarded([&] { *out = new sdns_comm{make_host_comm(size, rank, device, fn, user)}; });
+int sdns_comm_host_init(int size, int rank, int device, sdns_allgather_fn fn, sdns_group_fn gfn,
+                        void* user, sdns_comm** out) {
+  return guarded([&] { *out = new sdns_comm{make_host_comm(size, rank, device, fn, gfn, user)}; });
 }
 
 int sdns_comm_rank(const sdns_comm* c) { return c->c->rank(); }

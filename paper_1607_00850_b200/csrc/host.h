@@ -92,7 +92,7 @@ class Comm {
 
 std::shared_ptr<Comm> make_loopback_comm();
 std::shared_ptr<Comm> make_host_comm(int size, int rank, int device, sdns_allgather_fn fn,
-                                     void* user);
+                                     sdns_group_fn gfn, void* user);
 std::vector<std::shared_ptr<Comm>> make_inprocess_group(int size, int device, double timeout_s);
 void nccl_unique_id(unsigned char id[128]);
 std::shared_ptr<Comm> make_nccl_comm(const unsigned char id[128], int size, int rank, int device);

@@ -1,9 +1,9 @@
-"""One rank of the multi-process test (tests/test_gpu_multiprocess.py):
-slab p = world over the host-callback transport (gloo all-gather, CUDA IPC
-memory and events), several ranks sharing GPU 0. Saves this rank's RHS,
-two-step state and stats to <out>/r<rank>.npz.
+"""One rank of the multi-process test (tests/test_gpu_multiprocess.py): slab
+or pencil p = world over the host-callback transport (gloo all-gathers and
+groups, CUDA IPC memory and events), several ranks sharing GPU 0. Saves this
+rank's RHS, two-step state and stats to <out>/r<rank>.npz.
 
-    python tests/helpers/mp_slab_worker.py <rank> <world> <port> <out> <n> [decomp p1 p2]"""
+    python tests/helpers/mp_slab_worker.py <rank> <world> <port> <out> <n> [p1 p2]"""
 import os
 import sys
 
@@ -21,14 +21,18 @@ def main():
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
 
-    def allgather(data: bytes):
+    def allgather(data: bytes, group):
         t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
-        parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t)
+        size = dist.get_world_size(group)
+        parts = [torch.empty_like(t) for _ in range(size)]
+        dist.all_gather(parts, t, group=group)
         return [p.numpy().tobytes() for p in parts]
 
-    comm = S.Comm.host(world, rank, 0, allgather)
-    cfg = S.SolverConfig(n=n, p=world, nu=1e-3, dt=1e-3, t_end=1e-3)
+    comm = S.Comm.host(world, rank, 0, allgather, new_group=dist.new_group)
+    geom = {}
+    if len(sys.argv) > 7:
+        geom = dict(decomp="pencil", p1=int(sys.argv[6]), p2=int(sys.argv[7]))
+    cfg = S.SolverConfig(n=n, p=world, nu=1e-3, dt=1e-3, t_end=1e-3, **geom)
     with S.Context(cfg, rank=rank, device=0, comm=comm) as c:
         lo = c.layout
         uh0 = S.iso_init(n, S.build_layout(S.SolverConfig(n=n), 0), seed=9)

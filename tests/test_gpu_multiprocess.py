@@ -1,4 +1,4 @@
-"""GPU: the multi-process peer-direct path. Ranks are separate processes
+"""GPU: the multi-process peer-direct path (slab and pencil). Ranks are separate processes
 (one CUDA context each, sharing the one GPU here) over the host-callback
 transport: their buffers are mapped with CUDA IPC and the stream barriers
 wait on IPC events -- the same mapping code (ipc_map_peers) the NCCL backend
@@ -26,13 +26,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_multiprocess_slab_peer_direct_bitwise(tmp_path, world):
+@pytest.mark.parametrize("world,grid", [(2, None), (4, None), (2, (1, 2)), (4, (2, 2))])
+def test_multiprocess_peer_direct_bitwise(tmp_path, world, grid):
+    """slab p = 2, 4 and pencil 1x2, 2x2 (row / column sub-communicators
+    split through the transport's group callback)."""
     n = 32
     port = _free_port()
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    extra = [str(grid[0]), str(grid[1])] if grid else []
     procs = [subprocess.Popen([sys.executable, WORKER, str(r), str(world), str(port),
-                               str(tmp_path), str(n)], env=env,
+                               str(tmp_path), str(n)] + extra, env=env,
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
              for r in range(world)]
     outs = []
@@ -47,7 +50,8 @@ def test_multiprocess_slab_peer_direct_bitwise(tmp_path, world):
 
     # the same decomposition as threads in this process (same kernels, the
     # peers' buffers addressed directly): bitwise
-    cfg = S.SolverConfig(n=n, p=world, nu=1e-3, dt=1e-3, t_end=1e-3)
+    geom = dict(decomp="pencil", p1=grid[0], p2=grid[1]) if grid else {}
+    cfg = S.SolverConfig(n=n, p=world, nu=1e-3, dt=1e-3, t_end=1e-3, **geom)
     uh0 = S.iso_init(n, S.build_layout(S.SolverConfig(n=n), 0), seed=9)
 
     def body(rank, comm):
