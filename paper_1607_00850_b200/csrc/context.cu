@@ -157,6 +157,12 @@ struct sdns_ctx {
   // y-block q rows into member q's wd (d_seg_row), the z pass stores kz
   // segment q into member q's wc (zmo_row, an output RowMap).
   bool peer_row = false;
+  // true while the last thing on the stream was a peer-direct RHS: its
+  // closing barrier already orders the next fused stores after every
+  // rank's reads of the work buffers; any other entry point clears it and
+  // the next RHS opens with a barrier (stores into a peer's buffers must
+  // wait for whatever that peer still has queued on them).
+  bool peer_fresh = false;
   std::vector<void*> peer_wd, peer_wc;
   long long* d_seg_row = nullptr;
   RowMap zmo_row;
@@ -522,7 +528,11 @@ struct sdns_state {
 
 namespace {
 
-void set_device(sdns_ctx* c) { SDNS_CUDA(cudaSetDevice(c->device)); }
+// Every entry point starts here; see sdns_ctx::peer_fresh.
+void set_device(sdns_ctx* c) {
+  SDNS_CUDA(cudaSetDevice(c->device));
+  c->peer_fresh = false;
+}
 
 void require_spec(const sdns_field* f, int ncomp, const char* what) {
   if (!f || f->kind != SDNS_SPECTRAL || f->ncomp < ncomp)
@@ -674,6 +684,12 @@ void rhs_slab_peer(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& arg
 
 // One fused RHS evaluation: P1 .. P5 (kernels*.cu) with the transposes.
 void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args_in) {
+  if ((c->peer || c->peer_row) && !c->peer_fresh) {
+    const int tb = c->tick(SDNS_PASS_A2A_INV);
+    c->world->stream_barrier(c->stream);
+    c->tock(tb);
+  }
+  c->peer_fresh = c->peer || c->peer_row;
   if (c->peer && !c->pencil) {
     rhs_slab_peer(c, u_in, mode, args_in);
     return;
