@@ -816,9 +816,19 @@ void fft_forward_impl(sdns_ctx* c, const sdns_field* real, sdns_field* spec) {
     for (int f = 0; f < nc; ++f)
       sdns_dev::z_r2c(n, real->real() + f * c->real_cs, c->wb + f * c->spec_cs, c->zmap(true),
                       c->tw, s);
-    sdns_dev::col_plain(n, -1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw,
-                        s);
-    c->exchange(false, nc);
+    if (c->peer) {  // the y pass stores into the owners' x layouts
+      c->world->stream_barrier(s);  // the peers are done with their wa
+      ColGeom go = c->ygeom();
+      go.ps1 = 0;
+      go.seg = c->d_seg + c->peer_n;
+      sdns_dev::col_plain_to(n, -1, c->wb, c->wa, c->spec_cs, c->spec_cs, nc, c->ygeom(), go,
+                             c->tw, s);
+      c->world->stream_barrier(s);
+    } else {
+      sdns_dev::col_plain(n, -1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(),
+                          c->tw, s);
+      c->exchange(false, nc);
+    }
   } else {
     for (int f = 0; f < nc; ++f)
       sdns_dev::z_r2c(n, real->real() + f * c->real_cs, c->wd + f * c->cs_d, c->zmap(true), c->tw,
@@ -838,10 +848,21 @@ void fft_inverse_impl(sdns_ctx* c, const sdns_field* spec, sdns_field* real) {
   const int n = c->cfg.n;
   cudaStream_t s = c->stream;
   const int nc = std::min(real->ncomp, spec->ncomp);
-  sdns_dev::col_plain(n, +1, true, spec->spec(), c->wa, c->spec_cs, c->spec_cs, nc, c->xgeom(),
-                      c->tw, s);
+  if (c->peer && !c->pencil) {  // the x pass stores into the owners' receive layouts
+    c->world->stream_barrier(s);    // the peers are done with their wb
+    ColGeom go = c->xgeom();
+    go.pb_shift = ilog2(c->np);
+    go.ps1 = 0;
+    go.seg = c->d_seg;
+    sdns_dev::col_plain_to(n, +1, spec->spec(), c->wb, c->spec_cs, c->spec_cs, nc, c->xgeom(), go,
+                           c->tw, s, true);
+    c->world->stream_barrier(s);
+  } else {
+    sdns_dev::col_plain(n, +1, true, spec->spec(), c->wa, c->spec_cs, c->spec_cs, nc, c->xgeom(),
+                        c->tw, s);
+  }
   if (!c->pencil) {
-    c->exchange(true, nc);
+    if (!c->peer) c->exchange(true, nc);
     sdns_dev::col_plain(n, +1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, nc, c->ygeom(), c->tw,
                         s);
     for (int f = 0; f < nc; ++f)

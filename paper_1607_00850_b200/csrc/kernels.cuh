@@ -143,10 +143,11 @@ void y_inverse_curl(int n, double2* f, long long cs, const ColGeom& g, const dou
 // (pencil: col-receive layout in, row-send layout out).
 void y_inverse_curl_to(int n, const double2* fin, double2* fout, long long cs_in, long long cs_out,
                        const ColGeom& g, const ColGeom& go, const double2* tw, cudaStream_t s);
-// Plain column transform with a separate output geometry (pencil y passes).
+// Plain column transform with a separate output geometry (pencil y passes;
+// with go.seg, the peer-direct slab transposes -- xaxis picks the x tiles).
 void col_plain_to(int n, int dir, const double2* in, double2* out, long long in_cs,
                   long long out_cs, int nfields, const ColGeom& g, const ColGeom& go,
-                  const double2* tw, cudaStream_t s);
+                  const double2* tw, cudaStream_t s, bool xaxis = false);
 struct SpecGeom;
 // P5b: mask + projection + viscous + RK4 stage update, streaming over the
 // x layout (a.nl holds the x-forward-transformed nonlinear term).

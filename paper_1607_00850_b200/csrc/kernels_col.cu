@@ -766,9 +766,14 @@ static void col_plain_n(int dir, bool xaxis, const double2* in, double2* out, lo
                         long long out_cs, int nfields, const ColGeom& g, const ColGeom* go,
                         const double2* tw, cudaStream_t s) {
   constexpr int VX = N >= 1024 ? 9 : sdns_dev::VX, VY = sdns_dev::VY;
-  if (go && go->seg) {  // peer-direct output (slab y forward into the peers' x layouts)
-    if (dir < 0) plain_launch<N, -1, VY, 2>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
-    else plain_launch<N, +1, VY, 2>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+  if (go && go->seg) {  // peer-direct output (slab transposes fused into the pass)
+    if (xaxis) {
+      if (dir < 0) plain_launch<N, -1, VX, 2>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+      else plain_launch<N, +1, VX, 2>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+    } else {
+      if (dir < 0) plain_launch<N, -1, VY, 2>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+      else plain_launch<N, +1, VY, 2>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+    }
     return;
   }
   if (go) {  // separate output layout (pencil y passes; y-shaped tiles)
@@ -798,10 +803,10 @@ void col_plain(int n, int dir, bool xaxis, const double2* in, double2* out, long
 
 void col_plain_to(int n, int dir, const double2* in, double2* out, long long in_cs,
                   long long out_cs, int nfields, const ColGeom& g, const ColGeom& go,
-                  const double2* tw, cudaStream_t s) {
+                  const double2* tw, cudaStream_t s, bool xaxis) {
   switch (n) {
 #define X(NN) \
-  case NN: col_plain_n<NN>(dir, false, in, out, in_cs, out_cs, nfields, g, &go, tw, s); return;
+  case NN: col_plain_n<NN>(dir, xaxis, in, out, in_cs, out_cs, nfields, g, &go, tw, s); return;
     SDNS_FOR_N(X)
 #undef X
   }
