@@ -145,6 +145,10 @@ int sdns_comm_barrier(sdns_comm* c);                                 /* transpor
 /* In-place reduction in ascending rank order (op 0 sum, 1 max, 2 min). */
 int sdns_comm_allreduce(sdns_comm* c, double* values, int count, int op); /* :61 */
 int sdns_comm_destroy(sdns_comm* c);
+/* InProcessBackend::poison (transport.hpp:125-128): every pending and later
+ * collective of the group fails with SDNS_PROTOCOL_ERROR naming `reason`; a
+ * no-op on transports without shared state (loopback, NCCL, host). */
+int sdns_comm_poison(sdns_comm* c, const char* reason);
 /* split(color, key): members ordered by (key, rank) (transport.hpp:66-67). */
 int sdns_comm_split(sdns_comm* c, int color, int key, sdns_comm** out);
 /* all_to_all_bytes (transport.hpp:55-58, BlockTable :18-35) on DEVICE

@@ -222,6 +222,7 @@ def load_library(path: str = LIB_PATH):
             "sdns_device_layout": (I, [ctypes.POINTER(_Config), I, ctypes.POINTER(_DevLayout)]),
             "sdns_exchange_plan": (I, [ctypes.POINTER(_Config), I, I, I, P, ctypes.POINTER(I)]),
             "sdns_comm_split": (I, [P, I, I, PP]),
+            "sdns_comm_poison": (I, [P, ctypes.c_char_p]),
             "sdns_comm_host_init": (I, [I, I, I, ALLGATHER_FN, GROUP_FN, P, PP]),
             "sdns_ctx_transposes": (I, [P]),
             "sdns_comm_all_to_all_bytes": (I, [P, P, P, P, P, P]),
@@ -502,6 +503,26 @@ class Comm:
         _check(self._lib.sdns_comm_allreduce(self._h, _ptr(v), v.size,
                                              {"sum": 0, "max": 1, "min": 2}[op]))
         return v
+
+    def split(self, color: int, key: int) -> "Comm":
+        """split, transport.hpp:66-67: members ordered by (key, rank)."""
+        h = ctypes.c_void_p()
+        _check(self._lib.sdns_comm_split(self._h, color, key, ctypes.byref(h)))
+        return Comm(h)
+
+    def poison(self, reason: str):
+        """InProcessBackend::poison, transport.hpp:125-128."""
+        _check(self._lib.sdns_comm_poison(self._h, reason.encode()))
+
+    def all_to_all_bytes(self, send_ptr: int, send_bytes, recv_ptr: int, recv_bytes,
+                         stream: int = 0):
+        """all_to_all_bytes (transport.hpp:55-58) on DEVICE buffers; block q
+        of send goes to peer q (displacements = prefix sums of the counts)."""
+        sb = np.ascontiguousarray(send_bytes, dtype=np.int64)
+        rb = np.ascontiguousarray(recv_bytes, dtype=np.int64)
+        _check(self._lib.sdns_comm_all_to_all_bytes(self._h, ctypes.c_void_p(send_ptr), _ptr(sb),
+                                                    ctypes.c_void_p(recv_ptr), _ptr(rb),
+                                                    ctypes.c_void_p(stream) if stream else None))
 
     def close(self):
         if self._h:

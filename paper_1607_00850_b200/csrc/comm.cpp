@@ -79,6 +79,10 @@ struct Board {
   std::vector<std::vector<Xfer>> posted;
   std::vector<std::vector<double>> values;
   std::vector<void*> ptrs;
+  // collective kind each rank entered (transport.cpp: mismatched collectives
+  // raise ProtocolError on every rank); the verdict of the last rendezvous
+  std::vector<int> op;
+  std::string mismatch;
   std::vector<cudaEvent_t> ready, done;
   std::vector<std::pair<int, int>> split_req;
   std::map<std::pair<long long, int>, std::shared_ptr<Board>> children;
@@ -87,6 +91,7 @@ struct Board {
     posted.resize(n);
     values.resize(n);
     ptrs.resize(n);
+    op.assign(static_cast<size_t>(n), 0);
     split_req.resize(n);
     int prev = 0;
     cudaGetDevice(&prev);
@@ -119,11 +124,37 @@ struct Board {
     for (auto& k : kids) k->poison_all(why);
   }
 
+  // Rendezvous opening collective `kind` (1 all_to_all, 2 allreduce, 3
+  // barrier, 4 split, 5 map_peers, 6 stream_barrier): every rank must have
+  // entered the same kind, else all of them raise ProtocolError and the
+  // group is poisoned.
+  void enter(std::unique_lock<std::mutex>& lk, int rank, int kind) {
+    op[static_cast<size_t>(rank)] = kind;
+    wait_all(lk);
+    if (!mismatch.empty()) {
+      const std::string m = mismatch;
+      poisoned = true;
+      if (reason.empty()) reason = m;
+      cv.notify_all();
+      protocol_error(m);
+    }
+  }
+
   // Generation-counted barrier; throws on poison or timeout.
   void wait_all(std::unique_lock<std::mutex>& lk) {
     if (poisoned) protocol_error("group poisoned: " + reason);
     const long long my = gen;
     if (++arrived == size) {
+      // the last rank in judges the generation (read by every waiter before
+      // any rank can complete another one)
+      mismatch.clear();
+      for (int q = 1; q < size; ++q)
+        if (op[static_cast<size_t>(q)] != op[0]) {
+          mismatch = "mismatched collectives: rank 0 entered kind " + std::to_string(op[0]) +
+                     ", rank " + std::to_string(q) + " kind " +
+                     std::to_string(op[static_cast<size_t>(q)]);
+          break;
+        }
       arrived = 0;
       ++gen;
       cv.notify_all();
@@ -158,9 +189,31 @@ class InProcessComm final : public Comm {
     {
       std::unique_lock<std::mutex> lk(b.mu);
       b.posted[rank_] = xs;
+      b.enter(lk, rank_, 1);
+    }
+    try {
+      validate_and_copy(xs, s);
+    } catch (const Error& e) {
+      b.poison_all(e.what());  // the peers fail fast instead of timing out
+      throw;
+    }
+    SDNS_CUDA(cudaEventRecord(b.done[rank_], s));
+    {
+      std::unique_lock<std::mutex> lk(b.mu);
       b.wait_all(lk);
     }
-    // Validate tables and copy every block destined to me from its sender.
+    // My send buffers may be reused only after every peer copied from them.
+    for (int q = 0; q < size_; ++q)
+      if (q != rank_) SDNS_CUDA(cudaStreamWaitEvent(s, b.done[q], 0));
+    {
+      std::unique_lock<std::mutex> lk(b.mu);
+      b.wait_all(lk);
+    }
+  }
+
+  // Validate tables and copy every block destined to me from its sender.
+  void validate_and_copy(const std::vector<Xfer>& xs, cudaStream_t s) {
+    Board& b = *b_;
     std::vector<int> waited(size_, 0);
     std::vector<int> nth_from(size_, 0);
     for (const Xfer& x : xs) {
@@ -187,25 +240,13 @@ class InProcessComm final : public Comm {
       if (x.recv_bytes && match->send != x.recv)
         SDNS_CUDA(cudaMemcpyAsync(x.recv, match->send, x.recv_bytes, cudaMemcpyDeviceToDevice, s));
     }
-    SDNS_CUDA(cudaEventRecord(b.done[rank_], s));
-    {
-      std::unique_lock<std::mutex> lk(b.mu);
-      b.wait_all(lk);
-    }
-    // My send buffers may be reused only after every peer copied from them.
-    for (int q = 0; q < size_; ++q)
-      if (q != rank_) SDNS_CUDA(cudaStreamWaitEvent(s, b.done[q], 0));
-    {
-      std::unique_lock<std::mutex> lk(b.mu);
-      b.wait_all(lk);
-    }
   }
 
   void allreduce(double* v, int n, int op) override {
     Board& b = *b_;
     std::unique_lock<std::mutex> lk(b.mu);
     b.values[rank_].assign(v, v + n);
-    b.wait_all(lk);
+    b.enter(lk, rank_, 2);
     for (int q = 0; q < size_; ++q)
       if (static_cast<int>(b.values[q].size()) != n)
         protocol_error("allreduce: mismatched lengths across ranks");
@@ -217,7 +258,7 @@ class InProcessComm final : public Comm {
 
   void barrier() override {
     std::unique_lock<std::mutex> lk(b_->mu);
-    b_->wait_all(lk);
+    b_->enter(lk, rank_, 3);
   }
 
   // Ranks share the device: a peer's buffer is addressed directly.
@@ -225,7 +266,7 @@ class InProcessComm final : public Comm {
     Board& b = *b_;
     std::unique_lock<std::mutex> lk(b.mu);
     b.ptrs[rank_] = mine;
-    b.wait_all(lk);
+    b.enter(lk, rank_, 5);
     std::vector<void*> all = b.ptrs;
     b.wait_all(lk);
     return all;
@@ -238,7 +279,7 @@ class InProcessComm final : public Comm {
     Board& b = *b_;
     SDNS_CUDA(cudaEventRecord(b.ready[rank_], s));
     std::unique_lock<std::mutex> lk(b.mu);
-    b.wait_all(lk);
+    b.enter(lk, rank_, 6);
     for (int q = 0; q < size_; ++q)
       if (q != rank_) SDNS_CUDA(cudaStreamWaitEvent(s, b.ready[q], 0));
     b.wait_all(lk);
@@ -249,7 +290,7 @@ class InProcessComm final : public Comm {
     std::unique_lock<std::mutex> lk(b.mu);
     b.split_req[rank_] = {color, key};
     const long long g = b.gen;
-    b.wait_all(lk);
+    b.enter(lk, rank_, 4);
     std::vector<std::pair<int, int>> members;  // (key, rank)
     for (int q = 0; q < size_; ++q)
       if (b.split_req[q].first == color) members.push_back({b.split_req[q].second, q});

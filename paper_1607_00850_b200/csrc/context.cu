@@ -1287,6 +1287,9 @@ int sdns_comm_allreduce(sdns_comm* c, double* v, int n, int op) {
 int sdns_comm_destroy(sdns_comm* c) {
   return guarded([&] { delete c; });
 }
+int sdns_comm_poison(sdns_comm* c, const char* reason) {
+  return guarded([&] { c->c->poison(reason ? reason : "poisoned"); });
+}
 int sdns_comm_split(sdns_comm* c, int color, int key, sdns_comm** out) {
   return guarded([&] { *out = new sdns_comm{c->c->split(color, key)}; });
 }

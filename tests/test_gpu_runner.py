@@ -188,3 +188,20 @@ def test_run_rank_matches_run(tmp_path):
     assert a == b
     assert (tmp_path / "run" / "checkpoint.sdns").read_bytes() == \
         (tmp_path / "rank" / "checkpoint.sdns").read_bytes()
+
+
+def test_run_reruns_byte_identical_and_decomposition_invariant(tmp_path):
+    """test_app.cpp pins: a rerun writes byte-identical diagnostics and
+    checkpoint; p = 2 agrees with p = 1 to <= 1e-13."""
+    cfg = S.SolverConfig(n=32, t_end=0.03, out_every=3)
+    for d in ("a", "b"):
+        S.run(cfg, S.RunOptions(out_dir=str(tmp_path / d)))
+    for f in ("diagnostics.csv", "checkpoint.sdns"):
+        assert (tmp_path / "a" / f).read_bytes() == (tmp_path / "b" / f).read_bytes()
+    S.run(S.SolverConfig(n=32, p=2, t_end=0.03, out_every=3), S.RunOptions(out_dir=str(tmp_path / "p2")))
+    _, a = read_csv(tmp_path / "a" / "diagnostics.csv")
+    _, b = read_csv(tmp_path / "p2" / "diagnostics.csv")
+    np.testing.assert_allclose(b[:, 2:5], a[:, 2:5], rtol=1e-13, atol=0)
+    _, u1 = read_checkpoint(tmp_path / "a" / "checkpoint.sdns")
+    _, u2 = read_checkpoint(tmp_path / "p2" / "checkpoint.sdns")
+    assert np.max(np.abs(u1 - u2)) <= 1e-13 * np.max(np.abs(u1))
