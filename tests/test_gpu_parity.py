@@ -357,6 +357,79 @@ def test_divergence_error_on_nonfinite():
         st.close()
 
 
+@pytest.mark.parametrize("geom", [dict(p=2), dict(decomp="pencil", p=4, p1=2, p2=2)])
+def test_divergence_detection_is_collective(geom):
+    """test_rk4.cpp:164-189: one rank goes non-finite, every rank raises
+    DivergenceError at the same step."""
+    n = 16
+    cfg = S.SolverConfig(n=n, nu=0.01, dt=0.01, t_end=0.05, **geom)
+    uh0 = S.iso_init(n, S.build_layout(S.SolverConfig(n=n), 0), seed=5)
+
+    def body(rank, comm):
+        with S.Context(cfg, rank=rank, comm=comm) as c:
+            uh = _scatter_spec(uh0, c.layout).copy()
+            if rank == 0:
+                uh[1, 0, 0, 1] = np.inf
+            st = S.Rk4State(c)
+            st.set(c.spectral_field().upload(uh))
+            try:
+                st.advance()
+            except S.DivergenceError as e:
+                return e.step
+            finally:
+                st.close()
+            return None
+
+    assert S.run_group(cfg.p, body) == [1] * cfg.p
+
+
+@pytest.mark.parametrize("geom", [dict(), dict(p=4), dict(decomp="pencil", p=4, p1=2, p2=2)])
+def test_vector_transforms_equal_component_calls(geom):
+    """test_fft.cpp:129-156: the 3-component forward equals three
+    single-component calls bit for bit; the round trip is <= 1e-13."""
+    n = 16
+    cfg = S.SolverConfig(n=n, **geom)
+    u0 = np.random.default_rng(900).uniform(-1, 1, (3, n, n, n))
+
+    def body(rank, comm):
+        with S.Context(cfg, rank=rank, comm=comm) as c:
+            fft = S.DistributedFFT(c)
+            u = c.real_field().upload(_scatter_real(u0, c.layout))
+            fu = c.spectral_field()
+            fft.forward(u, fu)
+            whole = fu.download()
+            ok = True
+            for comp in range(3):
+                one_r = c.real_field(1).upload(_scatter_real(u0, c.layout)[comp:comp + 1])
+                one = c.spectral_field(1)
+                fft.forward(one_r, one)
+                ok &= np.array_equal(one.download()[0], whole[comp])
+            back = c.real_field()
+            fft.inverse(fu, back)
+            err = np.max(np.abs(back.download() - _scatter_real(u0, c.layout)))
+            return ok, err
+
+    for ok, err in S.run_group(cfg.p, body):
+        assert ok and err <= 1e-13
+
+
+def test_l2_diff_and_shells_of_taylor_green():
+    """test_diagnostics.cpp:80-145: TG energy lies in shell 2 and the shells
+    sum to E; l2_diff(u, 0) = sqrt(2E) = 0.5, l2_diff(u, u) = 0."""
+    n = 16
+    with S.Context(S.SolverConfig(n=n)) as c:
+        u = c.real_field().upload(O.taylor_green_reference(n))
+        uh = c.spectral_field()
+        S.DistributedFFT(c).forward(u, uh)
+        st = S.collect_stats(c, uh, 0.0)
+        assert abs(st.energy - 0.125) <= 1e-13
+        assert abs(st.spectrum[2] - st.energy) <= 1e-13
+        assert abs(st.spectrum.sum() - st.energy) <= 1e-13
+        zero = c.real_field().upload(np.zeros((3, n, n, n)))
+        assert abs(S.l2_diff(c, u, zero) - 0.5) <= 0.5e-13
+        assert S.l2_diff(c, u, u) == 0.0
+
+
 def test_config_errors():
     with pytest.raises(S.ConfigError):
         S.Context(S.SolverConfig(n=12))  # not a power of two on the GPU path
