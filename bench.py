@@ -329,26 +329,30 @@ def run_ours(args):
 
     peak, peak_kind = peaks()
     C = spectral_bytes(n, world)
+    ncu_bytes = {}
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if world == 1 and os.path.exists(tfile):
+        try:
+            with open(tfile) as f:
+                ncu_bytes = json.load(f).get(str(n), {})
+        except Exception:  # noqa: BLE001
+            ncu_bytes = {}
     per_pass = {k: {"avg_ms": v[0] / v[1], "launches": v[1], "share": None}
                 for k, v in passes.items() if v[1] > 0}
     kernel_total = sum(v[0] for k, v in passes.items() if not k.startswith("a2a"))
     for k, v in passes.items():
         if v[1] > 0:
             per_pass[k]["share"] = v[0] / max(kernel_total, 1e-30) if not k.startswith("a2a") else None
+            if k in ncu_bytes:  # DRAM bytes per launch (ncu) / live launch time
+                gbs = ncu_bytes[k] / (v[0] / v[1] * 1e-3) / 1e9
+                per_pass[k]["dram_gbs"] = gbs
+                per_pass[k]["dram_frac"] = gbs / peak
     launches = sum(v[1] for k, v in passes.items() if not k.startswith("a2a"))
     dom = max((k for k in per_pass if k in PASS_BYTES_C), key=lambda k: passes[k][0])
     dom_ms = per_pass[dom]["avg_ms"]
     dom_bytes = PASS_BYTES_C[dom] * C
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tfile):
-        try:
-            with open(tfile) as f:
-                tr = json.load(f).get(str(n), {})
-            traffic = tr.get(dom)
-        except Exception:  # noqa: BLE001
-            traffic = None
+    traffic = ncu_bytes.get(dom)
     step_bytes = STEP_BYTES_C * C
     step_gbs = step_bytes / (ms * 1e-3) / 1e9
     value = 1e3 / ms  # steps/s of the whole job (strong scaling: one problem on N GPUs)

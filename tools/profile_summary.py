@@ -90,6 +90,8 @@ def main():
     traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     tr = traffic.setdefault(str(n), {})
+    acc = {}  # pass -> [bytes per launch, ...]
+    plain_order = ["y_fwd", "x_fwd_fft"]  # the step's k_pipe_plain launches, in capture order
     for d in res:
         name = d["Kernel Name"][0]
         rd = to_bytes(*d["dram__bytes_read.sum"])
@@ -105,7 +107,11 @@ def main():
                      f"{g('l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum')} |")
         for key, pname in PASS_OF:
             if key in name.replace("(int)", ""):
-                tr[pname] = rd + wr
+                acc.setdefault(pname, []).append(rd + wr)
+        if "k_pipe_plain" in name and plain_order:
+            acc.setdefault(plain_order.pop(0), []).append(rd + wr)
+    for pname, v in acc.items():
+        tr[pname] = sum(v) / len(v)
     open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full_{n}.md"), "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(traffic_path, "w"), indent=1, sort_keys=True)
     print("\n".join(lines))
