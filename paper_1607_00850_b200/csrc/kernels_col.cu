@@ -57,6 +57,9 @@ namespace {
 #ifndef SDNS_COLTMA
 #define SDNS_COLTMA 1
 #endif
+#ifndef SDNS_L2PF  // TMA-fed rings: items prefetched into L2 beyond the ring (A/B only:
+#define SDNS_L2PF 0  // measured slower -- P5a 0.49 -> 0.62 ms, n = 1024 P1 33 -> 43 ms)
+#endif
 #ifndef SDNS_NB0
 #define SDNS_NB0 3
 #endif
@@ -277,6 +280,25 @@ __device__ __forceinline__ void tma_tile(double2* buf, const CUtensorMap* tm, co
     tma_load5(buf + h * BP * CS, tm, 2 * (tl.kz & 7), tl.kz >> 3, tl.row, h * BP, field, bar);
 }
 
+// L2 prefetch of a tile's boxes (no shared memory, no completion): keeps
+// more of the strided tile rows in flight than the ring alone holds.
+__device__ __forceinline__ void tma_prefetch5(const CUtensorMap* tm, int c0, int c1, int c2,
+                                              int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(tm),
+      "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
+template <int N, int CS>
+__device__ __forceinline__ void tma_prefetch_tile(const CUtensorMap* tm, const Tile& tl,
+                                                  int field) {
+  constexpr int BP = N < 256 ? N : 256;
+#pragma unroll
+  for (int h = 0; h < N / BP; ++h)
+    tma_prefetch5(tm, 2 * (tl.kz & 7), tl.kz >> 3, tl.row, h * BP, field);
+}
+
 // Tile stores by the tensor-memory accelerator from a dedicated staging
 // buffer (V = 10): the transformed tile is written there in the tile layout
 // and thread 0 issues two box stores that drain while the CTA transforms the
@@ -346,6 +368,10 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
     } else {
       issue_tile<N>(ring(slot), src(f), tl, po, ln.idx, t);
     }
+  };
+  // L2 prefetch of an item beyond the ring (TMA-fed rings only)
+  auto prefetch = [&](int f, const Tile& tl) {
+    if (SDNS_L2PF && tma && threadIdx.x == 0) tma_prefetch_tile<N, CS>(tm, tl, fld(f));
   };
   // A slot is refilled only after the barrier that ends its last transform
   // (block_fft's trailing barrier follows its last shared-memory access; the
@@ -449,6 +475,10 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
       const Item n2 = adv(n1);
       const Tile tn2 = tile_at(n2);
       if (n2.t0 < ntiles) issue((i + 2) % 3, n2.f, tn2);
+      if constexpr (SDNS_L2PF > 0) {
+        const Item n3 = adv(n2);
+        if (n3.t0 < ntiles) prefetch(n3.f, tile_at(n3));
+      }
       if (tma) {
         mbar_wait(&tbar[i % 3], (i / 3) & 1);
       } else {
@@ -463,6 +493,11 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
       tn1 = tn2;
     } else {
       if (n1.t0 < ntiles) issue((i + 1) & 1, n1.f, tn1);
+      if constexpr (SDNS_L2PF > 0) {
+        Item nx = adv(n1);
+        for (int d = 1; d < SDNS_L2PF; ++d) nx = adv(nx);
+        if (nx.t0 < ntiles) prefetch(nx.f, tile_at(nx));
+      }
       if (tma) {
         mbar_wait(&tbar[i & 1], (i >> 1) & 1);
       } else {

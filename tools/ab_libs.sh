@@ -7,6 +7,6 @@ show() { python3 -c "import json,sys; d=json.loads(sys.stdin.read().strip().spli
 for v in default "$@"; do
   if [ $v = default ]; then unset SDNS_LIB; else export SDNS_LIB=$PWD/libsdns_$v.so; fi
   for rep in 1 2; do
-    timeout 300 python bench.py --steps 5 --warmup 3 --e2e-steps 1 --no-cpu-baseline 2>/dev/null | show $v
+    timeout 300 python bench.py --steps 5 --warmup 3 --e2e-steps 1 --no-cpu-baseline --no-other-configs 2>/dev/null | show $v
   done
 done

@@ -11,5 +11,5 @@ F="$A -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $*"
 for f in kernels kernels_col context; do nvcc $F -c $f.cu -o $b/$f.o & done
 wait
 nvcc $A -shared -cudart static -o ../../libsdns_$name.so $b/kernels.o $b/kernels_col.o $b/context.o \
-  build/comm.o build/layout.o build/iso_init.o -ldl -lpthread
+  build/comm.o build/layout.o build/iso_init.o build/runner.o build/acceptance.o -ldl -lpthread
 rm -rf $b
