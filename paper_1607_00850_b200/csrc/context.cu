@@ -830,14 +830,30 @@ void fft_forward_impl(sdns_ctx* c, const sdns_field* real, sdns_field* spec) {
       c->exchange(false, nc);
     }
   } else {
-    for (int f = 0; f < nc; ++f)
-      sdns_dev::z_r2c(n, real->real() + f * c->real_cs, c->wd + f * c->cs_d, c->zmap(true), c->tw,
-                      s);
-    c->exchange_row(false, nc);
+    if (c->peer_row) {  // z r2c stores each kz segment into its owner's wc
+      c->row->stream_barrier(s);  // the row peers are done with their wc
+      for (int f = 0; f < nc; ++f)
+        sdns_dev::z_r2c_to(n, real->real() + f * c->real_cs, c->wc, c->zmap(true), c->zmo_row, f,
+                           c->tw, s);
+      c->row->stream_barrier(s);
+    } else {
+      for (int f = 0; f < nc; ++f)
+        sdns_dev::z_r2c(n, real->real() + f * c->real_cs, c->wd + f * c->cs_d, c->zmap(true),
+                        c->tw, s);
+      c->exchange_row(false, nc);
+    }
     ColGeom gi, go;
     pencil_yfwd_geoms(c, false, gi, go);
-    sdns_dev::col_plain_to(n, -1, c->wc, c->wb, c->cs_c, c->spec_cs, nc, gi, go, c->tw, s);
-    c->exchange_col(false, nc);
+    if (c->peer) {  // the y pass stores into the column owners' x layouts
+      c->col->stream_barrier(s);
+      go.ps1 = 0;
+      go.seg = c->d_seg + c->peer_n;
+      sdns_dev::col_plain_to(n, -1, c->wc, c->wa, c->cs_c, c->spec_cs, nc, gi, go, c->tw, s);
+      c->col->stream_barrier(s);
+    } else {
+      sdns_dev::col_plain_to(n, -1, c->wc, c->wb, c->cs_c, c->spec_cs, nc, gi, go, c->tw, s);
+      c->exchange_col(false, nc);
+    }
   }
   sdns_dev::col_plain(n, -1, true, c->wa, spec->spec(), c->spec_cs, c->spec_cs, nc, c->xgeom(),
                       c->tw, s);
@@ -848,15 +864,15 @@ void fft_inverse_impl(sdns_ctx* c, const sdns_field* spec, sdns_field* real) {
   const int n = c->cfg.n;
   cudaStream_t s = c->stream;
   const int nc = std::min(real->ncomp, spec->ncomp);
-  if (c->peer && !c->pencil) {  // the x pass stores into the owners' receive layouts
-    c->world->stream_barrier(s);    // the peers are done with their wb
+  if (c->peer) {  // the x pass stores into the (column) owners' receive layouts
+    c->peer_grp->stream_barrier(s);  // the peers are done with their wb
     ColGeom go = c->xgeom();
     go.pb_shift = ilog2(c->np);
     go.ps1 = 0;
     go.seg = c->d_seg;
     sdns_dev::col_plain_to(n, +1, spec->spec(), c->wb, c->spec_cs, c->spec_cs, nc, c->xgeom(), go,
                            c->tw, s, true);
-    c->world->stream_barrier(s);
+    c->peer_grp->stream_barrier(s);
   } else {
     sdns_dev::col_plain(n, +1, true, spec->spec(), c->wa, c->spec_cs, c->spec_cs, nc, c->xgeom(),
                         c->tw, s);
@@ -869,10 +885,20 @@ void fft_inverse_impl(sdns_ctx* c, const sdns_field* spec, sdns_field* real) {
       sdns_dev::z_c2r(n, c->wb + f * c->spec_cs, real->real() + f * c->real_cs, c->zmap(true),
                       c->norm, c->tw, s);
   } else {
-    c->exchange_col(true, nc);
-    sdns_dev::col_plain_to(n, +1, c->wb, c->wc, c->spec_cs, c->cs_c, nc, c->ygeom(),
-                           c->ygeom_row(), c->tw, s);
-    c->exchange_row(true, nc);
+    if (!c->peer) c->exchange_col(true, nc);
+    if (c->peer_row) {  // the y pass stores its y blocks into the row owners' z lines
+      c->row->stream_barrier(s);  // the row peers are done with their wd
+      ColGeom go = c->ygeom_row();
+      go.ps1 = 0;
+      go.seg = c->d_seg_row;
+      sdns_dev::col_plain_to(n, +1, c->wb, c->wd, c->spec_cs, c->cs_d, nc, c->ygeom(), go, c->tw,
+                             s);
+      c->row->stream_barrier(s);
+    } else {
+      sdns_dev::col_plain_to(n, +1, c->wb, c->wc, c->spec_cs, c->cs_c, nc, c->ygeom(),
+                             c->ygeom_row(), c->tw, s);
+      c->exchange_row(true, nc);
+    }
     for (int f = 0; f < nc; ++f)
       sdns_dev::z_c2r(n, c->wd + f * c->cs_d, real->real() + f * c->real_cs, c->zmap(true),
                       c->norm, c->tw, s);

@@ -575,10 +575,10 @@ k_z_c2r(const double2* __restrict__ spec, double* __restrict__ real, RowMap rm, 
 
 // Standalone r2c along z (DistributedFFT::forward head, fft.cpp:87): two real
 // rows in one complex FFT, split by the mirror relation.
-template <int N>
+template <int N, bool PO = false>
 __global__ void __launch_bounds__(ZCfg<N>::THREADS)
 k_z_r2c(const double* __restrict__ real, double2* __restrict__ spec, RowMap rm,
-        const double2* __restrict__ tw) {
+        const double2* __restrict__ tw, RowMap rmo = RowMap{}, int field = 0) {
   constexpr int E = ZCfg<N>::E, TPC = ZCfg<N>::TPC, RPC = ZCfg<N>::RPC;
   constexpr bool REG = N == 512;
   using Bar = typename std::conditional<(TPC >= 64), NamedBar, CtaBar>::type;
@@ -636,12 +636,19 @@ k_z_r2c(const double* __restrict__ real, double2* __restrict__ spec, RowMap rm,
       if (k <= N / 2) {
         const double2 d = reg[sw(k)];
         const double2 e = cconj(reg[sw((N - k) & (N - 1))]);
-        spec[zel(rm, ra, ri, k)] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
         const double2 dd = csub(d, e);
-        spec[zel(rm, rb, ri + 1, k)] = make_double2(0.5 * dd.y, -0.5 * dd.x);
+        if constexpr (PO) {  // peer-direct: kz segment -> its owner's y-pass layout
+          const ZDst za = zdst(rmo, ri, k), zb = zdst(rmo, ri + 1, k);
+          spec[za.el + field * za.cs] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
+          spec[zb.el + field * zb.cs] = make_double2(0.5 * dd.y, -0.5 * dd.x);
+        } else {
+          spec[zel(rm, ra, ri, k)] = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
+          spec[zel(rm, rb, ri + 1, k)] = make_double2(0.5 * dd.y, -0.5 * dd.x);
+        }
       }
     }
   }
+  if constexpr (PO) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -1143,6 +1150,27 @@ static void z_r2c_n(const double* real, double2* spec, const RowMap& rm, const d
   const size_t shm = sizeof(double2) * (N * C::RPC + N);
   SDNS_SET_SMEM((k_z_r2c<N>), shm);
   k_z_r2c<N><<<grid, C::THREADS, shm, s>>>(real, spec, rm, tw);
+}
+
+template <int N>
+static void z_r2c_to_n(const double* real, double2* out, const RowMap& rm, const RowMap& rmo,
+                       int field, const double2* tw, cudaStream_t s) {
+  using C = ZCfg<N>;
+  const int pairs = rm.nrows / 2;
+  const unsigned grid = static_cast<unsigned>((pairs + C::RPC - 1) / C::RPC);
+  const size_t shm = sizeof(double2) * (N * C::RPC + N);
+  SDNS_SET_SMEM((k_z_r2c<N, true>), shm);
+  k_z_r2c<N, true><<<grid, C::THREADS, shm, s>>>(real, out, rm, tw, rmo, field);
+}
+
+void z_r2c_to(int n, const double* real, double2* out, const RowMap& rm, const RowMap& rmo,
+              int field, const double2* tw, cudaStream_t s) {
+  switch (n) {
+#define X(NN) \
+  case NN: z_r2c_to_n<NN>(real, out, rm, rmo, field, tw, s); return;
+    SDNS_FOR_N(X)
+#undef X
+  }
 }
 
 void z_r2c(int n, const double* real, double2* spec, const RowMap& rm, const double2* tw,

@@ -167,6 +167,10 @@ void z_c2r(int n, const double2* spec, double* real, const RowMap& rm, double no
            const double2* tw, cudaStream_t s);
 void z_r2c(int n, const double* real, double2* spec, const RowMap& rm, const double2* tw,
            cudaStream_t s);
+// Same, storing component `field` through the segmented output map `rmo`
+// (see z_fused_to): the pencil forward row transpose fused into the z pass.
+void z_r2c_to(int n, const double* real, double2* out, const RowMap& rm, const RowMap& rmo,
+              int field, const double2* tw, cudaStream_t s);
 
 // Spectral-layout geometry for pointwise kernels.
 struct SpecGeom {

@@ -47,8 +47,14 @@ def main():
         uo = c.spectral_field()
         st.get(uo)
         stats = S.collect_stats(c, uo, 1e-3)
+        fft = S.DistributedFFT(c)  # the API transforms fuse their transposes too
+        ur = c.real_field()
+        fft.inverse(uo, ur)
+        fu = c.spectral_field()
+        fft.forward(ur, fu)
         np.savez(os.path.join(out, f"r{rank}.npz"), du=du.download(), u=uo.download(),
-                 e=stats.energy, z=stats.enstrophy, transposes=c.transposes)
+                 ur=ur.download(), fu=fu.download(), e=stats.energy, z=stats.enstrophy,
+                 transposes=c.transposes)
         st.close()
     comm.close()
     dist.barrier()

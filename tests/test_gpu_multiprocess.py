@@ -67,7 +67,13 @@ def test_multiprocess_peer_direct_bitwise(tmp_path, world, grid):
             uo = c.spectral_field()
             st.get(uo)
             stats = S.collect_stats(c, uo, 1e-3)
-            res = (du.download(), uo.download(), stats.energy, stats.enstrophy)
+            fft = S.DistributedFFT(c)
+            ur = c.real_field()
+            fft.inverse(uo, ur)
+            fu = c.spectral_field()
+            fft.forward(ur, fu)
+            res = (du.download(), uo.download(), stats.energy, stats.enstrophy, ur.download(),
+                   fu.download())
             st.close()
             return res
 
@@ -78,3 +84,4 @@ def test_multiprocess_peer_direct_bitwise(tmp_path, world, grid):
         assert np.array_equal(d["du"], ref[r][0])
         assert np.array_equal(d["u"], ref[r][1])
         assert float(d["e"]) == ref[r][2] and float(d["z"]) == ref[r][3]
+        assert np.array_equal(d["ur"], ref[r][4]) and np.array_equal(d["fu"], ref[r][5])
