@@ -97,6 +97,26 @@ std::vector<std::shared_ptr<Comm>> make_inprocess_group(int size, int device, do
 void nccl_unique_id(unsigned char id[128]);
 std::shared_ptr<Comm> make_nccl_comm(const unsigned char id[128], int size, int rank, int device);
 
+// Owners of C ABI handles for host code above the ABI (runner, acceptance).
+struct Ctx {
+  sdns_ctx* c = nullptr;
+  ~Ctx() {
+    if (c) sdns_ctx_destroy(c);
+  }
+};
+struct Fld {
+  sdns_field* f = nullptr;
+  ~Fld() {
+    if (f) sdns_field_free(f);
+  }
+};
+struct State {
+  sdns_state* s = nullptr;
+  ~State() {
+    if (s) sdns_state_destroy(s);
+  }
+};
+
 // runner.cpp: a failed C ABI call becomes the exception it reported; the
 // Taylor-Green real block of a rank; a case's initial spectral state.
 void ck(int rc);

@@ -311,26 +311,6 @@ void write_bench_csv(const std::string& path, const sdns_bench_row* rows, int co
   if (!out) io_error("short write to '" + path + "'");
 }
 
-// ---- per-rank resources ------------------------------------------------------
-
-struct Ctx {
-  sdns_ctx* c = nullptr;
-  ~Ctx() {
-    if (c) sdns_ctx_destroy(c);
-  }
-};
-struct Fld {
-  sdns_field* f = nullptr;
-  ~Fld() {
-    if (f) sdns_field_free(f);
-  }
-};
-struct State {
-  sdns_state* s = nullptr;
-  ~State() {
-    if (s) sdns_state_destroy(s);
-  }
-};
 
 }  // namespace
 
