@@ -246,16 +246,33 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
+    # --transport host (a harness check, not a bench): ranks share the GPUs
+    # present round-robin over the host-callback transport (gloo all-gathers,
+    # CUDA IPC), e.g. 2 ranks on one GPU
+    device = local if args.transport == "nccl" else local % torch.cuda.device_count()
+    torch.cuda.set_device(device)
     dist = None
+    red_dev = "cuda"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        uid = [S.Comm.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = S.Comm.nccl(uid[0], world, rank, local)
+        if args.transport == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+            uid = [S.Comm.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            comm = S.Comm.nccl(uid[0], world, rank, device)
+        else:
+            dist.init_process_group("gloo")
+            red_dev = "cpu"
+
+            def allgather(data, group):
+                t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+                parts = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+                dist.all_gather(parts, t, group=group)
+                return [x.numpy().tobytes() for x in parts]
+            comm = S.Comm.host(world, rank, device, allgather, new_group=dist.new_group)
     else:
         comm = S.Comm.loopback()
+    local = device
 
     n, nu, dt = args.n, 5e-4, 5e-4
     cfg = S.SolverConfig(n=n, p=world, nu=nu, dt=dt, t_end=args.steps * dt)
@@ -295,7 +312,7 @@ def run_ours(args):
     finite = state.rk4_step(dt, post_project=True, check=True)
     stats = S.collect_stats(ctx, state.u_hat, nu)
     if dist is not None:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
@@ -315,7 +332,7 @@ def run_ours(args):
     barrier()
     e2e_s = (time.perf_counter() - te) / e2e_steps
     if dist is not None:
-        t = torch.tensor([e2e_s], device="cuda")
+        t = torch.tensor([e2e_s], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     S.load_library().sdns_host_free(pinned)
@@ -363,7 +380,7 @@ def run_ours(args):
         "data": "synthetic (seeded isotropic field, BASELINE configs[2] construction)",
         "config": {"workload": f"configs[2]: isotropic {n}^3 fp64, nu=5e-4, dt=5e-4, slab x {world}",
                    "n": n, "decomp": "slab", "p": world, "global_points": n**3,
-                   "transposes": transposes,
+                   "transposes": transposes, "transport": args.transport if world > 1 else "loopback",
                    "l2": "inputs larger than L2 (u_hat alone is %.1f GB per rank)" % (3 * C / 1e9)},
         "ns_per_gridpoint_step": ms * 1e6 / n**3,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -416,6 +433,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                    help="N > 1: NCCL (one GPU per rank) or the host-callback transport "
+                         "(harness check; ranks may share a GPU)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
