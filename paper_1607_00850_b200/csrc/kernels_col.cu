@@ -57,6 +57,9 @@ namespace {
 #ifndef SDNS_COLTMA
 #define SDNS_COLTMA 1
 #endif
+#ifndef SDNS_FDIV  // tile index -> (row, kz) by float reciprocal instead of integer division
+#define SDNS_FDIV 1
+#endif
 #ifndef SDNS_L2PF  // TMA-fed rings: items prefetched into L2 beyond the ring (A/B only:
 #define SDNS_L2PF 0  // measured slower -- P5a 0.49 -> 0.62 ms, n = 1024 P1 33 -> 43 ms)
 #endif
@@ -122,8 +125,23 @@ struct CIdx {
 template <int CS>
 __device__ __forceinline__ Tile tile_of(int tile, int col, const ColGeom& g) {
   const int gc = tile * CS + col;
+#if SDNS_FDIV
+  // gc / pitch through a float reciprocal and one correction step (exact
+  // for gc < 2^24, far above any tile count here): the 32-bit integer
+  // division sequence showed up in the column passes' stall samples
+  int re = __float2int_rz(__int2float_rn(gc) * __frcp_rn(__int2float_rn(g.pitch)));
+  int kz = gc - re * g.pitch;
+  if (kz < 0) {
+    --re;
+    kz += g.pitch;
+  } else if (kz >= g.pitch) {
+    ++re;
+    kz -= g.pitch;
+  }
+#else
   const int re = gc / g.pitch;
   const int kz = gc - re * g.pitch;
+#endif
   const int row = re < g.seg_a ? re + g.off0 : re - g.seg_a + g.off1;
   Tile t;
   t.valid = re < g.nrows && kz < g.n2;
