@@ -313,7 +313,11 @@ struct ZFCfg {
   static constexpr int RPC = TPC >= 64 ? 4 : (256 / TPC > 64 ? 64 : 256 / TPC);
   static constexpr int THREADS = TPC * RPC;
   static constexpr int HP = N / 2 + 8;  // padded half-row (n/2+1 modes)
-  static constexpr size_t SMEM = sizeof(double2) * (static_cast<size_t>(RPC) * 6 * HP + N);
+  // n = 512: both twiddled radix-8 stages take their twiddles from
+  // registers (LastTw), so no table is staged in shared memory
+  static constexpr bool REG = N == 512 && SDNS_MIDREG;
+  static constexpr size_t SMEM =
+      sizeof(double2) * (static_cast<size_t>(RPC) * 6 * HP + (REG ? 0 : N));
   // CTAs per SM the shared memory allows (n = 1024: one -- then give the
   // 16-element transforms the registers, 128 would spill)
   static constexpr int MINB = SMEM * 2 <= 227 * 1024 ? 2 : 1;
@@ -363,8 +367,12 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   // staging area of pair p (2 half-rows, 2*HP >= n entries) then serves as
   // that pair's FFT exchange buffer. Pair results stay in registers.
   double2* S = smem + r * 6 * HP;
-  double2* tws = smem + RPC * 6 * HP;
-  load_twiddles(tws, tw, N);
+  const double2* tws = tw;  // REG: the 4 register twiddles come from L2
+  if constexpr (!ZFCfg<N>::REG) {
+    double2* t2 = smem + RPC * 6 * HP;
+    load_twiddles(t2, tw, N);
+    tws = t2;
+  }
   Bar bar;
   if constexpr (TPC >= 64) bar = Bar{1 + r, TPC};
   const SwzIdx sw;
