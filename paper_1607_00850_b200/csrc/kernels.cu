@@ -306,11 +306,15 @@ struct WarpBar {
 
 // Launch shape of the fused z pass: 4 rows of 64 threads at n >= 512 (each
 // row synchronises on its own named barrier), else whole rows per warp.
+#ifndef SDNS_ZRPC  // rows per CTA of the fused z pass at n = 512 (A/B)
+#define SDNS_ZRPC 4
+#endif
 template <int N>
 struct ZFCfg {
   static constexpr int E = fft_elems(N);
   static constexpr int TPC = N / E;
-  static constexpr int RPC = TPC >= 64 ? 4 : (256 / TPC > 64 ? 64 : 256 / TPC);
+  static constexpr int RPC =
+      TPC >= 64 ? (N == 512 ? SDNS_ZRPC : 4) : (256 / TPC > 64 ? 64 : 256 / TPC);
   static constexpr int THREADS = TPC * RPC;
   static constexpr int HP = N / 2 + 8;  // padded half-row (n/2+1 modes)
   // n = 512: both twiddled radix-8 stages take their twiddles from
@@ -320,7 +324,7 @@ struct ZFCfg {
       sizeof(double2) * (static_cast<size_t>(RPC) * 6 * HP + (REG ? 0 : N));
   // CTAs per SM the shared memory allows (n = 1024: one -- then give the
   // 16-element transforms the registers, 128 would spill)
-  static constexpr int MINB = SMEM * 2 <= 227 * 1024 ? 2 : 1;
+  static constexpr int MINB = SMEM * 4 <= 227 * 1024 ? 4 : (SMEM * 2 <= 227 * 1024 ? 2 : 1);
 };
 
 #ifndef SDNS_ZTMA

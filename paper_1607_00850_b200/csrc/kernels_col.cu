@@ -57,6 +57,9 @@ namespace {
 #ifndef SDNS_COLTMA
 #define SDNS_COLTMA 1
 #endif
+#ifndef SDNS_COLREG  // n = 512 column transforms: register twiddles (fft_core.cuh LastTw)
+#define SDNS_COLREG 1
+#endif
 #ifndef SDNS_FDIV  // tile index -> (row, kz) by float reciprocal instead of integer division
 #define SDNS_FDIV 1
 #endif
@@ -250,7 +253,13 @@ __device__ __forceinline__ void col_fft(double2 (&v)[fft_elems(N)], double2* sm,
 #ifdef SDNS_NOFFT
   bar();
 #else
-  block_fft<N, S>(v, sm, idx, t, tw, bar);
+  if constexpr (N == 512 && SDNS_COLREG) {
+    // both twiddled radix-8 stages from registers (LastTw: 4 table reads
+    // instead of 14 per transform)
+    block_fft_lt<N, S>(v, sm, idx, t, tw, bar, last_twiddles<N>(tw, t));
+  } else {
+    block_fft<N, S>(v, sm, idx, t, tw, bar);
+  }
 #endif
 }
 
