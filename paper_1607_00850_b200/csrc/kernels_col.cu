@@ -60,6 +60,9 @@ namespace {
 #ifndef SDNS_COLREG  // n = 512 column transforms: register twiddles (fft_core.cuh LastTw)
 #define SDNS_COLREG 1
 #endif
+#ifndef SDNS_PLAINLT  // plain passes hold the register twiddles for the whole kernel
+#define SDNS_PLAINLT 1
+#endif
 #ifndef SDNS_FDIV  // tile index -> (row, kz) by float reciprocal instead of integer division
 #define SDNS_FDIV 1
 #endif
@@ -260,6 +263,36 @@ __device__ __forceinline__ void col_fft(double2 (&v)[fft_elems(N)], double2* sm,
   } else {
     block_fft<N, S>(v, sm, idx, t, tw, bar);
   }
+#endif
+}
+#ifndef SDNS_YINVLT  // the y inverse pass holds the register twiddles for the whole kernel
+#define SDNS_YINVLT 1
+#endif
+template <int N, int S, class IDX, class BAR>
+__device__ __forceinline__ void col_fft_lt(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
+                                           const double2* __restrict__ tw, BAR bar,
+                                           const LastTw& lt);
+template <int N, int S, class IDX, class BAR>
+__device__ __forceinline__ void col_fft_y(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
+                                          const double2* __restrict__ tw, BAR bar,
+                                          const LastTw& lt) {
+  if constexpr (SDNS_YINVLT)
+    col_fft_lt<N, S>(v, sm, idx, t, tw, bar, lt);
+  else
+    col_fft<N, S>(v, sm, idx, t, tw, bar);
+}
+// Same with the register twiddles held by the caller (read once per kernel).
+template <int N, int S, class IDX, class BAR>
+__device__ __forceinline__ void col_fft_lt(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
+                                           const double2* __restrict__ tw, BAR bar,
+                                           const LastTw& lt) {
+#ifdef SDNS_NOFFT
+  bar();
+#else
+  if constexpr (N == 512 && SDNS_COLREG)
+    block_fft_lt<N, S>(v, sm, idx, t, tw, bar, lt);
+  else
+    block_fft<N, S>(v, sm, idx, t, tw, bar);
 #endif
 }
 
@@ -552,6 +585,9 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
              ColGeom g, ColGeom go, int ntiles, const double2* __restrict__ tw,
              const __grid_constant__ CUtensorMap tm) {
   const OutSel<N, SEP> os(go, Lanes<N, V>().t);
+  // one read of the register twiddles per kernel (from L2), not per item
+  LastTw lt{};
+  if constexpr (N == 512 && SDNS_COLREG && SDNS_PLAINLT) lt = last_twiddles<N>(tw, Lanes<N, V>().t);
   pipeline<N, V>(ntiles, 0, nfields, g, [&](int f) { return in + f * in_cs; },
                  [](int f) { return f; }, &tm, tw,
                  [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po,
@@ -560,7 +596,10 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
                    double2 v[fft_elems(N)];
                    read_own<N>(v, buf, ln.idx, t);
                    ln.bar();
-                   col_fft<N, S>(v, buf, ln.idx, t, tws, ln.bar);
+                   if constexpr (SDNS_PLAINLT)
+                     col_fft_lt<N, S>(v, buf, ln.idx, t, tws, ln.bar, lt);
+                   else
+                     col_fft<N, S>(v, buf, ln.idx, t, tws, ln.bar);
                    release();  // buffer no longer read: the next tile may load
                    store_own<N, SEP == 2>(out + f * out_cs, v, go, os.tile(tl, go), os.po(po), t);
                  });
@@ -648,6 +687,8 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
   constexpr int E = fft_elems(N), TPC = N / E;
   // field of item it: 0, 1, 3, 2, 4
   auto order = [](int it) { return it ^ ((it >> 1) & ~(it >> 2) & 1); };
+  LastTw lt{};  // register twiddles read once per kernel (SDNS_YINVLT)
+  if constexpr (N == 512 && SDNS_COLREG && SDNS_YINVLT) lt = last_twiddles<N>(tw, Lanes<N, V>().t);
   const OutSel<N, SEP> os(go, Lanes<N, V>().t);
   extern __shared__ __align__(128) double2 smem[];
   double2* const stage = smem + PipeCfg<N, V>::NBUF * N * PipeCfg<N, V>::CS;
@@ -675,19 +716,19 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
                        const double ky = wavenum(t + m * TPC, N);
                        v[m] = times_i(make_double2(ky * vin[m].x, ky * vin[m].y));
                      }
-                     col_fft<N, +1>(v, buf, ln.idx, t, tws, ln.bar);
+                     col_fft_y<N, +1>(v, buf, ln.idx, t, tws, ln.bar, lt);
                      put(3, v, tl, po, t);
                    }
                    if (it == 2) {  // w2' -> w2 = F(w2')
-                     col_fft<N, +1>(vin, buf, ln.idx, t, tws, ln.bar);
+                     col_fft_y<N, +1>(vin, buf, ln.idx, t, tws, ln.bar, lt);
                      put(5, vin, tl, po, t);
                    } else if (it == 4) {  // K2 -> w1' = F(-i K2)
 #pragma unroll
                      for (int m = 0; m < E; ++m) v[m] = times_mi(vin[m]);
-                     col_fft<N, +1>(v, buf, ln.idx, t, tws, ln.bar);
+                     col_fft_y<N, +1>(v, buf, ln.idx, t, tws, ln.bar, lt);
                      put(4, v, tl, po, t);
                    } else {  // U0, U1, U2 -> u_c
-                     col_fft<N, +1>(vin, buf, ln.idx, t, tws, ln.bar);
+                     col_fft_y<N, +1>(vin, buf, ln.idx, t, tws, ln.bar, lt);
                      put(order(it), vin, tl, po, t);
                    }
                  });
