@@ -225,6 +225,11 @@ struct NamedBar {
 
 // One Stockham stage (and the rest, recursively). `sm` points at this
 // column's element 0 in shared memory; element x lives at sm[idx(x)].
+// The stage with register twiddles besides the last: the radix-8 stage at
+// NS = 8 of the 8-element transforms (n = 128, 256, 512; at 512 it is also
+// the one before the last).
+__host__ __device__ constexpr int mid_ns(int n) { return n >= 128 ? 8 : 1; }
+
 // Stage twiddles held in registers by kernels that run several transforms
 // per thread (the z pass): W^k and W^{4k} of the radix-8 stages with NS =
 // N/64 (m*) and NS = N/8 (w*) (k = the thread's butterfly index, forward
@@ -270,7 +275,7 @@ __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx
     for (int r = 0; r < R; ++r) a[r] = v[b + r * NB];
     if constexpr (LREG && LAST && NS > 1 && R == 8 && NB == 1) {
       apply_tw8<S>(a, lt.w1, lt.w4);
-    } else if constexpr (SDNS_MIDREG && LREG && !LAST && NS == N / 64 && NS > 1 && R == 8 &&
+    } else if constexpr (SDNS_MIDREG && LREG && !LAST && NS == mid_ns(N) && NS > 1 && R == 8 &&
                          NB == 1) {
       apply_tw8<S>(a, lt.m1, lt.m4);
     } else if (NS > 1) {
@@ -317,7 +322,7 @@ __device__ __forceinline__ void block_fft_lt(double2 (&v)[fft_elems(N)], double2
 // with one butterfly per thread (tw = the stage-ordered table).
 template <int N>
 __device__ __forceinline__ LastTw last_twiddles(const double2* tw, int t) {
-  constexpr int NS = N / 8, MS = N >= 128 ? N / 64 : 1;
+  constexpr int NS = N / 8, MS = mid_ns(N);
   constexpr int TOFF = tw_stage_off(N, fft_elems(N), NS);
   constexpr int MOFF = tw_stage_off(N, fft_elems(N), MS);
   const int k = t & (NS - 1), km = t & (MS - 1);
