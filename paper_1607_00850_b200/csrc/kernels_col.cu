@@ -653,7 +653,11 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                          for (int m = 0; m < E; ++m) {
                            long long at = pout.o(m);
                            if constexpr (SEP == 2) at += __ldg(go.seg + ((t + m * TPC) >> go.pb_shift));
+#ifdef SDNS_NOU0  // A/B measurement only (wrong results): no U0 re-read
+                           const double2 a = make_double2(static_cast<double>(at), 0.0);
+#else
                            const double2 a = u0[at];
+#endif
                            v[m] = times_i(make_double2(v[m].x - ky * a.x, v[m].y - ky * a.y));
                          }
                        }
