@@ -96,7 +96,7 @@ def test_config2_256_ten_steps_vs_reference(ref):
 
 @pytest.mark.skipif(os.environ.get("SDNS_FULL_PARITY") != "1",
                     reason="full-size reference run (~2-4 min of host time): SDNS_FULL_PARITY=1")
-@pytest.mark.parametrize("geom", [dict(p=1), dict(p=4)])
+@pytest.mark.parametrize("geom", [dict(p=1), dict(p=4), dict(decomp="pencil", p=4, p1=2, p2=2)])
 def test_config3_512_ten_steps_vs_reference(ref, geom):
     """north_star's parity bar at the bench workload (BASELINE configs[2],
     512^3): u after 10 RK4 steps within 1e-11 relative L2 of the reference,
@@ -120,17 +120,19 @@ def test_config3_512_ten_steps_vs_reference(ref, geom):
             st.advance(lambda k, t: rows.append(S.collect_stats(c, st.u_hat, nu, t)))
             final = st.u_hat.download()
             st.close()
-            return rows, final, (o1, s1)
+            return rows, final, (o1, s1, o2, s2)
 
     res = S.run_group(cfg.p, body)
     rows = res[0][0]
-    final = np.concatenate([r[1] for r in res], axis=2)  # slab blocks along y
+    final = np.empty_like(gf)
+    for _, blk, (o1, s1, o2, s2) in res:  # each rank's (y, kz) block
+        final[:, :, o1:o1 + s1, o2:o2 + s2] = blk
     assert len(rows) == gs.shape[0] == steps + 1
     for r, g in zip(rows, gs):
         assert abs(r.energy - g[1]) <= 1e-12 * g[1]
         assert abs(r.enstrophy - g[2]) <= 1e-12 * g[2]
     err = rel(final, gf)
-    print(f"512^3 p={cfg.p}: rel L2(u_hat) after {steps} steps = {err:.3e}; "
+    print(f"512^3 {cfg.decomp} p={cfg.p}: rel L2(u_hat) after {steps} steps = {err:.3e}; "
           f"E {rows[-1].energy!r} vs {gs[-1][1]!r}")
     assert err <= 1e-11
 
