@@ -115,6 +115,11 @@ struct sdns_ctx {
   // with 64 KB strides.
   double2* wx = nullptr;
   long long cs_x = 0;
+  // p = 1 with wx: P2 .. P5a work in the chunked layout [x][kz chunk][y][8]
+  // (x planes padded to an odd multiple of 128 B): P2 and P4 move
+  // contiguous 64 KB tiles, the z pass stages each half-row as one
+  // tensor-map box of pitch/8 chunks
+  bool zchunk = false;
   long long spec_cs = 0;   // complex elements per spectral component (padded)
   int prow = 0;            // rows per x plane incl. one pad row (s1 + 1)
   long long real_cs = 0;   // doubles per real component
@@ -253,6 +258,49 @@ struct sdns_ctx {
     g.mpitch = pitch;
     g.mrows = static_cast<int>(n);
     return g;
+  }
+  // chunked work layout (zchunk): x-plane stride and the pass views
+  long long xpl() const { return static_cast<long long>(pitch / 8) * lo.spec_shape[1] * 8 + 8; }
+  ColGeom yc_geom() const {  // y passes: rows = x, positions = y
+    ColGeom g;
+    g.rs = xpl();
+    g.ps0 = 8;
+    g.ps1 = 0;
+    g.pb_shift = 30;
+    g.kcs = static_cast<long long>(lo.spec_shape[1]) * 8;
+    g.nrows = static_cast<int>(lo.spec_shape[0]);
+    g.n2 = static_cast<int>(lo.spec_shape[2]);
+    g.pitch = pitch;
+    g.mpitch = pitch;
+    g.mrows = static_cast<int>(lo.spec_shape[0]);
+    return g;
+  }
+  ColGeom yc_geom_fwd() const {  // forward y pass, pruned like ygeom_fwd
+    ColGeom g = yc_geom();
+    if (!cfg.dealias) return g;
+    const int K = keep_k();
+    const int kzk = std::max(0, std::min(g.n2, K + 1 - static_cast<int>(lo.spec_offset[2])));
+    g.n2 = kzk;
+    g.pitch = std::max(8, (kzk + 7) / 8 * 8);
+    g.keep_k = K;
+    return g;
+  }
+  ColGeom xc_geom_fwd() const {  // forward x pass input: rows = y, positions = x
+    ColGeom g = xgeom_fwd();     // (enumeration and pruning of the x layout)
+    g.rs = 8;
+    g.ps0 = xpl();
+    g.ps1 = 0;
+    g.pb_shift = 30;
+    g.kcs = static_cast<long long>(lo.spec_shape[1]) * 8;
+    g.mpitch = pitch;
+    g.mrows = static_cast<int>(lo.spec_shape[1]);
+    return g;
+  }
+  RowMap zmap_chunk() const {
+    RowMap r = zmap(false);
+    r.cstride = static_cast<int>(lo.spec_shape[1]) * 8;
+    r.xplane = xpl();
+    return r;
   }
   WaveGeom xwave() const {
     WaveGeom w;
@@ -722,8 +770,8 @@ void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args
   if (!c->pencil) {
     if (c->wx) {
       tk = c->tick(SDNS_PASS_Y_INV);
-      sdns_dev::y_inverse_curl_to(n, c->wx, c->wb, c->cs_x, c->spec_cs, c->xl_in(), c->ygeom(),
-                                  c->tw, s);
+      sdns_dev::y_inverse_curl_to(n, c->wx, c->wb, c->cs_x, c->spec_cs, c->xl_in(),
+                                  c->zchunk ? c->yc_geom() : c->ygeom(), c->tw, s);
     } else {
       c->exchange(true, 5);
       tk = c->tick(SDNS_PASS_Y_INV);
@@ -731,11 +779,17 @@ void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args
     }
     c->tock(tk);
     tk = c->tick(SDNS_PASS_Z_FUSED);
-    sdns_dev::z_fused(n, c->wb, c->spec_cs, zm, c->norm, c->tw, s);
+    if (c->zchunk) {
+      RowMap zc = c->zmap_chunk();
+      zc.kz_keep = zm.kz_keep;
+      sdns_dev::z_fused(n, c->wb, c->spec_cs, zc, c->norm, c->tw, s);
+    } else {
+      sdns_dev::z_fused(n, c->wb, c->spec_cs, zm, c->norm, c->tw, s);
+    }
     c->tock(tk);
     tk = c->tick(SDNS_PASS_Y_FWD);
-    sdns_dev::col_plain(n, -1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, 3, c->ygeom_fwd(),
-                        c->tw, s);
+    sdns_dev::col_plain(n, -1, false, c->wb, c->wb, c->spec_cs, c->spec_cs, 3,
+                        c->zchunk ? c->yc_geom_fwd() : c->ygeom_fwd(), c->tw, s);
     c->tock(tk);
     c->exchange(false, 3);
   } else {
@@ -799,8 +853,14 @@ void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args
   a.cs = c->spec_cs;
   a.dealias = c->cfg.dealias;
   tk = c->tick(SDNS_PASS_X_FWD_FFT);
-  sdns_dev::col_plain(n, -1, true, c->wa, c->wa, c->spec_cs, c->spec_cs, 3, c->xgeom_fwd(),
-                      c->tw, s);
+  if (c->zchunk) {  // chunked input, x-layout output in the free fields 3..5
+    a.nl = c->wa + 3 * c->spec_cs;
+    sdns_dev::col_plain_to(n, -1, c->wa, c->wa + 3 * c->spec_cs, c->spec_cs, c->spec_cs, 3,
+                           c->xc_geom_fwd(), c->xgeom_fwd(), c->tw, s, true);
+  } else {
+    sdns_dev::col_plain(n, -1, true, c->wa, c->wa, c->spec_cs, c->spec_cs, 3, c->xgeom_fwd(),
+                        c->tw, s);
+  }
   c->tock(tk);
   tk = c->tick(SDNS_PASS_X_FWD_TAIL + mode);
   sdns_dev::rk_update(mode, a, c->sgeom(), s);
@@ -1416,6 +1476,8 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
       if (cfg->p == 1 && n <= 512 && !(xl && xl[0] == '0')) {
         c->cs_x = static_cast<long long>(c->pitch) * c->lo.spec_shape[1] * n;
         c->wx = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * c->cs_x * 5));
+        const char* zc = std::getenv("SDNS_ZCHUNK");
+        c->zchunk = n == 512 && !(zc && zc[0] == '0');  // measured at 512
       }
     }
     const int stride = c->shells + 3;

@@ -17,6 +17,8 @@
 // round-to-nearest intrinsics (no FMA contraction), so the standalone
 // pointwise kernels are bitwise equal to the reference CPU functions.
 #include <cstdio>
+#include <cstring>
+#include <cudaTypedefs.h>
 #include <type_traits>
 #include <vector>
 
@@ -244,6 +246,7 @@ struct ZCfg {
 
 // Offset of element kz of z line ri: `ro` = zrow_off for unsegmented maps.
 __device__ __forceinline__ long long zel(const RowMap& rm, long long ro, int ri, int k) {
+  if (rm.cstride) return ro + static_cast<long long>(k >> 3) * rm.cstride + (k & 7);
   if (rm.nseg == 0) return ro + k;
   int sg = 0;
   while (sg + 1 < rm.nseg && k >= rm.seg_k0[sg + 1]) ++sg;
@@ -251,6 +254,10 @@ __device__ __forceinline__ long long zel(const RowMap& rm, long long ro, int ri,
 }
 
 __device__ __forceinline__ long long zrow_off(const RowMap& rm, int ri) {
+  if (rm.cstride) {
+    const int x = ri / rm.rpp, y = ri - x * rm.rpp;
+    return static_cast<long long>(x) * rm.xplane + static_cast<long long>(y) * 8;
+  }
   if (rm.blk == 0) {
     const int pl = ri / rm.rpp, r = ri - pl * rm.rpp;
     return (static_cast<long long>(pl) * rm.prow + r) * rm.pitch;
@@ -359,7 +366,7 @@ __device__ __forceinline__ ZDst zdst(const RowMap& rmo, int ri, int k) {
 template <int N, bool PO = false>
 __global__ void __launch_bounds__(ZFCfg<N>::THREADS, ZFCfg<N>::MINB)
 k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __restrict__ tw,
-          double2* fo = nullptr, RowMap rmo = RowMap{}) {
+          const __grid_constant__ CUtensorMap ztm, double2* fo = nullptr, RowMap rmo = RowMap{}) {
   constexpr int E = ZFCfg<N>::E, TPC = ZFCfg<N>::TPC, HP = ZFCfg<N>::HP, RPC = ZFCfg<N>::RPC;
   using Bar = typename std::conditional<(TPC >= 64), NamedBar, WarpBar>::type;
   extern __shared__ __align__(128) double2 smem[];
@@ -391,7 +398,14 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   __shared__ alignas(8) unsigned long long zbar[RPC];
   if (t == 0) mbar_init(&zbar[r], 1);
   __syncthreads();  // barrier init visible before anyone waits on it
-  if (valid && t == 0) {
+  if (valid && t == 0 && rm.cstride) {
+    // chunked rows: one tensor-map box (pitch/8 chunks of 128 B) per half-row
+    const int fld[6] = {0, 4, 1, 3, 2, 5};
+    const int x = ri / rm.rpp, y = ri - x * rm.rpp;
+    mbar_expect_tx(&zbar[r], 6u * static_cast<unsigned>(rm.pitch) * 16u);
+#pragma unroll
+    for (int sl = 0; sl < 6; ++sl) tma_load5(S + sl * HP, &ztm, 0, 0, y, x, fld[sl], &zbar[r]);
+  } else if (valid && t == 0) {
     const int fld[6] = {0, 4, 1, 3, 2, 5};
     mbar_expect_tx(&zbar[r], 6u * static_cast<unsigned>(rm.n2) * 16u);
 #pragma unroll
@@ -1099,7 +1113,41 @@ static void z_fused_n(double2* rows, long long cs, const RowMap& rm, double norm
   const unsigned grid = static_cast<unsigned>((rm.nrows + C::RPC - 1) / C::RPC);
   const size_t shm = C::SMEM;
   SDNS_SET_SMEM((k_z_fused<N>), shm);
-  k_z_fused<N><<<grid, C::THREADS, shm, s>>>(rows, cs, rm, norm, tw);
+  CUtensorMap tm;
+  std::memset(&tm, 0, sizeof(tm));
+  if (rm.cstride && !z_chunk_map(&tm, rows, cs, 6, rm, rm.pitch))
+    std::fprintf(stderr, "sdns: z pass chunk map could not be encoded\n");
+  k_z_fused<N><<<grid, C::THREADS, shm, s>>>(rows, cs, rm, norm, tw, tm);
+}
+
+bool z_chunk_map(void* tmap, const double2* base, long long cs, int nfields, const RowMap& rm,
+                 int pitch) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  if (!enc || rm.rpp <= 0) return false;
+  const int nch = pitch / 8;
+  const int nx = rm.nrows / rm.rpp;
+  const cuuint64_t B = sizeof(double2);
+  // doubles of a chunk, chunks, y, x, fields
+  const cuuint64_t dims[5] = {16, static_cast<cuuint64_t>(nch), static_cast<cuuint64_t>(rm.rpp),
+                              static_cast<cuuint64_t>(nx), static_cast<cuuint64_t>(nfields)};
+  const cuuint64_t strides[4] = {static_cast<cuuint64_t>(rm.cstride) * B, 8 * B,
+                                 static_cast<cuuint64_t>(rm.xplane) * B,
+                                 static_cast<cuuint64_t>(cs) * B};
+  const cuuint32_t box[5] = {16, static_cast<cuuint32_t>(nch), 1, 1, 1}, es[5] = {1, 1, 1, 1, 1};
+  return enc(static_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5,
+             const_cast<double2*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 void z_fused(int n, double2* rows, long long cs, const RowMap& rm, double norm,
@@ -1119,7 +1167,9 @@ static void z_fused_to_n(double2* rows, long long cs, const RowMap& rm, double2*
   const unsigned grid = static_cast<unsigned>((rm.nrows + C::RPC - 1) / C::RPC);
   const size_t shm = C::SMEM;
   SDNS_SET_SMEM((k_z_fused<N, true>), shm);
-  k_z_fused<N, true><<<grid, C::THREADS, shm, s>>>(rows, cs, rm, norm, tw, out, rmo);
+  CUtensorMap tm;
+  std::memset(&tm, 0, sizeof(tm));
+  k_z_fused<N, true><<<grid, C::THREADS, shm, s>>>(rows, cs, rm, norm, tw, tm, out, rmo);
 }
 
 void z_fused_to(int n, double2* rows, long long cs, const RowMap& rm, double2* out,

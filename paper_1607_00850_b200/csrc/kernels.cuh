@@ -69,6 +69,11 @@ struct RowMap {
   int pitch = 0;     // spectral row pitch (complex)
   int n2 = 0;        // valid kz entries (n/2+1 for a full z line)
   int kz_keep = 1 << 30;  // forward outputs stored only for kz < kz_keep
+  // Chunked rows (p = 1 work layout [x][kz chunk][y][8]): row
+  // ri = x*rpp + y starts at x*xplane + y*8 and kz chunk c lies cstride
+  // complex further per chunk. cstride == 0: the row maps above.
+  int cstride = 0;
+  long long xplane = 0;
   // Pencil: a z line is assembled from nseg kz blocks (one per row peer,
   // fft.cpp:141-160); block q holds rows ri at seg_base[q] + ri*seg_pitch[q]
   // for kz in [seg_k0[q], seg_k0[q+1]). nseg == 0: the row maps above.
@@ -157,6 +162,10 @@ void set_step_scalars(double* dts, double dt, cudaStream_t s);
 
 void z_fused(int n, double2* rows, long long cs, const RowMap& rm, double norm,
              const double2* tw, cudaStream_t s);
+// Encodes the tensor map the z pass stages chunked rows with (rm.cstride):
+// one box of pitch/8 chunks x 128 B per half-row. False if unavailable.
+bool z_chunk_map(void* tmap, const double2* base, long long cs, int nfields, const RowMap& rm,
+                 int pitch);
 // Same, storing the 3 outputs through the segmented output map `rmo`
 // (element (ri, kz) of component c at out + seg_base + c*seg_cs +
 // ri*seg_pitch + kz - seg_k0 of kz's segment): the pencil forward row

@@ -321,14 +321,7 @@ __device__ __forceinline__ double2 times_mi(double2 a) { return make_double2(a.y
 // kz chunk, kz chunks, rows, positions, fields), completing on the slot's
 // mbarrier. The box lands position-major, CS complex per position --
 // TileIdx<8>. Issued by thread 0 (its tile coordinates are column 0's).
-__device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
-                                          int c3, int c4, unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_addr(dst)),
-      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_addr(bar))
-      : "memory");
-}
+// (tma_load5: fft_core.cuh)
 
 template <int N, int CS>
 __device__ __forceinline__ void tma_tile(double2* buf, const CUtensorMap* tm, const ColGeom& g,
@@ -883,9 +876,14 @@ static void col_plain_n(int dir, bool xaxis, const double2* in, double2* out, lo
     }
     return;
   }
-  if (go) {  // separate output layout (pencil y passes; y-shaped tiles)
-    if (dir < 0) plain_launch<N, -1, VY, 1>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
-    else plain_launch<N, +1, VY, 1>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+  if (go) {  // separate output layout (pencil y passes; the chunked x forward)
+    if (xaxis) {
+      if (dir < 0) plain_launch<N, -1, VX, 1>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+      else plain_launch<N, +1, VX, 1>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+    } else {
+      if (dir < 0) plain_launch<N, -1, VY, 1>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+      else plain_launch<N, +1, VY, 1>(in, out, in_cs, out_cs, nfields, g, *go, tw, s);
+    }
     return;
   }
   if (dir < 0) {

@@ -198,8 +198,9 @@ def test_nccl_backend_pencil_1x1_exchange():
 
 def test_512_pipeline_variants_bitwise():
     """At 512^3 the column passes load tiles through TMA tensor maps and P1/P2
-    go through the chunk-major work layout; the LDGSTS loads (SDNS_NO_TMA=1)
-    and the plain layout (SDNS_XLAYOUT=0) run the same arithmetic, so one RHS
+    go through the chunk-major work layout and P2 .. P5a through the chunked
+    layout; the LDGSTS loads (SDNS_NO_TMA=1) and the plain layouts
+    (SDNS_XLAYOUT=0, SDNS_ZCHUNK=0) run the same arithmetic, so one RHS
     must agree bit for bit across all of them and across repeated runs (a
     pipeline race would show here)."""
     n = 512
@@ -227,6 +228,8 @@ def test_512_pipeline_variants_bitwise():
     assert np.array_equal(a, rhs())
     assert np.array_equal(a, rhs(SDNS_NO_TMA="1"))
     assert np.array_equal(a, rhs(SDNS_XLAYOUT="0"))
+    assert np.array_equal(a, rhs(SDNS_ZCHUNK="0"))  # natural layout after P2
+    assert np.array_equal(a, rhs(SDNS_ZCHUNK="0", SDNS_NO_TMA="1"))
     assert np.isfinite(a).all() and np.abs(a).max() > 0
 
 
