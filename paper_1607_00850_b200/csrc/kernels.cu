@@ -337,6 +337,9 @@ struct ZFCfg {
 #ifndef SDNS_ZTMA
 #define SDNS_ZTMA 1
 #endif
+#ifndef SDNS_ZPF  // chunked z rows: L2 prefetch of the rows SDNS_ZPF CTAs ahead (0: off)
+#define SDNS_ZPF 0  // measured: no gain (296 or 600 CTAs ahead)
+#endif
 
 // z-pass transform; SDNS_ZNOFFT builds a transform-free variant (wrong
 // results) for A/B measurements of the pass's memory/shared-memory floor.
@@ -405,6 +408,20 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
     mbar_expect_tx(&zbar[r], 6u * static_cast<unsigned>(rm.pitch) * 16u);
 #pragma unroll
     for (int sl = 0; sl < 6; ++sl) tma_load5(S + sl * HP, &ztm, 0, 0, y, x, fld[sl], &zbar[r]);
+    if constexpr (SDNS_ZPF > 0) {  // warm L2 with the row a later CTA will stage
+      const int rf = ri + SDNS_ZPF * RPC;
+      if (rf < rm.nrows) {
+        const int xf = rf / rm.rpp, yf = rf - xf * rm.rpp;
+#pragma unroll
+        for (int sl = 0; sl < 6; ++sl) {
+          asm volatile(
+              "cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(
+                  &ztm),
+              "r"(0), "r"(0), "r"(yf), "r"(xf), "r"(fld[sl])
+              : "memory");
+        }
+      }
+    }
   } else if (valid && t == 0) {
     const int fld[6] = {0, 4, 1, 3, 2, 5};
     mbar_expect_tx(&zbar[r], 6u * static_cast<unsigned>(rm.n2) * 16u);
