@@ -238,11 +238,17 @@ __device__ __forceinline__ void rk_elem(const XfArgs& a, const SpecGeom& g, long
   rk_finish<MODE>(a, g, e, i, j, k, in, finite, un);
 }
 
-#ifndef SDNS_RKILP
-#define SDNS_RKILP 1
+#ifndef SDNS_RKILP  // two modes per iteration: 1 stage 3, 2 + stages 1-2, 3 + stage 0
+#define SDNS_RKILP 2
+#endif
+#ifndef SDNS_RK3B  // CTAs per SM the stage-3 update is compiled for
+#define SDNS_RK3B 1
 #endif
 template <int MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, ((SDNS_RKILP > 1 && MODE == XF_RK12) ||
+                                       (SDNS_RKILP > 2 && MODE == XF_RK0))
+                                           ? 2
+                                           : (MODE == XF_RK3 ? SDNS_RK3B : 1))
 k_rk_update(XfArgs a, SpecGeom g) {
   const long long total = static_cast<long long>(g.s0) * g.prow * g.pitch;
   bool finite = true;
@@ -250,7 +256,8 @@ k_rk_update(XfArgs a, SpecGeom g) {
   // stage 3 (the most loads per mode): two modes per iteration, both modes'
   // loads issued before either's arithmetic and stores (3.29 -> 3.11 ms; the
   // other stages lose occupancy to the doubled registers and gain nothing)
-  if constexpr (SDNS_RKILP && MODE == XF_RK3) {
+  if constexpr (SDNS_RKILP && (MODE == XF_RK3 || (SDNS_RKILP > 1 && MODE == XF_RK12) ||
+                                (SDNS_RKILP > 2 && MODE == XF_RK0))) {
   for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += 2 * stride) {
     const long long e2 = e + stride;
