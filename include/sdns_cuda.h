@@ -144,6 +144,11 @@ int sdns_comm_size(const sdns_comm* c);
 int sdns_comm_barrier(sdns_comm* c);                                 /* transport.hpp:64 */
 /* In-place reduction in ascending rank order (op 0 sum, 1 max, 2 min). */
 int sdns_comm_allreduce(sdns_comm* c, double* values, int count, int op); /* :61 */
+/* broadcast_bytes (transport.hpp:62): the root's `nbytes` HOST bytes into
+ * every rank's `data`. root and nbytes must agree on every rank, else every
+ * rank fails with SDNS_PROTOCOL_ERROR (validate_broadcast,
+ * transport.cpp:332-349); the loopback accepts only root 0. Collective. */
+int sdns_comm_broadcast_bytes(sdns_comm* c, void* data, int64_t nbytes, int root);
 int sdns_comm_destroy(sdns_comm* c);
 /* InProcessBackend::poison (transport.hpp:125-128): every pending and later
  * collective of the group fails with SDNS_PROTOCOL_ERROR naming `reason`; a

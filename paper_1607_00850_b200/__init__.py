@@ -184,6 +184,7 @@ def load_library(path: str = LIB_PATH):
             "sdns_comm_size": (I, [P]),
             "sdns_comm_barrier": (I, [P]),
             "sdns_comm_allreduce": (I, [P, P, I, I]),
+            "sdns_comm_broadcast_bytes": (I, [P, P, ctypes.c_int64, I]),
             "sdns_comm_destroy": (I, [P]),
             "sdns_ctx_create": (I, [ctypes.POINTER(_Config), I, I, P, P, PP]),
             "sdns_ctx_destroy": (I, [P]),
@@ -503,6 +504,13 @@ class Comm:
         _check(self._lib.sdns_comm_allreduce(self._h, _ptr(v), v.size,
                                              {"sum": 0, "max": 1, "min": 2}[op]))
         return v
+
+    def broadcast_bytes(self, data, root: int = 0) -> bytes:
+        """broadcast_bytes, transport.hpp:62: the root's bytes on every rank
+        (`data`: bytes-like of the agreed length; the root's content is sent)."""
+        buf = ctypes.create_string_buffer(bytes(data), len(data))
+        _check(self._lib.sdns_comm_broadcast_bytes(self._h, buf, len(data), root))
+        return buf.raw
 
     def split(self, color: int, key: int) -> "Comm":
         """split, transport.hpp:66-67: members ordered by (key, rank)."""

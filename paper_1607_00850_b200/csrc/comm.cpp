@@ -54,6 +54,9 @@ class LoopbackComm final : public Comm {
   }
   void allreduce(double*, int, int) override {}
   void barrier() override {}
+  void broadcast(void*, size_t, int root) override {
+    if (root != 0) protocol_error("loopback broadcast root must be 0");  // transport.cpp:37-38
+  }
   std::vector<void*> map_peers(void* mine) override { return {mine}; }
   const char* kind() const override { return "loopback"; }
   std::shared_ptr<Comm> split(int, int) override { return std::make_shared<LoopbackComm>(); }
@@ -79,6 +82,7 @@ struct Board {
   std::vector<std::vector<Xfer>> posted;
   std::vector<std::vector<double>> values;
   std::vector<void*> ptrs;
+  std::vector<std::pair<int, size_t>> bcast;  // (root, nbytes) each rank posted
   // collective kind each rank entered (transport.cpp: mismatched collectives
   // raise ProtocolError on every rank); the verdict of the last rendezvous
   std::vector<int> op;
@@ -91,6 +95,7 @@ struct Board {
     posted.resize(n);
     values.resize(n);
     ptrs.resize(n);
+    bcast.resize(n);
     op.assign(static_cast<size_t>(n), 0);
     split_req.resize(n);
     int prev = 0;
@@ -125,7 +130,7 @@ struct Board {
   }
 
   // Rendezvous opening collective `kind` (1 all_to_all, 2 allreduce, 3
-  // barrier, 4 split, 5 map_peers, 6 stream_barrier): every rank must have
+  // barrier, 4 split, 5 map_peers, 6 stream_barrier, 7 broadcast): every rank must have
   // entered the same kind, else all of them raise ProtocolError and the
   // group is poisoned.
   void enter(std::unique_lock<std::mutex>& lk, int rank, int kind) {
@@ -261,6 +266,36 @@ class InProcessComm final : public Comm {
     b_->enter(lk, rank_, 3);
   }
 
+  // Every rank posts (data, root, nbytes); the arguments are checked against
+  // rank 0's (validate_broadcast, transport.cpp:332-349: a mismatch poisons
+  // the group), non-roots copy from the root's buffer, and a second
+  // rendezvous keeps the root's buffer alive until every copy is done.
+  void broadcast(void* data, size_t nbytes, int root) override {
+    Board& b = *b_;
+    std::unique_lock<std::mutex> lk(b.mu);
+    b.ptrs[rank_] = data;
+    b.bcast[rank_] = {root, nbytes};
+    b.enter(lk, rank_, 7);
+    const int r0 = b.bcast[0].first;
+    const size_t n0 = b.bcast[0].second;
+    std::string bad;
+    if (r0 < 0 || r0 >= size_) bad = "broadcast root " + std::to_string(r0) + " out of range";
+    for (int q = 1; q < size_ && bad.empty(); ++q)
+      if (b.bcast[q].first != r0 || b.bcast[q].second != n0)
+        bad = "broadcast argument mismatch at rank " + std::to_string(q);
+    if (!bad.empty()) {
+      b.poisoned = true;
+      if (b.reason.empty()) b.reason = bad;
+      b.cv.notify_all();
+      protocol_error(bad);
+    }
+    const void* src = b.ptrs[r0];
+    lk.unlock();
+    if (rank_ != r0 && nbytes) std::memcpy(data, src, nbytes);
+    lk.lock();
+    b.wait_all(lk);
+  }
+
   // Ranks share the device: a peer's buffer is addressed directly.
   std::vector<void*> map_peers(void* mine) override {
     Board& b = *b_;
@@ -354,6 +389,21 @@ void ipc_unmap_peers(const std::vector<void*>& ptrs, int rank) {
     if (q != rank && ptrs[static_cast<size_t>(q)]) cudaIpcCloseMemHandle(ptrs[static_cast<size_t>(q)]);
 }
 
+// Broadcast arguments checked over an all-gather (validate_broadcast,
+// transport.cpp:332-349): every rank sees every rank's (root, nbytes) and
+// raises the same ProtocolError.
+void bcast_check(int root, size_t nbytes, int size,
+                 const std::function<void(const void*, size_t, void*)>& gather) {
+  const long long mine[2] = {root, static_cast<long long>(nbytes)};
+  std::vector<long long> all(2 * static_cast<size_t>(size));
+  gather(mine, sizeof(mine), all.data());
+  const long long r0 = all[0], n0 = all[1];
+  if (r0 < 0 || r0 >= size) protocol_error("broadcast root " + std::to_string(r0) + " out of range");
+  for (int q = 1; q < size; ++q)
+    if (all[2 * static_cast<size_t>(q)] != r0 || all[2 * static_cast<size_t>(q) + 1] != n0)
+      protocol_error("broadcast argument mismatch at rank " + std::to_string(q));
+}
+
 // --------------------------------------------------------------------------
 // Host-callback transport: one process per rank (several may share a GPU)
 // with the caller's host all-gather (e.g. torch.distributed over gloo) as the
@@ -406,6 +456,15 @@ class HostComm final : public Comm {
     char b = 0;
     std::vector<char> all(static_cast<size_t>(size_));
     gather(&b, 1, all.data());
+  }
+  // (root, nbytes) are gathered and checked first, then every rank's bytes
+  // (the root's slice is kept).
+  void broadcast(void* data, size_t nbytes, int root) override {
+    bcast_check(root, nbytes, size_, [this](const void* a, size_t b, void* c) { gather(a, b, c); });
+    if (!nbytes) return;
+    std::vector<char> all(nbytes * static_cast<size_t>(size_));
+    gather(data, nbytes, all.data());
+    if (rank_ != root) std::memcpy(data, all.data() + nbytes * static_cast<size_t>(root), nbytes);
   }
   // Every rank gathers all (color, key) pairs, then the groups are created
   // through the caller's group callback in ascending color order with
@@ -488,6 +547,7 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
   static NcclApi& get() {
@@ -511,6 +571,7 @@ struct NcclApi {
       api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
       api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
       api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+      api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
       api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
     });
     if (!api.h || !api.GetUniqueId || !api.Send || !api.CommSplit)
@@ -585,6 +646,25 @@ class NcclComm final : public Comm {
   void barrier() override {
     double x = 0.0;
     allreduce(&x, 1, 0);
+  }
+
+  // (root, nbytes) are checked over the all-gather, then the bytes move by
+  // ncclBroadcast through the device staging buffer.
+  void broadcast(void* data, size_t nbytes, int root) override {
+    bcast_check(root, nbytes, size_, [this](const void* a, size_t b, void* c) { gather_bytes(a, b, c); });
+    auto& api = NcclApi::get();
+    if (!api.Broadcast) throw Error(SDNS_CUDA_ERROR, "ncclBroadcast not found");
+    const size_t chunk = sizeof(double) * static_cast<size_t>(kMaxVals) * static_cast<size_t>(size_);
+    char* h = static_cast<char*>(data);
+    for (size_t off = 0; off < nbytes; off += chunk) {
+      const size_t b = std::min(chunk, nbytes - off);
+      if (rank_ == root)
+        SDNS_CUDA(cudaMemcpyAsync(dbuf_, h + off, b, cudaMemcpyHostToDevice, side_));
+      nccl_check(api.Broadcast(dbuf_, dbuf_, b, ncclInt8, root, comm_, side_), "ncclBroadcast");
+      if (rank_ != root)
+        SDNS_CUDA(cudaMemcpyAsync(h + off, dbuf_, b, cudaMemcpyDeviceToHost, side_));
+      SDNS_CUDA(cudaStreamSynchronize(side_));
+    }
   }
 
   // CUDA IPC handles of every rank's buffer, exchanged over the

@@ -1370,6 +1370,13 @@ int sdns_comm_allreduce(sdns_comm* c, double* v, int n, int op) {
     c->c->allreduce(v, n, op);
   });
 }
+int sdns_comm_broadcast_bytes(sdns_comm* c, void* data, int64_t nbytes, int root) {
+  return guarded([&] {
+    if (nbytes < 0) config_error("broadcast: negative size");
+    if (nbytes && !data) config_error("broadcast: NULL buffer");
+    c->c->broadcast(data, static_cast<size_t>(nbytes), root);
+  });
+}
 int sdns_comm_destroy(sdns_comm* c) {
   return guarded([&] { delete c; });
 }

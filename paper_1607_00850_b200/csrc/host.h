@@ -62,6 +62,9 @@ class Comm {
   // 1 max, 2 min) like InProcessComm (transport.cpp:319-329).
   virtual void allreduce(double* v, int n, int op) = 0;
   virtual void barrier() = 0;
+  // broadcast_bytes (transport.hpp:62): root's `nbytes` host bytes into
+  // every rank's `data`; root and nbytes must agree across ranks.
+  virtual void broadcast(void* data, size_t nbytes, int root) = 0;
   // Split by color, ordered by (key, rank) (transport.hpp:66-67).
   virtual std::shared_ptr<Comm> split(int color, int key) = 0;
   virtual int device() const = 0;

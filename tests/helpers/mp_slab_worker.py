@@ -29,6 +29,7 @@ def main():
         return [p.numpy().tobytes() for p in parts]
 
     comm = S.Comm.host(world, rank, 0, allgather, new_group=dist.new_group)
+    bc = comm.broadcast_bytes(bytes([rank + 1]) * 24, root=world - 1)
     geom = {}
     if len(sys.argv) > 7:
         geom = dict(decomp="pencil", p1=int(sys.argv[6]), p2=int(sys.argv[7]))
@@ -54,7 +55,7 @@ def main():
         fft.forward(ur, fu)
         np.savez(os.path.join(out, f"r{rank}.npz"), du=du.download(), u=uo.download(),
                  ur=ur.download(), fu=fu.download(), e=stats.energy, z=stats.enstrophy,
-                 transposes=c.transposes)
+                 transposes=c.transposes, bcast=np.frombuffer(bc, dtype=np.uint8))
         st.close()
     comm.close()
     dist.barrier()

@@ -81,6 +81,7 @@ def test_multiprocess_peer_direct_bitwise(tmp_path, world, grid):
     for r in range(world):
         d = np.load(tmp_path / f"r{r}.npz")
         assert str(d["transposes"]) == "peer-direct"
+        assert d["bcast"].tolist() == [world] * 24  # broadcast_bytes from the last rank
         assert np.array_equal(d["du"], ref[r][0])
         assert np.array_equal(d["u"], ref[r][1])
         assert float(d["e"]) == ref[r][2] and float(d["z"]) == ref[r][3]

@@ -164,6 +164,10 @@ def test_nccl_backend_single_rank():
     comm = S.Comm.nccl(uid, 1, 0, 0)
     assert comm.size == 1 and comm.rank == 0
     assert comm.allreduce([1.5, -2.0], "sum").tolist() == [1.5, -2.0]
+    big = np.random.default_rng(2).bytes(100_000)  # > one staging chunk
+    assert comm.broadcast_bytes(big, root=0) == big
+    with pytest.raises(S.ProtocolError, match="out of range"):
+        comm.broadcast_bytes(b"ab", root=1)
     n = 32
     lo = S.build_layout(S.SolverConfig(n=n), 0)
     uh0 = S.iso_init(n, lo)

@@ -80,6 +80,34 @@ def test_all_to_all_random_tables_round_trip():
         assert list(res[r]) == want
 
 
+def test_broadcast_from_a_non_zero_root():  # test_transport.cpp:95-103
+    want = np.arange(10, 15, dtype=np.int32).tobytes()
+
+    def body(rank, comm):
+        buf = want if rank == 2 else bytes(len(want))
+        return comm.broadcast_bytes(buf, root=2)
+    assert S.run_group(4, body) == [want] * 4
+
+
+def test_broadcast_argument_mismatch_raises_everywhere():  # transport.cpp:332-349
+    errors = []
+
+    def body(rank, comm):
+        try:
+            comm.broadcast_bytes(bytes(8 if rank == 0 else 16), root=0)
+        except S.ProtocolError as e:
+            errors.append(str(e))
+            raise
+    with pytest.raises(S.ProtocolError):
+        S.run_group(3, body, timeout_s=10.0)
+    assert len(errors) == 3 and all("broadcast argument mismatch" in e for e in errors)
+
+    def bad_root(rank, comm):
+        comm.broadcast_bytes(b"x", root=5)
+    with pytest.raises(S.ProtocolError, match="out of range"):
+        S.run_group(2, bad_root, timeout_s=10.0)
+
+
 def test_mismatched_collectives_raise_protocol_error_everywhere():  # :119-137
     errors = []
 
@@ -149,5 +177,9 @@ def test_loopback_transport():  # :40-58
         assert list(c.allreduce([1.5, -2.0], "max")) == [1.5, -2.0]
         torch.cuda.set_device(0)
         assert list(_a2a(c, [3], [3], [1.0, 2.0, 3.0])) == [1.0, 2.0, 3.0]
+        b = np.array([7.0, 8.0]).tobytes()
+        assert c.broadcast_bytes(b, root=0) == b
+        with pytest.raises(S.ProtocolError, match="root must be 0"):
+            c.broadcast_bytes(b, root=1)
     finally:
         c.close()
