@@ -1415,8 +1415,8 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
       config_error("communicator size " + std::to_string(comm->c->size()) +
                    " does not match configured p=" + std::to_string(cfg->p));
     if (comm->c->rank() != rank) config_error("communicator rank does not match layout rank");
-    if (!is_pow2(cfg->n) || cfg->n < 8 || cfg->n > 1024)
-      config_error("the sm_100a path supports power-of-two n in [8, 1024], got n=" +
+    if (!is_pow2(cfg->n) || cfg->n < 4 || cfg->n > 1024)
+      config_error("the sm_100a path supports power-of-two n in [4, 1024], got n=" +
                    std::to_string(cfg->n));
     if (cfg->decomp == SDNS_PENCIL && (!is_pow2(cfg->p1) || !is_pow2(cfg->p2) ||
                                        cfg->p2 > sdns_dev::kMaxSeg))

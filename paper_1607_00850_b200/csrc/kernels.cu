@@ -1140,7 +1140,7 @@ void l2_local(const double* a, const double* b, long long count, double* d_parti
 // ---------------------------------------------------------------------------
 // Dispatch over the (power-of-two) transform length
 
-#define SDNS_FOR_N(X) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
+#define SDNS_FOR_N(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
 
 template <int MODE>
 static void rk_update_mode(const XfArgs& a, const SpecGeom& g, cudaStream_t s) {

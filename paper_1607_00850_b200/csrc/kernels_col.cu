@@ -736,7 +736,7 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
 // ---------------------------------------------------------------------------
 // Launchers
 
-#define SDNS_FOR_N(X) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
+#define SDNS_FOR_N(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
 
 static int num_sms() {
   static int sms = 0;

@@ -31,7 +31,7 @@ def ctx_for(n, nu=0.01, dt=0.01, steps=10, out_every=1, dealias=True):
 
 # --- transforms ------------------------------------------------------------------
 
-@pytest.mark.parametrize("n", [8, 16, 32, 64, 128, 256])
+@pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128, 256])
 def test_fft_forward_inverse_vs_numpy(n):
     rng = np.random.default_rng(42 + n)
     u = rng.uniform(-1, 1, (3, n, n, n))
@@ -135,7 +135,7 @@ def test_compute_rhs_matches_reference_golden():
             assert rel(du.download(), GOLD[key_out]) <= 1e-12
 
 
-@pytest.mark.parametrize("n", [16, 32, 64])
+@pytest.mark.parametrize("n", [4, 16, 32, 64])
 def test_compute_rhs_vs_numpy_oracle(n):
     rng = np.random.default_rng(n)
     wm = O.Wavenumbers(n)
@@ -232,6 +232,33 @@ def test_config1_taylor_green_64_100_steps_vs_reference(ref):
         assert abs(r.enstrophy - gr[2]) <= 1e-12 * gr[2]
         assert r.divergence_max <= 1e-10
     assert rel(final, gf) <= 1e-11
+
+
+def test_smallest_mesh_n4_10_steps_vs_reference(ref):
+    """n = 4, the smallest mesh the reference accepts (config.cpp:18-19):
+    10 RK4 steps of a random solenoidal field against the compiled reference."""
+    n, nu, dt = 4, 1e-2, 1e-2
+    rng = np.random.default_rng(44)
+    wm = O.Wavenumbers(n)
+    uh0 = O.project(O.forward(rng.uniform(-1, 1, (3, n, n, n))), wm) / n**3
+    gs, gf = ref.run(uh0, n, nu, dt, 10, out_every=1, init_project=False, p=2)
+    rows, final = run_gpu(n, uh0, nu, dt, 10, project_init=False)
+    for r, gr in zip(rows, gs):
+        assert abs(r.energy - gr[1]) <= 1e-12 * gr[1]
+        assert abs(r.enstrophy - gr[2]) <= 1e-12 * gr[2]
+    assert rel(final, gf) <= 1e-11
+
+
+def test_smallest_mesh_n4_decompositions_agree(tmp_path):
+    """n = 4 over slab p = 1, 2, 4 and pencil 2x2 (ranks as threads): the
+    same Taylor-Green samples."""
+    got = []
+    for i, geom in enumerate([dict(), dict(p=2), dict(p=4), dict(decomp="pencil", p=4, p1=2, p2=2)]):
+        cfg = S.SolverConfig(n=4, nu=1e-2, dt=1e-2, t_end=0.05, out_every=1, **geom)
+        r = S.run(cfg, S.RunOptions(out_dir=str(tmp_path / str(i))))
+        got.append([(st.energy, st.enstrophy) for _, st in r.samples])
+    for g in got[1:]:
+        assert np.allclose(g, got[0], rtol=1e-13, atol=0)
 
 
 @pytest.mark.parametrize("n", [32, 64])
@@ -435,6 +462,8 @@ def test_config_errors():
         S.Context(S.SolverConfig(n=12))  # not a power of two on the GPU path
     with pytest.raises(S.ConfigError):
         S.Context(S.SolverConfig(n=7))
+    with pytest.raises(S.ConfigError):
+        S.Context(S.SolverConfig(n=2))  # the reference's own minimum is 4
     with ctx_for(8) as c:
         u = c.spectral_field()
         with pytest.raises(S.ConfigError):
