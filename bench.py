@@ -1,21 +1,25 @@
 #!/usr/bin/env python
 """Benchmark of the B200-native RK4 step (BASELINE.json metric).
 
-Workload: BASELINE configs[2] -- seeded isotropic field at n = 512^3 fp64,
-nu = 5e-4, dt = 5e-4, slab decomposition along x over N GPUs (N = 1 fits one
-B200: ~21 GB). One "step" = one classical RK4 step (4 fused RHS evaluations)
-plus the post-step projection, exactly the reference's bench step
+Workload (default): BASELINE configs[2] -- seeded isotropic field at n = 512^3
+fp64, nu = 5e-4, dt = 5e-4, slab decomposition along x over N GPUs (N = 1
+fits one B200: ~21 GB). `--n 1024 --decomp pencil` is configs[3] (1024^3,
+pencil 2x4 at 8 GPUs; `--decomp slab` for its slab 1x8 comparison). One
+"step" = one classical RK4 step (4 fused RHS evaluations) plus the post-step
+projection, exactly the reference's bench step
 (proj/core/src/runner.cpp:356-359).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--n 512]
-  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
-  python bench.py --impl reference   # the reference C++ solver on host cores
+                  [--decomp slab|pencil] [--p1 P1 --p2 P2]
+  python bench.py --gpus 2          # re-launches itself under torch.distributed.run
+  python bench.py --impl reference  # the reference C++ solver on host cores
 
 Prints ONE JSON line on rank 0.
 """
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -26,15 +30,25 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+NVL_FALLBACK = 900.0   # GB/s per direction, NVLink 5 spec (no measured figure)
+NU_DT = {64: (0.01, 0.01), 256: (1e-3, 1e-3), 512: (5e-4, 5e-4), 1024: (2.5e-4, 2.5e-4)}
 
 
 def peaks():
+    """(HBM GB/s, its source, NVLink GB/s per direction, its source)."""
+    hbm, hsrc = HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+    nvl, nsrc = NVL_FALLBACK, "fallback: NVLink 5 spec 900 GB/s per direction (no measured figure)"
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        hbm, hsrc = float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        for k in ("nvlink_gbs", "nvlink_gbs_per_dir", "p2p_gbs"):
+            if k in d:
+                nvl, nsrc = float(d[k]), f"measured (MEASURED_PEAKS.json {k})"
+                break
     except Exception:  # noqa: BLE001
-        return HBM_FALLBACK, "fallback"
+        pass
+    return hbm, hsrc, nvl, nsrc
 
 
 def spectral_bytes(n, p):
@@ -42,10 +56,48 @@ def spectral_bytes(n, p):
     return 16.0 * n * n * (n // 2 + 1) / p
 
 
+def a2a_fraction(decomp, p, p1, p2):
+    """Share of a rank's transposed bytes that leave the GPU."""
+    if p <= 1:
+        return 0.0
+    if decomp == "slab":
+        return (p - 1) / p
+    return (p1 - 1) / p1 + (p2 - 1) / p2
+
+
+def step_roofline(n, decomp, p, p1, p2, hbm_gbs, nvl_gbs):
+    """BASELINE.md §3 / SURVEY §8(d): per GPU and step, HBM = 213 C/p bytes,
+    all-to-all egress = 36 (C/p) f; roofline = the slower of the two."""
+    C = spectral_bytes(n, p)
+    hbm = 213.0 * C
+    a2a = 36.0 * C * a2a_fraction(decomp, p, p1, p2)
+    t_h = hbm / hbm_gbs / 1e6
+    t_n = a2a / nvl_gbs / 1e6
+    return {"hbm_bytes_per_step": hbm, "a2a_bytes_per_step": a2a, "t_hbm_ms": t_h,
+            "t_nvlink_ms": t_n, "roofline_ms": max(t_h, t_n),
+            "bound": "nvlink" if t_n > t_h else "hbm"}
+
+
 # Algorithmic HBM bytes per launch, in units of C (SURVEY.md §8(d) table).
 PASS_BYTES_C = {"x_inv_curl": 8, "y_inv": 11, "z_fused": 9, "y_fwd": 6, "x_fwd_fft": 6, "x_fwd_rk0": 12,
                 "x_fwd_rk12": 18, "x_fwd_rk3": 21, "x_fwd_tail": 12}
-STEP_BYTES_C = 213
+
+
+def pass_a2a_c(name, decomp, p, p1, p2):
+    """Fields a pass stores into peers' buffers (peer-direct transposes,
+    DESIGN §5) times the fraction that leaves the GPU, in units of C."""
+    if p <= 1:
+        return 0.0
+    if decomp == "slab":
+        f = (p - 1) / p
+        return {"x_inv_curl": 5 * f, "y_fwd": 3 * f}.get(name, 0.0)
+    f1, f2 = (p1 - 1) / p1, (p2 - 1) / p2
+    return {"x_inv_curl": 5 * f1, "y_inv": 6 * f2, "z_fused": 3 * f2, "y_fwd": 3 * f1}.get(name, 0.0)
+
+
+def default_grid(world):
+    """Pencil grids of the reference's bench matrix (config_file.cpp:51-61)."""
+    return {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}.get(world, (1, world))
 
 
 class ClockSampler:
@@ -64,7 +116,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -122,52 +174,125 @@ def pow2_floor(x):
     return p
 
 
-def reference_timing(n, nu, dt, warmup, units, unit, threads):
-    """Times the UNMODIFIED reference (oracle/_ref) on `threads` host cores."""
-    from oracle import ref
-    if not ref.available():
-        raise RuntimeError("oracle/_ref/libsdns_ref.so not built")
-    p = min(pow2_floor(max(1, threads)), n)
-    sec = ref.time_units(n, p=p, nu=nu, dt=dt, warmup=warmup, units=units, unit=unit)
-    return sec, p
+def resolve(args, world):
+    """Decomposition of the GPU job and the config dict both arms print."""
+    n = args.n
+    decomp = args.decomp or "slab"
+    p1, p2 = 1, 1
+    if decomp == "pencil":
+        p1, p2 = (args.p1, args.p2) if args.p1 and args.p2 else default_grid(world)
+        if p1 * p2 != world:
+            raise SystemExit(f"pencil grid {p1}x{p2} does not match {world} ranks")
+    nu, dt = NU_DT.get(n, (5e-4, 5e-4))
+    if n == 1024:
+        wl = f"configs[3]: isotropic 1024^3 fp64, nu={nu:g}, dt={dt:g}, " + (
+            f"pencil {p1}x{p2}" if decomp == "pencil" else f"slab 1x{world}")
+    elif n == 512:
+        wl = f"configs[2]: isotropic 512^3 fp64, nu={nu:g}, dt={dt:g}, " + (
+            f"pencil {p1}x{p2}" if decomp == "pencil" else f"slab x {world}")
+    else:
+        wl = f"isotropic {n}^3 fp64, nu={nu:g}, dt={dt:g}, {decomp} x {world}"
+    C = spectral_bytes(n, world)
+    config = {"workload": wl, "n": n, "decomp": decomp, "p": world, "p1": p1, "p2": p2,
+              "nu": nu, "dt": dt, "seed": 1607, "global_points": n**3,
+              "l2": "inputs larger than L2 (u_hat alone is %.2f GB per rank)" % (3 * C / 1e9)}
+    return config
+
+
+def relaunch(args):
+    """`bench.py --gpus N` without torchrun: re-exec under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+# --- reference arm -------------------------------------------------------------
+
+REF_BUDGET_S = 240.0
 
 
 def run_reference(args):
+    """The UNMODIFIED reference (oracle/_ref: proj/core compiled against the
+    FFTW shim) timed on the host's cores with the reference's own bench method
+    (rk4_step + project per step between barriers, runner.cpp:336-373), on the
+    same seeded isotropic input (restated in the oracle), threads-as-ranks."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    n, nu, dt = args.n, 5e-4, 5e-4
+    config = resolve(args, world)
+    n, nu, dt = config["n"], config["nu"], config["dt"]
+    from oracle import ref
     threads = cpu_threads()
-    # Bounded sample per step: one compute_rhs (1/4 of the RK4 step's RHS
-    # work) at the full size, scaled to steps/s by x4 -- the step's 36 FFTs
-    # are 4 identical RHS evaluations; RK4 updates are excluded (optimistic
-    # for the reference).
-    unit = "rhs" if n >= 256 else "step"
-    # One untimed unit sizes the run: K units are timed, capped so the whole
-    # reference arm stays within a few minutes of host time.
-    warm_s, p = reference_timing(n, nu, dt, 0, 1, unit, threads)
-    units = max(1, min(args.steps, int(150.0 / max(warm_s, 1e-3))))
-    sec, p = reference_timing(n, nu, dt, 0, units, unit, threads)
-    step_s = sec * (4.0 if unit == "rhs" else 1.0)
-    value = 1.0 / step_s
-    line = {
-        "metric": "RK4 steps/s", "value": value, "unit": "steps/s", "impl": "reference",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Taylor-Green init)",
-        "config": {"workload": f"configs[2]: iso/TG {n}^3 fp64 RK4, slab", "n": n,
-                   "decomp": "slab", "p_cpu": p},
-        "ns_per_gridpoint_step": step_s * 1e9 / n**3,
-        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": p, "kind": "reference",
-                         "sample": (f"{units} x one compute_rhs at {n}^3 (x4 per step), "
-                                    f"after 1 untimed unit" if unit == "rhs"
-                                    else f"{units} RK4 steps at {n}^3"),
-                         "fft": "self-written FFTW guru64 shim (no libfftw3 in image)"},
-        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
+    p = min(pow2_floor(max(1, threads)), n)
+    base = {"metric": "RK4 steps/s", "unit": "steps/s", "impl": "reference", "n_gpus": world,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded isotropic field, BASELINE configs[2] construction)",
+            "config": config}
+    if not ref.available():
+        print(json.dumps({**base, "unavailable": "oracle/_ref/libsdns_ref.so not built"}))
+        return
+    if n > 512:
+        # ~36 C of host RAM (310 GB at 1024^3): beyond the box
+        print(json.dumps({**base, "value": None, "steps": 0, "warmup": 0,
+                          "unavailable": f"reference at {n}^3 needs ~{36 * spectral_bytes(n, 1) / 1e9:.0f} GB "
+                                         "of host RAM (SURVEY §8(d))"}))
+        return
+    uh0 = ref.iso_init(n, seed=1607)
+    # size the run: one compute_rhs (a quarter of a step's transforms) probes
+    probe = ref.time_units(n, p=p, nu=nu, dt=dt, warmup=0, units=1, unit="rhs", uhat0=uh0)
+    est = 4.2 * probe
+    warm, steps = args.warmup, args.steps
+    if (warm + steps) * est > REF_BUDGET_S:
+        warm = min(warm, 1)
+        steps = max(1, min(steps, int((REF_BUDGET_S - warm * est) / est)))
+    sec = ref.time_units(n, p=p, nu=nu, dt=dt, warmup=warm, units=steps, unit="step", uhat0=uh0)
+    value = 1.0 / sec
+    line = {**base, "value": value, "steps": steps, "warmup": warm, "ms_per_step": sec * 1e3,
+            "requested": {"steps": args.steps, "warmup": args.warmup},
+            "ns_per_gridpoint_step": sec * 1e9 / n**3,
+            "cpu_baseline": {"value": value, "unit": "steps/s", "cores": p, "kind": "reference",
+                             "sample": f"{steps} whole RK4 steps (rk4_step + project) at {n}^3 on the "
+                                       f"iso field after {warm} warm-up step(s), {p} threads-as-ranks "
+                                       "(slab), the reference's bench method (runner.cpp:336-373)",
+                             "fft": "self-written FFTW guru64 shim (no libfftw3 in image)"},
+            "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    if not args.no_cpu1:
+        s1 = ref.time_units(n, p=1, nu=nu, dt=dt, warmup=0, units=1, unit="rhs", uhat0=uh0)
+        line["cpu_p1"] = {"sec_per_rhs": s1, "est_sec_per_step": 4 * s1, "cores": 1,
+                          "sample": f"one compute_rhs at {n}^3 on 1 thread (p_cpu = 1), "
+                                    "x4 for a step (RK4 vector updates excluded)"}
+    try:
+        line["host"] = {"threads": threads, "nproc": os.cpu_count(),
+                        "mem_gb": os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 1e9}
+    except Exception:  # noqa: BLE001
+        pass
     print(json.dumps(line), flush=True)
 
+
+def cpu_baseline_leg(config):
+    """Our arm's cpu_baseline (rank 0, N = 1): whole reference steps on the
+    same iso input, bounded (1 warm-up + 2 timed steps at 512^3, ~30 s)."""
+    from oracle import ref
+    n, nu, dt = config["n"], config["nu"], config["dt"]
+    if not ref.available() or n > 512:
+        raise RuntimeError("reference unavailable at this size")
+    p = min(pow2_floor(cpu_threads()), n)
+    uh0 = ref.iso_init(n, seed=1607)
+    steps = 2 if n >= 512 else 5
+    sec = ref.time_units(n, p=p, nu=nu, dt=dt, warmup=1, units=steps, unit="step", uhat0=uh0)
+    return {"value": 1.0 / sec, "unit": "steps/s", "cores": p, "kind": "reference",
+            "sample": f"{steps} whole RK4 steps (rk4_step + project) at {n}^3 on the iso field "
+                      f"after 1 warm-up step, {p} threads-as-ranks (slab)",
+            "fft": "self-written FFTW guru64 shim (no libfftw3 in image)"}
+
+
+# --- our arm -------------------------------------------------------------------
 
 def other_configs(S, ctx, peak):
     """The other BASELINE configs, measured quickly beside the headline line
@@ -231,7 +356,9 @@ def other_configs(S, ctx, peak):
             st.advance(hook)
             c.sync()
             sec = time.perf_counter() - t0
+            rf = step_roofline(m, "slab", 1, 1, 1, peak, NVL_FALLBACK)
             out[key] = {"steps_per_s": steps / sec, "ms_per_step": sec / steps * 1e3,
+                        "step_roofline_frac": rf["roofline_ms"] / (sec / steps * 1e3),
                         "samples": len(rows), "energy_last": rows[-1].energy}
             st.close()
     return out
@@ -246,6 +373,9 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    config = resolve(args, world)
+    n, nu, dt = config["n"], config["nu"], config["dt"]
+    decomp, p1, p2 = config["decomp"], config["p1"], config["p2"]
     # --transport host (a harness check, not a bench): ranks share the GPUs
     # present round-robin over the host-callback transport (gloo all-gathers,
     # CUDA IPC), e.g. 2 ranks on one GPU
@@ -256,6 +386,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         if args.transport == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # the communicator log names every rank
             dist.init_process_group("nccl", device_id=torch.device("cuda", device))
             uid = [S.Comm.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
@@ -272,11 +403,10 @@ def run_ours(args):
             comm = S.Comm.host(world, rank, device, allgather, new_group=dist.new_group)
     else:
         comm = S.Comm.loopback()
-    local = device
 
-    n, nu, dt = args.n, 5e-4, 5e-4
-    cfg = S.SolverConfig(n=n, p=world, nu=nu, dt=dt, t_end=args.steps * dt)
-    ctx = S.Context(cfg, rank=rank, device=local, comm=comm)
+    cfg = S.SolverConfig(n=n, decomp=decomp, p=world, p1=p1, p2=p2, nu=nu, dt=dt,
+                         t_end=args.steps * dt)
+    ctx = S.Context(cfg, rank=rank, device=device, comm=comm)
     transposes = ctx.transposes if world > 1 else "none (p = 1)"
     lo = ctx.layout
     t0 = time.time()
@@ -286,11 +416,19 @@ def run_ours(args):
     u = ctx.spectral_field().upload(uh0)
     state.set(u)
     u.free()
+    del uh0
     stream = torch.cuda.ExternalStream(ctx.stream)
 
     def barrier():
         if dist is not None:
             dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], device=red_dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     for _ in range(args.warmup):
         state.rk4_step(dt, post_project=True, check=True)
@@ -298,7 +436,7 @@ def run_ours(args):
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx.timing(True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(device) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
@@ -308,33 +446,25 @@ def run_ours(args):
     barrier()
     passes = ctx.timing_read()
     ctx.timing(False)
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     finite = state.rk4_step(dt, post_project=True, check=True)
     stats = S.collect_stats(ctx, state.u_hat, nu)
-    if dist is not None:
-        t = torch.tensor([ms], device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
 
     # --- e2e: reference-facing host-buffer API (pinned host u_hat in/out) ---
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    host = np.empty((3,) + tuple(lo.spec_shape), dtype=np.complex128)
-    nbytes = host.nbytes
+    shape = (3,) + tuple(lo.spec_shape)
+    nbytes = int(np.prod(shape)) * 16
     pinned = S.load_library().sdns_host_alloc(nbytes)
     hbuf = np.ctypeslib.as_array((S.ctypes.c_double * (nbytes // 8)).from_address(pinned))
     hbuf[:] = state.u_hat.download().view(np.float64).ravel()
-    hview = hbuf.view(np.complex128).reshape(host.shape)
+    hview = hbuf.view(np.complex128).reshape(shape)
     state.step_host(hview, dt, 1)  # warm
     barrier()
     te = time.perf_counter()
     for _ in range(e2e_steps):
         state.step_host(hview, dt, 1)
     barrier()
-    e2e_s = (time.perf_counter() - te) / e2e_steps
-    if dist is not None:
-        t = torch.tensor([e2e_s], device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks((time.perf_counter() - te) / e2e_steps)
     S.load_library().sdns_host_free(pinned)
 
     if rank != 0:
@@ -344,7 +474,7 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
-    peak, peak_kind = peaks()
+    hbm_peak, hbm_src, nvl_peak, nvl_src = peaks()
     C = spectral_bytes(n, world)
     ncu_bytes = {}
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -360,35 +490,46 @@ def run_ours(args):
     for k, v in passes.items():
         if v[1] > 0:
             per_pass[k]["share"] = v[0] / max(kernel_total, 1e-30) if not k.startswith("a2a") else None
+            if k in PASS_BYTES_C:
+                per_pass[k]["hbm_frac_alg"] = PASS_BYTES_C[k] * C / (v[0] / v[1] * 1e-3) / 1e9 / hbm_peak
             if k in ncu_bytes:  # DRAM bytes per launch (ncu) / live launch time
                 gbs = ncu_bytes[k] / (v[0] / v[1] * 1e-3) / 1e9
                 per_pass[k]["dram_gbs"] = gbs
-                per_pass[k]["dram_frac"] = gbs / peak
+                per_pass[k]["dram_frac"] = gbs / hbm_peak
     launches = sum(v[1] for k, v in passes.items() if not k.startswith("a2a"))
     dom = max((k for k in per_pass if k in PASS_BYTES_C), key=lambda k: passes[k][0])
     dom_ms = per_pass[dom]["avg_ms"]
     dom_bytes = PASS_BYTES_C[dom] * C
-    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
-    traffic = ncu_bytes.get(dom)
-    step_bytes = STEP_BYTES_C * C
-    step_gbs = step_bytes / (ms * 1e-3) / 1e9
+    dom_nvl = pass_a2a_c(dom, decomp, world, p1, p2) * C
+    t_hbm, t_nvl = dom_bytes / hbm_peak, dom_nvl / nvl_peak
+    if t_nvl > t_hbm:
+        roof = {"bound": "nvlink", "achieved": dom_nvl / (dom_ms * 1e-3) / 1e9, "peak": nvl_peak,
+                "unit": "GB/s", "peak_source": nvl_src, "algorithmic_bytes_per_launch": dom_nvl,
+                "hbm_bytes_per_launch": dom_bytes}
+    else:
+        roof = {"bound": "hbm", "achieved": dom_bytes / (dom_ms * 1e-3) / 1e9, "peak": hbm_peak,
+                "unit": "GB/s", "peak_source": hbm_src, "algorithmic_bytes_per_launch": dom_bytes,
+                "nvlink_bytes_per_launch": dom_nvl}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = ncu_bytes.get(dom)
+    roof["kernel"] = dom
+    sr = step_roofline(n, decomp, world, p1, p2, hbm_peak, nvl_peak)
+    sr["frac"] = sr["roofline_ms"] / ms
+    sr["achieved_hbm_gbs"] = sr["hbm_bytes_per_step"] / (ms * 1e-3) / 1e9
+    sr["peaks"] = {"hbm_gbs": hbm_peak, "hbm_source": hbm_src, "nvlink_gbs": nvl_peak,
+                   "nvlink_source": nvl_src}
     value = 1e3 / ms  # steps/s of the whole job (strong scaling: one problem on N GPUs)
     line = {
         "metric": "RK4 steps/s", "value": value, "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded isotropic field, BASELINE configs[2] construction)",
-        "config": {"workload": f"configs[2]: isotropic {n}^3 fp64, nu=5e-4, dt=5e-4, slab x {world}",
-                   "n": n, "decomp": "slab", "p": world, "global_points": n**3,
-                   "transposes": transposes, "transport": args.transport if world > 1 else "loopback",
-                   "l2": "inputs larger than L2 (u_hat alone is %.1f GB per rank)" % (3 * C / 1e9)},
+        "config": config,
+        "transposes": transposes,
+        "transport": args.transport if world > 1 else "loopback",
         "ns_per_gridpoint_step": ms * 1e6 / n**3,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": dom,
-                     "algorithmic_bytes_per_launch": dom_bytes,
-                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
-        "step_roofline": {"bytes_per_step": step_bytes, "achieved_gbs": step_gbs,
-                          "frac": step_gbs / peak, "roofline_ms": step_bytes / peak / 1e6},
+        "roofline": roof,
+        "step_roofline": sr,
         "passes": per_pass,
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -401,20 +542,12 @@ def run_ours(args):
     }
     if world == 1 and n == 512 and not args.no_other_configs:
         state.close()
-        line["other_configs"] = other_configs(S, ctx, peak)
+        line["other_configs"] = other_configs(S, ctx, hbm_peak)
     state.close()
     ctx.close()
     if world == 1 and not args.no_cpu_baseline:
         try:
-            threads = cpu_threads()
-            unit = "rhs" if n >= 256 else "step"
-            sec, p = reference_timing(n, nu, dt, 0, 1, unit, threads)
-            step_s = sec * (4.0 if unit == "rhs" else 1.0)
-            line["cpu_baseline"] = {
-                "value": 1.0 / step_s, "unit": "steps/s", "cores": p, "kind": "reference",
-                "sample": (f"one compute_rhs at {n}^3 on {p} threads-as-ranks, x4 per RK4 step"
-                           if unit == "rhs" else f"one RK4 step at {n}^3"),
-                "fft": "self-written FFTW guru64 shim (no libfftw3 in image)"}
+            line["cpu_baseline"] = cpu_baseline_leg(config)
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": "steps/s", "cores": 0,
                                     "kind": "reference", "sample": f"unavailable: {e}"}
@@ -429,14 +562,20 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--decomp", choices=["slab", "pencil"], default=None)
+    ap.add_argument("--p1", type=int, default=0)
+    ap.add_argument("--p2", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu1", action="store_true", help="reference arm: skip the p_cpu = 1 sample")
     ap.add_argument("--no-other-configs", action="store_true")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
                     help="N > 1: NCCL (one GPU per rank) or the host-callback transport "
                          "(harness check; ranks may share a GPU)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

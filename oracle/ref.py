@@ -42,6 +42,9 @@ def lib():
         L.sdns_ref_spectrum_shells.argtypes = [I]
         L.sdns_ref_forward.argtypes = [I, I, I, I, I, P, P]
         L.sdns_ref_inverse.argtypes = [I, I, I, I, I, P, P]
+        L.sdns_ref_forward_scalar.argtypes = [I, I, I, I, I, I, P, P]
+        L.sdns_ref_inverse_scalar.argtypes = [I, I, I, I, I, I, P, P]
+        L.sdns_ref_iso_init.argtypes = [I, ctypes.c_ulonglong, D, D, P]
         L.sdns_ref_compute_rhs.argtypes = [I, I, I, I, I, D, I, P, P]
         L.sdns_ref_spectral_op.argtypes = [I, I, I, P, P]
         L.sdns_ref_cross.argtypes = [ctypes.c_int64, P, P, P]
@@ -92,6 +95,34 @@ def inverse(uh, n, decomp="slab", p=1, p1=1, p2=1):
     uh = np.ascontiguousarray(uh, dtype=np.complex128)
     out = np.zeros((3, n, n, n), dtype=np.float64)
     _check(lib().sdns_ref_inverse(n, DECOMP[decomp], p, p1, p2, _p(uh), _p(out)))
+    return out
+
+
+def iso_init(n, seed=1607, k0=4.0, energy=0.5):
+    """The seeded isotropic field, GLOBAL (3, n, n, n//2+1), restated in the
+    oracle (ref_driver.cpp sdns_ref_iso_init)."""
+    out = np.empty((3, n, n, n // 2 + 1), dtype=np.complex128)
+    _check(lib().sdns_ref_iso_init(n, seed, k0, energy, _p(out)))
+    return out
+
+
+def forward_scalar(u, n, decomp="slab", p=1, p1=1, p2=1):
+    """Component-wise forward through the scalar DistributedFFT overload
+    (fft.cpp:59-63); u is (ncomp, n, n, n)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    ncomp = u.shape[0]
+    out = np.empty((ncomp, n, n, n // 2 + 1), dtype=np.complex128)
+    _check(lib().sdns_ref_forward_scalar(n, DECOMP[decomp], p, p1, p2, ncomp, _p(u), _p(out)))
+    return out
+
+
+def inverse_scalar(uh, n, decomp="slab", p=1, p1=1, p2=1):
+    """Component-wise normalised inverse through the scalar overload
+    (fft.cpp:65-69); uh is (ncomp, n, n, n//2+1)."""
+    uh = np.ascontiguousarray(uh, dtype=np.complex128)
+    ncomp = uh.shape[0]
+    out = np.empty((ncomp, n, n, n), dtype=np.float64)
+    _check(lib().sdns_ref_inverse_scalar(n, DECOMP[decomp], p, p1, p2, ncomp, _p(uh), _p(out)))
     return out
 
 

@@ -22,6 +22,8 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <cmath>
 #include <vector>
 
 #include "sdns/checkpoint.hpp"
@@ -200,6 +202,174 @@ int sdns_ref_inverse(int n, int decomp, int p, int p1, int p2,
       std::lock_guard lk(mu);
       gather_real(f, n, lo.real, u);
     });
+  });
+}
+
+/// Distributed forward transform of `ncomp` global real components through
+/// the SCALAR overload DistributedFFT::forward(const RealField&, SpectralField&)
+/// (proj/core/src/fft.cpp:59-63), one component at a time; needs only one
+/// component's worth of reference buffers (used for the 1024^3 pins).
+int sdns_ref_forward_scalar(int n, int decomp, int p, int p1, int p2, int ncomp,
+                            const double* u, double* uhat) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, decomp, p, p1, p2, 0.0, 1.0, 0.0, 1, 1);
+    const std::int64_t nn = n, nf = n / 2 + 1;
+    group(p, [&](int rank, std::shared_ptr<Communicator> comm) {
+      const RankLayout lo = build_layout(cfg, rank);
+      DistributedFFT fft(cfg, lo, comm);
+      const Extents3& rx = lo.real;
+      const Extents3& sx = lo.spec;
+      RealField f(rx.shape);
+      SpectralField fu(sx.shape);
+      for (int c = 0; c < ncomp; ++c) {
+        const double* g = u + c * nn * nn * nn;
+        for (std::int64_t i = 0; i < rx.shape.n0; ++i)
+          for (std::int64_t j = 0; j < rx.shape.n1; ++j)
+            for (std::int64_t k = 0; k < rx.shape.n2; ++k)
+              f(i, j, k) = g[((rx.offset[0] + i) * nn + rx.offset[1] + j) * nn + rx.offset[2] + k];
+        fft.forward(f, fu);
+        double* o = uhat + 2 * c * nn * nn * nf;
+        for (std::int64_t i = 0; i < sx.shape.n0; ++i)
+          for (std::int64_t j = 0; j < sx.shape.n1; ++j)
+            for (std::int64_t k = 0; k < sx.shape.n2; ++k) {
+              const std::int64_t m = spec_index(nn, nf, sx, i, j, k);
+              o[2 * m] = fu(i, j, k).real();
+              o[2 * m + 1] = fu(i, j, k).imag();
+            }
+      }
+    });
+  });
+}
+
+/// Normalised inverse of `ncomp` global spectral components through the
+/// scalar overload DistributedFFT::inverse (proj/core/src/fft.cpp:65-69).
+int sdns_ref_inverse_scalar(int n, int decomp, int p, int p1, int p2, int ncomp,
+                            const double* uhat, double* u) {
+  return guarded([&] {
+    const SolverConfig cfg = make_cfg(n, decomp, p, p1, p2, 0.0, 1.0, 0.0, 1, 1);
+    const std::int64_t nn = n, nf = n / 2 + 1;
+    group(p, [&](int rank, std::shared_ptr<Communicator> comm) {
+      const RankLayout lo = build_layout(cfg, rank);
+      DistributedFFT fft(cfg, lo, comm);
+      const Extents3& rx = lo.real;
+      const Extents3& sx = lo.spec;
+      RealField f(rx.shape);
+      SpectralField fu(sx.shape);
+      for (int c = 0; c < ncomp; ++c) {
+        const double* g = uhat + 2 * c * nn * nn * nf;
+        for (std::int64_t i = 0; i < sx.shape.n0; ++i)
+          for (std::int64_t j = 0; j < sx.shape.n1; ++j)
+            for (std::int64_t k = 0; k < sx.shape.n2; ++k) {
+              const std::int64_t m = spec_index(nn, nf, sx, i, j, k);
+              fu(i, j, k) = Complex(g[2 * m], g[2 * m + 1]);
+            }
+        fft.inverse(fu, f);
+        double* o = u + c * nn * nn * nn;
+        for (std::int64_t i = 0; i < rx.shape.n0; ++i)
+          for (std::int64_t j = 0; j < rx.shape.n1; ++j)
+            for (std::int64_t k = 0; k < rx.shape.n2; ++k)
+              o[((rx.offset[0] + i) * nn + rx.offset[1] + j) * nn + rx.offset[2] + k] = f(i, j, k);
+      }
+    });
+  });
+}
+
+/// Oracle restatement of the seeded isotropic initial field (BASELINE
+/// configs 2-4), GLOBAL array (3, n, n, n/2+1).
+/// The reference has no such case, so the construction is restated here from
+/// the survey's recipe, independently of the product's csrc/iso_init.cpp, and
+/// a CPU test pins the two bit for bit: counter-based Box-Muller Gaussians
+/// keyed by (seed, component, global index), E(k) = k^4 exp(-2 (k/k0)^2)
+/// amplitudes, zero DC / Nyquist, Hermitian kz = 0 plane (the lexicographically
+/// smaller of (i, j) and (-i, -j) is drawn, the other is its conjugate), the
+/// reference project() per mode (navier_stokes.cpp:85-102), energy scaled to
+/// `energy` with the Hermitian weights (diagnostics.cpp:41-48), per-x-plane
+/// sums added in x order.
+int sdns_ref_iso_init(int n, unsigned long long seed, double k0, double energy,
+                      double* out) {
+  return guarded([&] {
+    const std::int64_t N = n, nf = n / 2 + 1, h = n / 2;
+    auto mix = [](std::uint64_t x) {
+      x += 0x9E3779B97F4A7C15ULL;
+      x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+      x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+      return x ^ (x >> 31);
+    };
+    auto kw = [&](std::int64_t j) { return static_cast<double>(j < h ? j : j - N); };
+    const std::uint64_t key = mix(seed);
+    // value of global mode (i, j, k), projected, before the energy scale
+    auto mode = [&](std::int64_t i, std::int64_t j, std::int64_t k, Complex v[3]) {
+      for (int c = 0; c < 3; ++c) v[c] = Complex(0.0, 0.0);
+      if ((i | j | k) == 0 || i == h || j == h || k == h) return;
+      bool flip = false;
+      if (k == 0) {
+        const std::int64_t mi = (N - i) % N, mj = (N - j) % N;
+        if (mi * N + mj < i * N + j) {
+          i = mi;
+          j = mj;
+          flip = true;
+        }
+      }
+      const double kx = kw(i), ky = kw(j), kz = static_cast<double>(k);
+      const double k2 = kx * kx + ky * ky + kz * kz;
+      const double kk = std::sqrt(k2);
+      const double amp = std::sqrt(k2 * k2 * std::exp(-2.0 * (kk / k0) * (kk / k0)) /
+                                   (4.0 * M_PI * k2));
+      const std::uint64_t g = static_cast<std::uint64_t>((i * N + j) * nf + k);
+      for (int c = 0; c < 3; ++c) {
+        const std::uint64_t ctr = (g * 3 + static_cast<std::uint64_t>(c)) * 2;
+        const double a = (static_cast<double>(mix(key ^ mix(ctr)) >> 11) + 1.0) * 0x1.0p-53;
+        const double b = (static_cast<double>(mix(key ^ mix(ctr + 1)) >> 11) + 1.0) * 0x1.0p-53;
+        const double r = std::sqrt(-2.0 * std::log(a));
+        v[c] = Complex(amp * r * std::cos(2.0 * M_PI * b), amp * r * std::sin(2.0 * M_PI * b));
+      }
+      const double inv = k2 > 0.0 ? 1.0 / k2 : 0.0;
+      const double ko[3] = {kx * inv, ky * inv, kz * inv};
+      const double dr = kx * v[0].real() + ky * v[1].real() + kz * v[2].real();
+      const double di = kx * v[0].imag() + ky * v[1].imag() + kz * v[2].imag();
+      for (int c = 0; c < 3; ++c) {
+        const double re = v[c].real() - ko[c] * dr;
+        const double im = v[c].imag() - ko[c] * di;
+        v[c] = Complex(re, flip ? -im : im);
+      }
+    };
+    unsigned nth = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    std::vector<double> plane(static_cast<std::size_t>(N), 0.0);
+    const std::int64_t comp = N * N * nf;
+    std::vector<std::thread> pool;
+    for (unsigned w = 0; w < nth; ++w)
+      pool.emplace_back([&, w] {
+        Complex v[3];
+        for (std::int64_t i = w; i < N; i += nth) {
+          double acc = 0.0;
+          for (std::int64_t j = 0; j < N; ++j)
+            for (std::int64_t k = 0; k < nf; ++k) {
+              mode(i, j, k, v);
+              const double e = std::norm(v[0]) + std::norm(v[1]) + std::norm(v[2]);
+              acc += (k == 0 || k == h ? 1.0 : 2.0) * e;
+              const std::int64_t m = (i * N + j) * nf + k;
+              for (int c = 0; c < 3; ++c) {
+                out[2 * (c * comp + m)] = v[c].real();
+                out[2 * (c * comp + m) + 1] = v[c].imag();
+              }
+            }
+          plane[static_cast<std::size_t>(i)] = acc;
+        }
+      });
+    for (auto& t : pool) t.join();
+    double sum = 0.0;
+    for (double v : plane) sum += v;
+    const double n3 = static_cast<double>(N) * static_cast<double>(N) * static_cast<double>(N);
+    const double e0 = 0.5 * sum / (n3 * n3);
+    const double scale = e0 > 0.0 ? std::sqrt(energy / e0) : 0.0;
+    pool.clear();
+    for (unsigned w = 0; w < nth; ++w)
+      pool.emplace_back([&, w] {
+        for (std::int64_t q = std::int64_t{w} * 4096; q < 6 * comp; q += std::int64_t{nth} * 4096)
+          for (std::int64_t r = q; r < std::min<std::int64_t>(q + 4096, 6 * comp); ++r)
+            out[r] *= scale;
+      });
+    for (auto& t : pool) t.join();
   });
 }
 

@@ -161,6 +161,14 @@ def test_iso_field_is_decomposition_independent(decomp, p, p1, p2):
         assert np.array_equal(S.iso_init(n, lo), g[:, o0:o0 + s0, o1:o1 + s1, o2:o2 + s2])
 
 
+@pytest.mark.parametrize("n,seed", [(8, 1607), (16, 3), (64, 1607)])
+def test_iso_field_matches_oracle_restatement(ref, n, seed):
+    """The product's iso_init (csrc/iso_init.cpp) and the oracle's independent
+    restatement of SURVEY §8(d)'s recipe (oracle/ref_driver.cpp) agree bit
+    for bit; the reference arm of bench.py builds its input from the latter."""
+    assert np.array_equal(_global_iso(n, seed), ref.iso_init(n, seed=seed))
+
+
 def test_iso_field_is_seeded():
     a, b = _global_iso(16, 1), _global_iso(16, 2)
     assert not np.array_equal(a, b) and np.array_equal(a, _global_iso(16, 1))

@@ -5,6 +5,10 @@ cannot follow, plus one mid-size trajectory against the reference.
   components, slab and pencil) and 1024^3 (1 component, one GPU);
 * config 2 at 256^3: 10 RK4 steps vs the compiled reference (16 host
   threads), E/Z <= 1e-12 relative per step, velocity rel L2 <= 1e-11;
+* config 3 at 512^3 (the bench workload): 10 RK4 steps at p = 1, slab 4 and
+  pencil 2x2 against ONE reference run, same bars;
+* the n = 512 and n = 1024 transforms against the reference's own
+  DistributedFFT (every mode, plus direct DFT sums of random modes);
 * config 3 at 512^3: energy balance dE/dt = -2 nu Z (acceptance criterion 4,
   proj/core/src/verification.cpp:246-253) and divergence-free evolution;
 * the NCCL backend on a 1-rank communicator (dlopen, init, grouped
@@ -94,21 +98,33 @@ def test_config2_256_ten_steps_vs_reference(ref):
     assert rel(final, gf) <= 1e-11
 
 
-@pytest.mark.skipif(os.environ.get("SDNS_FULL_PARITY") != "1",
-                    reason="full-size reference run (~2-4 min of host time): SDNS_FULL_PARITY=1")
-@pytest.mark.parametrize("geom", [dict(p=1), dict(p=4), dict(decomp="pencil", p=4, p1=2, p2=2)])
-def test_config3_512_ten_steps_vs_reference(ref, geom):
-    """north_star's parity bar at the bench workload (BASELINE configs[2],
-    512^3): u after 10 RK4 steps within 1e-11 relative L2 of the reference,
-    E and Z per step within 1e-12; the reference on the host's cores."""
-    n, nu, dt, steps = 512, 5e-4, 5e-4, 10
-    lo = S.build_layout(S.SolverConfig(n=n), 0)
-    uh0 = S.iso_init(n, lo, seed=1607)
+def _ref_threads():
     threads = max(1, min(16, len(os.sched_getaffinity(0))))
     p = 1
     while p * 2 <= threads:
         p *= 2
-    gs, gf = ref.run(uh0, n, nu, dt, steps, out_every=1, init_project=False, p=p)
+    return p
+
+
+@pytest.fixture(scope="module")
+def ref512(ref):
+    """ONE reference run at the bench workload (BASELINE configs[2]: iso 512^3,
+    nu = dt = 5e-4, 10 RK4 steps, E/Z sampled every step), on the host's
+    cores as threads-as-ranks; shared by every geometry below."""
+    n, nu, dt, steps = 512, 5e-4, 5e-4, 10
+    lo = S.build_layout(S.SolverConfig(n=n), 0)
+    uh0 = S.iso_init(n, lo, seed=1607)
+    gs, gf = ref.run(uh0, n, nu, dt, steps, out_every=1, init_project=False, p=_ref_threads())
+    return uh0, gs, gf
+
+
+@pytest.mark.parametrize("geom", [dict(p=1), dict(p=4), dict(decomp="pencil", p=4, p1=2, p2=2)])
+def test_config3_512_ten_steps_vs_reference(ref512, geom):
+    """north_star's parity bar at the bench workload (BASELINE configs[2],
+    512^3): u after 10 RK4 steps within 1e-11 relative L2 of the reference,
+    E and Z per step within 1e-12; the reference on the host's cores."""
+    n, nu, dt, steps = 512, 5e-4, 5e-4, 10
+    uh0, gs, gf = ref512
     cfg = S.SolverConfig(n=n, nu=nu, dt=dt, t_end=steps * dt, out_every=1, **geom)
 
     def body(rank, comm):
@@ -131,10 +147,69 @@ def test_config3_512_ten_steps_vs_reference(ref, geom):
     for r, g in zip(rows, gs):
         assert abs(r.energy - g[1]) <= 1e-12 * g[1]
         assert abs(r.enstrophy - g[2]) <= 1e-12 * g[2]
+        assert spectrum_close(r.spectrum, g[5:], g[1], rtol=1e-10)
     err = rel(final, gf)
     print(f"512^3 {cfg.decomp} p={cfg.p}: rel L2(u_hat) after {steps} steps = {err:.3e}; "
           f"E {rows[-1].energy!r} vs {gs[-1][1]!r}")
     assert err <= 1e-11
+
+
+def _chunked_maxabs(a, b):
+    """max |a - b| and max |b| over the leading axes without n^3 temporaries."""
+    d = m = 0.0
+    for i in range(a.shape[0]):
+        for j in range(0, a.shape[1], 64):
+            x, y = a[i, j:j + 64], b[i, j:j + 64]
+            d = max(d, float(np.abs(x - y).max()))
+            m = max(m, float(np.abs(y).max()))
+    return d, m
+
+
+@pytest.mark.parametrize("n", [512, 1024])
+def test_fft_full_size_vs_reference(ref, n):
+    """The n = 512 and n = 1024 transform kernels (register-twiddle stages,
+    chunked layouts, 16-element threads and 4-column tiles at 1024) against
+    the reference's own DistributedFFT (scalar overload, fft.cpp:59-69) on
+    one seeded uniform[-1,1) component: every mode of the forward within
+    1e-11 max|X| (the bar of proj/tests/test_fft.cpp:73-110), the inverse of
+    the reference's spectrum within 1e-13 max|u|, and a handful of random
+    non-DC modes against a direct DFT sum."""
+    u = _uniform(n, 1, 4242 + n)
+    want = ref.forward_scalar(u, n, p=_ref_threads())
+    with S.Context(S.SolverConfig(n=n)) as c:
+        fft = S.DistributedFFT(c)
+        ud = c.real_field(1).upload(u)
+        fd = c.spectral_field(1)
+        fft.forward(ud, fd)
+        got = fd.download()
+        ud.free()
+        d, m = _chunked_maxabs(got, want)
+        assert d <= 1e-11 * m, (d, m)
+        # a few modes away from DC, against the defining sum (exact in fp64
+        # to ~1e-9 relative of the field's L1 norm)
+        rng = np.random.default_rng(n)
+        x = 2 * np.pi * np.arange(n) / n
+        u0 = u[0]
+        for _ in range(4):
+            kx, ky, kz = (int(v) for v in rng.integers(1, n // 2, 3))
+            # real matrix-vector products only (no complex n^3 temporary)
+            zc = u0 @ np.cos(kz * x) - 1j * (u0 @ np.sin(kz * x))  # (x, y)
+            ey = np.exp(-1j * ky * x)
+            ex = np.exp(-1j * kx * x)
+            direct = ex @ (zc @ ey)
+            assert abs(got[0, kx, ky, kz] - direct) <= 1e-9 * np.abs(u0).sum() / n ** 1.5, \
+                (kx, ky, kz, got[0, kx, ky, kz], direct)
+        del got
+        # inverse of the REFERENCE spectrum (so a forward error cannot cancel)
+        fd.upload(want)
+        back = c.real_field(1)
+        fft.inverse(fd, back)
+        b = back.download()
+    rb = ref.inverse_scalar(want, n, p=_ref_threads())
+    d, m = _chunked_maxabs(b, rb)
+    assert d <= 1e-13 * max(m, 1.0), (d, m)
+    d, m = _chunked_maxabs(b, u)
+    assert d <= 1e-12, d
 
 
 def test_config3_512_energy_balance_and_divergence():
