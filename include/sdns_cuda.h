@@ -154,6 +154,15 @@ int sdns_comm_destroy(sdns_comm* c);
  * collective of the group fails with SDNS_PROTOCOL_ERROR naming `reason`; a
  * no-op on transports without shared state (loopback, NCCL, host). */
 int sdns_comm_poison(sdns_comm* c, const char* reason);
+/* Collective deadline in seconds (the reference's collective_timeout,
+ * runner.hpp:15, default 30 s; <= 0: none). On the NCCL and host-callback
+ * transports every host wait on a stream holding the group's collectives
+ * polls the stream and the transport (ncclCommGetAsyncError): a peer that
+ * stalls past the deadline raises SDNS_TIMEOUT_ERROR, an asynchronous
+ * transport error SDNS_PROTOCOL_ERROR (transport.cpp:105-140), the
+ * communicator is aborted (ncclCommAbort) and every later collective on it
+ * fails with the same status. Children made by split inherit the deadline. */
+int sdns_comm_set_timeout(sdns_comm* c, double seconds);
 /* split(color, key): members ordered by (key, rank) (transport.hpp:66-67). */
 int sdns_comm_split(sdns_comm* c, int color, int key, sdns_comm** out);
 /* all_to_all_bytes (transport.hpp:55-58, BlockTable :18-35) on DEVICE

@@ -71,6 +71,10 @@ class CudaError(SdnsError):
     code = 6
 
 
+# the reference's name (types.hpp:41-44); CollectiveTimeout does not shadow
+# the builtin inside this module
+TimeoutError = CollectiveTimeout  # noqa: A001
+
 _ERRORS = {1: ConfigError, 2: ProtocolError, 3: CollectiveTimeout, 4: DivergenceError,
            5: IoError, 6: CudaError}
 
@@ -225,6 +229,7 @@ def load_library(path: str = LIB_PATH):
             "sdns_comm_split": (I, [P, I, I, PP]),
             "sdns_comm_poison": (I, [P, ctypes.c_char_p]),
             "sdns_comm_host_init": (I, [I, I, I, ALLGATHER_FN, GROUP_FN, P, PP]),
+            "sdns_comm_set_timeout": (I, [P, D]),
             "sdns_ctx_transposes": (I, [P]),
             "sdns_comm_all_to_all_bytes": (I, [P, P, P, P, P, P]),
             "sdns_config_defaults": (V, [ctypes.POINTER(_Config)]),
@@ -465,8 +470,11 @@ class Comm:
                     return 1
                 ctypes.memmove(recv, buf, len(buf))
                 return 0
-            except BaseException:  # noqa: BLE001
-                return 1
+            except BaseException as e:  # noqa: BLE001
+                # a peer that stalled or died surfaces as the caller's
+                # transport timeout (gloo: "Timed out waiting ... ms")
+                m = str(e).lower()
+                return 2 if ("timed out" in m or "timeout" in m) else 1
 
         def gcb(ranks, n, user, child):
             try:
@@ -487,6 +495,13 @@ class Comm:
         c = Comm(h)
         c._keep = (fn, gfn, groups)  # the callbacks must outlive the communicator
         return c
+
+    def set_timeout(self, seconds: float) -> "Comm":
+        """Collective deadline (reference collective_timeout, default 30 s):
+        past it a host wait raises TimeoutError and the communicator is
+        aborted; later collectives fail fast with the same error."""
+        _check(self._lib.sdns_comm_set_timeout(self._h, float(seconds)))
+        return self
 
     @property
     def rank(self) -> int:

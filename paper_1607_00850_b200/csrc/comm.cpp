@@ -21,6 +21,7 @@
 #include <functional>
 #include <map>
 #include <mutex>
+#include <thread>
 
 #include "host.h"
 
@@ -29,6 +30,37 @@ namespace sdns_host {
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
     throw Error(SDNS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void Comm::wait(cudaStream_t s) { SDNS_CUDA(cudaStreamSynchronize(s)); }
+
+void Comm::check_failed() const {
+  if (failed_) throw Error(failed_, "communicator failed earlier: " + failed_why_);
+}
+
+void Comm::fail(int code, const std::string& why) {
+  abandon(code, why);
+  throw Error(code, why);
+}
+
+// Spins briefly (the common case: the stream is about to drain), then sleeps
+// between polls; the deadline counts from the call.
+void Comm::poll_wait(cudaStream_t s, const std::function<int(std::string&)>& health) {
+  check_failed();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (long it = 0;; ++it) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) cuda_check(q, "cudaStreamQuery");
+    std::string why;
+    if (health)
+      if (const int code = health(why)) fail(code, why);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_s_ > 0.0 && el > timeout_s_)
+      fail(SDNS_TIMEOUT_ERROR, "collective timed out after " + std::to_string(timeout_s_) +
+                                   " s waiting for peers (rank " + std::to_string(rank_) + ")");
+    if (it > 2000) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
 }
 
 namespace {
@@ -497,7 +529,9 @@ class HostComm final : public Comm {
         my_rank = static_cast<int>(std::find(ranks.begin(), ranks.end(), rank_) - ranks.begin());
       }
     }
-    return std::make_shared<HostComm>(my_rank, my_size, device_, fn_, gfn_, my_user);
+    auto child = std::make_shared<HostComm>(my_rank, my_size, device_, fn_, gfn_, my_user);
+    child->set_timeout(timeout_s_);
+    return child;
   }
   std::vector<void*> map_peers(void* mine) override {
     return ipc_map_peers(
@@ -508,6 +542,7 @@ class HostComm final : public Comm {
         });
   }
   void unmap_peers(const std::vector<void*>& ptrs) override { ipc_unmap_peers(ptrs, rank_); }
+  void wait(cudaStream_t s) override { poll_wait(s, nullptr); }
   void stream_barrier(cudaStream_t s) override {
     SDNS_CUDA(cudaEventRecord(ev_, s));
     barrier();
@@ -517,8 +552,15 @@ class HostComm final : public Comm {
   }
 
  private:
+  // The callback returns 0, or 2 when the caller's transport timed out (a
+  // peer stalled or died), any other value for other failures.
   void gather(const void* send, size_t bytes, void* recv) {
-    if (fn_(send, bytes, recv, user_) != 0) protocol_error("host all-gather callback failed");
+    check_failed();
+    const int rc = fn_(send, bytes, recv, user_);
+    if (rc == 2)
+      fail(SDNS_TIMEOUT_ERROR, "host all-gather timed out waiting for peers (rank " +
+                                   std::to_string(rank_) + ")");
+    if (rc != 0) fail(SDNS_PROTOCOL_ERROR, "host all-gather callback failed");
   }
   int device_;
   sdns_allgather_fn fn_;
@@ -549,6 +591,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 
   static NcclApi& get() {
     static NcclApi api;
@@ -573,6 +617,9 @@ struct NcclApi {
       api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
       api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
       api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+      api.CommGetAsyncError =
+          reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
+      api.CommAbort = reinterpret_cast<decltype(api.CommAbort)>(sym("ncclCommAbort"));
     });
     if (!api.h || !api.GetUniqueId || !api.Send || !api.CommSplit)
       throw Error(SDNS_CUDA_ERROR, "NCCL (libnccl.so.2) could not be loaded");
@@ -607,7 +654,24 @@ class NcclComm final : public Comm {
   int device() const override { return device_; }
   const char* kind() const override { return "nccl"; }
 
+  // Polls the stream and ncclCommGetAsyncError: an asynchronous NCCL error
+  // raises ProtocolError, a peer that stalls past the deadline TimeoutError;
+  // either aborts the communicator (ncclCommAbort) so nothing blocks on it.
+  void wait(cudaStream_t s) override {
+    auto& api = NcclApi::get();
+    poll_wait(s, [this, &api](std::string& why) {
+      if (!api.CommGetAsyncError || !comm_) return 0;
+      ncclResult_t st = 0;
+      if (api.CommGetAsyncError(comm_, &st) != 0) return 0;
+      if (st == 0 || st == kInProgress) return 0;
+      why = std::string("NCCL asynchronous error on rank ") + std::to_string(rank_) + ": " +
+            (api.GetErrorString ? api.GetErrorString(st) : "nccl error");
+      return static_cast<int>(SDNS_PROTOCOL_ERROR);
+    });
+  }
+
   void alltoall(const std::vector<Xfer>& xs, cudaStream_t s) override {
+    check_failed();
     auto& api = NcclApi::get();
     nccl_check(api.GroupStart(), "ncclGroupStart");
     for (const Xfer& x : xs) {
@@ -629,6 +693,7 @@ class NcclComm final : public Comm {
         allreduce(v + off, std::min(kMaxVals, n - off), op);
       return;
     }
+    check_failed();
     auto& api = NcclApi::get();
     double* mine = dbuf_ + static_cast<size_t>(kMaxVals) * size_;
     SDNS_CUDA(cudaMemcpyAsync(mine, v, sizeof(double) * n, cudaMemcpyHostToDevice, side_));
@@ -637,7 +702,7 @@ class NcclComm final : public Comm {
     std::vector<double> all(static_cast<size_t>(n) * size_);
     SDNS_CUDA(cudaMemcpyAsync(all.data(), dbuf_, sizeof(double) * n * size_,
                               cudaMemcpyDeviceToHost, side_));
-    SDNS_CUDA(cudaStreamSynchronize(side_));
+    wait(side_);
     std::vector<double> acc(all.begin(), all.begin() + n);
     for (int q = 1; q < size_; ++q) fold(acc.data(), all.data() + static_cast<size_t>(q) * n, n, op);
     std::memcpy(v, acc.data(), sizeof(double) * n);
@@ -651,6 +716,7 @@ class NcclComm final : public Comm {
   // (root, nbytes) are checked over the all-gather, then the bytes move by
   // ncclBroadcast through the device staging buffer.
   void broadcast(void* data, size_t nbytes, int root) override {
+    check_failed();
     bcast_check(root, nbytes, size_, [this](const void* a, size_t b, void* c) { gather_bytes(a, b, c); });
     auto& api = NcclApi::get();
     if (!api.Broadcast) throw Error(SDNS_CUDA_ERROR, "ncclBroadcast not found");
@@ -663,7 +729,7 @@ class NcclComm final : public Comm {
       nccl_check(api.Broadcast(dbuf_, dbuf_, b, ncclInt8, root, comm_, side_), "ncclBroadcast");
       if (rank_ != root)
         SDNS_CUDA(cudaMemcpyAsync(h + off, dbuf_, b, cudaMemcpyDeviceToHost, side_));
-      SDNS_CUDA(cudaStreamSynchronize(side_));
+      wait(side_);
     }
   }
 
@@ -686,6 +752,7 @@ class NcclComm final : public Comm {
   // on a rank only after every rank's stream reached it, and the producing
   // kernels end with a system-scope fence on their peer stores.
   void stream_barrier(cudaStream_t s) override {
+    check_failed();
     auto& api = NcclApi::get();
     if (!api.AllReduce) throw Error(SDNS_CUDA_ERROR, "ncclAllReduce not found");
     nccl_check(api.AllReduce(tok_, tok_, 1, ncclFloat64, 0 /* ncclSum */, comm_, s),
@@ -693,6 +760,7 @@ class NcclComm final : public Comm {
   }
 
   std::shared_ptr<Comm> split(int color, int key) override {
+    check_failed();
     auto& api = NcclApi::get();
     ncclComm_t nc = nullptr;
     nccl_check(api.CommSplit(comm_, color, key, &nc, nullptr), "ncclCommSplit");
@@ -707,11 +775,19 @@ class NcclComm final : public Comm {
       const int kq = static_cast<int>(all[2 * q + 1]);
       if (kq < key || (kq == key && q < rank_)) ++my;
     }
-    return std::make_shared<NcclComm>(nc, my, cnt, device_);
+    auto child = std::make_shared<NcclComm>(nc, my, cnt, device_);
+    child->set_timeout(timeout_s_);
+    return child;
   }
 
  private:
   static constexpr int kMaxVals = 4096;
+  static constexpr ncclResult_t kInProgress = 7;  // ncclInProgress
+  void abort_transport() override {
+    auto& api = NcclApi::get();
+    if (comm_ && api.CommAbort) api.CommAbort(comm_);
+    comm_ = nullptr;
+  }
   // Every rank's `bytes` (<= 8 * kMaxVals) in rank order, through the device
   // all-gather.
   void gather_bytes(const void* mine, size_t bytes, void* all) {
@@ -726,7 +802,7 @@ class NcclComm final : public Comm {
     std::vector<double> got(nd * size_);
     SDNS_CUDA(cudaMemcpyAsync(got.data(), dbuf_, sizeof(double) * nd * size_, cudaMemcpyDeviceToHost,
                               side_));
-    SDNS_CUDA(cudaStreamSynchronize(side_));
+    wait(side_);
     for (int q = 0; q < size_; ++q)
       std::memcpy(static_cast<char*>(all) + bytes * q, got.data() + nd * q, bytes);
   }
@@ -736,7 +812,7 @@ class NcclComm final : public Comm {
     SDNS_CUDA(cudaMemcpyAsync(d_mine, mine, sizeof(double) * 2, cudaMemcpyHostToDevice, side_));
     nccl_check(api.AllGather(d_mine, dbuf_, 2, ncclFloat64, comm_, side_), "ncclAllGather");
     SDNS_CUDA(cudaMemcpyAsync(all, dbuf_, sizeof(double) * 2 * size_, cudaMemcpyDeviceToHost, side_));
-    SDNS_CUDA(cudaStreamSynchronize(side_));
+    wait(side_);
   }
   ncclComm_t comm_ = nullptr;
   int device_ = 0;

@@ -132,6 +132,17 @@ struct sdns_ctx {
   // kz segments [q][x_l][y_l][pitch_q].
   bool pencil = false;
   std::shared_ptr<Comm> row, col;
+  // Host wait for the context stream through the world communicator's
+  // watchdog (Comm::wait); a failure also abandons the pencil sub-groups.
+  void wait() {
+    try {
+      world->wait(stream);
+    } catch (const Error& e) {
+      for (auto* g : {&row, &col})
+        if (*g) (*g)->abandon(e.code, e.what());
+      throw;
+    }
+  }
   double2* wc = nullptr;
   double2* wd = nullptr;
   long long cs_c = 0, cs_d = 0;
@@ -1047,7 +1058,7 @@ bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool wa
   st->step += 1;
   if (!want_flag) return true;
   SDNS_CUDA(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  SDNS_CUDA(cudaStreamSynchronize(c->stream));
+  c->wait();
   double ok = *c->h_flag != 0 ? 1.0 : 0.0;
   c->world->allreduce(&ok, 1, 2);
   return ok > 0.5;
@@ -1064,7 +1075,7 @@ void stats_impl(sdns_ctx* c, const sdns_field* u, double nu, double t, double* r
   const int stride = c->shells + 3;
   SDNS_CUDA(cudaMemcpyAsync(c->h_out, src, sizeof(double) * stride, cudaMemcpyDeviceToHost,
                             c->stream));
-  SDNS_CUDA(cudaStreamSynchronize(c->stream));
+  c->wait();
   std::vector<double> sums(static_cast<size_t>(2 + c->shells));
   sums[0] = c->h_out[0];
   sums[1] = c->h_out[1];
@@ -1148,7 +1159,7 @@ void ck_exchange(sdns_ctx* c, const std::vector<int64_t>& cnt, double* mine, dou
     off += cnt[static_cast<size_t>(q)];
   }
   c->world->alltoall(xs, c->stream);
-  SDNS_CUDA(cudaStreamSynchronize(c->stream));
+  c->wait();
 }
 
 void checkpoint_write_impl(sdns_ctx* c, const sdns_field* u, const std::string& path, double t,
@@ -1383,6 +1394,9 @@ int sdns_comm_destroy(sdns_comm* c) {
 int sdns_comm_poison(sdns_comm* c, const char* reason) {
   return guarded([&] { c->c->poison(reason ? reason : "poisoned"); });
 }
+int sdns_comm_set_timeout(sdns_comm* c, double seconds) {
+  return guarded([&] { c->c->set_timeout(seconds); });
+}
 int sdns_comm_split(sdns_comm* c, int color, int key, sdns_comm** out) {
   return guarded([&] { *out = new sdns_comm{c->c->split(color, key)}; });
 }
@@ -1402,7 +1416,7 @@ int sdns_comm_all_to_all_bytes(sdns_comm* c, const void* send, const int64_t* se
     SDNS_CUDA(cudaSetDevice(c->c->device()));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     c->c->alltoall(xs, s);
-    if (!stream) SDNS_CUDA(cudaStreamSynchronize(s));
+    if (!stream) c->c->wait(s);
   });
 }
 
@@ -1497,7 +1511,7 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
     c->d_flag = static_cast<int*>(dev_alloc(c.get(), sizeof(int)));
     SDNS_CUDA(cudaMallocHost(&c->h_out, sizeof(double) * stride));
     SDNS_CUDA(cudaMallocHost(&c->h_flag, sizeof(int)));
-    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    c->wait();
     post_launch("ctx create");
     *out = c.release();
   });
@@ -1554,7 +1568,7 @@ int sdns_ctx_transposes(const sdns_ctx* c) { return (c->peer ? 1 : 0) | (c->peer
 int sdns_ctx_sync(sdns_ctx* c) {
   return guarded([&] {
     set_device(c);
-    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    c->wait();
   });
 }
 int64_t sdns_ctx_device_bytes(const sdns_ctx* c) { return c->dev_bytes; }
@@ -1596,7 +1610,7 @@ int sdns_field_upload(sdns_ctx* c, sdns_field* f, const double* host) {
     } else {
       c->copy_spec_all(f->spec(), const_cast<double*>(host), f->ncomp, true);
     }
-    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    c->wait();
   });
 }
 
@@ -1609,7 +1623,7 @@ int sdns_field_download(sdns_ctx* c, const sdns_field* f, double* host) {
     } else {
       c->copy_spec_all(f->spec(), host, f->ncomp, false);
     }
-    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    c->wait();
   });
 }
 
@@ -1821,7 +1835,7 @@ int sdns_rk4_step_host(sdns_ctx* c, sdns_state* st, double* host, double dt, int
     c->copy_spec_all(st->u.spec(), host, 3, true);
     for (int k = 0; k < steps; ++k) step_impl(c, st, dt, 1, false);
     c->copy_spec_all(st->u.spec(), host, 3, false);
-    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    c->wait();
   });
 }
 
@@ -1841,7 +1855,7 @@ int sdns_l2_diff(sdns_ctx* c, const sdns_field* a, const sdns_field* b, double* 
     sdns_dev::l2_local(a->real(), b->real(), c->real_cs * a->ncomp, c->d_partial, c->d_out, c->stream);
     post_launch("l2_diff");
     SDNS_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    c->wait();
     double v = c->h_out[0];
     c->world->allreduce(&v, 1, 0);
     const double n3 = static_cast<double>(c->cfg.n) * c->cfg.n * c->cfg.n;
@@ -1854,7 +1868,7 @@ int sdns_checkpoint_write(sdns_ctx* c, const sdns_field* u, const char* path, do
   return guarded([&] {
     require_real(u, 3, "write_checkpoint");
     set_device(c);
-    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    c->wait();
     checkpoint_write_impl(c, u, path ? path : "", t, step);
   });
 }
@@ -1863,7 +1877,7 @@ int sdns_checkpoint_read(sdns_ctx* c, const char* path, sdns_field* u, double* t
   return guarded([&] {
     require_real(u, 3, "read_checkpoint");
     set_device(c);
-    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    c->wait();
     checkpoint_read_impl(c, path ? path : "", u, t, step);
   });
 }
@@ -1885,7 +1899,7 @@ int sdns_ctx_timing(sdns_ctx* c, int enable) {
 int sdns_ctx_timing_read(sdns_ctx* c, double* ms, int64_t* launches) {
   return guarded([&] {
     set_device(c);
-    SDNS_CUDA(cudaStreamSynchronize(c->stream));
+    c->wait();
     for (int t = 0; t < SDNS_NPASS; ++t) {
       ms[t] = 0.0;
       launches[t] = 0;

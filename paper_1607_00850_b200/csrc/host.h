@@ -87,10 +87,44 @@ class Comm {
   // Work enqueued on `s` after this call starts only after the work every
   // rank enqueued on its stream before the call has completed. Collective.
   virtual void stream_barrier(cudaStream_t s) { (void)s; }
+  // Host wait for stream `s` (which may hold this group's device-side
+  // collectives). Transports whose peers are other processes poll instead of
+  // blocking: a peer that stalls past the timeout, or an asynchronous
+  // transport error, fails the wait -- TimeoutError / ProtocolError, like the
+  // reference's collective deadline (transport.cpp:105-140) -- and poisons
+  // the communicator so every later collective fails fast with the same
+  // error. Loopback and in-process groups block (no remote peer to lose).
+  virtual void wait(cudaStream_t s);
+  // Collective deadline in seconds (reference default 30 s,
+  // runner.hpp:15); <= 0 waits forever.
+  void set_timeout(double s) { timeout_s_ = s; }
+  // Marks the communicator failed without throwing (a sibling group of the
+  // same decomposition failed) and tears the transport down.
+  void abandon(int code, const std::string& why) {
+    if (!failed_) {
+      failed_ = code;
+      failed_why_ = why;
+      abort_transport();
+    }
+  }
+  double timeout() const { return timeout_s_; }
 
  protected:
   Comm(int r, int s) : rank_(r), size_(s) {}
+  // Polling wait shared by the multi-process transports: `health` returns 0
+  // while the transport is sound, else an error code (throws through fail).
+  void poll_wait(cudaStream_t s, const std::function<int(std::string&)>& health);
+  // Marks the communicator failed (code SDNS_TIMEOUT_ERROR or
+  // SDNS_PROTOCOL_ERROR) and throws; later collectives rethrow.
+  [[noreturn]] void fail(int code, const std::string& why);
+  void check_failed() const;
+  // Tears the transport down on failure (NCCL: ncclCommAbort) so no later
+  // call can block on the lost peer.
+  virtual void abort_transport() {}
   int rank_, size_;
+  double timeout_s_ = 30.0;
+  int failed_ = 0;
+  std::string failed_why_;
 };
 
 std::shared_ptr<Comm> make_loopback_comm();

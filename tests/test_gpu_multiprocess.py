@@ -86,3 +86,26 @@ def test_multiprocess_peer_direct_bitwise(tmp_path, world, grid):
         assert np.array_equal(d["u"], ref[r][1])
         assert float(d["e"]) == ref[r][2] and float(d["z"]) == ref[r][3]
         assert np.array_equal(d["ur"], ref[r][4]) and np.array_equal(d["fu"], ref[r][5])
+
+
+def test_stalled_peer_raises_timeout_error(tmp_path):
+    """A rank whose peer stalls inside the step sees TimeoutError (the
+    reference's collective deadline, transport.cpp:105-140) instead of
+    hanging, and the communicator is poisoned: the next collective fails
+    at once with the same error."""
+    worker = os.path.join(ROOT, "tests", "helpers", "mp_stall_worker.py")
+    port = _free_port()
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), str(port), str(tmp_path)], env=env,
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+             for r in range(2)]
+    try:
+        out0 = procs[0].communicate(timeout=240)[0]
+    finally:
+        procs[1].kill()
+        procs[1].communicate()
+    assert procs[0].returncode == 0, out0
+    lines = (tmp_path / "stall.txt").read_text().splitlines()
+    assert lines[0].startswith("TimeoutError"), lines
+    assert lines[1].startswith("barrier TimeoutError"), lines
+    assert float(lines[1].split("after ")[1].split(" s")[0]) < 1.0, lines  # fails fast
