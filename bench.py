@@ -9,7 +9,7 @@ pencil 2x4 at 8 GPUs; `--decomp slab` for its slab 1x8 comparison). One
 projection, exactly the reference's bench step
 (proj/core/src/runner.cpp:356-359).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 512]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--size 512]
                   [--decomp slab|pencil] [--p1 P1 --p2 P2]
   python bench.py --gpus 2          # re-launches itself under torch.distributed.run
   python bench.py --impl reference  # the reference C++ solver on host cores
@@ -207,7 +207,10 @@ def relaunch(args):
         port = s.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
-           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+           f"--master-port={port}", os.path.abspath(__file__)]
+    # torch.distributed.run would read "--n" as an abbreviation of its own options
+    cmd += ["--size" if a == "--n" else ("--size=" + a[4:] if a.startswith("--n=") else a)
+            for a in sys.argv[1:]]
     return subprocess.call(cmd)
 
 
@@ -561,7 +564,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--size", "--n", dest="n", type=int, default=512,
+                    help="grid points per axis (512: configs[2], 1024: configs[3])")
     ap.add_argument("--decomp", choices=["slab", "pencil"], default=None)
     ap.add_argument("--p1", type=int, default=0)
     ap.add_argument("--p2", type=int, default=0)

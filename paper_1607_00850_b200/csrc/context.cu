@@ -328,6 +328,7 @@ struct sdns_ctx {
     g.ps0 = pitch;
     g.ps1 = np * plane();
     g.pb_shift = ilog2(np);
+    g.pblk = np;
     g.nrows = np;
     g.n2 = static_cast<int>(lo.spec_shape[2]);
     g.pitch = pitch;
@@ -399,6 +400,7 @@ struct sdns_ctx {
     g.ps0 = pitch;
     g.ps1 = static_cast<long long>(np) * yl * pitch;
     g.pb_shift = ilog2(yl);
+    g.pblk = yl;
     g.nrows = np;
     g.n2 = static_cast<int>(lo.spec_shape[2]);
     g.pitch = pitch;
@@ -702,6 +704,7 @@ void rhs_slab_peer(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& arg
   int tk = c->tick(SDNS_PASS_X_INV_CURL);
   ColGeom go1 = c->xgeom();
   go1.pb_shift = ilog2(c->np);
+  go1.pblk = c->np;
   go1.ps1 = 0;
   go1.seg = c->d_seg;
   sdns_dev::x_inverse_split(n, u_in, sc, c->wb, sc, c->xgeom(), &go1, c->tw, s);
@@ -766,6 +769,7 @@ void rhs_pipeline(sdns_ctx* c, const double2* u_in, int mode, const XfArgs& args
   } else if (c->peer) {  // pencil: P1 stores into the column peers' wb (see rhs_slab_peer)
     ColGeom go1 = c->xgeom();
     go1.pb_shift = ilog2(c->np);
+    go1.pblk = c->np;
     go1.ps1 = 0;
     go1.seg = c->d_seg;
     sdns_dev::x_inverse_split(n, u_in, c->spec_cs, c->wb, c->spec_cs, c->xgeom(), &go1, c->tw, s);
@@ -939,6 +943,7 @@ void fft_inverse_impl(sdns_ctx* c, const sdns_field* spec, sdns_field* real) {
     c->peer_grp->stream_barrier(s);  // the peers are done with their wb
     ColGeom go = c->xgeom();
     go.pb_shift = ilog2(c->np);
+    go.pblk = c->np;
     go.ps1 = 0;
     go.seg = c->d_seg;
     sdns_dev::col_plain_to(n, +1, spec->spec(), c->wb, c->spec_cs, c->spec_cs, nc, c->xgeom(), go,
@@ -1429,12 +1434,15 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
       config_error("communicator size " + std::to_string(comm->c->size()) +
                    " does not match configured p=" + std::to_string(cfg->p));
     if (comm->c->rank() != rank) config_error("communicator rank does not match layout rank");
-    if (!is_pow2(cfg->n) || cfg->n < 4 || cfg->n > 1024)
-      config_error("the sm_100a path supports power-of-two n in [4, 1024], got n=" +
+    // power-of-two n in [4, 1024] run the tuned kernels, every other even n
+    // (validate: n >= 4, even) the generic mixed-radix ones (kernels_gen.cu);
+    // their z pass holds a line's six half rows and five complex lines in
+    // shared memory
+    if (sdns_dev::gen_z_smem(cfg->n) > 227 * 1024)
+      config_error("the sm_100a path supports n <= 1024, or non-power-of-two n up to 1780, got n=" +
                    std::to_string(cfg->n));
-    if (cfg->decomp == SDNS_PENCIL && (!is_pow2(cfg->p1) || !is_pow2(cfg->p2) ||
-                                       cfg->p2 > sdns_dev::kMaxSeg))
-      config_error("the sm_100a pencil path needs power-of-two p1, p2 (p2 <= 16)");
+    if (cfg->decomp == SDNS_PENCIL && cfg->p2 > sdns_dev::kMaxSeg)
+      config_error("the sm_100a pencil path needs p2 <= 16");
     auto c = std::make_unique<sdns_ctx>();
     c->cfg = *cfg;
     c->lo = build_layout(*cfg, rank);
@@ -1494,7 +1502,7 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
       }
       const char* xl = std::getenv("SDNS_XLAYOUT");
       // (not at 1024^3: a p = 1 RK4 state + work then needs ~157 GB without it)
-      if (cfg->p == 1 && n <= 512 && !(xl && xl[0] == '0')) {
+      if (cfg->p == 1 && n <= 512 && is_pow2(n) && !(xl && xl[0] == '0')) {
         c->cs_x = static_cast<long long>(c->pitch) * c->lo.spec_shape[1] * n;
         c->wx = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * c->cs_x * 5));
         const char* zc = std::getenv("SDNS_ZCHUNK");

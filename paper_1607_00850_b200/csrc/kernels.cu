@@ -24,6 +24,7 @@
 
 #include "fft_core.cuh"
 #include "kernels.cuh"
+#include "rowmap.cuh"
 
 namespace sdns_dev {
 
@@ -102,7 +103,12 @@ __global__ void k_twiddles(int n, int e, double2* tw) {
   }
 }
 
+void make_twiddles_plain(int n, double2* d_tw, cudaStream_t s);  // kernels_gen.cu
 void make_twiddles(int n, double2* d_tw, cudaStream_t s) {
+  if (!tuned_length(n)) {
+    make_twiddles_plain(n, d_tw, s);
+    return;
+  }
   const int total = tw_stage_total(n);
   if (total > 0) k_twiddles<<<(total + 255) / 256, 256, 0, s>>>(n, fft_elems(n), d_tw);
 }
@@ -311,29 +317,6 @@ struct ZCfg {
   static constexpr int HP = N / 2 + 8;  // padded half-row (n/2+1 modes)
 };
 
-// Offset of element kz of z line ri: `ro` = zrow_off for unsegmented maps.
-__device__ __forceinline__ long long zel(const RowMap& rm, long long ro, int ri, int k) {
-  if (rm.cstride) return ro + static_cast<long long>(k >> 3) * rm.cstride + (k & 7);
-  if (rm.nseg == 0) return ro + k;
-  int sg = 0;
-  while (sg + 1 < rm.nseg && k >= rm.seg_k0[sg + 1]) ++sg;
-  return rm.seg_base[sg] + static_cast<long long>(ri) * rm.seg_pitch[sg] + (k - rm.seg_k0[sg]);
-}
-
-__device__ __forceinline__ long long zrow_off(const RowMap& rm, int ri) {
-  if (rm.cstride) {
-    const int x = ri / rm.rpp, y = ri - x * rm.rpp;
-    return static_cast<long long>(x) * rm.xplane + static_cast<long long>(y) * 8;
-  }
-  if (rm.blk == 0) {
-    const int pl = ri / rm.rpp, r = ri - pl * rm.rpp;
-    return (static_cast<long long>(pl) * rm.prow + r) * rm.pitch;
-  }
-  const int xl = ri / rm.ny, y = ri - xl * rm.ny;
-  const int q = y / rm.blk, yl = y - q * rm.blk;
-  return (static_cast<long long>(q * rm.blk + xl) * rm.prow + yl) * rm.pitch;
-}
-
 // Full-length spectrum sample at position pos of A + iB from half spectra.
 template <int N>
 __device__ __forceinline__ double2 pair_sample(const double2* A, const double2* B, int pos) {
@@ -418,19 +401,6 @@ __device__ __forceinline__ void zfft(double2 (&v)[fft_elems(N)], double2* sm, Sw
 #else
   block_fft_lt<N, S>(v, sm, sw, t, tws, bar, lt);
 #endif
-}
-
-// Output element (ri, kz k) of a peer-direct z pass and its destination's
-// component stride (see z_fused_to).
-struct ZDst {
-  long long el, cs;
-};
-__device__ __forceinline__ ZDst zdst(const RowMap& rmo, int ri, int k) {
-  int sg = 0;
-  while (sg + 1 < rmo.nseg && k >= rmo.seg_k0[sg + 1]) ++sg;
-  return ZDst{rmo.seg_base[sg] + static_cast<long long>(ri) * rmo.seg_pitch[sg] +
-                  (k - rmo.seg_k0[sg]),
-              rmo.seg_cs[sg]};
 }
 
 template <int N, bool PO = false>
@@ -1236,6 +1206,10 @@ bool z_chunk_map(void* tmap, const double2* base, long long cs, int nfields, con
 
 void z_fused(int n, double2* rows, long long cs, const RowMap& rm, double norm,
              const double2* tw, cudaStream_t s) {
+  if (!tuned_length(n)) {
+    gen_z_fused(n, rows, cs, rm, rows, nullptr, norm, tw, s);
+    return;
+  }
   switch (n) {
 #define X(NN) \
   case NN: z_fused_n<NN>(rows, cs, rm, norm, tw, s); return;
@@ -1258,6 +1232,10 @@ static void z_fused_to_n(double2* rows, long long cs, const RowMap& rm, double2*
 
 void z_fused_to(int n, double2* rows, long long cs, const RowMap& rm, double2* out,
                 const RowMap& rmo, double norm, const double2* tw, cudaStream_t s) {
+  if (!tuned_length(n)) {
+    gen_z_fused(n, rows, cs, rm, out, &rmo, norm, tw, s);
+    return;
+  }
   switch (n) {
 #define X(NN) \
   case NN: z_fused_to_n<NN>(rows, cs, rm, out, rmo, norm, tw, s); return;
@@ -1279,6 +1257,10 @@ static void z_c2r_n(const double2* spec, double* real, const RowMap& rm, double 
 
 void z_c2r(int n, const double2* spec, double* real, const RowMap& rm, double norm,
            const double2* tw, cudaStream_t s) {
+  if (!tuned_length(n)) {
+    gen_z_c2r(n, spec, real, rm, norm, tw, s);
+    return;
+  }
   switch (n) {
 #define X(NN) \
   case NN: z_c2r_n<NN>(spec, real, rm, norm, tw, s); return;
@@ -1311,6 +1293,10 @@ static void z_r2c_to_n(const double* real, double2* out, const RowMap& rm, const
 
 void z_r2c_to(int n, const double* real, double2* out, const RowMap& rm, const RowMap& rmo,
               int field, const double2* tw, cudaStream_t s) {
+  if (!tuned_length(n)) {
+    gen_z_r2c(n, real, out, rm, &rmo, field, tw, s);
+    return;
+  }
   switch (n) {
 #define X(NN) \
   case NN: z_r2c_to_n<NN>(real, out, rm, rmo, field, tw, s); return;
@@ -1321,6 +1307,10 @@ void z_r2c_to(int n, const double* real, double2* out, const RowMap& rm, const R
 
 void z_r2c(int n, const double* real, double2* spec, const RowMap& rm, const double2* tw,
            cudaStream_t s) {
+  if (!tuned_length(n)) {
+    gen_z_r2c(n, real, spec, rm, nullptr, 0, tw, s);
+    return;
+  }
   switch (n) {
 #define X(NN) \
   case NN: z_r2c_n<NN>(real, spec, rm, tw, s); return;

@@ -26,6 +26,10 @@ struct ColGeom {
   long long kcs = 8;  // stride of 8-column kz chunks: 8 = plain rows; larger
                       // for chunk-major layouts ((kz>>3)*kcs + (kz&7))
   int pb_shift = 30;
+  // position block size of the same split (pos / pblk, pos % pblk) for the
+  // generic-length kernels, whose blocks need not be powers of two; 0: no
+  // split (pb_shift = 30)
+  int pblk = 0;
   int nrows = 0;
   int n2 = 0;     // transformed kz entries per row
   int pitch = 0;  // kz slots per enumerated row (multiple of the tile width)
@@ -125,8 +129,38 @@ struct XfArgs {
   int shells = 0;
 };
 
-// twiddle table exp(-2 pi i q / n), q in [0, n)
+// twiddle table of length-n transforms: the stage-ordered table of the
+// radix-8/16 kernels (power-of-two n <= 1024), else exp(-2 pi i q / n),
+// q in [0, n), for the generic-length kernels
 void make_twiddles(int n, double2* d_tw, cudaStream_t s);
+
+// Power-of-two n in [4, 1024] run the tuned kernels; every other even n runs
+// the generic mixed-radix kernels of kernels_gen.cu behind the same
+// launchers and geometries (the reference accepts any even n >= 4,
+// config.cpp:17-19).
+inline bool tuned_length(int n) { return n >= 4 && n <= 1024 && (n & (n - 1)) == 0; }
+// Shared memory the generic z pass needs at length n (0 if n is tuned).
+size_t gen_z_smem(int n);
+
+// Generic-length column pass: `nitems` items per tile, item i reads field
+// it[i].fin of `in` (geometry g), applies the pre-op, transforms (dir -1
+// forward, +1 inverse), applies the post-op and stores field it[i].fout of
+// `out` (geometry go; go.seg: peer-direct). Items of a tile run in order,
+// so an in-place pass may overwrite a field an earlier item consumed.
+enum GPre : int { G_NONE = 0, G_K = 1, G_IK = 2, G_MI = 3 };  // x, k x, i k x, -i x
+enum GPost : int { G_PLAIN = 0, G_W2 = 1 };  // w2' = i (v - k_row U0), U0 = out field 0
+struct GItem {
+  int fin, fout, pre, post;
+};
+void gen_col(int n, int dir, const double2* in, double2* out, long long in_cs, long long out_cs,
+             int nitems, const GItem* it, const ColGeom& g, const ColGeom& go, const double2* tw,
+             cudaStream_t s);
+void gen_z_fused(int n, double2* rows, long long cs, const RowMap& rm, double2* out,
+                 const RowMap* rmo, double norm, const double2* tw, cudaStream_t s);
+void gen_z_c2r(int n, const double2* spec, double* real, const RowMap& rm, double norm,
+               const double2* tw, cudaStream_t s);
+void gen_z_r2c(int n, const double* real, double2* spec, const RowMap& rm, const RowMap* rmo,
+               int field, const double2* tw, cudaStream_t s);
 
 // xaxis selects the tile shape tuned for the large-stride (x) axis.
 void col_plain(int n, int dir, bool xaxis, const double2* in, double2* out, long long in_cs,

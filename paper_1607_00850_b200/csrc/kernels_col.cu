@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -895,9 +896,25 @@ static void col_plain_n(int dir, bool xaxis, const double2* in, double2* out, lo
   }
 }
 
+// Generic-length items (kernels_gen.cu): the plain pass, P1's components
+// and P2's items in the tuned kernels' order.
+static void gen_plain(int n, int dir, const double2* in, double2* out, long long in_cs,
+                      long long out_cs, int nfields, const ColGeom& g, const ColGeom& go,
+                      const double2* tw, cudaStream_t s) {
+  GItem it[8];
+  for (int f = 0; f < nfields; ++f) it[f] = GItem{f, f, G_NONE, G_PLAIN};
+  for (int f0 = 0; f0 < nfields; f0 += 8)
+    gen_col(n, dir, in + f0 * in_cs, out + f0 * out_cs, in_cs, out_cs, std::min(8, nfields - f0),
+            it, g, go, tw, s);
+}
+
 void col_plain(int n, int dir, bool xaxis, const double2* in, double2* out, long long in_cs,
                long long out_cs, int nfields, const ColGeom& g, const double2* tw,
                cudaStream_t s) {
+  if (!tuned_length(n)) {
+    gen_plain(n, dir, in, out, in_cs, out_cs, nfields, g, g, tw, s);
+    return;
+  }
   switch (n) {
 #define X(NN) \
   case NN: col_plain_n<NN>(dir, xaxis, in, out, in_cs, out_cs, nfields, g, nullptr, tw, s); return;
@@ -909,6 +926,10 @@ void col_plain(int n, int dir, bool xaxis, const double2* in, double2* out, long
 void col_plain_to(int n, int dir, const double2* in, double2* out, long long in_cs,
                   long long out_cs, int nfields, const ColGeom& g, const ColGeom& go,
                   const double2* tw, cudaStream_t s, bool xaxis) {
+  if (!tuned_length(n)) {
+    gen_plain(n, dir, in, out, in_cs, out_cs, nfields, g, go, tw, s);
+    return;
+  }
   switch (n) {
 #define X(NN) \
   case NN: col_plain_n<NN>(dir, xaxis, in, out, in_cs, out_cs, nfields, g, &go, tw, s); return;
@@ -947,6 +968,19 @@ static void x_inv_n(const double2* u, long long u_cs, double2* out, long long ou
 void x_inverse_split(int n, const double2* u, long long u_cs, double2* out, long long out_cs,
                      const ColGeom& g, const ColGeom* go, const double2* tw, cudaStream_t s,
                      int comp_lo, int comp_cnt) {
+  if (!tuned_length(n)) {
+    // component c: U_c (field c); c = 1 also w2' = i(F(kx u1) - ky U0)
+    // (field 3), c = 2 also K2 = F(kx u2) (field 4)
+    GItem it[8];
+    int ni = 0;
+    for (int c = comp_lo; c < comp_lo + comp_cnt; ++c) {
+      it[ni++] = GItem{c, c, G_NONE, G_PLAIN};
+      if (c == 1) it[ni++] = GItem{1, 3, G_K, G_W2};
+      if (c == 2) it[ni++] = GItem{2, 4, G_K, G_PLAIN};
+    }
+    gen_col(n, +1, u, out, u_cs, out_cs, ni, it, g, go ? *go : g, tw, s);
+    return;
+  }
   switch (n) {
 #define X(NN) \
   case NN: x_inv_n<NN>(u, u_cs, out, out_cs, g, go, comp_lo, comp_cnt, tw, s); return;
@@ -998,8 +1032,30 @@ static void y_inv_n(const double2* fin, double2* f, long long cs_in, long long c
   }
 }
 
+// P2 items 0..4 (U0, U1, w2', U2, K2) as generic items.
+static int gen_yinv_items(int item_lo, int item_cnt, GItem* it) {
+  int ni = 0;
+  for (int i = item_lo; i < item_lo + item_cnt; ++i) {
+    if (i == 0) it[ni++] = GItem{0, 0, G_NONE, G_PLAIN};
+    if (i == 1) it[ni++] = GItem{1, 1, G_NONE, G_PLAIN};
+    if (i == 2) it[ni++] = GItem{3, 5, G_NONE, G_PLAIN};  // w2 = F(w2')
+    if (i == 3) {
+      it[ni++] = GItem{2, 3, G_IK, G_PLAIN};  // w0' = F(i ky U2)
+      it[ni++] = GItem{2, 2, G_NONE, G_PLAIN};
+    }
+    if (i == 4) it[ni++] = GItem{4, 4, G_MI, G_PLAIN};  // w1' = F(-i K2)
+  }
+  return ni;
+}
+
 void y_inverse_curl(int n, double2* f, long long cs, const ColGeom& g, const double2* tw,
                     cudaStream_t s, int item_lo, int item_cnt) {
+  if (!tuned_length(n)) {
+    GItem it[8];
+    const int ni = gen_yinv_items(item_lo, item_cnt, it);
+    gen_col(n, +1, f, f, cs, cs, ni, it, g, g, tw, s);
+    return;
+  }
   switch (n) {
 #define X(NN) \
   case NN: y_inv_n<NN>(f, f, cs, cs, g, nullptr, item_lo, item_cnt, tw, s); return;
@@ -1010,6 +1066,12 @@ void y_inverse_curl(int n, double2* f, long long cs, const ColGeom& g, const dou
 
 void y_inverse_curl_to(int n, const double2* fin, double2* fout, long long cs_in, long long cs_out,
                        const ColGeom& g, const ColGeom& go, const double2* tw, cudaStream_t s) {
+  if (!tuned_length(n)) {
+    GItem it[8];
+    const int ni = gen_yinv_items(0, 5, it);
+    gen_col(n, +1, fin, fout, cs_in, cs_out, ni, it, g, go, tw, s);
+    return;
+  }
   switch (n) {
 #define X(NN) \
   case NN: y_inv_n<NN>(fin, fout, cs_in, cs_out, g, &go, 0, 5, tw, s); return;

@@ -134,8 +134,8 @@ def test_bench_rows_and_csv(tmp_path):
     assert all(np.isfinite(r.sec_per_step) and r.sec_per_step > 0 for r in rows)
     assert (rows[2].entry.p1, rows[2].entry.p2) == (2, 2)
     assert [r.nodes_per_rank for r in rows] == [4096, 16384, 8192, 262144]
-    bad = S.bench([S.BenchEntry(6, "slab", 1)], 2)
-    assert bad[0].status.startswith("the sm_100a path supports power-of-two n")
+    bad = S.bench([S.BenchEntry(2048, "slab", 1)], 2)
+    assert bad[0].status.startswith("the sm_100a path supports n <= 1024")
     S.write_bench_csv(str(tmp_path / "b.csv"), rows + bad)
     lines = open(tmp_path / "b.csv").read().splitlines()
     assert lines[0] == "n,decomp,p,p1,p2,nodes_per_rank,sec_per_step,status"
