@@ -8,8 +8,9 @@ cd "$(dirname "$0")/../paper_1607_00850_b200/csrc"
 b=build_$name; mkdir -p $b
 A="-gencode arch=compute_100a,code=sm_100a"
 F="$A -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $*"
-for f in kernels kernels_col context; do nvcc $F -c $f.cu -o $b/$f.o & done
+K="kernels kernels_col kernels_gen kernels_z512 context"
+for f in $K; do nvcc $F -c $f.cu -o $b/$f.o & done
 wait
-nvcc $A -shared -cudart static -o ../../libsdns_$name.so $b/kernels.o $b/kernels_col.o $b/context.o \
+nvcc $A -shared -cudart static -o ../../libsdns_$name.so $(for f in $K; do echo $b/$f.o; done) \
   build/comm.o build/layout.o build/iso_init.o build/runner.o build/acceptance.o -ldl -lpthread
 rm -rf $b
