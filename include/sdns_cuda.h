@@ -133,8 +133,12 @@ int sdns_comm_nccl_init(const unsigned char id[128], int size, int rank, int dev
  * group `user`) on every rank, and the child uses child_user (NULL group
  * callback: no split). Buffers and stream barriers go through CUDA IPC
  * (memory and events), so several ranks may share one GPU and no kernel
- * waits on another. Carries the peer-direct transposes only: all_to_all
- * raises SDNS_PROTOCOL_ERROR. Collective. */
+ * waits on another. The RHS transposes run peer-direct; all_to_all (the
+ * checkpoint gathers/scatters, sdns_comm_all_to_all_bytes) goes through the
+ * all-gather (every rank receives every packed buffer). The callback
+ * returns 2 when the caller's transport timed out (SDNS_TIMEOUT_ERROR),
+ * any other nonzero value for other failures (SDNS_PROTOCOL_ERROR).
+ * Collective. */
 typedef int (*sdns_allgather_fn)(const void* send, size_t bytes, void* recv, void* user);
 typedef int (*sdns_group_fn)(const int* ranks, int n, void* user, void** child_user);
 int sdns_comm_host_init(int size, int rank, int device, sdns_allgather_fn allgather,

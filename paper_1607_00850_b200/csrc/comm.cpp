@@ -441,9 +441,9 @@ void bcast_check(int root, size_t nbytes, int size,
 // with the caller's host all-gather (e.g. torch.distributed over gloo) as the
 // only primitive (plus a group callback for split). Reductions fold gathered
 // values in rank order; buffers are exchanged by CUDA IPC and stream barriers
-// wait on the ranks' IPC events, so no kernel ever waits on another. It
-// carries the peer-direct transposes only: the all-to-all is not provided
-// (ProtocolError).
+// wait on the ranks' IPC events, so no kernel ever waits on another. The
+// RHS transposes run peer-direct; the all-to-all (checkpoints, the API call)
+// goes through the host all-gather.
 class HostComm final : public Comm {
  public:
   HostComm(int rank, int size, int device, sdns_allgather_fn fn, sdns_group_fn gfn, void* user)
@@ -466,16 +466,62 @@ class HostComm final : public Comm {
   int device() const override { return device_; }
   const char* kind() const override { return "host"; }
 
-  // Only the blocks a rank sends itself (a one-member group's transposes).
+  // Variable all-to-all through the caller's all-gather (the transport's
+  // only primitive): every rank packs its send blocks on the host, the send
+  // tables and the packed buffers (padded to the largest) are all-gathered,
+  // and each rank unpacks the blocks addressed to it. Every rank receives
+  // every buffer, so this serves the infrequent exchanges (checkpoint
+  // gathers and scatters, the API's all_to_all); the RHS transposes run
+  // peer-direct over CUDA IPC. Tables are checked like InProcessComm's.
   void alltoall(const std::vector<Xfer>& xs, cudaStream_t s) override {
+    check_failed();
+    const size_t p = static_cast<size_t>(size_);
+    std::vector<int64_t> mine(2 * p, 0);  // [send to q | recv from q] bytes
     for (const Xfer& x : xs) {
-      if (x.peer != rank_)
-        protocol_error("host-callback transport: all_to_all between ranks is not provided "
-                       "(peer-direct transposes only)");
-      if (x.send_bytes != x.recv_bytes) protocol_error("all_to_all: self block size mismatch");
-      if (x.send_bytes && x.send != x.recv)
-        SDNS_CUDA(cudaMemcpyAsync(x.recv, x.send, x.send_bytes, cudaMemcpyDeviceToDevice, s));
+      if (x.peer < 0 || x.peer >= size_) protocol_error("all_to_all: peer out of range");
+      mine[static_cast<size_t>(x.peer)] += static_cast<int64_t>(x.send_bytes);
+      mine[p + static_cast<size_t>(x.peer)] += static_cast<int64_t>(x.recv_bytes);
     }
+    std::vector<int64_t> tab(2 * p * p);
+    gather(mine.data(), sizeof(int64_t) * 2 * p, tab.data());
+    for (size_t q = 0; q < p; ++q)  // what q sends me == what I expect from q
+      if (tab[q * 2 * p + static_cast<size_t>(rank_)] != mine[p + q])
+        protocol_error("all_to_all: send/recv block sizes disagree between rank " +
+                       std::to_string(q) + " and rank " + std::to_string(rank_));
+    int64_t total = 0, maxtot = 0;
+    for (size_t q = 0; q < p; ++q) {
+      int64_t tq = 0;
+      for (size_t d = 0; d < p; ++d) tq += tab[q * 2 * p + d];
+      maxtot = std::max(maxtot, tq);
+      if (static_cast<int>(q) == rank_) total = tq;
+    }
+    if (maxtot == 0) return;
+    // pack: blocks in (destination, call order) order
+    std::vector<char> pack(static_cast<size_t>(maxtot), 0);
+    std::vector<int64_t> doff(p, 0);
+    for (size_t d = 1; d < p; ++d) doff[d] = doff[d - 1] + mine[d - 1];
+    std::vector<int64_t> put = doff;
+    SDNS_CUDA(cudaStreamSynchronize(s));
+    for (const Xfer& x : xs)
+      if (x.send_bytes) {
+        SDNS_CUDA(cudaMemcpy(pack.data() + put[static_cast<size_t>(x.peer)], x.send, x.send_bytes,
+                             cudaMemcpyDeviceToHost));
+        put[static_cast<size_t>(x.peer)] += static_cast<int64_t>(x.send_bytes);
+      }
+    (void)total;
+    std::vector<char> all(static_cast<size_t>(maxtot) * p);
+    gather(pack.data(), static_cast<size_t>(maxtot), all.data());
+    // unpack: from q's buffer, the region q packed for me, in call order
+    std::vector<int64_t> get(p, 0);
+    for (size_t q = 0; q < p; ++q)
+      for (int d = 0; d < rank_; ++d) get[q] += tab[q * 2 * p + static_cast<size_t>(d)];
+    for (const Xfer& x : xs)
+      if (x.recv_bytes) {
+        const size_t q = static_cast<size_t>(x.peer);
+        SDNS_CUDA(cudaMemcpy(x.recv, all.data() + q * static_cast<size_t>(maxtot) + get[q],
+                             x.recv_bytes, cudaMemcpyHostToDevice));
+        get[q] += static_cast<int64_t>(x.recv_bytes);
+      }
   }
   void allreduce(double* v, int n, int op) override {
     std::vector<double> all(static_cast<size_t>(n) * size_);

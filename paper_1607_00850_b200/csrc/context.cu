@@ -143,6 +143,38 @@ struct sdns_ctx {
       throw;
     }
   }
+  // Releases whatever has been allocated, also when sdns_ctx_create throws
+  // part way (an OOM on a work buffer, a failed peer mapping).
+  ~sdns_ctx() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (cstream) {
+      cudaStreamSynchronize(cstream);
+      for (auto& e : xev)
+        if (e) cudaEventDestroy(e);
+      cudaStreamDestroy(cstream);
+    }
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (peer_grp && !peer_wb.empty()) peer_grp->unmap_peers(peer_wb);
+    if (peer_grp && !peer_wa.empty()) peer_grp->unmap_peers(peer_wa);
+    if (row && !peer_wd.empty()) row->unmap_peers(peer_wd);
+    if (row && !peer_wc.empty()) row->unmap_peers(peer_wc);
+    for (void* p : {static_cast<void*>(d_seg), static_cast<void*>(d_seg_row),
+                    static_cast<void*>(tw), static_cast<void*>(wc), static_cast<void*>(wd),
+                    static_cast<void*>(wx), static_cast<void*>(d_partial),
+                    static_cast<void*>(d_fpartial), static_cast<void*>(d_dts),
+                    static_cast<void*>(d_fout), static_cast<void*>(d_out),
+                    static_cast<void*>(d_flag)})
+      if (p) cudaFree(p);
+    if (wb && wb != wa) cudaFree(wb);
+    if (wa) cudaFree(wa);
+    if (h_out) cudaFreeHost(h_out);
+    if (h_flag) cudaFreeHost(h_flag);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
   double2* wc = nullptr;
   double2* wd = nullptr;
   long long cs_c = 0, cs_d = 0;
@@ -1112,22 +1144,15 @@ struct CkHeader {
 };
 static_assert(sizeof(CkHeader) == 32, "reference checkpoint header is 32 bytes");
 
-// Root's verdict to every rank (the reference broadcasts the message, so a
-// bad path fails all ranks instead of hanging them): an allreduce-sum of
-// the message bytes, zeros from the other ranks.
+// Root's verdict to every rank, as the reference shares it (length, then
+// the bytes, by broadcast_bytes; checkpoint.cpp:104-110): a bad path or file
+// raises IoError on every rank instead of hanging the others.
 void share_io_error(sdns_ctx* c, const std::string& root_err) {
-  constexpr int kMax = 480;
-  std::vector<double> buf(kMax + 1, 0.0);
-  if (c->world->rank() == 0 && !root_err.empty()) {
-    const int len = static_cast<int>(std::min<size_t>(root_err.size(), kMax));
-    buf[0] = len;
-    for (int i = 0; i < len; ++i) buf[1 + i] = static_cast<unsigned char>(root_err[i]);
-  }
-  c->world->allreduce(buf.data(), static_cast<int>(buf.size()), 0);
-  const int len = static_cast<int>(buf[0]);
-  if (len <= 0) return;
-  std::string m(static_cast<size_t>(len), ' ');
-  for (int i = 0; i < len; ++i) m[static_cast<size_t>(i)] = static_cast<char>(buf[1 + i]);
+  uint64_t len = c->world->rank() == 0 ? root_err.size() : 0;
+  c->world->broadcast(&len, sizeof(len), 0);
+  if (len == 0) return;
+  std::string m = c->world->rank() == 0 ? root_err : std::string(static_cast<size_t>(len), ' ');
+  c->world->broadcast(m.data(), static_cast<size_t>(len), 0);
   throw Error(SDNS_IO_ERROR, m);
 }
 
@@ -1167,28 +1192,47 @@ void ck_exchange(sdns_ctx* c, const std::vector<int64_t>& cnt, double* mine, dou
   c->wait();
 }
 
-void checkpoint_write_impl(sdns_ctx* c, const sdns_field* u, const std::string& path, double t,
-                           int64_t step) {
-  const int64_t n = c->cfg.n, n3 = n * n * n;
-  const bool root = c->world->rank() == 0;
+// Root-side resources of a checkpoint transfer, released on every exit path.
+struct CkRoot {
+  FILE* fp = nullptr;
+  double* stage = nullptr;  // device: one gathered component (n^3 doubles)
+  ~CkRoot() {
+    if (fp) std::fclose(fp);
+    if (stage) cudaFree(stage);
+  }
+};
+
+std::vector<int64_t> ck_counts(const sdns_ctx* c, std::vector<sdns_layout>& lays) {
   std::vector<int64_t> cnt;
-  std::vector<sdns_layout> lays;
   for (int r = 0; r < c->cfg.p; ++r) {
     lays.push_back(build_layout(c->cfg, r));
     cnt.push_back(lays.back().real_shape[0] * lays.back().real_shape[1] * lays.back().real_shape[2]);
   }
-  FILE* fp = nullptr;
+  return cnt;
+}
+
+// write_checkpoint (checkpoint.cpp:64-113): the root opens the file, writes
+// the header and allocates its staging buffers BEFORE any collective, then
+// shares the verdict; components are gathered to the root and written in
+// global x-major order.
+void checkpoint_write_impl(sdns_ctx* c, const sdns_field* u, const std::string& path, double t,
+                           int64_t step) {
+  const int64_t n = c->cfg.n, n3 = n * n * n;
+  const bool root = c->world->rank() == 0;
+  std::vector<sdns_layout> lays;
+  const std::vector<int64_t> cnt = ck_counts(c, lays);
+  CkRoot rs;
+  std::vector<double> blocks, global;
   std::string err;
   if (root) {
     try {
-      const auto dir = std::filesystem::path(path).parent_path();
-      if (!dir.empty()) std::filesystem::create_directories(dir);
-    } catch (const std::exception&) {
-    }
-    fp = std::fopen(path.c_str(), "wb");
-    if (!fp) {
-      err = "cannot open checkpoint '" + path + "' for writing";
-    } else {
+      try {
+        const auto dir = std::filesystem::path(path).parent_path();
+        if (!dir.empty()) std::filesystem::create_directories(dir);
+      } catch (const std::exception&) {
+      }
+      rs.fp = std::fopen(path.c_str(), "wb");
+      if (!rs.fp) throw Error(SDNS_IO_ERROR, "cannot open checkpoint '" + path + "' for writing");
       CkHeader h{};
       std::memcpy(h.magic, kCkMagic, 4);
       h.version = kCkVersion;
@@ -1196,84 +1240,88 @@ void checkpoint_write_impl(sdns_ctx* c, const sdns_field* u, const std::string& 
       h.components = 3;
       h.t = t;
       h.step = static_cast<uint64_t>(step);
-      if (std::fwrite(&h, sizeof(h), 1, fp) != 1) err = "short write to checkpoint '" + path + "'";
+      if (std::fwrite(&h, sizeof(h), 1, rs.fp) != 1)
+        throw Error(SDNS_IO_ERROR, "short write to checkpoint '" + path + "'");
+      if (cudaMalloc(&rs.stage, sizeof(double) * static_cast<size_t>(n3)) != cudaSuccess) {
+        cudaGetLastError();
+        rs.stage = nullptr;
+        throw Error(SDNS_IO_ERROR, "checkpoint '" + path + "': cannot allocate the " +
+                                       std::to_string(8 * n3) + "-byte device staging buffer");
+      }
+      blocks.resize(static_cast<size_t>(n3));
+      global.resize(static_cast<size_t>(n3));
+    } catch (const std::exception& e) {
+      err = e.what();
     }
   }
-  try {
-    share_io_error(c, err);
-  } catch (...) {
-    if (fp) std::fclose(fp);
-    throw;
-  }
-  double* stage = nullptr;
-  std::vector<double> blocks, global;
-  if (root) {
-    SDNS_CUDA(cudaMalloc(&stage, sizeof(double) * static_cast<size_t>(n3)));
-    blocks.resize(static_cast<size_t>(n3));
-    global.resize(static_cast<size_t>(n3));
-  }
+  share_io_error(c, err);
   bool ok = true;
   for (int comp = 0; comp < 3; ++comp) {
-    ck_exchange(c, cnt, u->real() + comp * c->real_cs, stage, true);
+    ck_exchange(c, cnt, u->real() + comp * c->real_cs, rs.stage, true);
     if (!root) continue;
-    SDNS_CUDA(cudaMemcpy(blocks.data(), stage, sizeof(double) * static_cast<size_t>(n3),
-                         cudaMemcpyDeviceToHost));
+    SDNS_CUDA(cudaMemcpyAsync(blocks.data(), rs.stage, sizeof(double) * static_cast<size_t>(n3),
+                              cudaMemcpyDeviceToHost, c->stream));
+    c->wait();
     int64_t off = 0;
     for (int r = 0; r < c->cfg.p; ++r) {
       blit_block(lays[static_cast<size_t>(r)], n, global.data(), blocks.data() + off, true);
       off += cnt[static_cast<size_t>(r)];
     }
-    ok = ok && std::fwrite(global.data(), sizeof(double), global.size(), fp) == global.size();
+    ok = ok && std::fwrite(global.data(), sizeof(double), global.size(), rs.fp) == global.size();
   }
   if (root) {
-    cudaFree(stage);
-    ok = (std::fclose(fp) == 0) && ok;
+    ok = (std::fclose(rs.fp) == 0) && ok;
+    rs.fp = nullptr;
     if (!ok) throw Error(SDNS_IO_ERROR, "short write to checkpoint '" + path + "'");
   }
 }
 
+// read_checkpoint (checkpoint.cpp:115-187): the root validates and reads the
+// whole file and allocates its staging buffer before any collective, shares
+// the verdict, scatters every component (the host copy into the staging
+// buffer is ordered on the context stream with the exchange), then t and
+// step reach every rank by broadcast.
 void checkpoint_read_impl(sdns_ctx* c, const std::string& path, sdns_field* u, double* t,
                           int64_t* step) {
   const int64_t n = c->cfg.n, n3 = n * n * n;
   const bool root = c->world->rank() == 0;
-  std::vector<int64_t> cnt;
   std::vector<sdns_layout> lays;
-  for (int r = 0; r < c->cfg.p; ++r) {
-    lays.push_back(build_layout(c->cfg, r));
-    cnt.push_back(lays.back().real_shape[0] * lays.back().real_shape[1] * lays.back().real_shape[2]);
-  }
-  std::vector<double> global;
+  const std::vector<int64_t> cnt = ck_counts(c, lays);
+  std::vector<double> global, blocks;
   CkHeader h{};
+  CkRoot rs;
   std::string err;
   if (root) {
-    FILE* fp = std::fopen(path.c_str(), "rb");
-    if (!fp) {
-      err = "cannot open checkpoint '" + path + "'";
-    } else {
-      if (std::fread(&h, sizeof(h), 1, fp) != 1 || std::memcmp(h.magic, kCkMagic, 4) != 0)
-        err = "checkpoint '" + path + "': bad magic";
-      else if (h.version != kCkVersion)
-        err = "checkpoint '" + path + "': unsupported version " + std::to_string(h.version);
-      else if (h.n != static_cast<uint32_t>(n))
-        err = "checkpoint '" + path + "': grid size " + std::to_string(h.n) +
-              " does not match configured n=" + std::to_string(n);
-      else if (h.components != 3)
-        err = "checkpoint '" + path + "': expected 3 components";
-      if (err.empty()) {
-        global.resize(static_cast<size_t>(3 * n3));
-        if (std::fread(global.data(), sizeof(double), global.size(), fp) != global.size())
-          err = "checkpoint '" + path + "': truncated payload";
+    try {
+      rs.fp = std::fopen(path.c_str(), "rb");
+      if (!rs.fp) throw Error(SDNS_IO_ERROR, "cannot open checkpoint '" + path + "'");
+      if (std::fread(&h, sizeof(h), 1, rs.fp) != 1 || std::memcmp(h.magic, kCkMagic, 4) != 0)
+        throw Error(SDNS_IO_ERROR, "checkpoint '" + path + "': bad magic");
+      if (h.version != kCkVersion)
+        throw Error(SDNS_IO_ERROR,
+                    "checkpoint '" + path + "': unsupported version " + std::to_string(h.version));
+      if (h.n != static_cast<uint32_t>(n))
+        throw Error(SDNS_IO_ERROR, "checkpoint '" + path + "': grid size " + std::to_string(h.n) +
+                                       " does not match configured n=" + std::to_string(n));
+      if (h.components != 3)
+        throw Error(SDNS_IO_ERROR, "checkpoint '" + path + "': expected 3 components");
+      global.resize(static_cast<size_t>(3 * n3));
+      if (std::fread(global.data(), sizeof(double), global.size(), rs.fp) != global.size())
+        throw Error(SDNS_IO_ERROR, "checkpoint '" + path + "': truncated payload");
+      std::fclose(rs.fp);
+      rs.fp = nullptr;
+      if (cudaMalloc(&rs.stage, sizeof(double) * static_cast<size_t>(n3)) != cudaSuccess) {
+        cudaGetLastError();
+        rs.stage = nullptr;
+        throw Error(SDNS_IO_ERROR, "checkpoint '" + path + "': cannot allocate the " +
+                                       std::to_string(8 * n3) + "-byte device staging buffer");
       }
-      std::fclose(fp);
+      blocks.resize(static_cast<size_t>(n3));
+    } catch (const std::exception& e) {
+      err = e.what();
     }
   }
   share_io_error(c, err);
-  double* stage = nullptr;
-  std::vector<double> blocks;
-  if (root) {
-    SDNS_CUDA(cudaMalloc(&stage, sizeof(double) * static_cast<size_t>(n3)));
-    blocks.resize(static_cast<size_t>(n3));
-  }
   for (int comp = 0; comp < 3; ++comp) {
     if (root) {
       int64_t off = 0;
@@ -1282,15 +1330,14 @@ void checkpoint_read_impl(sdns_ctx* c, const std::string& path, sdns_field* u, d
                    false);
         off += cnt[static_cast<size_t>(r)];
       }
-      SDNS_CUDA(cudaMemcpy(stage, blocks.data(), sizeof(double) * static_cast<size_t>(n3),
-                           cudaMemcpyHostToDevice));
+      SDNS_CUDA(cudaMemcpyAsync(rs.stage, blocks.data(), sizeof(double) * static_cast<size_t>(n3),
+                                cudaMemcpyHostToDevice, c->stream));
     }
-    ck_exchange(c, cnt, u->real() + comp * c->real_cs, stage, false);
+    ck_exchange(c, cnt, u->real() + comp * c->real_cs, rs.stage, false);
   }
-  if (root) cudaFree(stage);
   // every rank learns t and step from the root's header
   double meta[2] = {root ? h.t : 0.0, root ? static_cast<double>(h.step) : 0.0};
-  c->world->allreduce(meta, 2, 0);
+  c->world->broadcast(meta, sizeof(meta), 0);
   if (t) *t = meta[0];
   if (step) *step = static_cast<int64_t>(meta[1]);
 }
@@ -1526,44 +1573,7 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
 }
 
 int sdns_ctx_destroy(sdns_ctx* c) {
-  return guarded([&] {
-    if (!c) return;
-    cudaSetDevice(c->device);
-    cudaStreamSynchronize(c->stream);
-    for (auto& g : c->graphs)
-      if (g.exec) cudaGraphExecDestroy(g.exec);
-    if (c->cstream) {
-      cudaStreamSynchronize(c->cstream);
-      for (auto& e : c->xev) cudaEventDestroy(e);
-      cudaStreamDestroy(c->cstream);
-    }
-    if (c->peer) {
-      c->peer_grp->unmap_peers(c->peer_wb);
-      c->peer_grp->unmap_peers(c->peer_wa);
-      cudaFree(c->d_seg);
-    }
-    if (c->peer_row) {
-      c->row->unmap_peers(c->peer_wd);
-      c->row->unmap_peers(c->peer_wc);
-      cudaFree(c->d_seg_row);
-    }
-    cudaFree(c->tw);
-    if (c->wb != c->wa) cudaFree(c->wb);
-    if (c->wc) cudaFree(c->wc);
-    if (c->wd) cudaFree(c->wd);
-    if (c->wx) cudaFree(c->wx);
-    cudaFree(c->wa);
-    cudaFree(c->d_partial);
-    cudaFree(c->d_fpartial);
-    cudaFree(c->d_dts);
-    cudaFree(c->d_fout);
-    cudaFree(c->d_out);
-    cudaFree(c->d_flag);
-    cudaFreeHost(c->h_out);
-    cudaFreeHost(c->h_flag);
-    if (c->own_stream) cudaStreamDestroy(c->stream);
-    delete c;
-  });
+  return guarded([&] { delete c; });  // ~sdns_ctx releases everything
 }
 
 int sdns_ctx_layout(const sdns_ctx* c, sdns_layout* out) {

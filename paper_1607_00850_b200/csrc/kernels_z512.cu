@@ -227,19 +227,38 @@ k_z512w(double2* f, long long cs, RowMap rm, double norm, const double2* __restr
   mbar_wait(&zbar[r], 0);
 
   double2 p0[16], p1[16], x[16];
-  zinverse<+1>(p0, S, S + ZHP, t, z);            // u0 + i w1
+  zinverse<+1>(p0, S, S + ZHP, t, z);                // u0 + i w1
   zinverse<-1>(p1, S + 2 * ZHP, S + 3 * ZHP, t, z);  // u1 + i w0
-  zinverse<0>(x, S + 4 * ZHP, S + 5 * ZHP, t, z);    // u2 + i w2
-  // 1/n^3 (fft.cpp:125), u x omega (navier_stokes.cpp:45-49) in
-  // k_z_fused's operation order; n0 + i n1 in x, n2 in p0.x
+  // u2 + i w2: stages A and B, then stage C one butterfly at a time fused
+  // with 1/n^3 (fft.cpp:125) and u x omega (navier_stokes.cpp:45-49) in
+  // k_z_fused's operation order (fewer live registers): n0 + i n1 -> x,
+  // n2 -> p0
+  {
+    double2* A = S + 4 * ZHP;
+    zsample<0>(A, S + 5 * ZHP, t, x);
+    __syncwarp();
+    zstage_a<+1>(x, A, t, t ? 64 - t : 32);
+    zstage_b<+1>(x, A, t, z);
+    double2 w1b, w4b;
+    tw_plus32(z, w1b, w4b);
 #pragma unroll
-  for (int m = 0; m < 16; ++m) {
-    const double ua = zmul(p0[m].x, norm), ub = zmul(p1[m].x, norm), uc = zmul(x[m].x, norm);
-    const double wa = zmul(p1[m].y, norm), wb = zmul(p0[m].y, norm), wc = zmul(x[m].y, norm);
-    const double n0 = zsub(zmul(ub, wc), zmul(uc, wb));
-    const double n1 = zsub(zmul(uc, wa), zmul(ua, wc));
-    p0[m] = make_double2(zsub(zmul(ua, wb), zmul(ub, wa)), 0.0);
-    x[m] = make_double2(n0, n1);
+    for (int h = 0; h < 2; ++h) {
+      double2 a[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = A[zsw(t + 32 * h + 64 * q)];
+      apply_tw8<+1>(a, h ? w1b : z.w1, h ? w4b : z.w4);
+      Dft<8, +1>::run(a);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int m = 8 * h + q;
+        const double ua = zmul(p0[m].x, norm), ub = zmul(p1[m].x, norm), uc = zmul(a[q].x, norm);
+        const double wa = zmul(p1[m].y, norm), wb = zmul(p0[m].y, norm), wc = zmul(a[q].y, norm);
+        const double n0 = zsub(zmul(ub, wc), zmul(uc, wb));
+        const double n1 = zsub(zmul(uc, wa), zmul(ua, wc));
+        p0[m] = make_double2(zsub(zmul(ua, wb), zmul(ub, wa)), 0.0);
+        x[m] = make_double2(n0, n1);
+      }
+    }
   }
   // forward transform of n0 + i n1 (input positions are the inverse
   // results' t + 64 r, t + 32 + 64 r); last stage on the mirrored pairs

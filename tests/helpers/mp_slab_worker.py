@@ -53,7 +53,14 @@ def main():
         fft.inverse(uo, ur)
         fu = c.spectral_field()
         fft.forward(ur, fu)
-        np.savez(os.path.join(out, f"r{rank}.npz"), du=du.download(), u=uo.download(),
+        # checkpoints over this transport (the gathers/scatters go through the
+        # host all-gather): write, then read back into a fresh field
+        ck = os.path.join(out, "ck.sdns")
+        S.write_checkpoint(c, ck, ur, 0.25, 7)
+        back = c.real_field()
+        tt, stp = S.read_checkpoint(c, ck, back)
+        ck_ok = bool(np.array_equal(back.download(), ur.download())) and (tt, stp) == (0.25, 7)
+        np.savez(os.path.join(out, f"r{rank}.npz"), du=du.download(), u=uo.download(), ck_ok=ck_ok,
                  ur=ur.download(), fu=fu.download(), e=stats.energy, z=stats.enstrophy,
                  transposes=c.transposes, bcast=np.frombuffer(bc, dtype=np.uint8))
         st.close()

@@ -3,7 +3,9 @@
 transport: their buffers are mapped with CUDA IPC and the stream barriers
 wait on IPC events -- the same mapping code (ipc_map_peers) the NCCL backend
 uses across GPUs. One RHS and two RK4 steps must equal the single-process
-result bit for bit."""
+result bit for bit; the checkpoint gathers and scatters run over the same
+transport (its all-to-all goes through the host all-gather), and the file
+is the reference's format (compared with the threads-as-ranks file)."""
 import os
 import socket
 import subprocess
@@ -78,9 +80,20 @@ def test_multiprocess_peer_direct_bitwise(tmp_path, world, grid):
             return res
 
     ref = S.run_group(world, body)
+    # the multi-process checkpoint equals one written by the threads-as-ranks run
+    with S.Context(S.SolverConfig(n=n)) as c1:
+        u1 = c1.real_field()
+        t1, s1 = S.read_checkpoint(c1, str(tmp_path / "ck.sdns"), u1)
+        g = u1.download()
+    assert (t1, s1) == (0.25, 7)
+    for r in range(world):
+        lo = S.build_layout(cfg, r)
+        (a0, a1, a2), (b0, b1, b2) = lo.real_shape, lo.real_offset
+        assert np.array_equal(g[:, b0:b0 + a0, b1:b1 + a1, b2:b2 + a2], ref[r][4])
     for r in range(world):
         d = np.load(tmp_path / f"r{r}.npz")
         assert str(d["transposes"]) == "peer-direct"
+        assert bool(d["ck_ok"])  # checkpoint round trip over the host transport
         assert d["bcast"].tolist() == [world] * 24  # broadcast_bytes from the last rank
         assert np.array_equal(d["du"], ref[r][0])
         assert np.array_equal(d["u"], ref[r][1])
