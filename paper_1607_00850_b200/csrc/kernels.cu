@@ -1160,23 +1160,9 @@ void rk_update(int mode, const XfArgs& a, const SpecGeom& g, cudaStream_t s) {
   }
 }
 
-#ifndef SDNS_Z512W  // n = 512: the one-warp-per-line z pass (kernels_z512.cu)
-#define SDNS_Z512W 1
-#endif
-void z512w_launch(double2* rows, long long cs, const RowMap& rm, double norm, const double2* tw,
-                  const CUtensorMap& tm, double2* out, const RowMap* rmo, cudaStream_t s);
-
 template <int N>
 static void z_fused_n(double2* rows, long long cs, const RowMap& rm, double norm,
                       const double2* tw, cudaStream_t s) {
-  if constexpr (N == 512 && SDNS_Z512W) {
-    CUtensorMap tm;
-    std::memset(&tm, 0, sizeof(tm));
-    if (rm.cstride && !z_chunk_map(&tm, rows, cs, 6, rm, rm.pitch))
-      std::fprintf(stderr, "sdns: z pass chunk map could not be encoded\n");
-    z512w_launch(rows, cs, rm, norm, tw, tm, nullptr, nullptr, s);
-    return;
-  }
   using C = ZFCfg<N>;
   const unsigned grid = static_cast<unsigned>((rm.nrows + C::RPC - 1) / C::RPC);
   const size_t shm = C::SMEM;
@@ -1235,12 +1221,6 @@ void z_fused(int n, double2* rows, long long cs, const RowMap& rm, double norm,
 template <int N>
 static void z_fused_to_n(double2* rows, long long cs, const RowMap& rm, double2* out,
                          const RowMap& rmo, double norm, const double2* tw, cudaStream_t s) {
-  if constexpr (N == 512 && SDNS_Z512W) {
-    CUtensorMap tm;
-    std::memset(&tm, 0, sizeof(tm));
-    z512w_launch(rows, cs, rm, norm, tw, tm, out, &rmo, s);
-    return;
-  }
   using C = ZFCfg<N>;
   const unsigned grid = static_cast<unsigned>((rm.nrows + C::RPC - 1) / C::RPC);
   const size_t shm = C::SMEM;

@@ -31,7 +31,13 @@ namespace {
 
 constexpr int ZN = 512;
 constexpr int ZHP = ZN / 2 + 8;  // padded half row
-constexpr int ZRPC = 4;          // lines (warps) per CTA: 2 CTAs of 101 KB per SM
+#ifndef SDNS_Z512RPC
+#define SDNS_Z512RPC 4
+#endif
+#ifndef SDNS_Z512PF  // L2 prefetch of the lines the CTA SDNS_Z512PF SM-waves ahead will stage
+#define SDNS_Z512PF 0
+#endif
+constexpr int ZRPC = SDNS_Z512RPC;  // lines (warps) per CTA
 
 __device__ __forceinline__ double zmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double zsub(double a, double b) { return __dsub_rn(a, b); }
@@ -175,7 +181,7 @@ __device__ __forceinline__ void zinverse(double2 (&x)[16], double2* A, double2* 
 }  // namespace
 
 template <bool PO>
-__global__ void __launch_bounds__(32 * ZRPC, 2)
+__global__ void __launch_bounds__(32 * ZRPC, 8 / ZRPC)
 k_z512w(double2* f, long long cs, RowMap rm, double norm, const double2* __restrict__ tw,
         const __grid_constant__ CUtensorMap ztm, double2* fo, RowMap rmo) {
   extern __shared__ __align__(128) double2 smem[];
@@ -214,6 +220,18 @@ k_z512w(double2* f, long long cs, RowMap rm, double norm, const double2* __restr
           }
         }
       }
+    }
+  }
+  if constexpr (SDNS_Z512PF > 0) {  // warm L2 for the line a later CTA on this SM stages
+    const int rf = ri + SDNS_Z512PF * static_cast<int>(gridDim.x > 0 ? 0 : 0) +
+                   SDNS_Z512PF * ZRPC * 148 * (8 / ZRPC);
+    if (t < 6 && rf < rm.nrows && rm.cstride) {
+      const int fl[6] = {0, 4, 1, 3, 2, 5};
+      const int xf = rf / rm.rpp, yf = rf - xf * rm.rpp;
+      asm volatile(
+          "cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(&ztm),
+          "r"(0), "r"(0), "r"(yf), "r"(xf), "r"(fl[t])
+          : "memory");
     }
   }
   // register twiddles (from L2) while the line arrives

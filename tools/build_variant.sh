@@ -8,7 +8,7 @@ cd "$(dirname "$0")/../paper_1607_00850_b200/csrc"
 b=build_$name; mkdir -p $b
 A="-gencode arch=compute_100a,code=sm_100a"
 F="$A -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $*"
-K="kernels kernels_col kernels_gen kernels_z512 context"
+K="kernels kernels_col kernels_gen context"
 for f in $K; do nvcc $F -c $f.cu -o $b/$f.o & done
 wait
 nvcc $A -shared -cudart static -o ../../libsdns_$name.so $(for f in $K; do echo $b/$f.o; done) \
