@@ -182,6 +182,21 @@ int sdns_comm_all_to_all_bytes(sdns_comm* c, const void* send, const int64_t* se
  * cudaStream_t or NULL (the context then owns a stream). */
 int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* comm,
                     void* stream, sdns_ctx** out);
+/* Execution choices of a context; none changes a result bit (every
+ * combination runs the same transforms and arithmetic). Zero-initialised
+ * options are the defaults sdns_ctx_create uses. Nothing is read from the
+ * environment. */
+typedef struct sdns_ctx_options {
+  int all_to_all;   /* 1: transposes as all-to-alls (NCCL send/recv, copies)
+                       instead of peer-direct stores fused into the passes */
+  int serial;       /* 1: slab all-to-alls not overlapped with the passes */
+  int ldgsts_tiles; /* 1: column-pass tiles by LDGSTS instead of TMA boxes */
+  int plain_layout; /* 1: p = 1 keeps the natural work layouts (no chunk-major
+                       P1 output / chunked P2..P5a layout) */
+  int no_graph;     /* 1: p = 1 steps launch eagerly, not as a captured graph */
+} sdns_ctx_options;
+int sdns_ctx_create_ex(const sdns_config* cfg, int rank, int device, sdns_comm* comm,
+                       void* stream, const sdns_ctx_options* opts, sdns_ctx** out);
 int sdns_ctx_destroy(sdns_ctx* ctx);
 int sdns_ctx_layout(const sdns_ctx* ctx, sdns_layout* out);
 void* sdns_ctx_stream(const sdns_ctx* ctx);
@@ -300,6 +315,7 @@ typedef struct sdns_run_options {
   double collective_timeout_s;  /* default 30 */
   int device;                   /* CUDA device of every rank of sdns_run */
   uint64_t seed;                /* case "isotropic" only */
+  sdns_ctx_options ctx;         /* execution options of every rank's context */
 } sdns_run_options;
 /* RunResult (runner.hpp:28-36). samples: optional caller buffers of
  * sample_cap rows (step, and 5 + shells doubles: t, E, Z, eps, div_max,

@@ -11,6 +11,7 @@ fallback: if the library or a GPU is missing, calls raise.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import threading
@@ -116,10 +117,16 @@ class _ParsedConfig(ctypes.Structure):
                 ("notices", ctypes.c_char * 512)]
 
 
+class _CtxOptions(ctypes.Structure):
+    _fields_ = [("all_to_all", ctypes.c_int), ("serial", ctypes.c_int),
+                ("ldgsts_tiles", ctypes.c_int), ("plain_layout", ctypes.c_int),
+                ("no_graph", ctypes.c_int)]
+
+
 class _RunOptions(ctypes.Structure):
     _fields_ = [("out_dir", ctypes.c_char_p), ("backend", ctypes.c_char_p),
                 ("collective_timeout_s", ctypes.c_double), ("device", ctypes.c_int),
-                ("seed", ctypes.c_uint64)]
+                ("seed", ctypes.c_uint64), ("ctx", _CtxOptions)]
 
 
 class _RunResult(ctypes.Structure):
@@ -191,6 +198,7 @@ def load_library(path: str = LIB_PATH):
             "sdns_comm_broadcast_bytes": (I, [P, P, ctypes.c_int64, I]),
             "sdns_comm_destroy": (I, [P]),
             "sdns_ctx_create": (I, [ctypes.POINTER(_Config), I, I, P, P, PP]),
+            "sdns_ctx_create_ex": (I, [ctypes.POINTER(_Config), I, I, P, P, P, PP]),
             "sdns_ctx_destroy": (I, [P]),
             "sdns_ctx_layout": (I, [P, ctypes.POINTER(_Layout)]),
             "sdns_ctx_stream": (P, [P]),
@@ -586,21 +594,53 @@ def run_group(size: int, body: Callable[[int, Comm], object], device: int = 0,
 
 # --- context and fields -----------------------------------------------------------
 
+_OPTION_KEYS = ("all_to_all", "serial", "ldgsts_tiles", "plain_layout", "no_graph")
+_default_options: dict = {}
+
+
+@contextlib.contextmanager
+def context_options(**kw):
+    """Default execution options of the Contexts created inside the block
+    (sdns_ctx_options: all_to_all, serial, ldgsts_tiles, plain_layout,
+    no_graph); none changes a result bit. The library reads no environment."""
+    global _default_options
+    bad = set(kw) - set(_OPTION_KEYS)
+    if bad:
+        raise ConfigError(f"unknown context options {sorted(bad)}")
+    old = _default_options
+    _default_options = {**old, **kw}
+    try:
+        yield
+    finally:
+        _default_options = old
+
+
+def _ctx_options(options: Optional[dict]) -> _CtxOptions:
+    opt = {**_default_options, **(options or {})}
+    bad = set(opt) - set(_OPTION_KEYS)
+    if bad:
+        raise ConfigError(f"unknown context options {sorted(bad)}")
+    return _CtxOptions(*[int(bool(opt.get(k, 0))) for k in _OPTION_KEYS])
+
+
 class Context:
     """One rank's device context: DistributedFFT + WavenumberMesh + RhsWorkspace
-    (proj/core/src/fft.cpp:15-57, mesh.cpp:23-72, navier_stokes.hpp:32-41)."""
+    (proj/core/src/fft.cpp:15-57, mesh.cpp:23-72, navier_stokes.hpp:32-41).
+    `options`: execution choices (see context_options)."""
 
     def __init__(self, cfg: SolverConfig, rank: int = 0, device: int = 0,
-                 comm: Optional[Comm] = None, stream: Optional[int] = None):
+                 comm: Optional[Comm] = None, stream: Optional[int] = None,
+                 options: Optional[dict] = None):
         self.cfg = cfg
         self._lib = load_library()
         self._own_comm = comm is None
         self.comm = comm if comm is not None else Comm.loopback()
         c = cfg.to_c()
         h = ctypes.c_void_p()
-        _check(self._lib.sdns_ctx_create(ctypes.byref(c), rank, device, self.comm._h,
-                                         ctypes.c_void_p(stream) if stream else None,
-                                         ctypes.byref(h)))
+        copt = _ctx_options(options)
+        _check(self._lib.sdns_ctx_create_ex(ctypes.byref(c), rank, device, self.comm._h,
+                                            ctypes.c_void_p(stream) if stream else None,
+                                            ctypes.byref(copt), ctypes.byref(h)))
         self._h = h
         # fields and states allocated under this context: freed before it
         self._children = weakref.WeakSet()
@@ -945,10 +985,12 @@ class RunOptions:
     collective_timeout_s: float = 30.0
     device: int = 0
     seed: int = 1607
+    options: Optional[dict] = None  # context execution options (context_options)
 
     def to_c(self) -> _RunOptions:
         return _RunOptions(os.fsencode(self.out_dir), self.backend.encode(),
-                           self.collective_timeout_s, self.device, self.seed)
+                           self.collective_timeout_s, self.device, self.seed,
+                           _ctx_options(self.options))
 
 
 @dataclass

@@ -116,7 +116,7 @@ int cmd_run(Args& a) {  // sdns.cpp:36-66
   const int64_t cap = sdns_step_count(cfg.t_end, cfg.dt) / cfg.out_every + 2;
   std::vector<int64_t> steps(static_cast<size_t>(cap));
   std::vector<double> rows(static_cast<size_t>(cap * (5 + shells)));
-  sdns_run_options opts{out_dir.c_str(), backend.c_str(), 30.0, device, seed};
+  sdns_run_options opts{out_dir.c_str(), backend.c_str(), 30.0, device, seed, {}};
   sdns_run_result r{};
   r.sample_cap = cap;
   r.sample_steps = steps.data();
@@ -156,7 +156,7 @@ int cmd_bench(Args& a) {  // sdns.cpp:68-92
   std::cout << "benchmarking " << entries.size() << " entries, " << steps
             << " timed steps each\n";
   std::vector<sdns_bench_row> rows(entries.size());
-  sdns_run_options opts{"out", "auto", 30.0, device, 1607};
+  sdns_run_options opts{"out", "auto", 30.0, device, 1607, {}};
   ck(sdns_bench(entries.data(), count, steps, &opts, rows.data()));
   ck(sdns_write_bench_csv(out_csv.c_str(), rows.data(), count));
   bool all_ok = true;

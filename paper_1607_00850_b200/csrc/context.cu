@@ -101,6 +101,7 @@ struct sdns_field;
 
 struct sdns_ctx {
   sdns_config cfg{};
+  sdns_ctx_options opt{};
   sdns_layout lo{};
   int device = 0;
   std::shared_ptr<Comm> world;
@@ -272,7 +273,7 @@ struct sdns_ctx {
     g.n2 = static_cast<int>(lo.spec_shape[2]);
     g.pitch = pitch;
     g.row_off = static_cast<int>(lo.spec_offset[1]);
-    g.mpitch = pitch;
+    g.mpitch = opt.ldgsts_tiles ? 0 : pitch;  // 0: no tensor map, LDGSTS tiles
     g.mrows = prow;
     return g;
   }
@@ -298,7 +299,7 @@ struct sdns_ctx {
     g.nrows = static_cast<int>(n);
     g.n2 = static_cast<int>(lo.spec_shape[2]);
     g.pitch = pitch;
-    g.mpitch = pitch;
+    g.mpitch = opt.ldgsts_tiles ? 0 : pitch;  // 0: no tensor map, LDGSTS tiles
     g.mrows = static_cast<int>(n);
     return g;
   }
@@ -314,7 +315,7 @@ struct sdns_ctx {
     g.nrows = static_cast<int>(lo.spec_shape[0]);
     g.n2 = static_cast<int>(lo.spec_shape[2]);
     g.pitch = pitch;
-    g.mpitch = pitch;
+    g.mpitch = opt.ldgsts_tiles ? 0 : pitch;  // 0: no tensor map, LDGSTS tiles
     g.mrows = static_cast<int>(lo.spec_shape[0]);
     return g;
   }
@@ -335,7 +336,7 @@ struct sdns_ctx {
     g.ps1 = 0;
     g.pb_shift = 30;
     g.kcs = static_cast<long long>(lo.spec_shape[1]) * 8;
-    g.mpitch = pitch;
+    g.mpitch = opt.ldgsts_tiles ? 0 : pitch;  // 0: no tensor map, LDGSTS tiles
     g.mrows = static_cast<int>(lo.spec_shape[1]);
     return g;
   }
@@ -364,7 +365,7 @@ struct sdns_ctx {
     g.nrows = np;
     g.n2 = static_cast<int>(lo.spec_shape[2]);
     g.pitch = pitch;
-    g.mpitch = pitch;
+    g.mpitch = opt.ldgsts_tiles ? 0 : pitch;  // 0: no tensor map, LDGSTS tiles
     g.mrows = np;
     return g;
   }
@@ -442,11 +443,10 @@ struct sdns_ctx {
   // group, whose transposes move x blocks <-> y blocks exactly like the
   // slab's): map every member's wb and wa and build the store offsets
   // d_seg = [inverse (wb) | forward (wa)], member q's block for this rank
-  // at its offset grp->rank() * blk. Collective over grp; SDNS_PEER=0 or a
-  // transport that cannot map keeps the all-to-all.
+  // at its offset grp->rank() * blk. Collective over grp; the all_to_all
+  // option or a transport that cannot map keeps the all-to-all.
   void map_peer_blocks(Comm* grp, int gp) {
-    const char* pe = std::getenv("SDNS_PEER");
-    if (gp <= 1 || (pe && pe[0] == '0')) return;
+    if (gp <= 1 || opt.all_to_all) return;
     peer_wb = grp->map_peers(wb);
     peer_wa = grp->map_peers(wa);
     if (peer_wb.empty() || peer_wa.empty()) {
@@ -478,9 +478,8 @@ struct sdns_ctx {
   // Pencil row group (same coord1, ordered by coord2 = its kz block): map
   // the members' wd and wc; collective over the row group.
   void map_row_peers() {
-    const char* pe = std::getenv("SDNS_PEER");
     const int p2 = cfg.p2;
-    if (!pencil || p2 <= 1 || (pe && pe[0] == '0')) return;
+    if (!pencil || p2 <= 1 || opt.all_to_all) return;
     peer_wd = row->map_peers(wd);
     peer_wc = row->map_peers(wc);
     if (peer_wd.empty() || peer_wc.empty()) {
@@ -1062,8 +1061,7 @@ void step_stages(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool 
 // kernels are short (64^3: config 1). Per-pass timing runs eagerly.
 bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool want_flag,
                bool want_stats = false) {
-  const char* gv = std::getenv("SDNS_GRAPH");
-  const bool graph = c->cfg.p == 1 && !c->timing && !(gv && gv[0] == '0');
+  const bool graph = c->cfg.p == 1 && !c->timing && !c->opt.no_graph;
   if (!graph) {
     step_stages(c, st, dt, post_project, want_stats);
   } else {
@@ -1474,6 +1472,11 @@ int sdns_comm_all_to_all_bytes(sdns_comm* c, const void* send, const int64_t* se
 
 int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* comm, void* stream,
                     sdns_ctx** out) {
+  return sdns_ctx_create_ex(cfg, rank, device, comm, stream, nullptr, out);
+}
+
+int sdns_ctx_create_ex(const sdns_config* cfg, int rank, int device, sdns_comm* comm,
+                       void* stream, const sdns_ctx_options* opts, sdns_ctx** out) {
   return guarded([&] {
     validate(*cfg);
     if (!comm) config_error("ctx: communicator is NULL");
@@ -1492,6 +1495,7 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
       config_error("the sm_100a pencil path needs p2 <= 16");
     auto c = std::make_unique<sdns_ctx>();
     c->cfg = *cfg;
+    if (opts) c->opt = *opts;
     c->lo = build_layout(*cfg, rank);
     c->device = device;
     c->world = comm->c;
@@ -1542,18 +1546,15 @@ int sdns_ctx_create(const sdns_config* cfg, int rank, int device, sdns_comm* com
     } else {
       c->wb = cfg->p == 1 ? c->wa : static_cast<double2*>(dev_alloc(c.get(), wbytes));
       c->map_peer_blocks(c->world.get(), cfg->p);
-      const char* ov = std::getenv("SDNS_OVERLAP");
-      if (cfg->p > 1 && !c->peer && !(ov && ov[0] == '0')) {
+      if (cfg->p > 1 && !c->peer && !c->opt.serial) {
         SDNS_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
         for (auto& e : c->xev) SDNS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       }
-      const char* xl = std::getenv("SDNS_XLAYOUT");
       // (not at 1024^3: a p = 1 RK4 state + work then needs ~157 GB without it)
-      if (cfg->p == 1 && n <= 512 && is_pow2(n) && !(xl && xl[0] == '0')) {
+      if (cfg->p == 1 && n <= 512 && is_pow2(n) && !c->opt.plain_layout) {
         c->cs_x = static_cast<long long>(c->pitch) * c->lo.spec_shape[1] * n;
         c->wx = static_cast<double2*>(dev_alloc(c.get(), sizeof(double2) * c->cs_x * 5));
-        const char* zc = std::getenv("SDNS_ZCHUNK");
-        c->zchunk = n == 512 && !(zc && zc[0] == '0');  // measured at 512
+        c->zchunk = n == 512;  // measured at 512
       }
     }
     const int stride = c->shells + 3;

@@ -800,16 +800,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 
 // L2 promotion of the tile loads: a tile row is exactly one 128 B line; a
 // 256 B promotion drags in the neighbouring line, which belongs to another
-// tile and is often evicted before that tile runs. SDNS_TMA_PROMO=0/64/128/256
-// overrides (A/B measurements).
-static CUtensorMapL2promotion tma_promotion() {
-  const char* e = std::getenv("SDNS_TMA_PROMO");
-  const int v = e ? std::atoi(e) : 128;
-  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                          : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                                     : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-}
+// tile and is often evicted before that tile runs (64 / 256 B / none
+// measured no better).
+constexpr CUtensorMapL2promotion kTilePromotion = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
 
 template <int N, int CS>
 static ColGeom with_tile_map(const ColGeom& g, const double2* base, long long fcs, int nfields,
@@ -819,8 +812,6 @@ static ColGeom with_tile_map(const ColGeom& g, const double2* base, long long fc
   std::memset(tm, 0, sizeof(*tm));
   if (!SDNS_COLTMA || (CS != 8 && !(CS == 4 && SDNS_CS4TMA)) || g.mpitch <= 0 || g.mrows <= 0 || ((N - 1) >> g.pb_shift) != 0)
     return r;
-  const char* off = std::getenv("SDNS_NO_TMA");  // LDGSTS tile loads (parity checks)
-  if (off && off[0] == '1') return r;
   const auto enc = tmap_encoder();
   if (!enc) return r;
   constexpr cuuint32_t BP = N < 256 ? N : 256;
@@ -835,14 +826,9 @@ static ColGeom with_tile_map(const ColGeom& g, const double2* base, long long fc
   const cuuint32_t box[5] = {2 * CS, 1, 1, BP, 1}, es[5] = {1, 1, 1, 1, 1};
   const CUresult e = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2*>(base), dims,
                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_NONE, tma_promotion(),
+                         CU_TENSOR_MAP_SWIZZLE_NONE, kTilePromotion,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (e == CUDA_SUCCESS) {
-    r.tma = 1;
-  } else if (std::getenv("SDNS_DEBUG_TMA")) {
-    std::fprintf(stderr, "sdns: tensor map encode failed (%d), LDGSTS tile loads\n",
-                 static_cast<int>(e));
-  }
+  if (e == CUDA_SUCCESS) r.tma = 1;  // else: LDGSTS tiles (same results)
   return r;
 }
 

@@ -459,6 +459,7 @@ struct Opts {
   double timeout_s = 30.0;
   int device = 0;
   uint64_t seed = 1607;
+  sdns_ctx_options ctx{};
 };
 
 Opts read_opts(const sdns_run_options* o) {
@@ -469,6 +470,7 @@ Opts read_opts(const sdns_run_options* o) {
   if (o->collective_timeout_s > 0) r.timeout_s = o->collective_timeout_s;
   r.device = o->device;
   r.seed = o->seed;
+  r.ctx = o->ctx;
   return r;
 }
 
@@ -478,7 +480,7 @@ void run_worker(const sdns_config& cfg, const std::string& icase, const Opts& o,
                 sdns_comm* comm, int device, sdns_run_result& out) {
   sdns_run_result res = out;
   Ctx ctx;
-  ck(sdns_ctx_create(&cfg, rank, device, comm, nullptr, &ctx.c));
+  ck(sdns_ctx_create_ex(&cfg, rank, device, comm, nullptr, &o.ctx, &ctx.c));
   Fld u_hat, snap;
   ck(sdns_field_alloc(ctx.c, SDNS_SPECTRAL, 3, &u_hat.f));
   ck(sdns_field_alloc(ctx.c, SDNS_REAL, 3, &snap.f));
@@ -601,7 +603,7 @@ double bench_entry_seconds(const sdns_config& cfg, int steps, const Opts& o) {
   std::mutex mu;
   drive_workers(cfg, o, [&](int rank, sdns_comm* comm) {
     Ctx ctx;
-    ck(sdns_ctx_create(&cfg, rank, o.device, comm, nullptr, &ctx.c));
+    ck(sdns_ctx_create_ex(&cfg, rank, o.device, comm, nullptr, &o.ctx, &ctx.c));
     Fld u_hat;
     ck(sdns_field_alloc(ctx.c, SDNS_SPECTRAL, 3, &u_hat.f));
     initial_state(ctx.c, cfg, "taylor_green", o.seed, u_hat.f);

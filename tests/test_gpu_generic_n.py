@@ -54,20 +54,19 @@ def test_fft_generic_length_vs_numpy(n):
 
 @pytest.mark.parametrize("n", [12, 18, 24])
 @pytest.mark.parametrize("gi", range(len(GEOMS)))
-@pytest.mark.parametrize("peer", ["1", "0"])
-def test_fft_generic_length_decompositions(n, gi, peer, monkeypatch):
+@pytest.mark.parametrize("a2a", [0, 1])
+def test_fft_generic_length_decompositions(n, gi, a2a):
     """Slab and pencil with blocks that are not powers of two (n/p = 9, 6, 4;
     pencil kz blocks 4/3/3 of n/2+1 = 10), peer-direct and all-to-all."""
     geom = GEOMS[gi]
     if not _valid(n, geom):
         pytest.skip("p does not divide n")
-    monkeypatch.setenv("SDNS_PEER", peer)
     u = np.random.default_rng(n).uniform(-1, 1, (3, n, n, n))
     expect = O.forward(u)
     cfg = S.SolverConfig(n=n, **geom)
 
     def body(rank, comm):
-        with S.Context(cfg, rank=rank, comm=comm) as c:
+        with S.Context(cfg, rank=rank, comm=comm, options={"all_to_all": a2a}) as c:
             lo = c.layout
             fd = c.spectral_field()
             fft = S.DistributedFFT(c)

@@ -549,7 +549,7 @@ def test_inprocess_transpose_modes_bitwise(geom):
     default (stores straight into the owning rank's buffer, a stream barrier
     after each: peer-direct), else as
     all-to-alls -- overlapped with the next group's transforms for slab
-    (SDNS_PEER=0), else serial (SDNS_OVERLAP=0 as well). The transforms and
+    (context option all_to_all), else serial (all_to_all + serial). The transforms and
     arithmetic are the same, so one RHS and two RK4 steps must agree bit for
     bit across the modes."""
     n = 32
@@ -580,14 +580,10 @@ def test_inprocess_transpose_modes_bitwise(geom):
         return S.run_group(p, body)
 
     modes = {}
-    for name, env in (("peer", {}), ("overlap", {"SDNS_PEER": "0"}),
-                      ("serial", {"SDNS_PEER": "0", "SDNS_OVERLAP": "0"})):
-        os.environ.update(env)
-        try:
+    for name, opt in (("peer", {}), ("overlap", {"all_to_all": 1}),
+                      ("serial", {"all_to_all": 1, "serial": 1})):
+        with S.context_options(**opt):
             modes[name] = run()
-        finally:
-            for k in env:
-                os.environ.pop(k, None)
     for name in ("overlap", "serial"):
         for a, b in zip(modes["peer"], modes[name]):
             for x, y in zip(a, b):

@@ -278,8 +278,8 @@ def test_nccl_backend_pencil_1x1_exchange():
 def test_512_pipeline_variants_bitwise():
     """At 512^3 the column passes load tiles through TMA tensor maps and P1/P2
     go through the chunk-major work layout and P2 .. P5a through the chunked
-    layout; the LDGSTS loads (SDNS_NO_TMA=1) and the plain layouts
-    (SDNS_XLAYOUT=0, SDNS_ZCHUNK=0) run the same arithmetic, so one RHS
+    layout; the LDGSTS loads (context option ldgsts_tiles) and the plain
+    layouts (plain_layout) run the same arithmetic, so one RHS
     must agree bit for bit across all of them and across repeated runs (a
     pipeline race would show here)."""
     n = 512
@@ -287,28 +287,18 @@ def test_512_pipeline_variants_bitwise():
     uh = S.iso_init(n, lo, seed=1607)
     cfg = S.SolverConfig(n=n, nu=5e-4, dt=5e-4, t_end=5e-4)
 
-    def rhs(**env):
-        old = {k: os.environ.get(k) for k in env}
-        os.environ.update(env)
-        try:
-            with S.Context(cfg) as c:
-                u = c.spectral_field().upload(uh)
-                du = c.spectral_field()
-                S.compute_rhs(c, u, cfg.nu, du)
-                return du.download()
-        finally:
-            for k, v in old.items():
-                if v is None:
-                    os.environ.pop(k, None)
-                else:
-                    os.environ[k] = v
+    def rhs(**opt):
+        with S.Context(cfg, options=opt) as c:
+            u = c.spectral_field().upload(uh)
+            du = c.spectral_field()
+            S.compute_rhs(c, u, cfg.nu, du)
+            return du.download()
 
     a = rhs()
     assert np.array_equal(a, rhs())
-    assert np.array_equal(a, rhs(SDNS_NO_TMA="1"))
-    assert np.array_equal(a, rhs(SDNS_XLAYOUT="0"))
-    assert np.array_equal(a, rhs(SDNS_ZCHUNK="0"))  # natural layout after P2
-    assert np.array_equal(a, rhs(SDNS_ZCHUNK="0", SDNS_NO_TMA="1"))
+    assert np.array_equal(a, rhs(ldgsts_tiles=1))
+    assert np.array_equal(a, rhs(plain_layout=1))  # natural layouts throughout
+    assert np.array_equal(a, rhs(plain_layout=1, ldgsts_tiles=1))
     assert np.isfinite(a).all() and np.abs(a).max() > 0
 
 
