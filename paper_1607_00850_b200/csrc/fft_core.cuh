@@ -21,10 +21,6 @@
 
 namespace sdns_dev {
 
-#ifndef SDNS_MIDREG
-#define SDNS_MIDREG 1
-#endif
-
 // LDGSTS: 16-byte global->shared copy (zero-filled when !valid).
 __device__ __forceinline__ void cp_async16(double2* dst, const double2* src, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -286,7 +282,7 @@ __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx
     for (int r = 0; r < R; ++r) a[r] = v[b + r * NB];
     if constexpr (LREG && LAST && NS > 1 && R == 8 && NB == 1) {
       apply_tw8<S>(a, lt.w1, lt.w4);
-    } else if constexpr (SDNS_MIDREG && LREG && !LAST && NS == mid_ns(N) && NS > 1 && R == 8 &&
+    } else if constexpr (LREG && !LAST && NS == mid_ns(N) && NS > 1 && R == 8 &&
                          NB == 1) {
       apply_tw8<S>(a, lt.m1, lt.m4);
     } else if (NS > 1) {

@@ -244,26 +244,18 @@ __device__ __forceinline__ void rk_elem(const XfArgs& a, const SpecGeom& g, long
   rk_finish<MODE>(a, g, e, i, j, k, in, finite, un);
 }
 
-#ifndef SDNS_RKILP  // two modes per iteration: 1 stage 3, 2 + stages 1-2, 3 + stage 0
-#define SDNS_RKILP 2
-#endif
-#ifndef SDNS_RK3B  // CTAs per SM the stage-3 update is compiled for
-#define SDNS_RK3B 1
-#endif
+// Stages 1-3 update two modes per iteration (both modes' loads issued
+// before either's arithmetic); stages 1-2 are compiled for 2 CTAs/SM.
 template <int MODE>
-__global__ void __launch_bounds__(256, ((SDNS_RKILP > 1 && MODE == XF_RK12) ||
-                                       (SDNS_RKILP > 2 && MODE == XF_RK0))
-                                           ? 2
-                                           : (MODE == XF_RK3 ? SDNS_RK3B : 1))
+__global__ void __launch_bounds__(256, MODE == XF_RK12 ? 2 : 1)
 k_rk_update(XfArgs a, SpecGeom g) {
   const long long total = static_cast<long long>(g.s0) * g.prow * g.pitch;
   bool finite = true;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  // stage 3 (the most loads per mode): two modes per iteration, both modes'
-  // loads issued before either's arithmetic and stores (3.29 -> 3.11 ms; the
-  // other stages lose occupancy to the doubled registers and gain nothing)
-  if constexpr (SDNS_RKILP && (MODE == XF_RK3 || (SDNS_RKILP > 1 && MODE == XF_RK12) ||
-                                (SDNS_RKILP > 2 && MODE == XF_RK0))) {
+  // stages 1-3: two modes per iteration, both modes' loads issued before
+  // either's arithmetic and stores (stage 3 3.29 -> 3.11 ms, stages 1-2
+  // 2.52 -> 2.44 ms; stage 0, write-bound, gains nothing)
+  if constexpr (MODE == XF_RK3 || MODE == XF_RK12) {
   for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += 2 * stride) {
     const long long e2 = e + stride;
@@ -363,20 +355,17 @@ struct WarpBar {
 
 // Launch shape of the fused z pass: 4 rows of 64 threads at n >= 512 (each
 // row synchronises on its own named barrier), else whole rows per warp.
-#ifndef SDNS_ZRPC  // rows per CTA of the fused z pass at n = 512 (A/B)
-#define SDNS_ZRPC 4
-#endif
 template <int N>
 struct ZFCfg {
   static constexpr int E = fft_elems(N);
   static constexpr int TPC = N / E;
   static constexpr int RPC =
-      TPC >= 64 ? (N == 512 ? SDNS_ZRPC : 4) : (256 / TPC > 64 ? 64 : 256 / TPC);
+      TPC >= 64 ? 4 : (256 / TPC > 64 ? 64 : 256 / TPC);
   static constexpr int THREADS = TPC * RPC;
   static constexpr int HP = N / 2 + 8;  // padded half-row (n/2+1 modes)
   // n = 512: both twiddled radix-8 stages take their twiddles from
   // registers (LastTw), so no table is staged in shared memory
-  static constexpr bool REG = N == 512 && SDNS_MIDREG;
+  static constexpr bool REG = N == 512;
   static constexpr size_t SMEM =
       sizeof(double2) * (static_cast<size_t>(RPC) * 6 * HP + (REG ? 0 : N));
   // CTAs per SM the shared memory allows (n = 1024: one -- then give the
@@ -384,23 +373,11 @@ struct ZFCfg {
   static constexpr int MINB = SMEM * 4 <= 227 * 1024 ? 4 : (SMEM * 2 <= 227 * 1024 ? 2 : 1);
 };
 
-#ifndef SDNS_ZTMA
-#define SDNS_ZTMA 1
-#endif
-#ifndef SDNS_ZPF  // chunked z rows: L2 prefetch of the rows SDNS_ZPF CTAs ahead (0: off)
-#define SDNS_ZPF 0  // measured: no gain (296 or 600 CTAs ahead)
-#endif
-
-// z-pass transform; SDNS_ZNOFFT builds a transform-free variant (wrong
-// results) for A/B measurements of the pass's memory/shared-memory floor.
+// z-pass transform.
 template <int N, int S, class Bar>
 __device__ __forceinline__ void zfft(double2 (&v)[fft_elems(N)], double2* sm, SwzIdx sw, int t,
                                      const double2* tws, Bar bar, const LastTw& lt) {
-#ifdef SDNS_ZNOFFT
-  bar();
-#else
   block_fft_lt<N, S>(v, sm, sw, t, tws, bar, lt);
-#endif
 }
 
 template <int N, bool PO = false>
@@ -431,7 +408,6 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   // (u0, w1') (u1, w0') (u2, w2) -- slot s holds field kZSlot[s] -- all of
   // the row in flight at once. The z part of the curl (w0 = w0' - i kz u1,
   // w1 = w1' + i kz u0) is applied when the pair is sampled.
-#if SDNS_ZTMA
   // One thread per row hands the 6 contiguous half-rows (n2 * 16 B each; one
   // piece per kz segment on pencil rows) to the bulk-copy engine; the row
   // waits on its mbarrier.
@@ -445,20 +421,6 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
     mbar_expect_tx(&zbar[r], 6u * static_cast<unsigned>(rm.pitch) * 16u);
 #pragma unroll
     for (int sl = 0; sl < 6; ++sl) tma_load5(S + sl * HP, &ztm, 0, 0, y, x, fld[sl], &zbar[r]);
-    if constexpr (SDNS_ZPF > 0) {  // warm L2 with the row a later CTA will stage
-      const int rf = ri + SDNS_ZPF * RPC;
-      if (rf < rm.nrows) {
-        const int xf = rf / rm.rpp, yf = rf - xf * rm.rpp;
-#pragma unroll
-        for (int sl = 0; sl < 6; ++sl) {
-          asm volatile(
-              "cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(
-                  &ztm),
-              "r"(0), "r"(0), "r"(yf), "r"(xf), "r"(fld[sl])
-              : "memory");
-        }
-      }
-    }
   } else if (valid && t == 0) {
     const int fld[6] = {0, 4, 1, 3, 2, 5};
     mbar_expect_tx(&zbar[r], 6u * static_cast<unsigned>(rm.n2) * 16u);
@@ -480,26 +442,6 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   }
   __syncthreads();  // twiddles
   if (valid) mbar_wait(&zbar[r], 0);
-#else
-  if (valid) {
-#pragma unroll
-    for (int k0 = 0; k0 <= N / 2; k0 += TPC) {
-      const int k = k0 + t;
-      if (k <= N / 2) {
-        const long long e = zel(rm, ro, ri, k);
-        cp_async16(S + k, f + e, true);
-        cp_async16(S + HP + k, f + 4 * cs + e, true);
-        cp_async16(S + 2 * HP + k, f + cs + e, true);
-        cp_async16(S + 3 * HP + k, f + 3 * cs + e, true);
-        cp_async16(S + 4 * HP + k, f + 2 * cs + e, true);
-        cp_async16(S + 5 * HP + k, f + 5 * cs + e, true);
-      }
-    }
-  }
-  cp_commit();
-  cp_wait0();
-  __syncthreads();  // twiddles + staging
-#endif
   const LastTw lt = last_twiddles<N>(tws, t);
   double2 v[E], p1[E];
 #pragma unroll

@@ -37,43 +37,10 @@ namespace sdns_dev {
 
 namespace {
 
-#ifndef SDNS_VX
-#define SDNS_VX 0
-#endif
-#ifndef SDNS_VY
-#define SDNS_VY 0
-#endif
-#ifndef SDNS_VYI
-#define SDNS_VYI 10
-#endif
-#ifndef SDNS_VXI
-#define SDNS_VXI 8
-#endif
-#ifndef SDNS_PAIR  // n = 1024 4-column tiles: both 64 B halves of a 128 B row back to back
-#define SDNS_PAIR 1
-#endif
-#ifndef SDNS_CS4TMA  // 4-column tiles (n = 1024 inverse passes) also load by TMA
-#define SDNS_CS4TMA 1
-#endif
-#ifndef SDNS_COLTMA
-#define SDNS_COLTMA 1
-#endif
-#ifndef SDNS_COLREG  // n = 512 column transforms: register twiddles (fft_core.cuh LastTw)
-#define SDNS_COLREG 1
-#endif
-#ifndef SDNS_PLAINLT  // plain passes hold the register twiddles for the whole kernel
-#define SDNS_PLAINLT 1
-#endif
-#ifndef SDNS_FDIV  // tile index -> (row, kz) by float reciprocal instead of integer division
-#define SDNS_FDIV 1
-#endif
-#ifndef SDNS_L2PF  // TMA-fed rings: items prefetched into L2 beyond the ring (A/B only:
-#define SDNS_L2PF 0  // measured slower -- P5a 0.49 -> 0.62 ms, n = 1024 P1 33 -> 43 ms)
-#endif
-#ifndef SDNS_NB0
-#define SDNS_NB0 3
-#endif
-enum : int { VX = SDNS_VX, VY = SDNS_VY, VYI = SDNS_VYI, VXI = SDNS_VXI };
+// Pass variants of PipeCfg: 0 = plain y/x passes below n = 1024, 8 = P1
+// (ring of two + scratch tile), 9 = plain passes at n = 1024 (single 128 KB
+// buffer), 10 = P2 (ring of two + TMA-store staging tile).
+enum : int { VX = 0, VY = 0, VYI = 10, VXI = 8 };
 
 template <int N, int V>
 struct PipeCfg {
@@ -89,7 +56,7 @@ struct PipeCfg {
   static constexpr int CS = (N >= 1024 && V != 9) ? 4 : CS0;
   static constexpr int THREADS = TPC * CS;
   static constexpr int NBUF = (V == 2 || V == 3 || V == 4 || V == 9) ? 1
-                             : (V == 0 && N == 512) ? SDNS_NB0 : 2;
+                             : (V == 0 && N == 512) ? 3 : 2;
   static constexpr int MINB = V == 1 ? 3 : (V == 2 ? 4 : (V == 3 ? 2 : 1));
   // V = 8: one extra tile-sized exchange buffer (the x inverse pass runs its
   // first transform there and re-reads the input tile for the second)
@@ -118,7 +85,7 @@ struct Tile {
 template <int CS>
 struct TileIdx {
   __device__ __forceinline__ int operator()(int x) const {
-    return (CS == 4 && !SDNS_CS4TMA ? (x ^ ((x >> 3) & 1)) : x) * CS;
+    return x * CS;
   }
 };
 
@@ -132,7 +99,6 @@ struct CIdx {
 template <int CS>
 __device__ __forceinline__ Tile tile_of(int tile, int col, const ColGeom& g) {
   const int gc = tile * CS + col;
-#if SDNS_FDIV
   // gc / pitch through a float reciprocal and one correction step (exact
   // for gc < 2^24, far above any tile count here): the 32-bit integer
   // division sequence showed up in the column passes' stall samples
@@ -145,10 +111,6 @@ __device__ __forceinline__ Tile tile_of(int tile, int col, const ColGeom& g) {
     ++re;
     kz -= g.pitch;
   }
-#else
-  const int re = gc / g.pitch;
-  const int kz = gc - re * g.pitch;
-#endif
   const int row = re < g.seg_a ? re + g.off0 : re - g.seg_a + g.off1;
   Tile t;
   t.valid = re < g.nrows && kz < g.n2;
@@ -197,9 +159,6 @@ __device__ __forceinline__ void store_own(double2* dst, const double2 (&v)[fft_e
                                           const ColGeom& g, const Tile& tl, const PosOff<N>& po,
                                           int t) {
   constexpr int E = fft_elems(N), TPC = N / E;
-#ifdef SDNS_NOSTORE  // A/B measurement only (wrong results)
-  if (tl.valid || !tl.valid) return;
-#endif
   if (!tl.valid) return;
   double2* b = dst + tl.base;
 #pragma unroll
@@ -249,52 +208,25 @@ __device__ __forceinline__ void peer_fence() {
   if constexpr (SEP == 2) __threadfence_system();
 }
 
-// Column transform; SDNS_NOFFT builds a memory-only variant (wrong results)
-// for A/B measurements of the pipelines' memory ceiling.
+// Column transform. At n = 512 both twiddled radix-8 stages take their
+// twiddles from registers (LastTw: 4 table reads instead of 14 per transform).
 template <int N, int S, class IDX, class BAR>
 __device__ __forceinline__ void col_fft(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
                                         const double2* __restrict__ tw, BAR bar) {
-#ifdef SDNS_NOFFT
-  bar();
-#else
-  if constexpr (N == 512 && SDNS_COLREG) {
-    // both twiddled radix-8 stages from registers (LastTw: 4 table reads
-    // instead of 14 per transform)
+  if constexpr (N == 512)
     block_fft_lt<N, S>(v, sm, idx, t, tw, bar, last_twiddles<N>(tw, t));
-  } else {
-    block_fft<N, S>(v, sm, idx, t, tw, bar);
-  }
-#endif
-}
-#ifndef SDNS_YINVLT  // the y inverse pass holds the register twiddles for the whole kernel
-#define SDNS_YINVLT 1
-#endif
-template <int N, int S, class IDX, class BAR>
-__device__ __forceinline__ void col_fft_lt(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
-                                           const double2* __restrict__ tw, BAR bar,
-                                           const LastTw& lt);
-template <int N, int S, class IDX, class BAR>
-__device__ __forceinline__ void col_fft_y(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
-                                          const double2* __restrict__ tw, BAR bar,
-                                          const LastTw& lt) {
-  if constexpr (SDNS_YINVLT)
-    col_fft_lt<N, S>(v, sm, idx, t, tw, bar, lt);
   else
-    col_fft<N, S>(v, sm, idx, t, tw, bar);
+    block_fft<N, S>(v, sm, idx, t, tw, bar);
 }
 // Same with the register twiddles held by the caller (read once per kernel).
 template <int N, int S, class IDX, class BAR>
 __device__ __forceinline__ void col_fft_lt(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
                                            const double2* __restrict__ tw, BAR bar,
                                            const LastTw& lt) {
-#ifdef SDNS_NOFFT
-  bar();
-#else
-  if constexpr (N == 512 && SDNS_COLREG)
+  if constexpr (N == 512)
     block_fft_lt<N, S>(v, sm, idx, t, tw, bar, lt);
   else
     block_fft<N, S>(v, sm, idx, t, tw, bar);
-#endif
 }
 
 // Lane roles: column-minor (col = tid % CS, t = tid / CS), so a warp's
@@ -332,25 +264,6 @@ __device__ __forceinline__ void tma_tile(double2* buf, const CUtensorMap* tm, co
 #pragma unroll
   for (int h = 0; h < N / BP; ++h)
     tma_load5(buf + h * BP * CS, tm, 2 * (tl.kz & 7), tl.kz >> 3, tl.row, h * BP, field, bar);
-}
-
-// L2 prefetch of a tile's boxes (no shared memory, no completion): keeps
-// more of the strided tile rows in flight than the ring alone holds.
-__device__ __forceinline__ void tma_prefetch5(const CUtensorMap* tm, int c0, int c1, int c2,
-                                              int c3, int c4) {
-  asm volatile(
-      "cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(tm),
-      "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-      : "memory");
-}
-
-template <int N, int CS>
-__device__ __forceinline__ void tma_prefetch_tile(const CUtensorMap* tm, const Tile& tl,
-                                                  int field) {
-  constexpr int BP = N < 256 ? N : 256;
-#pragma unroll
-  for (int h = 0; h < N / BP; ++h)
-    tma_prefetch5(tm, 2 * (tl.kz & 7), tl.kz >> 3, tl.row, h * BP, field);
 }
 
 // Tile stores by the tensor-memory accelerator from a dedicated staging
@@ -423,10 +336,6 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
       issue_tile<N>(ring(slot), src(f), tl, po, ln.idx, t);
     }
   };
-  // L2 prefetch of an item beyond the ring (TMA-fed rings only)
-  auto prefetch = [&](int f, const Tile& tl) {
-    if (SDNS_L2PF && tma && threadIdx.x == 0) tma_prefetch_tile<N, CS>(tm, tl, fld(f));
-  };
   // A slot is refilled only after the barrier that ends its last transform
   // (block_fft's trailing barrier follows its last shared-memory access; the
   // single-buffer path has an explicit one): the same release the mbarrier
@@ -494,7 +403,7 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
   // of every 128 B row are requested one item apart and the second is served
   // by L2 (measured: walking single tiles, persistent CTAs drift apart and
   // DRAM delivers every 128 B line twice). Items of one tile keep their order.
-  constexpr bool PAIR = CS == 4 && N >= 1024 && SDNS_PAIR;
+  constexpr bool PAIR = CS == 4 && N >= 1024;
   constexpr int TS = PAIR ? 2 : 1;
   struct Item {
     int t0, f, h;  // pair base (PAIR) or tile, item, half
@@ -529,10 +438,6 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
       const Item n2 = adv(n1);
       const Tile tn2 = tile_at(n2);
       if (n2.t0 < ntiles) issue((i + 2) % 3, n2.f, tn2);
-      if constexpr (SDNS_L2PF > 0) {
-        const Item n3 = adv(n2);
-        if (n3.t0 < ntiles) prefetch(n3.f, tile_at(n3));
-      }
       if (tma) {
         mbar_wait(&tbar[i % 3], (i / 3) & 1);
       } else {
@@ -547,11 +452,6 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
       tn1 = tn2;
     } else {
       if (n1.t0 < ntiles) issue((i + 1) & 1, n1.f, tn1);
-      if constexpr (SDNS_L2PF > 0) {
-        Item nx = adv(n1);
-        for (int d = 1; d < SDNS_L2PF; ++d) nx = adv(nx);
-        if (nx.t0 < ntiles) prefetch(nx.f, tile_at(nx));
-      }
       if (tma) {
         mbar_wait(&tbar[i & 1], (i >> 1) & 1);
       } else {
@@ -581,7 +481,7 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
   const OutSel<N, SEP> os(go, Lanes<N, V>().t);
   // one read of the register twiddles per kernel (from L2), not per item
   LastTw lt{};
-  if constexpr (N == 512 && SDNS_COLREG && SDNS_PLAINLT) lt = last_twiddles<N>(tw, Lanes<N, V>().t);
+  if constexpr (N == 512) lt = last_twiddles<N>(tw, Lanes<N, V>().t);
   pipeline<N, V>(ntiles, 0, nfields, g, [&](int f) { return in + f * in_cs; },
                  [](int f) { return f; }, &tm, tw,
                  [&](int f, double2* buf, const Tile& tl, const PosOff<N>& po,
@@ -590,10 +490,7 @@ k_pipe_plain(const double2* in, double2* out, long long in_cs, long long out_cs,
                    double2 v[fft_elems(N)];
                    read_own<N>(v, buf, ln.idx, t);
                    ln.bar();
-                   if constexpr (SDNS_PLAINLT)
-                     col_fft_lt<N, S>(v, buf, ln.idx, t, tws, ln.bar, lt);
-                   else
-                     col_fft<N, S>(v, buf, ln.idx, t, tws, ln.bar);
+                   col_fft_lt<N, S>(v, buf, ln.idx, t, tws, ln.bar, lt);
                    release();  // buffer no longer read: the next tile may load
                    store_own<N, SEP == 2>(out + f * out_cs, v, go, os.tile(tl, go), os.po(po), t);
                  });
@@ -647,11 +544,7 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                          for (int m = 0; m < E; ++m) {
                            long long at = pout.o(m);
                            if constexpr (SEP == 2) at += __ldg(go.seg + ((t + m * TPC) >> go.pb_shift));
-#ifdef SDNS_NOU0  // A/B measurement only (wrong results): no U0 re-read
-                           const double2 a = make_double2(static_cast<double>(at), 0.0);
-#else
                            const double2 a = u0[at];
-#endif
                            v[m] = times_i(make_double2(v[m].x - ky * a.x, v[m].y - ky * a.y));
                          }
                        }
@@ -685,8 +578,8 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
   constexpr int E = fft_elems(N), TPC = N / E;
   // field of item it: 0, 1, 3, 2, 4
   auto order = [](int it) { return it ^ ((it >> 1) & ~(it >> 2) & 1); };
-  LastTw lt{};  // register twiddles read once per kernel (SDNS_YINVLT)
-  if constexpr (N == 512 && SDNS_COLREG && SDNS_YINVLT) lt = last_twiddles<N>(tw, Lanes<N, V>().t);
+  LastTw lt{};  // register twiddles read once per kernel
+  if constexpr (N == 512) lt = last_twiddles<N>(tw, Lanes<N, V>().t);
   const OutSel<N, SEP> os(go, Lanes<N, V>().t);
   extern __shared__ __align__(128) double2 smem[];
   double2* const stage = smem + PipeCfg<N, V>::NBUF * N * PipeCfg<N, V>::CS;
@@ -714,19 +607,19 @@ k_pipe_yinv(const double2* fin, double2* f, long long cs_in, long long cs, ColGe
                        const double ky = wavenum(t + m * TPC, N);
                        v[m] = times_i(make_double2(ky * vin[m].x, ky * vin[m].y));
                      }
-                     col_fft_y<N, +1>(v, buf, ln.idx, t, tws, ln.bar, lt);
+                     col_fft_lt<N, +1>(v, buf, ln.idx, t, tws, ln.bar, lt);
                      put(3, v, tl, po, t);
                    }
                    if (it == 2) {  // w2' -> w2 = F(w2')
-                     col_fft_y<N, +1>(vin, buf, ln.idx, t, tws, ln.bar, lt);
+                     col_fft_lt<N, +1>(vin, buf, ln.idx, t, tws, ln.bar, lt);
                      put(5, vin, tl, po, t);
                    } else if (it == 4) {  // K2 -> w1' = F(-i K2)
 #pragma unroll
                      for (int m = 0; m < E; ++m) v[m] = times_mi(vin[m]);
-                     col_fft_y<N, +1>(v, buf, ln.idx, t, tws, ln.bar, lt);
+                     col_fft_lt<N, +1>(v, buf, ln.idx, t, tws, ln.bar, lt);
                      put(4, v, tl, po, t);
                    } else {  // U0, U1, U2 -> u_c
-                     col_fft_y<N, +1>(vin, buf, ln.idx, t, tws, ln.bar, lt);
+                     col_fft_lt<N, +1>(vin, buf, ln.idx, t, tws, ln.bar, lt);
                      put(order(it), vin, tl, po, t);
                    }
                  });
@@ -770,7 +663,7 @@ static unsigned persistent_grid(K kernel, int threads, size_t smem, long long nt
 // walks pairs (n = 1024, 4-column tiles).
 template <int N, int V>
 static long long work_units(long long ntiles) {
-  return (PipeCfg<N, V>::CS == 4 && N >= 1024 && SDNS_PAIR) ? (ntiles + 1) / 2 : ntiles;
+  return (PipeCfg<N, V>::CS == 4 && N >= 1024) ? (ntiles + 1) / 2 : ntiles;
 }
 
 template <int N, int V>
@@ -810,7 +703,7 @@ static ColGeom with_tile_map(const ColGeom& g, const double2* base, long long fc
   ColGeom r = g;
   r.tma = 0;
   std::memset(tm, 0, sizeof(*tm));
-  if (!SDNS_COLTMA || (CS != 8 && !(CS == 4 && SDNS_CS4TMA)) || g.mpitch <= 0 || g.mrows <= 0 || ((N - 1) >> g.pb_shift) != 0)
+  if ((CS != 8 && CS != 4) || g.mpitch <= 0 || g.mrows <= 0 || ((N - 1) >> g.pb_shift) != 0)
     return r;
   const auto enc = tmap_encoder();
   if (!enc) return r;
