@@ -367,6 +367,68 @@ def other_configs(S, ctx, peak):
     return out
 
 
+def other_configs_1024(S, peak):
+    """n = 1024 on one GPU (informational): config 5's 3-component round trip
+    (rfftn + irfftn) against 3*(2R + 10C) bytes, and one RK4 step of the
+    configs[3] field (state + work ~155 GB) against the 213 C step roofline.
+    The round trip's real input is the inverse transform of that field
+    (timing is data-independent; its parity is pinned by the tests)."""
+    import torch
+
+    out = {}
+    n = 1024
+    R, C = 8.0 * n**3, spectral_bytes(n, 1)
+    nu, dt = NU_DT[n]
+    lo = S.build_layout(S.SolverConfig(n=n), 0)
+    t0 = time.time()
+    uh0 = S.iso_init(n, lo, seed=1607)
+    out["iso_init_s"] = time.time() - t0
+    with S.Context(S.SolverConfig(n=n)) as c:
+        stream = torch.cuda.ExternalStream(c.stream)
+        fft = S.DistributedFFT(c)
+        ur, ub, fu = c.real_field(), c.real_field(), c.spectral_field()
+        fu.upload(uh0)
+        fft.inverse(fu, ur)
+        fft.forward(ur, fu)
+        fft.inverse(fu, ub)
+        c.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(2):
+            fft.forward(ur, fu)
+            fft.inverse(fu, ub)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 2
+        rt = 3 * (2 * R + 10 * C)
+        out["config5_round_trip_1024"] = {
+            "ms": ms, "roofline_ms": rt / peak / 1e6, "frac": rt / (ms * 1e-3) / 1e9 / peak,
+            "rel_l2": S.l2_diff(c, ub, ur) / S.l2_diff(c, ur, c.real_field())}
+        for f in (ur, ub, fu):
+            f.free()
+    with S.Context(S.SolverConfig(n=n, nu=nu, dt=dt, t_end=dt)) as c:
+        stream = torch.cuda.ExternalStream(c.stream)
+        st = S.Rk4State(c)
+        u = c.spectral_field().upload(uh0)
+        st.set(u)
+        u.free()
+        del uh0
+        st.rk4_step(dt, post_project=True, check=True)  # warm
+        c.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(2):
+            st.rk4_step(dt, post_project=True, check=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 2
+        rf = step_roofline(n, "slab", 1, 1, 1, peak, NVL_FALLBACK)
+        out["config4_size_step_1024_one_gpu"] = {
+            "ms_per_step": ms, "roofline_ms": rf["roofline_ms"], "frac": rf["roofline_ms"] / ms}
+        st.close()
+    return out
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -548,6 +610,11 @@ def run_ours(args):
         line["other_configs"] = other_configs(S, ctx, hbm_peak)
     state.close()
     ctx.close()
+    if world == 1 and n == 512 and not args.no_other_configs and not args.no_1024:
+        try:
+            line.setdefault("other_configs", {}).update(other_configs_1024(S, hbm_peak))
+        except Exception as e:  # noqa: BLE001
+            line.setdefault("other_configs", {})["n1024"] = f"not run: {e}"
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_leg(config)
@@ -574,6 +641,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu1", action="store_true", help="reference arm: skip the p_cpu = 1 sample")
     ap.add_argument("--no-other-configs", action="store_true")
+    ap.add_argument("--no-1024", action="store_true", help="skip the n = 1024 one-GPU lines")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
                     help="N > 1: NCCL (one GPU per rank) or the host-callback transport "
                          "(harness check; ranks may share a GPU)")
