@@ -42,15 +42,11 @@ namespace {
 // buffer), 10 = P2 (ring of two + TMA-store staging tile).
 enum : int { VX = 0, VY = 0, VYI = 10, VXI = 8 };
 
-#ifndef SDNS_P1CS4  // n = 512 P1 on 4-column tiles walked in pairs, 2 CTAs/SM (A/B)
-#define SDNS_P1CS4 0
-#endif
 template <int N, int V>
 struct PipeCfg {
   static constexpr int E = fft_elems(N);
   static constexpr int TPC = N / E;
-  static constexpr int CSW =
-      (V == 1 || V == 2 || (V == 8 && N == 512 && SDNS_P1CS4)) ? 4 : 8;  // columns at TPC >= 64
+  static constexpr int CSW = (V == 1 || V == 2) ? 4 : 8;  // columns at TPC >= 64
   // n < 512: threads per CTA (measured at n = 64/128/256: small CTAs win
   // except for the two-transform inverse passes at 256)
   static constexpr int ST = (N >= 256 && (V == 8 || V == 10)) ? 512 : 64;
@@ -61,8 +57,7 @@ struct PipeCfg {
   static constexpr int THREADS = TPC * CS;
   static constexpr int NBUF = (V == 2 || V == 3 || V == 4 || V == 9) ? 1
                              : (V == 0 && N == 512) ? 3 : 2;
-  static constexpr int MINB =
-      V == 1 ? 3 : (V == 2 ? 4 : (V == 3 ? 2 : ((V == 8 && N == 512 && CS == 4) ? 2 : 1)));
+  static constexpr int MINB = V == 1 ? 3 : (V == 2 ? 4 : (V == 3 ? 2 : 1));
   // V = 8: one extra tile-sized exchange buffer (the x inverse pass runs its
   // first transform there and re-reads the input tile for the second)
   // V = 10: one extra tile buffer staging the y inverse pass's outputs for
@@ -408,7 +403,7 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
   // of every 128 B row are requested one item apart and the second is served
   // by L2 (measured: walking single tiles, persistent CTAs drift apart and
   // DRAM delivers every 128 B line twice). Items of one tile keep their order.
-  constexpr bool PAIR = CS == 4 && N >= 512;
+  constexpr bool PAIR = CS == 4 && N >= 1024;
   constexpr int TS = PAIR ? 2 : 1;
   struct Item {
     int t0, f, h;  // pair base (PAIR) or tile, item, half
@@ -668,7 +663,7 @@ static unsigned persistent_grid(K kernel, int threads, size_t smem, long long nt
 // walks pairs (n = 1024, 4-column tiles).
 template <int N, int V>
 static long long work_units(long long ntiles) {
-  return (PipeCfg<N, V>::CS == 4 && N >= 512) ? (ntiles + 1) / 2 : ntiles;
+  return (PipeCfg<N, V>::CS == 4 && N >= 1024) ? (ntiles + 1) / 2 : ntiles;
 }
 
 template <int N, int V>
