@@ -435,6 +435,8 @@ def run_ours(args):
 
     import paper_1607_00850_b200 as S
 
+    if args.lib:
+        S.use_library(args.lib)
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
@@ -642,6 +644,7 @@ def main():
     ap.add_argument("--no-cpu1", action="store_true", help="reference arm: skip the p_cpu = 1 sample")
     ap.add_argument("--no-other-configs", action="store_true")
     ap.add_argument("--no-1024", action="store_true", help="skip the n = 1024 one-GPU lines")
+    ap.add_argument("--lib", default=None, help="A/B: another build of the product library")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
                     help="N > 1: NCCL (one GPU per rank) or the host-callback transport "
                          "(harness check; ranks may share a GPU)")

@@ -35,7 +35,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SDNS_LIB", os.path.join(_HERE, "libsdns_cuda.so"))
+LIB_PATH = os.path.join(_HERE, "libsdns_cuda.so")
 
 
 # --- errors (proj/core/include/sdns/types.hpp:28-62) ------------------------
@@ -166,9 +166,19 @@ _lib = None
 _lib_lock = threading.Lock()
 
 
-def load_library(path: str = LIB_PATH):
+def use_library(path: str):
+    """Selects another build of the library (A/B variants from
+    tools/build_variant.sh) before the first call loads one."""
+    global LIB_PATH
+    if _lib is not None and os.path.abspath(path) != os.path.abspath(LIB_PATH):
+        raise CudaError("the library is already loaded; call use_library first")
+    LIB_PATH = path
+
+
+def load_library(path: Optional[str] = None):
     """Loads libsdns_cuda.so (built by __graft_entry__.build()). Raises if absent."""
     global _lib
+    path = path or LIB_PATH
     with _lib_lock:
         if _lib is not None:
             return _lib

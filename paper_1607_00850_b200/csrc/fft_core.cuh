@@ -264,10 +264,12 @@ __device__ __forceinline__ void apply_tw8(double2* a, double2 w1, double2 w4) {
   a[7] = cmul(a[7], cmul(w4, w3));
 }
 
+// jf / jl: butterfly index this thread runs in the first / last stage
+// (default t; the z pass remaps them so mirrored butterflies share a warp).
 template <int N, int E, int S, int NS, class IDX, class BAR = CtaBar, bool LREG = false>
 __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx, int t,
                                            const double2* __restrict__ tw, BAR bar = BAR{},
-                                           LastTw lt = LastTw{}) {
+                                           LastTw lt = LastTw{}, int jf = -1, int jl = -1) {
   constexpr int REM = N / NS;
   constexpr int R = REM >= E ? E : REM;
   constexpr int NB = E / R;
@@ -276,7 +278,7 @@ __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     double2 a[R];
-    const int j = t + b * TPC;
+    const int j = (NS == 1 && jf >= 0 ? jf : (LAST && jl >= 0 ? jl : t)) + b * TPC;
     const int k = j & (NS - 1);
 #pragma unroll
     for (int r = 0; r < R; ++r) a[r] = v[b + r * NB];
@@ -301,11 +303,13 @@ __device__ __forceinline__ void fft_stages(double2 (&v)[E], double2* sm, IDX idx
     }
   }
   if constexpr (!LAST) {
+    constexpr int NS2 = NS * R, REM2 = N / NS2, R2 = REM2 >= E ? E : REM2;
+    const int tn = (NS2 * R2 == N && jl >= 0) ? jl : t;  // the next stage's butterfly
     bar();
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = sm[idx(t + m * TPC)];
+    for (int m = 0; m < E; ++m) v[m] = sm[idx(tn + m * TPC)];
     bar();
-    fft_stages<N, E, S, NS * R, IDX, BAR, LREG>(v, sm, idx, t, tw, bar, lt);
+    fft_stages<N, E, S, NS * R, IDX, BAR, LREG>(v, sm, idx, t, tw, bar, lt, jf, jl);
   }
 }
 
@@ -321,8 +325,8 @@ __device__ __forceinline__ void block_fft(double2 (&v)[fft_elems(N)], double2* s
 template <int N, int S, class IDX, class BAR>
 __device__ __forceinline__ void block_fft_lt(double2 (&v)[fft_elems(N)], double2* sm, IDX idx,
                                              int t, const double2* __restrict__ tw, BAR bar,
-                                             const LastTw& lt) {
-  fft_stages<N, fft_elems(N), S, 1, IDX, BAR, true>(v, sm, idx, t, tw, bar, lt);
+                                             const LastTw& lt, int jf = -1, int jl = -1) {
+  fft_stages<N, fft_elems(N), S, 1, IDX, BAR, true>(v, sm, idx, t, tw, bar, lt, jf, jl);
 }
 
 // LastTw of thread t for length-N transforms whose last stage is radix 8

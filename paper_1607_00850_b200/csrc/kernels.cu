@@ -353,6 +353,59 @@ struct WarpBar {
   __device__ __forceinline__ void operator()() const { __syncwarp(); }
 };
 
+// n = 512 z pass, mirrored butterflies: the first stage of
+// the inverse transforms and the last stage of the forward n0 + i n1
+// transform run butterfly jm(t) instead of t, chosen so that jm and 64 - jm
+// (whose positions p and n - p pair up through the Hermitian symmetry) sit
+// on lanes l and l ^ 16 of one warp; (0, 32) are self-mirrored on warp 0's
+// lanes 0 and 16. A staged mode is then read once for both positions (the
+// mirrored value crosses by one shuffle), and the r2c split finds X[n - k]
+// by a shuffle instead of parking the spectrum in shared memory. Same
+// butterflies and operations: bitwise the plain kernel's results.
+__device__ __forceinline__ int z512_jm(int t) {
+  const int lane = t & 31;
+  if (t < 32) return lane < 16 ? lane : (lane == 16 ? 32 : 80 - lane);
+  return lane < 16 ? 16 + lane : 64 - lane;
+}
+__device__ __forceinline__ double2 shfl16(double2 v) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, 16), __shfl_xor_sync(0xffffffffu, v.y, 16));
+}
+// Samples of A + iB (SG: z part of the curl, as pair_sample_kz / pair_sample)
+// at the positions jm + 64 m of butterfly jm; whole warps.
+template <int SG>
+__device__ __forceinline__ void z512_sample(const double2* A, const double2* B, int jm,
+                                            double2 (&v)[8]) {
+  auto one = [&](int k, double2& lo, double2& hi) {
+    double2 a = A[k], b = B[k];
+    const double kz = static_cast<double>(k);
+    if (SG > 0)
+      b = make_double2(b.x - kz * a.y, b.y + kz * a.x);
+    else if (SG < 0)
+      b = make_double2(b.x + kz * a.y, b.y - kz * a.x);
+    if (k == 0 || k == 256) {  // FFTW c2r: imaginary parts of DC and Nyquist ignored
+      a.y = 0.0;
+      b.y = 0.0;
+    }
+    lo = make_double2(a.x - b.y, a.y + b.x);
+    hi = make_double2(a.x + b.y, b.x - a.y);  // conj a + i conj b: the value at n - k
+  };
+  double2 h[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    one(jm + 64 * q, v[q], h[q]);
+    const double2 rcv = shfl16(h[q]);  // the partner's mirror of position jm + 64 (7 - q)
+    v[7 - q] = jm == 32 ? h[q] : rcv;
+  }
+  if (jm == 0) {  // positions 64 m: self-mirrored (n - 64 m = 64 (8 - m)), plus k = 256
+    v[7] = h[1];
+    v[6] = h[2];
+    v[5] = h[3];
+    double2 lo, hi;
+    one(256, lo, hi);
+    v[4] = lo;
+  }
+}
+
 // Launch shape of the fused z pass: 4 rows of 64 threads at n >= 512 (each
 // row synchronises on its own named barrier), else whole rows per warp.
 template <int N>
@@ -376,8 +429,9 @@ struct ZFCfg {
 // z-pass transform.
 template <int N, int S, class Bar>
 __device__ __forceinline__ void zfft(double2 (&v)[fft_elems(N)], double2* sm, SwzIdx sw, int t,
-                                     const double2* tws, Bar bar, const LastTw& lt) {
-  block_fft_lt<N, S>(v, sm, sw, t, tws, bar, lt);
+                                     const double2* tws, Bar bar, const LastTw& lt, int jf = -1,
+                                     int jl = -1) {
+  block_fft_lt<N, S>(v, sm, sw, t, tws, bar, lt, jf, jl);
 }
 
 template <int N, bool PO = false>
@@ -443,30 +497,56 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   __syncthreads();  // twiddles
   if (valid) mbar_wait(&zbar[r], 0);
   const LastTw lt = last_twiddles<N>(tws, t);
+#ifndef SDNS_ZMIR
+#define SDNS_ZMIR 1
+#endif
+  constexpr bool MIR = N == 512 && SDNS_ZMIR;  // mirrored first / last stages (z512_jm)
+  const int jm = MIR ? z512_jm(t) : t;
   double2 v[E], p1[E];
+  if constexpr (MIR) {
+    z512_sample<+1>(S, S + HP, jm, v);
+  } else {
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = pair_sample_kz<N, +1>(S, S + HP, t + m * TPC);
+    for (int m = 0; m < E; ++m) v[m] = pair_sample_kz<N, +1>(S, S + HP, t + m * TPC);
+  }
   bar();
-  zfft<N, +1>(v, S, sw, t, tws, bar, lt);
+  zfft<N, +1>(v, S, sw, t, tws, bar, lt, MIR ? jm : -1);
   // pair 0 result parks in its own (now free) region at this thread's positions
+  if constexpr (MIR) {
 #pragma unroll
-  for (int m = 0; m < E; ++m) {
-    S[sw(t + m * TPC)] = v[m];
-    v[m] = pair_sample_kz<N, -1>(S + 2 * HP, S + 3 * HP, t + m * TPC);
+    for (int m = 0; m < E; ++m) S[sw(t + m * TPC)] = v[m];
+    z512_sample<-1>(S + 2 * HP, S + 3 * HP, jm, v);
+  } else {
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      S[sw(t + m * TPC)] = v[m];
+      v[m] = pair_sample_kz<N, -1>(S + 2 * HP, S + 3 * HP, t + m * TPC);
+    }
   }
   bar();
-  zfft<N, +1>(v, S + 2 * HP, sw, t, tws, bar, lt);
+  zfft<N, +1>(v, S + 2 * HP, sw, t, tws, bar, lt, MIR ? jm : -1);
+  if constexpr (MIR) {
 #pragma unroll
-  for (int m = 0; m < E; ++m) {
-    p1[m] = v[m];
-    v[m] = pair_sample<N>(S + 4 * HP, S + 5 * HP, t + m * TPC);
+    for (int m = 0; m < E; ++m) p1[m] = v[m];
+    z512_sample<0>(S + 4 * HP, S + 5 * HP, jm, v);
+  } else {
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      p1[m] = v[m];
+      v[m] = pair_sample<N>(S + 4 * HP, S + 5 * HP, t + m * TPC);
+    }
   }
   bar();
-  zfft<N, +1>(v, S + 4 * HP, sw, t, tws, bar, lt);
+  zfft<N, +1>(v, S + 4 * HP, sw, t, tws, bar, lt, MIR ? jm : -1);
   // (u0,w1) = p0, (u1,w0) = p1, (u2,w2) = v; 1/n^3 then u x omega. The third
   // product parks in pair 2's (now free) region: each thread re-reads its own
   // slots, so no barrier, and 8 fewer live registers through the next FFT.
+#ifndef SDNS_ZN2REG
+#define SDNS_ZN2REG 0
+#endif
   double* n2r = reinterpret_cast<double*>(S + 4 * HP);
+  double n2k[SDNS_ZN2REG ? E : 1];
+  (void)n2k;
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const double2 q0 = S[sw(t + m * TPC)];
@@ -475,10 +555,45 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
     const double wa = dmul(q1.y, norm), wb = dmul(q0.y, norm), wc = dmul(v[m].y, norm);
     const double n0 = dsub(dmul(ub, wc), dmul(uc, wb));
     const double n1 = dsub(dmul(uc, wa), dmul(ua, wc));
-    n2r[t + m * TPC] = dsub(dmul(ua, wb), dmul(ub, wa));
+    if constexpr (SDNS_ZN2REG) n2k[m] = dsub(dmul(ua, wb), dmul(ub, wa));
+    else n2r[t + m * TPC] = dsub(dmul(ua, wb), dmul(ub, wa));
     v[m] = make_double2(n0, n1);
   }
   bar();  // every thread has read its parked pair-0 values
+  if constexpr (MIR) {
+    // last stage on butterfly jm: its twiddles W^jm, W^4jm from the table
+    constexpr int TOFF = tw_stage_off(N, E, N / 8);
+    LastTw lf = lt;
+    lf.w1 = __ldg(tws + TOFF + jm);
+    lf.w4 = __ldg(tws + TOFF + 3 * (N / 8) + jm);
+    zfft<N, -1>(v, S, sw, t, tws, bar, lf, -1, jm);
+    // r2c split: X[k] here, X[n - k] on the partner lane (or on this lane
+    // for the self-mirrored butterflies 0 and 32)
+    const int keep = rm.kz_keep < N / 2 + 1 ? rm.kz_keep : N / 2 + 1;
+    auto put = [&](int k, double2 d, double2 m) {
+      if (!valid || k >= keep) return;
+      const double2 e = cconj(m);
+      const double2 dd = csub(d, e);
+      const double2 o0 = make_double2(0.5 * (d.x + e.x), 0.5 * (d.y + e.y));
+      const double2 o1 = make_double2(0.5 * dd.y, -0.5 * dd.x);
+      if constexpr (PO) {
+        const ZDst z = zdst(rmo, ri, k);
+        fo[z.el] = o0;
+        fo[z.el + z.cs] = o1;
+      } else {
+        const long long el = zel(rm, ro, ri, k);
+        f[el] = o0;
+        f[cs + el] = o1;
+      }
+    };
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const double2 rcv = shfl16(v[7 - m]);
+      const double2 mir = jm == 0 ? v[(8 - m) & 7] : (jm == 32 ? v[7 - m] : rcv);
+      put(jm + 64 * m, v[m], mir);
+    }
+    if (jm == 0) put(256, v[4], v[4]);
+  } else {
   zfft<N, -1>(v, S, sw, t, tws, bar, lt);
 #pragma unroll
   for (int m = 0; m < E; ++m) S[sw(t + m * TPC)] = v[m];
@@ -505,8 +620,9 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
       }
     }
   }
+  }
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = make_double2(n2r[t + m * TPC], 0.0);
+  for (int m = 0; m < E; ++m) v[m] = make_double2(SDNS_ZN2REG ? n2k[m] : n2r[t + m * TPC], 0.0);
   zfft<N, -1>(v, S + 2 * HP, sw, t, tws, bar, lt);
   if (valid) {
     double2* o2 = f + 2 * cs;

@@ -183,3 +183,21 @@ def test_errors_map_to_reference_exception_types():
     rc = lib.sdns_build_layout(ctypes.byref(S.SolverConfig(n=9).to_c()), 0,
                                ctypes.byref(S._Layout()))
     assert rc == 1 and b"even" in lib.sdns_last_error()
+
+
+def test_context_options_are_explicit():
+    """Execution choices are API options (sdns_ctx_options), not environment
+    variables: unknown names are rejected, and the library reads no
+    environment (no getenv in the product sources)."""
+    with pytest.raises(S.ConfigError):
+        with S.context_options(bogus=1):
+            pass
+    with S.context_options(all_to_all=1):
+        assert S._ctx_options(None).all_to_all == 1
+        assert S._ctx_options({"serial": 1}).serial == 1
+    assert S._ctx_options(None).all_to_all == 0
+    csrc = os.path.join(os.path.dirname(S.__file__), "csrc")
+    for f in os.listdir(csrc):
+        if f.endswith((".cu", ".cuh", ".cpp", ".h")):
+            assert "getenv" not in open(os.path.join(csrc, f)).read(), f
+    assert "os.environ" not in open(S.__file__).read()

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Builds an A/B variant of the product library with extra -D flags:
 #   tools/build_variant.sh NAME -DSDNS_X=1 ...  ->  libsdns_NAME.so (repo root)
-# Benchmark it with SDNS_LIB=$PWD/libsdns_NAME.so python bench.py ...
+# Benchmark it with python bench.py --lib $PWD/libsdns_NAME.so ... (tools/ab_libs.sh)
 set -e
 name=$1; shift
 cd "$(dirname "$0")/../paper_1607_00850_b200/csrc"

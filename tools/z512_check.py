@@ -8,6 +8,9 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1607_00850_b200 as S  # noqa: E402
 
+if os.environ.get("AB_LIB"):  # tool-level A/B: another build of the library
+    S.use_library(os.environ["AB_LIB"])
+
 tag = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 512
 geom = {}
