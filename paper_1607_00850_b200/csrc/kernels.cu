@@ -497,10 +497,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   __syncthreads();  // twiddles
   if (valid) mbar_wait(&zbar[r], 0);
   const LastTw lt = last_twiddles<N>(tws, t);
-#ifndef SDNS_ZMIR
-#define SDNS_ZMIR 1
-#endif
-  constexpr bool MIR = N == 512 && SDNS_ZMIR;  // mirrored first / last stages (z512_jm)
+  constexpr bool MIR = N == 512;  // mirrored first / last stages (z512_jm)
   const int jm = MIR ? z512_jm(t) : t;
   double2 v[E], p1[E];
   if constexpr (MIR) {
@@ -538,15 +535,10 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   }
   bar();
   zfft<N, +1>(v, S + 4 * HP, sw, t, tws, bar, lt, MIR ? jm : -1);
-  // (u0,w1) = p0, (u1,w0) = p1, (u2,w2) = v; 1/n^3 then u x omega. The third
-  // product parks in pair 2's (now free) region: each thread re-reads its own
-  // slots, so no barrier, and 8 fewer live registers through the next FFT.
-#ifndef SDNS_ZN2REG
-#define SDNS_ZN2REG 0
-#endif
-  double* n2r = reinterpret_cast<double*>(S + 4 * HP);
-  double n2k[SDNS_ZN2REG ? E : 1];
-  (void)n2k;
+  // (u0,w1) = p0 (parked), (u1,w0) = p1, (u2,w2) = v; 1/n^3 then u x omega.
+  // The real third product stays in registers through the next transform
+  // (parking it cost 3% of the shared-memory wavefronts).
+  double n2k[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const double2 q0 = S[sw(t + m * TPC)];
@@ -555,8 +547,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
     const double wa = dmul(q1.y, norm), wb = dmul(q0.y, norm), wc = dmul(v[m].y, norm);
     const double n0 = dsub(dmul(ub, wc), dmul(uc, wb));
     const double n1 = dsub(dmul(uc, wa), dmul(ua, wc));
-    if constexpr (SDNS_ZN2REG) n2k[m] = dsub(dmul(ua, wb), dmul(ub, wa));
-    else n2r[t + m * TPC] = dsub(dmul(ua, wb), dmul(ub, wa));
+    n2k[m] = dsub(dmul(ua, wb), dmul(ub, wa));
     v[m] = make_double2(n0, n1);
   }
   bar();  // every thread has read its parked pair-0 values
@@ -622,7 +613,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   }
   }
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = make_double2(SDNS_ZN2REG ? n2k[m] : n2r[t + m * TPC], 0.0);
+  for (int m = 0; m < E; ++m) v[m] = make_double2(n2k[m], 0.0);
   zfft<N, -1>(v, S + 2 * HP, sw, t, tws, bar, lt);
   if (valid) {
     double2* o2 = f + 2 * cs;
