@@ -412,8 +412,7 @@ template <int N>
 struct ZFCfg {
   static constexpr int E = fft_elems(N);
   static constexpr int TPC = N / E;
-  static constexpr int RPC =
-      TPC >= 64 ? 4 : (256 / TPC > 64 ? 64 : 256 / TPC);
+  static constexpr int RPC = TPC >= 64 ? 4 : (256 / TPC > 64 ? 64 : 256 / TPC);
   static constexpr int THREADS = TPC * RPC;
   static constexpr int HP = N / 2 + 8;  // padded half-row (n/2+1 modes)
   // n = 512: both twiddled radix-8 stages take their twiddles from

@@ -40,6 +40,10 @@ struct ColGeom {
   // the number of kz chunks) and storage-row extent of the source; tma = 1:
   // tiles come from the tensor map, 0: LDGSTS path.
   int mpitch = 0, mrows = 0, tma = 0;
+  // Launcher-set: the CTAs walk (tile, item) units instead of whole tiles
+  // (small grids: more CTAs, each a shorter chain; only where items of a
+  // tile are independent)
+  int split = 0;
   // Peer-direct output (slab transposes fused into the producing pass,
   // DESIGN.md §5): element offset of segment pos >> pb_shift's destination
   // block from the output base -- another rank's buffer on this device or

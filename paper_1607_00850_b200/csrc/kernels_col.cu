@@ -408,7 +408,14 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
   struct Item {
     int t0, f, h;  // pair base (PAIR) or tile, item, half
   };
+  const bool split = !PAIR && g.split;  // unit u = tile * items + (f - f_lo)
   auto adv = [&](Item it) {
+    if (split) {
+      const int u = it.t0 * items + (it.f - f_lo) + G;
+      it.t0 = u / items;
+      it.f = f_lo + (u - it.t0 * items);
+      return it;
+    }
     if constexpr (PAIR) {
       if (it.h == 0) {
         it.h = 1;
@@ -424,8 +431,12 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
   };
   auto tile_at = [&](const Item& it) { return tile_of<CS>(it.t0 + it.h, col, g); };
   Item cur{static_cast<int>(blockIdx.x) * TS, f_lo, 0};
+  if (split) {
+    cur.t0 = static_cast<int>(blockIdx.x) / items;
+    cur.f = f_lo + static_cast<int>(blockIdx.x) - cur.t0 * items;
+  }
   Tile tc = tile_at(cur);
-  if (cur.t0 < ntiles) issue(0, f_lo, tc);
+  if (cur.t0 < ntiles) issue(0, cur.f, tc);
   cp_commit();
   Item n1 = adv(cur);
   Tile tn1 = tile_at(n1);
@@ -662,8 +673,28 @@ static unsigned persistent_grid(K kernel, int threads, size_t smem, long long nt
 // Work units of a column pass: tiles, or tile pairs where the pipeline
 // walks pairs (n = 1024, 4-column tiles).
 template <int N, int V>
+constexpr int NBUF_RING() {
+  return PipeCfg<N, V>::NBUF;
+}
+
+template <int N, int V>
 static long long work_units(long long ntiles) {
   return (PipeCfg<N, V>::CS == 4 && N >= 1024) ? (ntiles + 1) / 2 : ntiles;
+}
+
+// Fields of a tile are independent items in the plain passes and in P2
+// with separate input and output buffers: when the tiles alone cannot fill
+// the GPU (small n), the CTAs walk (tile, item) units so more of them run
+// shorter chains (the ring pipeline is unchanged).
+template <int N, int V>
+static void split_units(ColGeom& g, long long nt, int items, int occ, unsigned& grid) {
+  constexpr bool PAIR = PipeCfg<N, V>::CS == 4 && N >= 1024;
+  const long long cap = static_cast<long long>(occ) * num_sms();
+  // (measured: 64^3 step 0.170 -> 0.156 ms, bitwise equal; no gain at 128)
+  if (N > 64 || PAIR || items <= 1 || nt >= cap || NBUF_RING<N, V>() < 2) return;
+  g.split = 1;
+  const long long units = nt * items;
+  grid = static_cast<unsigned>(units < cap ? units : cap);
 }
 
 template <int N, int V>
@@ -733,10 +764,11 @@ static void plain_launch(const double2* in, double2* out, long long in_cs, long 
   const long long nt = ntiles_of<N, V>(g);
   if (nt <= 0) return;
   static int occ = 0;
-  const unsigned grid =
+  unsigned grid =
       persistent_grid(k_pipe_plain<N, S, V, SEP>, C::THREADS, C::SMEM, work_units<N, V>(nt), &occ);
   CUtensorMap tm;
-  const ColGeom gt = with_tile_map<N, C::CS>(g, in, in_cs, nfields, &tm);
+  ColGeom gt = with_tile_map<N, C::CS>(g, in, in_cs, nfields, &tm);
+  split_units<N, V>(gt, nt, nfields, occ, grid);
   k_pipe_plain<N, S, V, SEP><<<grid, C::THREADS, C::SMEM, s>>>(in, out, in_cs, out_cs, nfields,
                                                                gt, go, static_cast<int>(nt), tw, tm);
 }
@@ -886,12 +918,13 @@ static void y_inv_n(const double2* fin, double2* f, long long cs_in, long long c
     got.tma = 0;
     k_pipe_yinv<N, VYI, 2><<<grid, C::THREADS, C::SMEM, s>>>(
         fin, f, cs_in, cs, gt, got, static_cast<int>(nt), f_lo, f_cnt, tw, tm, tmo);
-  } else if (go) {
+  } else if (go) {  // separate input and output buffers: items independent
     static int occ = 0;
-    const unsigned grid =
+    unsigned grid =
         persistent_grid(k_pipe_yinv<N, VYI, 1>, C::THREADS, C::SMEM, work_units<N, VYI>(nt), &occ);
     CUtensorMap tm;
-    const ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
+    ColGeom gt = with_tile_map<N, C::CS>(g, fin, cs_in, 5, &tm);
+    split_units<N, VYI>(gt, nt, f_cnt, occ, grid);
     CUtensorMap tmo;
     const ColGeom got = with_tile_map<N, C::CS>(*go, f, cs, 6, &tmo);
     k_pipe_yinv<N, VYI, 1><<<grid, C::THREADS, C::SMEM, s>>>(

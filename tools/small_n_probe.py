@@ -11,6 +11,9 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1607_00850_b200 as S  # noqa: E402
 
+if os.environ.get("AB_LIB"):  # tool-level A/B: another build of the library
+    S.use_library(os.environ["AB_LIB"])
+
 for n in (32, 64, 128):
     steps = 200
     lo = S.build_layout(S.SolverConfig(n=n), 0)
@@ -41,5 +44,8 @@ for n in (32, 64, 128):
         e1.record(stream)
         torch.cuda.synchronize()
         res["graph-only"] = e0.elapsed_time(e1) / steps
+        import hashlib
+        res["sha"] = hashlib.sha1(st.u_hat.download().tobytes()).hexdigest()[:12]
         st.close()
-        print(n, {k: round(v, 4) for k, v in res.items()}, "ms/step", flush=True)
+        print(n, {k: (round(v, 4) if isinstance(v, float) else v) for k, v in res.items()},
+              "ms/step", flush=True)
