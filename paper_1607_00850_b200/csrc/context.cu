@@ -173,6 +173,7 @@ struct sdns_ctx {
     if (wb && wb != wa) cudaFree(wb);
     if (wa) cudaFree(wa);
     if (h_out) cudaFreeHost(h_out);
+    if (h_fout) cudaFreeHost(h_fout);
     if (h_flag) cudaFreeHost(h_flag);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -189,6 +190,11 @@ struct sdns_ctx {
   double* d_fpartial = nullptr;
   double* d_fout = nullptr;
   const sdns_field* fused_u = nullptr;
+  // pinned copy of d_fout fetched with the sampled step's finite flag (one
+  // host synchronisation per sampled step instead of two); valid while
+  // fused_on_host
+  double* h_fout = nullptr;
+  bool fused_on_host = false;
   double* d_dts = nullptr;  // dt-dependent scalars of captured steps
   // slab p > 1: transposes on their own stream, overlapped with the FFT
   // passes of the other field groups (events order the two streams)
@@ -1091,9 +1097,14 @@ bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool wa
   }
   st->t += dt;
   st->step += 1;
+  c->fused_on_host = false;
   if (!want_flag) return true;
   SDNS_CUDA(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  if (want_stats)
+    SDNS_CUDA(cudaMemcpyAsync(c->h_fout, c->d_fout, sizeof(double) * (c->shells + 3),
+                              cudaMemcpyDeviceToHost, c->stream));
   c->wait();
+  c->fused_on_host = want_stats;
   double ok = *c->h_flag != 0 ? 1.0 : 0.0;
   c->world->allreduce(&ok, 1, 2);
   return ok > 0.5;
@@ -1102,20 +1113,25 @@ bool step_impl(sdns_ctx* c, sdns_state* st, double dt, int post_project, bool wa
 void stats_impl(sdns_ctx* c, const sdns_field* u, double nu, double t, double* row) {
   const SpecGeom g = c->sgeom();
   const double* src = c->d_fout;
-  if (u != c->fused_u) {
-    sdns_dev::stats_local(u->spec(), g, c->shells, c->d_partial, c->d_out, c->stream);
-    post_launch("collect_stats");
-    src = c->d_out;
+  const double* h = c->h_out;
+  if (u == c->fused_u && c->fused_on_host) {
+    h = c->h_fout;  // fetched with the step's finite flag
+  } else {
+    if (u != c->fused_u) {
+      sdns_dev::stats_local(u->spec(), g, c->shells, c->d_partial, c->d_out, c->stream);
+      post_launch("collect_stats");
+      src = c->d_out;
+    }
+    const int stride = c->shells + 3;
+    SDNS_CUDA(cudaMemcpyAsync(c->h_out, src, sizeof(double) * stride, cudaMemcpyDeviceToHost,
+                              c->stream));
+    c->wait();
   }
-  const int stride = c->shells + 3;
-  SDNS_CUDA(cudaMemcpyAsync(c->h_out, src, sizeof(double) * stride, cudaMemcpyDeviceToHost,
-                            c->stream));
-  c->wait();
   std::vector<double> sums(static_cast<size_t>(2 + c->shells));
-  sums[0] = c->h_out[0];
-  sums[1] = c->h_out[1];
-  for (int i = 0; i < c->shells; ++i) sums[2 + i] = c->h_out[3 + i];
-  double dmax = c->h_out[2];
+  sums[0] = h[0];
+  sums[1] = h[1];
+  for (int i = 0; i < c->shells; ++i) sums[2 + i] = h[3 + i];
+  double dmax = h[2];
   c->world->allreduce(sums.data(), static_cast<int>(sums.size()), 0);
   c->world->allreduce(&dmax, 1, 1);
   const double n3 = static_cast<double>(c->cfg.n) * c->cfg.n * c->cfg.n;
@@ -1566,6 +1582,7 @@ int sdns_ctx_create_ex(const sdns_config* cfg, int rank, int device, sdns_comm* 
     c->d_out = static_cast<double*>(dev_alloc(c.get(), sizeof(double) * stride));
     c->d_flag = static_cast<int*>(dev_alloc(c.get(), sizeof(int)));
     SDNS_CUDA(cudaMallocHost(&c->h_out, sizeof(double) * stride));
+    SDNS_CUDA(cudaMallocHost(&c->h_fout, sizeof(double) * stride));
     SDNS_CUDA(cudaMallocHost(&c->h_flag, sizeof(int)));
     c->wait();
     post_launch("ctx create");
@@ -1835,7 +1852,10 @@ int sdns_advance_hooks_run(sdns_ctx* c, sdns_state* st, const sdns_advance_hooks
         c->fused_u = &st->u;
         struct Clear {
           sdns_ctx* c;
-          ~Clear() { c->fused_u = nullptr; }
+          ~Clear() {
+            c->fused_u = nullptr;
+            c->fused_on_host = false;
+          }
         } clear{c};
         sample(k, st->t, user);
       }

@@ -52,7 +52,8 @@ def full(path):
             "launch__shared_mem_per_block_dynamic", "launch__block_size",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
             "smsp__issue_active.avg.pct_of_peak_sustained_active",
-            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
     units = rows[1]
     res = []
     for r in rows[2:]:
@@ -85,8 +86,8 @@ def main():
     res = [d for fp in fpaths for d in full(fp)]
     lines = [f"# {tag}: ncu --set full, n = {n} (one launch per kernel, --clock-control none)", "",
              "| kernel | ms | DRAM read GB | DRAM write GB | DRAM % | warps active % | regs | smem KB |"
-             " block | fp64 pipe % | issue % | smem bank conflicts |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             " block | fp64 pipe % | issue % | smem bank conflicts | smem wavefronts |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     tr = traffic.setdefault(str(n), {})
@@ -104,7 +105,8 @@ def main():
                      f"{g('launch__block_size')} | "
                      f"{float(g('sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active')):.1f} | "
                      f"{float(g('smsp__issue_active.avg.pct_of_peak_sustained_active')):.1f} | "
-                     f"{g('l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum')} |")
+                     f"{g('l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum')} | "
+                     f"{g('l1tex__data_pipe_lsu_wavefronts_mem_shared.sum')} |")
         for key, pname in PASS_OF:
             if key in name.replace("(int)", ""):
                 acc.setdefault(pname, []).append(rd + wr)
