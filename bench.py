@@ -458,6 +458,9 @@ def run_ours(args):
             uid = [S.Comm.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
             comm = S.Comm.nccl(uid[0], world, rank, device)
+            # the deadline catches dead peers, not slow ones (host-side setup
+            # such as the 1024^3 iso field can desynchronise ranks by minutes)
+            comm.set_timeout(900.0)
         else:
             dist.init_process_group("gloo")
             red_dev = "cpu"
@@ -468,6 +471,7 @@ def run_ours(args):
                 dist.all_gather(parts, t, group=group)
                 return [x.numpy().tobytes() for x in parts]
             comm = S.Comm.host(world, rank, device, allgather, new_group=dist.new_group)
+            comm.set_timeout(900.0)
     else:
         comm = S.Comm.loopback()
 
@@ -485,6 +489,8 @@ def run_ours(args):
     u.free()
     del uh0
     stream = torch.cuda.ExternalStream(ctx.stream)
+    if dist is not None:
+        dist.barrier()  # every rank's host setup done before the first collective
 
     def barrier():
         if dist is not None:
