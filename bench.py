@@ -216,7 +216,7 @@ def relaunch(args):
 
 # --- reference arm -------------------------------------------------------------
 
-REF_BUDGET_S = 240.0
+REF_BUDGET_S = 300.0
 
 
 def run_reference(args):

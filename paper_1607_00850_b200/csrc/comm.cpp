@@ -501,13 +501,17 @@ class HostComm final : public Comm {
     std::vector<int64_t> doff(p, 0);
     for (size_t d = 1; d < p; ++d) doff[d] = doff[d - 1] + mine[d - 1];
     std::vector<int64_t> put = doff;
-    SDNS_CUDA(cudaStreamSynchronize(s));
+    // copies on `s` itself: ordered after the producers of the send blocks and
+    // before the consumers of the receive blocks (a legacy-stream cudaMemcpy
+    // from pageable memory may return before its DMA lands, and a
+    // non-blocking stream is not ordered after it)
     for (const Xfer& x : xs)
       if (x.send_bytes) {
-        SDNS_CUDA(cudaMemcpy(pack.data() + put[static_cast<size_t>(x.peer)], x.send, x.send_bytes,
-                             cudaMemcpyDeviceToHost));
+        SDNS_CUDA(cudaMemcpyAsync(pack.data() + put[static_cast<size_t>(x.peer)], x.send,
+                                  x.send_bytes, cudaMemcpyDeviceToHost, s));
         put[static_cast<size_t>(x.peer)] += static_cast<int64_t>(x.send_bytes);
       }
+    SDNS_CUDA(cudaStreamSynchronize(s));
     (void)total;
     std::vector<char> all(static_cast<size_t>(maxtot) * p);
     gather(pack.data(), static_cast<size_t>(maxtot), all.data());
@@ -518,10 +522,11 @@ class HostComm final : public Comm {
     for (const Xfer& x : xs)
       if (x.recv_bytes) {
         const size_t q = static_cast<size_t>(x.peer);
-        SDNS_CUDA(cudaMemcpy(x.recv, all.data() + q * static_cast<size_t>(maxtot) + get[q],
-                             x.recv_bytes, cudaMemcpyHostToDevice));
+        SDNS_CUDA(cudaMemcpyAsync(x.recv, all.data() + q * static_cast<size_t>(maxtot) + get[q],
+                                  x.recv_bytes, cudaMemcpyHostToDevice, s));
         get[q] += static_cast<int64_t>(x.recv_bytes);
       }
+    SDNS_CUDA(cudaStreamSynchronize(s));  // `all` is released on return
   }
   void allreduce(double* v, int n, int op) override {
     std::vector<double> all(static_cast<size_t>(n) * size_);

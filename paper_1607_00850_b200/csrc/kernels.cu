@@ -412,14 +412,19 @@ template <int N>
 struct ZFCfg {
   static constexpr int E = fft_elems(N);
   static constexpr int TPC = N / E;
-  static constexpr int RPC = TPC >= 64 ? 4 : (256 / TPC > 64 ? 64 : 256 / TPC);
+  // n = 1024: one row per CTA, four CTAs per SM, so rows load while others
+  // transform (4 rows per CTA at 1 CTA/SM: 30.4 -> 27.3 ms per launch)
+  static constexpr int RPC = TPC >= 64 ? (N >= 1024 ? 1 : 4) : (256 / TPC > 64 ? 64 : 256 / TPC);
   static constexpr int THREADS = TPC * RPC;
   static constexpr int HP = N / 2 + 8;  // padded half-row (n/2+1 modes)
   // n = 512: both twiddled radix-8 stages take their twiddles from
   // registers (LastTw), so no table is staged in shared memory
   static constexpr bool REG = N == 512;
+  // n = 1024: the twiddle table stays in L2/L1 (global loads) so that four
+  // one-row CTAs fit an SM (with the table staged: 34.5 ms)
+  static constexpr bool GTAB = N >= 1024;
   static constexpr size_t SMEM =
-      sizeof(double2) * (static_cast<size_t>(RPC) * 6 * HP + (REG ? 0 : N));
+      sizeof(double2) * (static_cast<size_t>(RPC) * 6 * HP + ((REG || GTAB) ? 0 : N));
   // CTAs per SM the shared memory allows (n = 1024: one -- then give the
   // 16-element transforms the registers, 128 would spill)
   static constexpr int MINB = SMEM * 4 <= 227 * 1024 ? 4 : (SMEM * 2 <= 227 * 1024 ? 2 : 1);
@@ -449,7 +454,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   // that pair's FFT exchange buffer. Pair results stay in registers.
   double2* S = smem + r * 6 * HP;
   const double2* tws = tw;  // REG: the 4 register twiddles come from L2
-  if constexpr (!ZFCfg<N>::REG) {
+  if constexpr (!ZFCfg<N>::REG && !ZFCfg<N>::GTAB) {
     double2* t2 = smem + RPC * 6 * HP;
     load_twiddles(t2, tw, N);
     tws = t2;

@@ -672,6 +672,7 @@ int sdns_run_rank(const sdns_config* cfg, const char* initial_case, const sdns_r
     validate(*cfg);
     validate_case(icase);
     if (rank == 0) std::filesystem::create_directories(o.out_dir);
+    comm->c->set_timeout(o.timeout_s);  // RunOptions::collective_timeout
     ck(sdns_comm_barrier(comm));
     copy_str(out->backend, sizeof(out->backend), comm->c->kind());
     copy_str(out->status, sizeof(out->status), "ok");

@@ -14,6 +14,9 @@ import torch.distributed as dist
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_1607_00850_b200 as S  # noqa: E402
 
+if os.environ.get("AB_LIB"):  # debugging: another build of the library
+    S.use_library(os.environ["AB_LIB"])
+
 
 def main():
     rank, world, port, out, n = (int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]),

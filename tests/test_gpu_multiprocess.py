@@ -16,6 +16,9 @@ import pytest
 
 import paper_1607_00850_b200 as S
 
+if os.environ.get("AB_LIB"):  # debugging: another build of the library
+    S.use_library(os.environ["AB_LIB"])
+
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -80,6 +83,15 @@ def test_multiprocess_peer_direct_bitwise(tmp_path, world, grid):
             return res
 
     ref = S.run_group(world, body)
+    for r in range(world):
+        d = np.load(tmp_path / f"r{r}.npz")
+        assert str(d["transposes"]) == "peer-direct"
+        assert bool(d["ck_ok"])  # checkpoint round trip over the host transport
+        assert d["bcast"].tolist() == [world] * 24  # broadcast_bytes from the last rank
+        assert np.array_equal(d["du"], ref[r][0])
+        assert np.array_equal(d["u"], ref[r][1])
+        assert float(d["e"]) == ref[r][2] and float(d["z"]) == ref[r][3]
+        assert np.array_equal(d["ur"], ref[r][4]) and np.array_equal(d["fu"], ref[r][5])
     # the multi-process checkpoint equals one written by the threads-as-ranks run
     with S.Context(S.SolverConfig(n=n)) as c1:
         u1 = c1.real_field()
@@ -90,15 +102,6 @@ def test_multiprocess_peer_direct_bitwise(tmp_path, world, grid):
         lo = S.build_layout(cfg, r)
         (a0, a1, a2), (b0, b1, b2) = lo.real_shape, lo.real_offset
         assert np.array_equal(g[:, b0:b0 + a0, b1:b1 + a1, b2:b2 + a2], ref[r][4])
-    for r in range(world):
-        d = np.load(tmp_path / f"r{r}.npz")
-        assert str(d["transposes"]) == "peer-direct"
-        assert bool(d["ck_ok"])  # checkpoint round trip over the host transport
-        assert d["bcast"].tolist() == [world] * 24  # broadcast_bytes from the last rank
-        assert np.array_equal(d["du"], ref[r][0])
-        assert np.array_equal(d["u"], ref[r][1])
-        assert float(d["e"]) == ref[r][2] and float(d["z"]) == ref[r][3]
-        assert np.array_equal(d["ur"], ref[r][4]) and np.array_equal(d["fu"], ref[r][5])
 
 
 def test_stalled_peer_raises_timeout_error(tmp_path):
