@@ -214,9 +214,14 @@ struct ColIdx {
 };
 // Placement of a contiguous line with an XOR swizzle on 16-byte slots so the
 // stride-R writes of the first Stockham stage do not serialise on one bank.
-struct SwzIdx {
-  __device__ __forceinline__ int operator()(int x) const { return x ^ ((x >> 3) & 7); }
+// SH = log2 of the elements per thread: the first stage of E-element threads
+// writes positions E*j + r, so lanes j must land in distinct 16 B slots (the
+// shift of 3 alone left the radix-16 stages of n = 1024 2-way conflicted).
+template <int SH = 3>
+struct SwzIdxT {
+  __device__ __forceinline__ int operator()(int x) const { return x ^ ((x >> SH) & 7); }
 };
+using SwzIdx = SwzIdxT<3>;
 
 // Barrier policies: the whole CTA, or a named barrier over the threads that
 // own one transform (lets independent transforms in a CTA drift apart).

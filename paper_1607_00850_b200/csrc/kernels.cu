@@ -430,11 +430,19 @@ struct ZFCfg {
   static constexpr int MINB = SMEM * 4 <= 227 * 1024 ? 4 : (SMEM * 2 <= 227 * 1024 ? 2 : 1);
 };
 
+// Shared-memory swizzle of the z passes' exchange buffers (see SwzIdxT).
+template <int N>
+using ZSwz = SwzIdxT<(fft_elems(N) >= 16 ? 4 : 3)>;
+
 // z-pass transform.
 template <int N, int S, class Bar>
-__device__ __forceinline__ void zfft(double2 (&v)[fft_elems(N)], double2* sm, SwzIdx sw, int t,
+__device__ __forceinline__ void zfft(double2 (&v)[fft_elems(N)], double2* sm, ZSwz<N> sw, int t,
                                      const double2* tws, Bar bar, const LastTw& lt, int jf = -1,
                                      int jl = -1) {
+  // global twiddle table (n = 1024): an opaque copy of the pointer per
+  // transform keeps the compiler from holding every stage's twiddles in
+  // registers across all five transforms (it spilled them)
+  if constexpr (ZFCfg<N>::GTAB) asm volatile("" : "+l"(tws));
   block_fft_lt<N, S>(v, sm, sw, t, tws, bar, lt, jf, jl);
 }
 
@@ -461,7 +469,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   }
   Bar bar;
   if constexpr (TPC >= 64) bar = Bar{1 + r, TPC};
-  const SwzIdx sw;
+  const ZSwz<N> sw;
   // fields: 0..2 = u, 3 = w0', 4 = w1', 5 = w2, staged as the pairs
   // (u0, w1') (u1, w0') (u2, w2) -- slot s holds field kZSlot[s] -- all of
   // the row in flight at once. The z part of the curl (w0 = w0' - i kz u1,
@@ -693,8 +701,8 @@ k_z_c2r(const double2* __restrict__ spec, double* __restrict__ real, RowMap rm, 
   for (int m = 0; m < E; ++m)
     v[m] = valid ? pair_sample<N>(S, S + HP, t + m * TPC) : make_double2(0.0, 0.0);
   bar();
-  if constexpr (REG) block_fft_lt<N, +1>(v, S, SwzIdx{}, t, tws, bar, lt);
-  else block_fft<N, +1>(v, S, SwzIdx{}, t, tws, bar);
+  if constexpr (REG) block_fft_lt<N, +1>(v, S, ZSwz<N>{}, t, tws, bar, lt);
+  else block_fft<N, +1>(v, S, ZSwz<N>{}, t, tws, bar);
   if (valid) {
     double* a = real + static_cast<long long>(ri) * N;
     double* b = a + N;
@@ -724,7 +732,7 @@ k_z_r2c(const double* __restrict__ real, double2* __restrict__ spec, RowMap rm,
   if constexpr (TPC >= 64) bar = Bar{1 + r, TPC};
   __shared__ alignas(8) unsigned long long zbar[RPC];
   double2* reg = smem + r * N;
-  const SwzIdx sw;
+  const ZSwz<N> sw;
   double2 v[E];
   // the pair's two real rows (2 x 8n B, contiguous) arrive by bulk copy into
   // its region, which then serves as the transform's exchange buffer

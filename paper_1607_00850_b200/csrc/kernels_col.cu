@@ -92,8 +92,24 @@ struct TileIdx {
 // Shared-memory index of (position x, column col) of a tile buffer.
 template <int CS>
 struct CIdx {
+  static constexpr int kCS = CS;
   int col;
   __device__ __forceinline__ int operator()(int x) const { return TileIdx<CS>{}(x) + col; }
+};
+
+// Placement of the Stockham exchanges inside a tile buffer. A phase of a
+// 128-bit access is 8 lanes = 8 / CS positions x CS columns; with 4-column
+// tiles and 16-element threads (n = 1024) the first stage's writes (positions
+// 16 j + r) put the two positions of a phase on the same banks. Flipping the
+// position's low bit with its bit 4 separates them (exchanges only: tiles
+// arrive and leave in the linear TileIdx layout).
+template <int N, int CS>
+struct XIdx {
+  int col;
+  __device__ __forceinline__ int operator()(int x) const {
+    if constexpr (CS == 4 && fft_elems(N) == 16) x ^= (x >> 4) & 1;
+    return TileIdx<CS>{}(x) + col;
+  }
 };
 
 template <int CS>
@@ -213,20 +229,22 @@ __device__ __forceinline__ void peer_fence() {
 template <int N, int S, class IDX, class BAR>
 __device__ __forceinline__ void col_fft(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
                                         const double2* __restrict__ tw, BAR bar) {
+  const XIdx<N, IDX::kCS> xi{idx.col};
   if constexpr (N == 512)
-    block_fft_lt<N, S>(v, sm, idx, t, tw, bar, last_twiddles<N>(tw, t));
+    block_fft_lt<N, S>(v, sm, xi, t, tw, bar, last_twiddles<N>(tw, t));
   else
-    block_fft<N, S>(v, sm, idx, t, tw, bar);
+    block_fft<N, S>(v, sm, xi, t, tw, bar);
 }
 // Same with the register twiddles held by the caller (read once per kernel).
 template <int N, int S, class IDX, class BAR>
 __device__ __forceinline__ void col_fft_lt(double2 (&v)[fft_elems(N)], double2* sm, IDX idx, int t,
                                            const double2* __restrict__ tw, BAR bar,
                                            const LastTw& lt) {
+  const XIdx<N, IDX::kCS> xi{idx.col};
   if constexpr (N == 512)
-    block_fft_lt<N, S>(v, sm, idx, t, tw, bar, lt);
+    block_fft_lt<N, S>(v, sm, xi, t, tw, bar, lt);
   else
-    block_fft<N, S>(v, sm, idx, t, tw, bar);
+    block_fft<N, S>(v, sm, xi, t, tw, bar);
 }
 
 // Lane roles: column-minor (col = tid % CS, t = tid / CS), so a warp's
