@@ -439,10 +439,6 @@ template <int N, int S, class Bar>
 __device__ __forceinline__ void zfft(double2 (&v)[fft_elems(N)], double2* sm, ZSwz<N> sw, int t,
                                      const double2* tws, Bar bar, const LastTw& lt, int jf = -1,
                                      int jl = -1) {
-  // global twiddle table (n = 1024): an opaque copy of the pointer per
-  // transform keeps the compiler from holding every stage's twiddles in
-  // registers across all five transforms (it spilled them)
-  if constexpr (ZFCfg<N>::GTAB) asm volatile("" : "+l"(tws));
   block_fft_lt<N, S>(v, sm, sw, t, tws, bar, lt, jf, jl);
 }
 
