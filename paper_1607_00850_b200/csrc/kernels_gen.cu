@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <vector>
 
+#include "fft_core.cuh"
 #include "kernels.cuh"
 #include "rowmap.cuh"
 
@@ -31,7 +32,8 @@ namespace {
 constexpr int kGThreads = 256;
 constexpr int kMaxStages = 24;
 
-// Prime factorisation of n (the Stockham stage radices, smallest first).
+// Stockham stage radices of n: 8s, then a 4 or a 2 for the rest of the
+// power of two, then the odd prime factors smallest first.
 struct GPlan {
   int nst = 0;
   int rad[kMaxStages] = {};
@@ -40,7 +42,19 @@ struct GPlan {
 GPlan plan_of(int n) {
   GPlan p;
   int m = n;
-  for (int f = 2; m > 1 && p.nst < kMaxStages; ++f) {
+  while (m % 8 == 0 && p.nst < kMaxStages) {
+    p.rad[p.nst++] = 8;
+    m /= 8;
+  }
+  if (m % 4 == 0) {
+    p.rad[p.nst++] = 4;
+    m /= 4;
+  }
+  if (m % 2 == 0) {
+    p.rad[p.nst++] = 2;
+    m /= 2;
+  }
+  for (int f = 3; m > 1 && p.nst < kMaxStages; f += 2) {
     while (m % f == 0 && p.nst < kMaxStages) {
       p.rad[p.nst++] = f;
       m /= f;
@@ -61,10 +75,63 @@ __device__ __forceinline__ double gwave(int j, int n) {
   return static_cast<double>(j <= n / 2 - 1 ? j : j - n);
 }
 
+__device__ __forceinline__ double2 gtw(const double2* __restrict__ tw, int q, int dir) {
+  double2 w = __ldg(tw + q);
+  if (dir > 0) w.y = -w.y;
+  return w;
+}
+
+// One butterfly of a radix-R Stockham stage held in registers: x[r] =
+// input j + r m (twiddled by W_n^{r k span}), outputs (j - k) R + k + q ns.
+// R = 2, 4, 8 use the tuned DFTs of fft_core.cuh; other radices sum
+// directly with the table's R-th roots of unity.
+template <int R>
+__device__ __forceinline__ void gbfly(const double2* __restrict__ x, double2* __restrict__ y,
+                                      int j, int k, int m, int ns, int span, int n,
+                                      const double2* __restrict__ tw, int dir) {
+  double2 v[R];
+  v[0] = x[j];
+  int qq = 0;
+  const int step = k * span;
+#pragma unroll
+  for (int r = 1; r < R; ++r) {
+    qq += step;
+    if (qq >= n) qq -= n;
+    const double2 a = x[j + r * m];
+    v[r] = step ? gmul(a, gtw(tw, qq, dir)) : a;
+  }
+  if constexpr (R == 2 || R == 4 || R == 8) {
+    if (dir < 0) Dft<R, -1>::run(v);
+    else Dft<R, +1>::run(v);
+  } else {
+    double2 o[R];
+    const int root = n / R;  // W_R = W_n^root
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      double2 acc = v[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const int e = (r * q) % R;
+        const double2 t = e ? gmul(v[r], gtw(tw, e * root, dir)) : v[r];
+        acc.x += t.x;
+        acc.y += t.y;
+      }
+      o[q] = acc;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = o[q];
+  }
+  const int base = (j - k) * R + k;
+#pragma unroll
+  for (int q = 0; q < R; ++q) y[base + q * ns] = v[q];
+}
+
 // In-place (ping-pong) transform of `nl` lines of length n stored at
 // a + l*n; returns the buffer holding the result (a or b). dir -1 forward,
 // +1 inverse (conjugate twiddles); unnormalised. Every thread of the CTA
-// calls it; it begins and ends with a barrier.
+// calls it; it begins and ends with a barrier. A thread runs whole
+// butterflies (each element read and written once per stage); radices
+// without a register butterfly (primes > 7) sum each output directly.
 __device__ double2* gfft(double2* a, double2* b, int nl, int n, const GPlan& pl,
                          const double2* __restrict__ tw, int dir) {
   __syncthreads();
@@ -73,27 +140,42 @@ __device__ double2* gfft(double2* a, double2* b, int nl, int n, const GPlan& pl,
     const int R = pl.rad[st];
     const int m = n / R;            // butterflies per line
     const int span = n / (ns * R);  // twiddle stride of this stage
-    for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
-      const int l = idx / n, o = idx - l * n;
-      // output o = (j / ns) * ns * R + k + q * ns, j = (o / (ns R)) ns + k
-      const int blk = o / (ns * R), rem = o - blk * ns * R;
-      const int q = rem / ns, k = rem - q * ns;
-      const int j = blk * ns + k;
-      // y[o] = sum_r x[j + r m] W_n^{r (k span + q m)}
-      const int step = (k * span + q * m) % n;
-      const double2* x = a + l * n + j;
-      double2 acc = x[0];
-      int qq = 0;
-      for (int r = 1; r < R; ++r) {
-        qq += step;
-        if (qq >= n) qq -= n;
-        double2 w = __ldg(tw + qq);
-        if (dir > 0) w.y = -w.y;
-        const double2 v = gmul(x[r * m], w);
-        acc.x += v.x;
-        acc.y += v.y;
+    if (R <= 8 && R != 6) {
+      for (int idx = threadIdx.x; idx < nl * m; idx += blockDim.x) {
+        const int l = idx / m, j = idx - l * m;
+        const int k = j % ns;
+        const double2* x = a + l * n;
+        double2* y = b + l * n;
+        switch (R) {
+          case 2: gbfly<2>(x, y, j, k, m, ns, span, n, tw, dir); break;
+          case 3: gbfly<3>(x, y, j, k, m, ns, span, n, tw, dir); break;
+          case 4: gbfly<4>(x, y, j, k, m, ns, span, n, tw, dir); break;
+          case 5: gbfly<5>(x, y, j, k, m, ns, span, n, tw, dir); break;
+          case 7: gbfly<7>(x, y, j, k, m, ns, span, n, tw, dir); break;
+          default: gbfly<8>(x, y, j, k, m, ns, span, n, tw, dir); break;
+        }
       }
-      b[l * n + o] = acc;
+    } else {
+      for (int idx = threadIdx.x; idx < nl * n; idx += blockDim.x) {
+        const int l = idx / n, o = idx - l * n;
+        // output o = (j / ns) * ns * R + k + q * ns, j = (o / (ns R)) ns + k
+        const int blk = o / (ns * R), rem = o - blk * ns * R;
+        const int q = rem / ns, k = rem - q * ns;
+        const int j = blk * ns + k;
+        // y[o] = sum_r x[j + r m] W_n^{r (k span + q m)}
+        const int step = (k * span + q * m) % n;
+        const double2* x = a + l * n + j;
+        double2 acc = x[0];
+        int qq = 0;
+        for (int r = 1; r < R; ++r) {
+          qq += step;
+          if (qq >= n) qq -= n;
+          const double2 v = gmul(x[r * m], gtw(tw, qq, dir));
+          acc.x += v.x;
+          acc.y += v.y;
+        }
+        b[l * n + o] = acc;
+      }
     }
     __syncthreads();
     double2* t = a;
