@@ -454,6 +454,7 @@ def run_ours(args):
         import torch.distributed as dist
         if args.transport == "nccl":
             os.environ.setdefault("NCCL_DEBUG", "INFO")  # the communicator log names every rank
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")  # ... at init only
             dist.init_process_group("nccl", device_id=torch.device("cuda", device))
             uid = [S.Comm.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
@@ -544,6 +545,7 @@ def run_ours(args):
         state.close()
         ctx.close()
         if dist is not None:
+            dist.barrier()  # rank 0 has printed its line: no log output can cut into it
             dist.destroy_process_group()
         return
 
@@ -631,6 +633,7 @@ def run_ours(args):
                                     "kind": "reference", "sample": f"unavailable: {e}"}
     print(json.dumps(line), flush=True)
     if dist is not None:
+        dist.barrier()
         dist.destroy_process_group()
 
 
