@@ -555,17 +555,30 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
                    }
                    if (f > 0) {
                      if constexpr (!SCR) ln.bar();  // the transform below reuses buf
+                     // n <= 64: small grids walk (tile, component) units on
+                     // separate CTAs (split_units), where U0 of this tile may
+                     // not exist yet, so w2' = i F(kx u1 - ky u0) by linearity
+                     // with u0 read directly (at every p and transpose mode,
+                     // so all of them agree bit for bit)
+                     const bool lin = N <= 64 && f == 1 && tl.valid;
+                     const double ky = wavenum(g.row_off + tl.row, N);
 #pragma unroll
                      for (int m = 0; m < E; ++m) {
                        const double kx = wavenum(t + m * TPC, N);
                        v[m] = make_double2(kx * v[m].x, kx * v[m].y);
+                       if (lin) {
+                         const double2 a = u[tl.base + po.o(m)];
+                         v[m] = make_double2(v[m].x - ky * a.x, v[m].y - ky * a.y);
+                       }
                      }
                      col_fft<N, +1>(v, SCR ? scr : buf, ln.idx, t, tws, ln.bar);
-                     if (f == 1) {
+                     if (lin) {
+#pragma unroll
+                       for (int m = 0; m < E; ++m) v[m] = times_i(v[m]);
+                     } else if (f == 1) {
                        // w2' = i (K1 - ky U0): ky is constant along an x column and
                        // U0 of this tile was stored by item 0 (L2-resident)
                        if (tl.valid) {
-                         const double ky = wavenum(g.row_off + tl.row, N);
                          const Tile to = os.tile(tl, go);
                          const PosOff<N>& pout = os.po(po);
                          const double2* u0 = out + to.base;
@@ -877,20 +890,26 @@ static void x_inv_n(const double2* u, long long u_cs, double2* out, long long ou
   const ColGeom gt = with_tile_map<N, C::CS>(g, u, u_cs, 3, &tm);
   if (go && go->seg) {  // peer-direct output (slab x inverse into the peers' receive layouts)
     static int occ = 0;
-    const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, 2>, C::THREADS, C::SMEM, work_units<N, VXI>(nt), &occ);
+    unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, 2>, C::THREADS, C::SMEM, work_units<N, VXI>(nt), &occ);
+    ColGeom gs = gt;
+    split_units<N, VXI>(gs, nt, f_cnt, occ, grid);
     k_pipe_xinv<N, VXI, 2><<<grid, C::THREADS, C::SMEM, s>>>(
-        u, u_cs, out, out_cs, gt, *go, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
+        u, u_cs, out, out_cs, gs, *go, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   } else if (go) {
     static int occ = 0;
-    const unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, 1>, C::THREADS, C::SMEM, work_units<N, VXI>(nt), &occ);
+    unsigned grid = persistent_grid(k_pipe_xinv<N, VXI, 1>, C::THREADS, C::SMEM, work_units<N, VXI>(nt), &occ);
+    ColGeom gs = gt;
+    split_units<N, VXI>(gs, nt, f_cnt, occ, grid);
     k_pipe_xinv<N, VXI, 1><<<grid, C::THREADS, C::SMEM, s>>>(
-        u, u_cs, out, out_cs, gt, *go, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
+        u, u_cs, out, out_cs, gs, *go, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   } else {
     static int occ = 0;
-    const unsigned grid =
+    unsigned grid =
         persistent_grid(k_pipe_xinv<N, VXI, 0>, C::THREADS, C::SMEM, work_units<N, VXI>(nt), &occ);
+    ColGeom gs = gt;
+    split_units<N, VXI>(gs, nt, f_cnt, occ, grid);
     k_pipe_xinv<N, VXI, 0><<<grid, C::THREADS, C::SMEM, s>>>(
-        u, u_cs, out, out_cs, gt, gt, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
+        u, u_cs, out, out_cs, gs, gt, static_cast<int>(nt), f_lo, f_cnt, tw, tm);
   }
 }
 

@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kGThreads) k_gen_col(const __grid_constant__ G
         if (go.keep_k >= 0 && pos > go.keep_k && pos < n - go.keep_k) continue;
         long long e = static_cast<long long>(row) * go.rs +
                       static_cast<long long>(kz >> 3) * go.kcs + (kz & 7) + gpos(go, pos);
-        if (go.seg) e += __ldg(go.seg + pos / go.pblk);
+        if (go.seg) e += __ldg(go.seg + (go.pblk > 0 ? pos / go.pblk : 0));
         double2 v = r[c * n + pos];
         if (I.post == G_W2) {
           const double2 w = u0[e];
