@@ -437,6 +437,8 @@ def run_ours(args):
 
     if args.lib:
         S.use_library(args.lib)
+    if args.opt:  # A/B only: the defaults are what the line reports
+        S.set_default_options(**{k: int(v) for k, v in (kv.split("=") for kv in args.opt.split(","))})
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
@@ -654,6 +656,7 @@ def main():
     ap.add_argument("--no-other-configs", action="store_true")
     ap.add_argument("--no-1024", action="store_true", help="skip the n = 1024 one-GPU lines")
     ap.add_argument("--lib", default=None, help="A/B: another build of the product library")
+    ap.add_argument("--opt", default="", help="A/B: context options, e.g. p1_single=1,plain_layout=1")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
                     help="N > 1: NCCL (one GPU per rank) or the host-callback transport "
                          "(harness check; ranks may share a GPU)")

@@ -194,6 +194,11 @@ typedef struct sdns_ctx_options {
   int plain_layout; /* 1: p = 1 keeps the natural work layouts (no chunk-major
                        P1 output / chunked P2..P5a layout) */
   int no_graph;     /* 1: p = 1 steps launch eagerly, not as a captured graph */
+  int p1_single;    /* x inverse pass (P1) as five single-transform items on one
+                       128 B-row tile buffer instead of three items with two
+                       transforms and a scratch tile. 0: by size (on at
+                       n >= 1024, where two 128 B-row tiles do not fit), 1: on
+                       (tuned n >= 128), -1: off */
 } sdns_ctx_options;
 int sdns_ctx_create_ex(const sdns_config* cfg, int rank, int device, sdns_comm* comm,
                        void* stream, const sdns_ctx_options* opts, sdns_ctx** out);

@@ -120,7 +120,7 @@ class _ParsedConfig(ctypes.Structure):
 class _CtxOptions(ctypes.Structure):
     _fields_ = [("all_to_all", ctypes.c_int), ("serial", ctypes.c_int),
                 ("ldgsts_tiles", ctypes.c_int), ("plain_layout", ctypes.c_int),
-                ("no_graph", ctypes.c_int)]
+                ("no_graph", ctypes.c_int), ("p1_single", ctypes.c_int)]
 
 
 class _RunOptions(ctypes.Structure):
@@ -604,7 +604,7 @@ def run_group(size: int, body: Callable[[int, Comm], object], device: int = 0,
 
 # --- context and fields -----------------------------------------------------------
 
-_OPTION_KEYS = ("all_to_all", "serial", "ldgsts_tiles", "plain_layout", "no_graph")
+_OPTION_KEYS = ("all_to_all", "serial", "ldgsts_tiles", "plain_layout", "no_graph", "p1_single")
 _default_options: dict = {}
 
 
@@ -612,7 +612,7 @@ _default_options: dict = {}
 def context_options(**kw):
     """Default execution options of the Contexts created inside the block
     (sdns_ctx_options: all_to_all, serial, ldgsts_tiles, plain_layout,
-    no_graph); none changes a result bit. The library reads no environment."""
+    no_graph, p1_single); none changes a result bit. The library reads no environment."""
     global _default_options
     bad = set(kw) - set(_OPTION_KEYS)
     if bad:
@@ -625,12 +625,21 @@ def context_options(**kw):
         _default_options = old
 
 
+def set_default_options(**kw) -> None:
+    """Execution options of every Context created from now on (A/B runs)."""
+    global _default_options
+    bad = set(kw) - set(_OPTION_KEYS)
+    if bad:
+        raise ConfigError(f"unknown context options {sorted(bad)}")
+    _default_options = {**_default_options, **kw}
+
+
 def _ctx_options(options: Optional[dict]) -> _CtxOptions:
     opt = {**_default_options, **(options or {})}
     bad = set(opt) - set(_OPTION_KEYS)
     if bad:
         raise ConfigError(f"unknown context options {sorted(bad)}")
-    return _CtxOptions(*[int(bool(opt.get(k, 0))) for k in _OPTION_KEYS])
+    return _CtxOptions(*[int(opt.get(k, 0)) for k in _OPTION_KEYS])
 
 
 class Context:

@@ -281,6 +281,7 @@ struct sdns_ctx {
     g.row_off = static_cast<int>(lo.spec_offset[1]);
     g.mpitch = opt.ldgsts_tiles ? 0 : pitch;  // 0: no tensor map, LDGSTS tiles
     g.mrows = prow;
+    g.single = opt.p1_single > 0 || (opt.p1_single == 0 && cfg.n >= 1024);
     return g;
   }
   ColGeom xl_out() const {  // x-pass view of wx: rows = y, positions = x

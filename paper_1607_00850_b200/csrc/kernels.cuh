@@ -44,6 +44,9 @@ struct ColGeom {
   // (small grids: more CTAs, each a shorter chain; only where items of a
   // tile are independent)
   int split = 0;
+  // x inverse pass (P1): five single-transform items on one tile buffer
+  // (k_pipe_xinv1) instead of three items with a scratch tile
+  int single = 0;
   // Peer-direct output (slab transposes fused into the producing pass,
   // DESIGN.md §5): element offset of segment pos >> pb_shift's destination
   // block from the output base -- another rank's buffer on this device or

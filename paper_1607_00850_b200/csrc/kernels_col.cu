@@ -606,6 +606,57 @@ k_pipe_xinv(const double2* u, long long u_cs, double2* out, long long out_cs, Co
   peer_fence<SEP>();
 }
 
+// P1 with one transform per item on a single 8-column tile buffer (n = 1024,
+// where two 128 B-row tiles plus a scratch tile do not fit): items
+//   0: U0 = F(u0)   1: w2' = i (F(kx u1) - ky U0)   2: U1 = F(u1)
+//   3: K2 = F(kx u2)   4: U2 = F(u2)
+// The second item of a component reloads its tile (from L2: the same CTA
+// loaded it one item earlier). Same transforms and operations as k_pipe_xinv.
+template <int N, int V, int SEP>
+__global__ void __launch_bounds__(PipeCfg<N, V>::THREADS, PipeCfg<N, V>::MINB)
+k_pipe_xinv1(const double2* u, long long u_cs, double2* out, long long out_cs, ColGeom g,
+             ColGeom go, int ntiles, int it_lo, int it_cnt, const double2* __restrict__ tw,
+             const __grid_constant__ CUtensorMap tm) {
+  constexpr int E = fft_elems(N), TPC = N / E;
+  const OutSel<N, SEP> os(go, Lanes<N, V>().t);
+  auto comp = [](int it) { return (it + 1) >> 1; };
+  pipeline<N, V>(ntiles, it_lo, it_cnt, g, [&](int it) { return u + comp(it) * u_cs; }, comp, &tm,
+                 tw,
+                 [&](int it, double2* buf, const Tile& tl, const PosOff<N>& po,
+                     const Lanes<N, V>& ln, const double2* tws, auto&& release) {
+                   const int t = ln.t;
+                   const bool kxm = it & 1;
+                   double2 v[E];
+                   read_own<N>(v, buf, ln.idx, t);
+                   if (kxm) {
+#pragma unroll
+                     for (int m = 0; m < E; ++m) {
+                       const double kx = wavenum(t + m * TPC, N);
+                       v[m] = make_double2(kx * v[m].x, kx * v[m].y);
+                     }
+                   }
+                   ln.bar();
+                   col_fft<N, +1>(v, buf, ln.idx, t, tws, ln.bar);
+                   release();  // buffer no longer read: the next tile may load
+                   const Tile to = os.tile(tl, go);
+                   const PosOff<N>& pout = os.po(po);
+                   if (it == 1 && tl.valid) {
+                     const double ky = wavenum(g.row_off + tl.row, N);
+                     const double2* u0 = out + to.base;
+#pragma unroll
+                     for (int m = 0; m < E; ++m) {
+                       long long at = pout.o(m);
+                       if constexpr (SEP == 2) at += __ldg(go.seg + ((t + m * TPC) >> go.pb_shift));
+                       const double2 a = u0[at];
+                       v[m] = times_i(make_double2(v[m].x - ky * a.x, v[m].y - ky * a.y));
+                     }
+                   }
+                   const int of = kxm ? 2 + comp(it) : comp(it);
+                   store_own<N, SEP == 2>(out + of * out_cs, v, go, to, pout, t);
+                 });
+  peer_fence<SEP>();
+}
+
 // ---------------------------------------------------------------------------
 // P2: y inverse of fields 0..4 = [U0, U1, U2, w2', K2] of `fin`, producing
 // [u0, u1, u2, w0', w1', w2] in fields 0..5 of `f` (in place for the slab
@@ -880,10 +931,50 @@ void col_plain_to(int n, int dir, const double2* in, double2* out, long long in_
   }
 }
 
+// P1 as five single-transform items (k_pipe_xinv1): the default at n = 1024
+// (single 8-column tile buffer); selectable at n >= 128 (ColGeom::single).
+template <int N>
+static void x_inv1_n(const double2* u, long long u_cs, double2* out, long long out_cs,
+                     const ColGeom& g, const ColGeom* go, int f_lo, int f_cnt, const double2* tw,
+                     cudaStream_t s) {
+  constexpr int V = N >= 1024 ? 9 : 0;
+  using C = PipeCfg<N, V>;
+  const long long nt = ntiles_of<N, V>(g);
+  if (nt <= 0) return;
+  // components [f_lo, f_lo + f_cnt) -> items: component 0 is item 0,
+  // component c > 0 items 2c - 1 and 2c
+  const int it_lo = f_lo == 0 ? 0 : 2 * f_lo - 1, it_hi = 2 * (f_lo + f_cnt) - 1;
+  CUtensorMap tm;
+  const ColGeom gt = with_tile_map<N, C::CS>(g, u, u_cs, 3, &tm);
+  const int ntl = static_cast<int>(nt);
+  if (go && go->seg) {
+    static int occ = 0;
+    const unsigned grid = persistent_grid(k_pipe_xinv1<N, V, 2>, C::THREADS, C::SMEM, nt, &occ);
+    k_pipe_xinv1<N, V, 2><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, gt, *go, ntl,
+                                                            it_lo, it_hi - it_lo, tw, tm);
+  } else if (go) {
+    static int occ = 0;
+    const unsigned grid = persistent_grid(k_pipe_xinv1<N, V, 1>, C::THREADS, C::SMEM, nt, &occ);
+    k_pipe_xinv1<N, V, 1><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, gt, *go, ntl,
+                                                            it_lo, it_hi - it_lo, tw, tm);
+  } else {
+    static int occ = 0;
+    const unsigned grid = persistent_grid(k_pipe_xinv1<N, V, 0>, C::THREADS, C::SMEM, nt, &occ);
+    k_pipe_xinv1<N, V, 0><<<grid, C::THREADS, C::SMEM, s>>>(u, u_cs, out, out_cs, gt, gt, ntl,
+                                                            it_lo, it_hi - it_lo, tw, tm);
+  }
+}
+
 template <int N>
 static void x_inv_n(const double2* u, long long u_cs, double2* out, long long out_cs,
                     const ColGeom& g, const ColGeom* go, int f_lo, int f_cnt, const double2* tw,
                     cudaStream_t s) {
+  if constexpr (N >= 128) {
+    if (g.single) {
+      x_inv1_n<N>(u, u_cs, out, out_cs, g, go, f_lo, f_cnt, tw, s);
+      return;
+    }
+  }
   using C = PipeCfg<N, VXI>;
   const long long nt = ntiles_of<N, VXI>(g);
   CUtensorMap tm;

@@ -590,6 +590,49 @@ def test_inprocess_transpose_modes_bitwise(geom):
                 assert np.array_equal(x, y), name
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,geom", [(128, dict(p=1)), (256, dict(p=1)), (256, dict(p=2)),
+                                    (128, dict(decomp="pencil", p=4, p1=2, p2=2)),
+                                    (512, dict(p=1))])
+def test_p1_single_transform_items(n, geom):
+    """The x inverse pass (P1) as five single-transform items on one tile
+    buffer -- what n = 1024 runs, where two 128 B-row tiles plus a scratch
+    tile do not fit -- forced at smaller n (context option p1_single) against
+    the default three-item kernel: the same transforms and operations, so one
+    RHS must agree to rounding (the compiler contracts the kx products into
+    FMAs differently in the two kernels: bitwise at 256, 512 and 1024, 3e-16
+    at 128) at p = 1 (chunk-major and plain layouts), slab and pencil with
+    peer-direct stores, and with all-to-all transposes; the variants of the
+    single-item kernel itself (TMA / LDGSTS tiles, layouts, transposes) must
+    agree bit for bit."""
+    p = geom["p"]
+    uh0 = S.iso_init(n, S.build_layout(S.SolverConfig(n=n), 0), seed=11)
+    cfg = S.SolverConfig(n=n, nu=1e-3, dt=1e-3, t_end=1e-3, **geom)
+
+    def run():
+        def body(rank, comm):
+            with S.Context(cfg, rank=rank, comm=comm) as c:
+                u = c.spectral_field().upload(_scatter_spec(uh0, c.layout))
+                du = c.spectral_field()
+                S.compute_rhs(c, u, 1e-3, du)
+                return du.download()
+        return S.run_group(p, body)
+
+    base = run()
+    variants = [dict(p1_single=1), dict(p1_single=1, ldgsts_tiles=1)]
+    variants.append(dict(p1_single=1, plain_layout=1) if p == 1 else dict(p1_single=1, all_to_all=1))
+    first = None
+    for opt in variants:
+        with S.context_options(**opt):
+            got = run()
+        for a, b in zip(base, got):
+            assert np.abs(a - b).max() <= 4e-15 * np.abs(a).max(), opt
+        if first is None:
+            first = got
+        for a, b in zip(first, got):
+            assert np.array_equal(a, b), opt
+
+
 # --- pencil decomposition (fft.cpp:130-227) on one GPU ---------------------------
 
 PENCILS = [(2, 1), (1, 2), (2, 2), (2, 4), (4, 2)]
