@@ -625,8 +625,12 @@ def test_p1_single_transform_items(n, geom):
     for opt in variants:
         with S.context_options(**opt):
             got = run()
+        # one scale for all ranks: a pencil rank that owns only high kz holds
+        # values ~1e-13 of the field's largest modes, and the rounding noise
+        # of the unnormalised transforms is absolute, not relative to them
+        scale = max(np.abs(a).max() for a in base)
         for a, b in zip(base, got):
-            assert np.abs(a - b).max() <= 4e-15 * np.abs(a).max(), opt
+            assert np.abs(a - b).max() <= 4e-15 * scale, opt
         if first is None:
             first = got
         for a, b in zip(first, got):
