@@ -458,11 +458,7 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
   // that pair's FFT exchange buffer. Pair results stay in registers.
   double2* S = smem + r * 6 * HP;
   const double2* tws = tw;  // REG: the 4 register twiddles come from L2
-  if constexpr (!ZFCfg<N>::REG && !ZFCfg<N>::GTAB) {
-    double2* t2 = smem + RPC * 6 * HP;
-    load_twiddles(t2, tw, N);
-    tws = t2;
-  }
+  if constexpr (!ZFCfg<N>::REG && !ZFCfg<N>::GTAB) tws = smem + RPC * 6 * HP;
   Bar bar;
   if constexpr (TPC >= 64) bar = Bar{1 + r, TPC};
   const ZSwz<N> sw;
@@ -502,6 +498,9 @@ k_z_fused(double2* f, long long cs, RowMap rm, double norm, const double2* __res
       }
     }
   }
+  // the table is staged after the rows are requested (small n: the kernel is
+  // one latency chain, the two fetches overlap)
+  if constexpr (!ZFCfg<N>::REG && !ZFCfg<N>::GTAB) load_twiddles(smem + RPC * 6 * HP, tw, N);
   __syncthreads();  // twiddles
   if (valid) mbar_wait(&zbar[r], 0);
   const LastTw lt = last_twiddles<N>(tws, t);

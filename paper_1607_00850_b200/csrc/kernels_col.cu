@@ -340,10 +340,15 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
   const PosOff<N> po(g, t);
   const bool tma = g.tma != 0;
   double2* tws = smem + (NBUF + PipeCfg<N, V>::SCR) * N * CS;
-  load_twiddles(tws, tw_global, N);
   if (tma && threadIdx.x == 0)
     for (int j = 0; j < NBUF; ++j) mbar_init(&tbar[j], 1);
-  __syncthreads();
+  // The twiddle table is staged after the first tiles are requested (they
+  // depend only on thread 0's barrier init or on nothing, LDGSTS): at small n
+  // a kernel is one latency chain and the two fetches then overlap.
+  auto stage_twiddles = [&] {
+    load_twiddles(tws, tw_global, N);
+    __syncthreads();  // table and barrier init visible to every thread
+  };
   // ring slot j at smem + j*N*CS (arithmetic, not a pointer array: that
   // would live in local memory)
   auto ring = [&](int j) { return smem + j * (N * CS); };
@@ -369,6 +374,7 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
     // the next tile loads while this one is stored from registers
     Tile tl = tile_of<CS>(tile, col, g);
     if (tile < ntiles) issue(0, f, tl);
+    stage_twiddles();
     for (int i = 0; tile < ntiles; ++i) {
       int fn = f + 1, tn = tile;
       if (fn == f_hi) {
@@ -394,6 +400,7 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
     return;
   }
   if (NBUF == 1) {
+    stage_twiddles();
     for (int i = 0; tile < ntiles; ++i) {
       const Tile tl = tile_of<CS>(tile, col, g);
       issue(0, f, tl);
@@ -462,6 +469,7 @@ __device__ __forceinline__ void pipeline(int ntiles, int f_lo, int items, const 
     if (n1.t0 < ntiles) issue(1, n1.f, tn1);
     cp_commit();
   }
+  stage_twiddles();
   for (int i = 0; cur.t0 < ntiles; ++i) {
     if (NBUF > 2) {
       const Item n2 = adv(n1);
