@@ -350,7 +350,10 @@ def _embed_band(small, ns, nb, K):
 
 
 @pytest.mark.parametrize("n,geom", [(1024, dict(p=1)), (1024, dict(p=4)), (1024, dict(p=8)),
-                                    (512, dict(p=2))])
+                                    (512, dict(p=2)),
+                                    (512, dict(decomp="pencil", p=8, p1=2, p2=4)),
+                                    (512, dict(decomp="pencil", p=8, p1=4, p2=2)),
+                                    (768, dict(p=1)), (384, dict(p=3))])
 def test_rhs_full_size_band_limited_vs_reference(ref, n, geom):
     """The fused RHS pipeline of the largest grids (n = 1024: config 4's
     per-GPU kernels -- five single-transform P1 items, 4-column y tiles,
@@ -362,7 +365,9 @@ def test_rhs_full_size_band_limited_vs_reference(ref, n, geom):
     the RHS is the same set of Fourier coefficients on every grid, scaled by
     the grid ratio cubed. The reference runs at 128^3; every mode of the
     device result must match it (<= 1e-12 max|du|, the RHS bar) and every
-    mode outside the band must vanish to the same tolerance."""
+    mode outside the band must vanish to the same tolerance. Also run: the
+    pencil grids of config 4 (2x4, 4x2) at 512^3, and the generic-length
+    kernels at production sizes (768^3; 384^3 on three slabs)."""
     ns, kin, nu = 128, 21, 1e-3
     kout = 2 * kin
     assert kout < ns / 3 and kout < n / 3
@@ -402,14 +407,15 @@ def test_rhs_full_size_band_limited_vs_reference(ref, n, geom):
                 # intersect the big-grid block with this rank's (x, y) range
                 x0, x1 = max(bx.start, o0), min(bx.stop, o0 + s0)
                 y0, y1 = max(by.start, o1), min(by.stop, o1 + s1)
-                if x0 >= x1 or y0 >= y1 or o2 != 0:
+                z0, z1 = max(0, o2), min(kout + 1, o2 + got.shape[3])  # pencil: kz blocks
+                if x0 >= x1 or y0 >= y1 or z0 >= z1:
                     continue
                 gx = slice(x0 - o0, x1 - o0)
                 gy = slice(y0 - o1, y1 - o1)
                 wx = slice(sx.start + x0 - bx.start, sx.start + x1 - bx.start)
                 wy = slice(sy.start + y0 - by.start, sy.start + y1 - by.start)
-                w = scale * want_small[:, wx, wy, :kout + 1]
-                g = got[:, gx, gy, :kout + 1]
+                w = scale * want_small[:, wx, wy, z0:z1]
+                g = got[:, gx, gy, z0 - o2:z1 - o2]
                 worst_band = max(worst_band, float(np.abs(g - w).max()))
                 g[...] = 0.0
         for i in range(got.shape[0]):
