@@ -61,18 +61,6 @@ __device__ __forceinline__ double2 i_cross(double a, double2 x, double b, double
   return make_double2(-im, re);
 }
 
-// Launch shape of the column passes.
-template <int N>
-struct ColCfg {
-  static constexpr int E = fft_elems(N);
-  static constexpr int TPC = N / E;
-  // columns per CTA: fill ~256-512 threads, 8-column (128 B) tiles at least
-  static constexpr int CS = TPC >= 64 ? 4 : (256 / TPC < 8 ? 8 : 256 / TPC);
-  // fused forward x-pass keeps 3 components in shared memory
-  static constexpr int CSF = N >= 512 ? 4 : (CS > 16 ? 16 : CS);
-  static constexpr int THREADSF = TPC * CSF;
-};
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
