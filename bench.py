@@ -619,7 +619,10 @@ def run_ours(args):
     }
     if world == 1 and n == 512 and not args.no_other_configs:
         state.close()
-        line["other_configs"] = other_configs(S, ctx, hbm_peak)
+        try:
+            line["other_configs"] = other_configs(S, ctx, hbm_peak)
+        except Exception as e:  # noqa: BLE001  (informational lines never cost the headline)
+            line["other_configs"] = {"error": f"not run: {e}"}
     state.close()
     ctx.close()
     if world == 1 and n == 512 and not args.no_other_configs and not args.no_1024:
