@@ -144,6 +144,17 @@ struct PosOff {
   int t, ps0, ps1, shift;
   __device__ __forceinline__ PosOff(const ColGeom& g, int t_)
       : t(t_), ps0(static_cast<int>(g.ps0)), ps1(static_cast<int>(g.ps1)), shift(g.pb_shift) {}
+  // A copy whose strides the compiler cannot trace back: the offsets derived
+  // from it are recomputed where they are used instead of being hoisted out
+  // of the item loop. In the 16-element kernels at the 128-register limit
+  // (n = 1024) the hoisted offsets were spilled, and every store then waited
+  // for local-memory reloads (L1 is carved down to almost nothing here): 25%
+  // of the x inverse pass's stall samples (P1 at 1024: 22.0 -> 21.5 ms).
+  __device__ __forceinline__ PosOff fresh() const {
+    PosOff q = *this;
+    asm volatile("" : "+r"(q.ps0), "+r"(q.ps1), "+r"(q.t));
+    return q;
+  }
   __device__ __forceinline__ int o(int m) const {
     const int pos = t + m * (N / fft_elems(N));
     return (pos >> shift) * ps1 + (pos & ((1 << shift) - 1)) * ps0;
@@ -177,14 +188,15 @@ __device__ __forceinline__ void store_own(double2* dst, const double2 (&v)[fft_e
   constexpr int E = fft_elems(N), TPC = N / E;
   if (!tl.valid) return;
   double2* b = dst + tl.base;
+  const PosOff<N> q = E >= 16 ? po.fresh() : po;
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const int pos = t + m * TPC;
     if (g.keep_k >= 0 && pos > g.keep_k && pos < N - g.keep_k) continue;  // masked mode
     if constexpr (PEER)
-      b[po.o(m) + __ldg(g.seg + (pos >> g.pb_shift))] = v[m];
+      b[q.o(m) + __ldg(g.seg + (pos >> g.pb_shift))] = v[m];
     else
-      b[po.o(m)] = v[m];
+      b[q.o(m)] = v[m];
   }
 }
 
@@ -647,7 +659,7 @@ k_pipe_xinv1(const double2* u, long long u_cs, double2* out, long long out_cs, C
                    col_fft<N, +1>(v, buf, ln.idx, t, tws, ln.bar);
                    release();  // buffer no longer read: the next tile may load
                    const Tile to = os.tile(tl, go);
-                   const PosOff<N>& pout = os.po(po);
+                   const PosOff<N> pout = E >= 16 ? os.po(po).fresh() : os.po(po);
                    if (it == 1 && tl.valid) {
                      const double ky = wavenum(g.row_off + tl.row, N);
                      const double2* u0 = out + to.base;
