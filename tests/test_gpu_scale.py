@@ -457,7 +457,12 @@ def test_1024_rk4_step_band_limited_vs_reference(ref):
     with S.Context(cfg) as c:
         st = S.Rk4State(c)
         st.step_host(big, dt, 1)  # host in, one step (+ projection), host out
+        stats = S.collect_stats(c, st.u_hat, nu)
         st.close()
+    # energy and enstrophy of a band-limited field do not depend on the grid
+    rs = ref.collect_stats(want_small, ns, nu, p=_ref_threads())
+    assert abs(stats.energy - rs[1]) <= 1e-12 * rs[1], (stats.energy, rs[1])
+    assert abs(stats.enstrophy - rs[2]) <= 1e-12 * rs[2], (stats.enstrophy, rs[2])
     num = 0.0
     den = 0.0
     worst = 0.0
